@@ -1,0 +1,151 @@
+/*
+ * pagetopk_b200.h -- C ABI of the B200-native UNIQUE decode hot path.
+ *
+ * The reference (`pagetopk`, /root/reference/pkg/src/pagetopk/) crosses exactly one
+ * boundary on this path: the kernel-backend module contract of backend.py:14-58,
+ * i.e. three functions bound from Python (`_kernels_cy.pyx`, `_kernels_py.py`).
+ * Section A mirrors those three calls one for one (host buffers in, host buffers out,
+ * same argument meaning) so a maintainer can register this library as a third backend
+ * (INTEGRATION.md).  Section B is the batched, stream-ordered device API the package
+ * `paper_2605_27740_b200` drives: caller-allocated device buffers, no host sync,
+ * graph-capturable.
+ *
+ * Conventions: every entry point returns 0 on success, a PT_ERR_* precondition code,
+ * or PT_ERR_CUDA_BASE + cudaError_t.  `stream` is a cudaStream_t passed as void*.
+ * Units are (sequence b, kv-head h) pairs, u = b * H_kv + h; query heads are grouped
+ * contiguously, q-head h_q -> kv-head h_q / G (attention.py:138).
+ */
+#ifndef PAGETOPK_B200_H
+#define PAGETOPK_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define PT_API __attribute__((visibility("default")))
+#else
+#define PT_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* element types of the KV pool / page means / queries */
+#define PT_F32 0
+#define PT_BF16 1
+
+/* status codes */
+#define PT_OK 0
+#define PT_ERR_INVALID 1     /* bad argument (null pointer, negative size, ...)          */
+#define PT_ERR_UNSUPPORTED 2 /* shape outside the compiled envelope (D, G, S limits)     */
+#define PT_ERR_K 3           /* k < 1: "k must be at least 1" (select.py:94-95)          */
+#define PT_ERR_EMPTY 4       /* no pages: "no pages to select from" (select.py:98-99)    */
+#define PT_ERR_CAPACITY 5    /* pool exhausted: CapacityError (kvcache.py:164-166)       */
+#define PT_ERR_CUDA_BASE 1000
+
+/* library identity */
+PT_API int pt_version(void);
+PT_API const char *pt_status_string(int status);
+
+/* ======================================================================== */
+/* A. Reference backend contract, host buffers (backend.py:14-58)            */
+/* ======================================================================== */
+
+/* _kernels_cy.pyx:19-43 fused_scores(queries f32[G,D], norms f32[G], means f32[P,D],
+ * stds f32[P], lam) -> f32[P].  Bit-identical to the reference's compiled backend. */
+PT_API int pt_fused_scores_host(const float *queries, const float *norms, const float *means,
+                         const float *stds, int G, int64_t P, int D, float lam, float *out);
+
+/* _kernels_cy.pyx:46-126 radix_select_desc(keys u16[P], k) -> (ids int64[k] (unordered;
+ * emitted here in ascending index order), threshold, kplus1, passes=3).
+ * Precondition 1 <= k < P as in the reference. */
+PT_API int pt_radix_select_desc_host(const uint16_t *keys, int64_t P, int64_t k, int64_t *ids_out,
+                              int *threshold_out, int *kplus1_out);
+
+/* _kernels_cy.pyx:129-172 stream_attention(q f32[D], keys f32[N,D], values f32[N,D],
+ * scale, block, block_bias f32[ceil(N/block)] or NULL) -> (out f32[D], lse). */
+PT_API int pt_stream_attention_host(const float *q, const float *keys, const float *values, int64_t n,
+                             int D, float scale, int64_t block, const float *block_bias,
+                             float *out, double *lse);
+
+/* ======================================================================== */
+/* B. Batched device API (device pointers, stream-ordered, no host sync)     */
+/* ======================================================================== */
+/*
+ * Device layouts:
+ *   k_pool, v_pool : [num_phys_pages][S][D]           kv_dtype
+ *   page_table     : int32 [U][Pmax]  logical -> physical page id   (kvcache.py:74-120)
+ *   seq_len        : int32 [U]        tokens per unit
+ *   means          : page-interleaved tiles [U][Pmax/32][D/V][32][V], V = 16 B / elem,
+ *                    stats_dtype (f32 = exact reference stats; bf16 = compact mode)
+ *   stds           : f32 [U][Pmax]
+ *   keys           : u16 [U][Pmax]    ordered bf16 score keys (select.py:51-57)
+ *   Pmax % 32 == 0.
+ */
+
+/* K1. kvcache.py:59-71 + :178-183: page statistics of logical pages
+ * [page_begin[u], ceil(seq_len[u]/S)) of every unit (page_begin NULL -> all pages).
+ * float64 accumulation in numpy's order; means rounded to stats_dtype, std to f32. */
+PT_API int pt_page_stats(const void *k_pool, int kv_dtype, const int32_t *page_table,
+                  const int32_t *seq_len, const int32_t *page_begin, int U, int S, int D,
+                  int Pmax, void *means, int stats_dtype, float *stds, void *stream);
+
+/* K1b. kvcache.py:185-208 append, batched: one new K/V row per unit ([U][D] kv_dtype)
+ * lands in the unit's tail page; a full/absent tail page takes a fresh physical page
+ * (free list first, then bump; deterministic in unit order, kvcache.py:154-176); the
+ * touched page's stats are recomputed exactly.  pool_state int32[4] =
+ * {bump_next, free_count, max_pages, error_flag}; error_flag set to PT_ERR_CAPACITY
+ * when the pool is exhausted (that unit is left unchanged).  slot_scratch: int32 [U]
+ * device scratch (the per-unit target page of this append). */
+PT_API int pt_append(const void *k_new, const void *v_new, void *k_pool, void *v_pool, int kv_dtype,
+              int32_t *page_table, int32_t *seq_len, int U, int S, int D, int Pmax, void *means,
+              int stats_dtype, float *stds, int32_t *pool_state, const int32_t *free_list,
+              int32_t *slot_scratch, void *stream);
+
+/* Copy n_rows[u] rows per unit from a dense [U][n_max][D] staging buffer into the pool
+ * starting at token position row_begin[u] (kvcache.py:210-233 extend; pages must
+ * already be mapped by the caller). */
+PT_API int pt_write_rows(const void *k_rows, const void *v_rows, int n_max, const int32_t *row_begin,
+                  const int32_t *n_rows, void *k_pool, void *v_pool, int kv_dtype,
+                  const int32_t *page_table, int U, int S, int D, int Pmax, void *stream);
+
+/* K2. scoring.py:108-124 + _kernels_cy.pyx:19-43 + bf16.py:18-33 + select.py:51-57:
+ * q [U*G][D] (q_dtype); norms f32 [U*G] or NULL (computed as scoring.py:39-47);
+ * score = max_g fl(fl(sum_d q*mean) + fl(fl(lam*norm_g)*std)), sequential d order;
+ * writes keys u16 [U][Pmax] and optionally scores f32 [U][Pmax]. */
+PT_API int pt_score(const void *q, int q_dtype, const float *norms, const void *means, int stats_dtype,
+             const float *stds, const int32_t *seq_len, int U, int G, int D, int S, int Pmax,
+             float lam, uint16_t *keys, float *scores, void *stream);
+
+/* K3. select.py:87-115 + _kernels_cy.pyx:46-126: per unit, k highest keys, ties to the
+ * lowest logical index; P <= k takes every page.  sel: int32 [U][k] physical ids in
+ * ascending logical order (sel_logical, if non-NULL, the logical ids); n_sel[U];
+ * kth[U] = ordered key of the k-th pick; kplus1[U] = key just below the cut or -1. */
+PT_API int pt_topk(const uint16_t *keys, const int32_t *seq_len, const int32_t *page_table, int U,
+            int S, int Pmax, int k, int32_t *sel, int32_t *sel_logical, int32_t *n_sel,
+            int32_t *kth, int32_t *kplus1, void *stream);
+
+/* K4. attention.py:94-107 + :57-75 + _kernels_cy.pyx:129-172: split-KV paged decode.
+ * For unit u, the G query heads attend over the n_sel[u] pages sel[u][0..n_sel) (physical
+ * ids, row stride sel_stride); a page equal to the unit's tail page holds
+ * seq_len - (P-1)*S rows, others S.  bias f32 [U][sel_stride] per page or NULL.
+ * n_sel == NULL selects dense mode (attention.py:78-91): every page of the unit, i.e.
+ * pass sel = page_table, sel_stride = Pmax.
+ * out f32 [U*G][D], lse f32 [U*G].  workspace: pt_attend_workspace_bytes();
+ * tickets int32 [U] zero-initialised once (self-resetting).  nsplit 0 = automatic. */
+PT_API size_t pt_attend_workspace_bytes(int U, int G, int D, int sel_stride);
+PT_API int pt_attend(const void *q, int q_dtype, const void *k_pool, const void *v_pool, int kv_dtype,
+              const int32_t *sel, int sel_stride, const int32_t *n_sel,
+              const int32_t *page_table, const int32_t *seq_len, int U, int G, int D, int S,
+              int Pmax, const float *bias, float scale, float *out, float *lse, void *workspace,
+              size_t workspace_bytes, int32_t *tickets, int nsplit, void *stream);
+
+/* Layout helper: row-major means f32 [U][P][D] -> tiled stats layout (stats_dtype). */
+PT_API int pt_tile_means(const float *means_rowmajor, int U, int P, int D, int Pmax, void *means_tiled,
+                  int stats_dtype, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PAGETOPK_B200_H */

@@ -1,0 +1,178 @@
+// common.cuh -- shared device helpers for the pagetopk B200 kernels (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/pagetopk_b200.h"
+
+namespace pt {
+
+// ---------------------------------------------------------------------------
+// element access: the KV pool and the page means are bf16 or f32
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float bf16_bits_to_f32(uint32_t b) { return __uint_as_float(b << 16); }
+__device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+
+template <int DT>
+__device__ __forceinline__ float load_elem(const void *base, int64_t i) {
+    if constexpr (DT == PT_F32) {
+        return static_cast<const float *>(base)[i];
+    } else {
+        return bf16_bits_to_f32(static_cast<const uint16_t *>(base)[i]);
+    }
+}
+
+// bf16.py:18-33 -- round to nearest even, NaN quieted (identical to __float2bfloat16_rn
+// for non-NaN inputs; written out so the NaN payload rule matches the reference).
+__device__ __forceinline__ uint16_t f32_to_bf16_rne(float x) {
+    uint32_t b = __float_as_uint(x);
+    if (x != x) return (uint16_t)((b >> 16) | 0x0040u);
+    return (uint16_t)((b + 0x7FFFu + ((b >> 16) & 1u)) >> 16);
+}
+
+// select.py:51-57 -- order-preserving key of a bf16 pattern
+__device__ __forceinline__ uint16_t encode_ordered(uint16_t b) {
+    return (b & 0x8000u) ? (uint16_t)~b : (uint16_t)(b | 0x8000u);
+}
+
+template <int DT>
+__device__ __forceinline__ void store_elem(void *base, int64_t i, float v) {
+    if constexpr (DT == PT_F32) {
+        static_cast<float *>(base)[i] = v;
+    } else {
+        static_cast<uint16_t *>(base)[i] = f32_to_bf16_rne(v);
+    }
+}
+
+// Means are kept in a page-interleaved tile layout so that one thread can walk one
+// page's mean vector in the reference's sequential d order while every warp-wide
+// load is a contiguous 512-byte, 128-bit-per-lane access:
+//   means[u][p / 32][d / V][p % 32][d % V],  V = 16 bytes / sizeof(elem)
+// Pmax is a multiple of 32.
+template <int DT>
+struct StatsTile {
+    static constexpr int V = DT == PT_F32 ? 4 : 8;
+};
+
+__host__ __device__ __forceinline__ int64_t mean_offset(int64_t u, int64_t p, int d, int D,
+                                                        int64_t Pmax, int V) {
+    return u * Pmax * D + (p >> 5) * 32 * D + (int64_t)(d / V) * 32 * V + (p & 31) * V + (d % V);
+}
+
+// ---------------------------------------------------------------------------
+// async bulk copy (TMA 1-D) + mbarrier helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
+                     smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// global -> shared bulk copy, completion counted on an mbarrier (SASS: UBLKCP)
+__device__ __forceinline__ void bulk_g2s(void *smem_dst, const void *gmem_src, uint32_t bytes,
+                                         uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(smem_dst)),
+        "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// numpy pairwise_sum over n float64 values x(0..n-1), run by ONE thread
+// (numpy/_core/src/umath/loops_utils.h.src; a 1-D np.sum is 0.0 + pairwise(x, n),
+// identity-initialised -- pinned against numpy in tests/test_oracle_golden.py).
+// X is any accessor `double operator()(int i)`.
+template <class X>
+__device__ __forceinline__ double np_pairwise_leaf(const X &x, int off, int n) {
+    if (n < 8) {
+        double res = 0.0;
+        for (int i = 0; i < n; i++) res = __dadd_rn(res, x(off + i));
+        return res;
+    }
+    double r[8];
+    int i;
+#pragma unroll
+    for (int j = 0; j < 8; j++) r[j] = x(off + j);
+    for (i = 8; i < n - (n % 8); i += 8)
+#pragma unroll
+        for (int j = 0; j < 8; j++) r[j] = __dadd_rn(r[j], x(off + i + j));
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; i++) res = __dadd_rn(res, x(off + i));
+    return res;
+}
+
+template <int DEPTH, class X>
+__device__ __forceinline__ double np_pairwise(const X &x, int off, int n) {
+    if constexpr (DEPTH == 0) {
+        return np_pairwise_leaf(x, off, n);  // caller guarantees n <= 128 * 2^DEPTH
+    } else {
+        if (n <= 128) return np_pairwise_leaf(x, off, n);
+        int n2 = n / 2;
+        n2 -= n2 % 8;
+        return __dadd_rn(np_pairwise<DEPTH - 1>(x, off, n2),
+                         np_pairwise<DEPTH - 1>(x, off + n2, n - n2));
+    }
+}
+
+// np.sum of n <= 2048 float64 values
+template <class X>
+__device__ __forceinline__ double np_sum(const X &x, int n) {
+    return __dadd_rn(0.0, np_pairwise<4>(x, 0, n));
+}
+
+struct DoubleArray {
+    const double *a;
+    __device__ __forceinline__ double operator()(int i) const { return a[i]; }
+};
+// squares of f32 values widened to f64: np.sum(f64(q)**2) (scoring.py:45)
+struct SquaresOfF32 {
+    const float *a;
+    __device__ __forceinline__ double operator()(int i) const {
+        const double v = (double)a[i];
+        return __dmul_rn(v, v);
+    }
+};
+
+}  // namespace pt
+
+#define PT_CUDA_TRY(expr)                                                  \
+    do {                                                                   \
+        cudaError_t _e = (expr);                                           \
+        if (_e != cudaSuccess) return PT_ERR_CUDA_BASE + (int)_e;          \
+    } while (0)

@@ -1,0 +1,327 @@
+// stats.cu -- K1: per-page key statistics (prefill build + decode append).
+//
+// Restates kvcache.py:59-71 compute_page_stats and :178-183 _refresh_stats with the
+// reference's float64 operation order (numpy: sequential row sums for axis-0 means and
+// variances, pairwise summation for var.sum()), so cached stats are bit-identical to
+// the reference cache built from the same rows.  DFMA contraction is prevented with
+// explicit __dadd_rn/__dmul_rn.
+//
+// Layout: one warp per page; lane owns dims d = lane + 32*j (a warp load is one
+// contiguous row slice, coalesced); float64 per-dim accumulators live in registers;
+// the D per-dim variances go through shared memory for numpy's pairwise sum.
+#include "common.cuh"
+
+namespace pt {
+
+constexpr int kStatsWarps = 8;
+constexpr int kMaxD = 512;
+
+template <int DT, int SDT, int DJ>
+__device__ __forceinline__ void page_stats_warp(const void *k_pool, int64_t pid, int rows, int S,
+                                                int D, int64_t u, int64_t p, int64_t Pmax,
+                                                void *means, float *stds, double *var_smem) {
+    const int lane = threadIdx.x & 31;
+    const int64_t base = pid * (int64_t)S * D;
+    double mean[DJ];
+#pragma unroll
+    for (int j = 0; j < DJ; j++) {
+        const int d = lane + 32 * j;
+        double s = 0.0;
+        if (d < D) {
+            for (int r = 0; r < rows; r++)
+                s = __dadd_rn(s, (double)load_elem<DT>(k_pool, base + (int64_t)r * D + d));
+        }
+        mean[j] = __ddiv_rn(s, (double)rows);
+    }
+#pragma unroll
+    for (int j = 0; j < DJ; j++) {
+        const int d = lane + 32 * j;
+        if (d < D) {
+            double s = 0.0;
+            for (int r = 0; r < rows; r++) {
+                double t = __dsub_rn((double)load_elem<DT>(k_pool, base + (int64_t)r * D + d), mean[j]);
+                s = __dadd_rn(s, __dmul_rn(t, t));
+            }
+            var_smem[d] = __ddiv_rn(s, (double)rows);
+            constexpr int V = StatsTile<SDT>::V;
+            store_elem<SDT>(means, mean_offset(u, p, d, D, Pmax, V), __double2float_rn(mean[j]));
+        }
+    }
+    __syncwarp();
+    if (lane == 0) stds[u * Pmax + p] = __double2float_rn(__dsqrt_rn(np_sum(DoubleArray{var_smem}, D)));
+    __syncwarp();
+}
+
+// grid: (ceil(Pmax / kStatsWarps), U); warp w of block x handles logical page x*8+w.
+template <int DT, int SDT, int DJ>
+__global__ void __launch_bounds__(kStatsWarps * 32)
+    k_page_stats(const void *__restrict__ k_pool, const int32_t *__restrict__ page_table,
+                 const int32_t *__restrict__ seq_len, const int32_t *__restrict__ page_begin,
+                 int S, int D, int Pmax, void *__restrict__ means, float *__restrict__ stds) {
+    __shared__ double var_smem[kStatsWarps][kMaxD];
+    const int warp = threadIdx.x >> 5;
+    const int64_t u = blockIdx.y;
+    const int64_t p = (int64_t)blockIdx.x * kStatsWarps + warp;
+    const int n = seq_len[u];
+    const int P = (n + S - 1) / S;
+    const int p0 = page_begin ? page_begin[u] : 0;
+    if (p >= P || p < p0) return;
+    const int rows = (p == P - 1) ? n - (int)p * S : S;
+    const int64_t pid = page_table[u * Pmax + p];
+    page_stats_warp<DT, SDT, DJ>(k_pool, pid, rows, S, D, u, p, Pmax, means, stds, var_smem[warp]);
+}
+
+// ---------------------------------------------------------------------------
+// decode append (kvcache.py:185-208), batched over units
+// ---------------------------------------------------------------------------
+// Phase 1 (one CTA): deterministic physical-page allocation in unit order, the
+// batched form of _alloc_page (kvcache.py:154-176): free list popped from its end
+// first (list.pop()), then the bump pointer; exhaustion -> error flag, unit skipped.
+constexpr int kAllocThreads = 1024;
+
+__global__ void __launch_bounds__(kAllocThreads)
+    k_append_alloc(int32_t *__restrict__ page_table, const int32_t *__restrict__ seq_len, int U,
+                   int S, int Pmax, int32_t *__restrict__ pool_state,
+                   const int32_t *__restrict__ free_list, int32_t *__restrict__ slot) {
+    __shared__ int warp_tot[kAllocThreads / 32];
+    __shared__ int carry;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int bump0 = pool_state[0], free0 = pool_state[1], max_pages = pool_state[2];
+    if (tid == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < U; base += kAllocThreads) {
+        const int u = base + tid;
+        int n = 0, need = 0;
+        if (u < U) {
+            n = seq_len[u];
+            need = (n % S == 0) ? 1 : 0;
+        }
+        // block exclusive scan of need
+        unsigned m = __ballot_sync(0xffffffffu, need);
+        int wpre = __popc(m & ((1u << lane) - 1u));
+        if (lane == 0) warp_tot[warp] = __popc(m);
+        __syncthreads();
+        int before = carry;
+        for (int w = 0; w < warp; w++) before += warp_tot[w];
+        int chunk_total = 0;
+        for (int w = 0; w < kAllocThreads / 32; w++) chunk_total += warp_tot[w];
+        const int rank = before + wpre;
+        if (u < U) {
+            int target;
+            if (need) {
+                int pid;
+                if (rank < free0) pid = free_list[free0 - 1 - rank];
+                else pid = bump0 + (rank - free0);
+                const int lp = n / S;
+                if (pid >= max_pages || lp >= Pmax) {
+                    target = -1;
+                    pool_state[3] = PT_ERR_CAPACITY;
+                } else {
+                    page_table[(int64_t)u * Pmax + lp] = pid;
+                    target = pid;
+                }
+            } else {
+                target = page_table[(int64_t)u * Pmax + n / S];
+            }
+            slot[u] = target;
+        }
+        __syncthreads();
+        if (tid == 0) carry += chunk_total;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        const int tot = carry;
+        const int from_free = tot < free0 ? tot : free0;
+        int bump = bump0 + (tot - from_free);
+        pool_state[1] = free0 - from_free;
+        pool_state[0] = bump < max_pages ? bump : max_pages;
+    }
+}
+
+// Phase 2: one warp per unit writes the K/V row and recomputes the touched page.
+template <int DT, int SDT, int DJ>
+__global__ void __launch_bounds__(kStatsWarps * 32)
+    k_append_rows(const void *__restrict__ k_new, const void *__restrict__ v_new,
+                  void *__restrict__ k_pool, void *__restrict__ v_pool,
+                  int32_t *__restrict__ seq_len, const int32_t *__restrict__ slot, int U, int S,
+                  int D, int Pmax, void *__restrict__ means, float *__restrict__ stds) {
+    __shared__ double var_smem[kStatsWarps][kMaxD];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t u = (int64_t)blockIdx.x * kStatsWarps + warp;
+    if (u >= U) return;
+    const int pid = slot[u];
+    if (pid < 0) return;
+    const int n = seq_len[u];
+    const int row = n % S;
+    const int64_t dst = ((int64_t)pid * S + row) * D;
+    for (int d = lane; d < D; d += 32) {
+        if constexpr (DT == PT_F32) {
+            static_cast<float *>(k_pool)[dst + d] = static_cast<const float *>(k_new)[u * D + d];
+            static_cast<float *>(v_pool)[dst + d] = static_cast<const float *>(v_new)[u * D + d];
+        } else {
+            static_cast<uint16_t *>(k_pool)[dst + d] = static_cast<const uint16_t *>(k_new)[u * D + d];
+            static_cast<uint16_t *>(v_pool)[dst + d] = static_cast<const uint16_t *>(v_new)[u * D + d];
+        }
+    }
+    __syncwarp();
+    __threadfence_block();
+    page_stats_warp<DT, SDT, DJ>(k_pool, pid, row + 1, S, D, u, n / S, Pmax, means, stds,
+                                 var_smem[warp]);
+    if (lane == 0) seq_len[u] = n + 1;
+}
+
+// extend (kvcache.py:210-233): scatter dense staged rows into mapped pages
+template <typename E>
+__global__ void k_write_rows(const E *__restrict__ k_rows, const E *__restrict__ v_rows,
+                             int n_max, const int32_t *__restrict__ row_begin,
+                             const int32_t *__restrict__ n_rows, E *__restrict__ k_pool,
+                             E *__restrict__ v_pool, const int32_t *__restrict__ page_table,
+                             int S, int D, int Pmax) {
+    const int64_t u = blockIdx.y;
+    const int nr = n_rows[u];
+    const int r0 = row_begin[u];
+    const int64_t total = (int64_t)nr * D;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(i / D), d = (int)(i % D);
+        const int pos = r0 + r;
+        const int64_t pid = page_table[u * Pmax + pos / S];
+        const int64_t dst = (pid * S + pos % S) * D + d;
+        const int64_t src = (u * n_max + r) * D + d;
+        k_pool[dst] = k_rows[src];
+        v_pool[dst] = v_rows[src];
+    }
+}
+
+}  // namespace pt
+
+using namespace pt;
+
+template <int DT, int SDT>
+static int launch_stats(const void *k_pool, const int32_t *pt_, const int32_t *sl,
+                        const int32_t *pb, int U, int S, int D, int Pmax, void *means,
+                        float *stds, cudaStream_t st) {
+    dim3 grid((Pmax + kStatsWarps - 1) / kStatsWarps, U);
+    const int dj = (D + 31) / 32;
+#define PT_STATS_CASE(DJ_)                                                                    \
+    case DJ_:                                                                                 \
+        k_page_stats<DT, SDT, DJ_><<<grid, kStatsWarps * 32, 0, st>>>(k_pool, pt_, sl, pb, S, D, \
+                                                                       Pmax, means, stds);    \
+        break;
+    switch (dj) {
+        PT_STATS_CASE(1)
+        PT_STATS_CASE(2)
+        PT_STATS_CASE(3)
+        PT_STATS_CASE(4)
+        PT_STATS_CASE(8)
+        PT_STATS_CASE(16)
+        default: return PT_ERR_UNSUPPORTED;
+    }
+#undef PT_STATS_CASE
+    PT_CUDA_TRY(cudaGetLastError());
+    return PT_OK;
+}
+
+static int stats_dj_ok(int D) {
+    const int dj = (D + 31) / 32;
+    return D >= 1 && D <= kMaxD && (dj <= 4 || dj == 8 || dj == 16);
+}
+
+extern "C" int pt_page_stats(const void *k_pool, int kv_dtype, const int32_t *page_table,
+                             const int32_t *seq_len, const int32_t *page_begin, int U, int S,
+                             int D, int Pmax, void *means, int stats_dtype, float *stds,
+                             void *stream) {
+    if (!k_pool || !page_table || !seq_len || !means || !stds || U < 0 || S < 1 || Pmax % 32)
+        return PT_ERR_INVALID;
+    if (!stats_dj_ok(D)) return PT_ERR_UNSUPPORTED;
+    if (U == 0) return PT_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (kv_dtype == PT_F32 && stats_dtype == PT_F32)
+        return launch_stats<PT_F32, PT_F32>(k_pool, page_table, seq_len, page_begin, U, S, D, Pmax, means, stds, st);
+    if (kv_dtype == PT_BF16 && stats_dtype == PT_F32)
+        return launch_stats<PT_BF16, PT_F32>(k_pool, page_table, seq_len, page_begin, U, S, D, Pmax, means, stds, st);
+    if (kv_dtype == PT_BF16 && stats_dtype == PT_BF16)
+        return launch_stats<PT_BF16, PT_BF16>(k_pool, page_table, seq_len, page_begin, U, S, D, Pmax, means, stds, st);
+    if (kv_dtype == PT_F32 && stats_dtype == PT_BF16)
+        return launch_stats<PT_F32, PT_BF16>(k_pool, page_table, seq_len, page_begin, U, S, D, Pmax, means, stds, st);
+    return PT_ERR_INVALID;
+}
+
+template <int DT, int SDT>
+static int launch_append_rows(const void *kn, const void *vn, void *kp, void *vp, int32_t *sl,
+                              const int32_t *slot, int U, int S, int D, int Pmax, void *means,
+                              float *stds, cudaStream_t st) {
+    const int blocks = (U + kStatsWarps - 1) / kStatsWarps;
+    const int dj = (D + 31) / 32;
+#define PT_APP_CASE(DJ_)                                                                  \
+    case DJ_:                                                                             \
+        k_append_rows<DT, SDT, DJ_><<<blocks, kStatsWarps * 32, 0, st>>>(kn, vn, kp, vp, sl, \
+                                                                         slot, U, S, D, Pmax, \
+                                                                         means, stds);     \
+        break;
+    switch (dj) {
+        PT_APP_CASE(1)
+        PT_APP_CASE(2)
+        PT_APP_CASE(3)
+        PT_APP_CASE(4)
+        PT_APP_CASE(8)
+        PT_APP_CASE(16)
+        default: return PT_ERR_UNSUPPORTED;
+    }
+#undef PT_APP_CASE
+    PT_CUDA_TRY(cudaGetLastError());
+    return PT_OK;
+}
+
+extern "C" int pt_append(const void *k_new, const void *v_new, void *k_pool, void *v_pool,
+                         int kv_dtype, int32_t *page_table, int32_t *seq_len, int U, int S, int D,
+                         int Pmax, void *means, int stats_dtype, float *stds,
+                         int32_t *pool_state, const int32_t *free_list, int32_t *slot_scratch,
+                         void *stream) {
+    if (!k_new || !v_new || !k_pool || !v_pool || !page_table || !seq_len || !means || !stds ||
+        !pool_state || !slot_scratch || U < 0 || S < 1 || Pmax % 32)
+        return PT_ERR_INVALID;
+    if (!stats_dj_ok(D)) return PT_ERR_UNSUPPORTED;
+    if (U == 0) return PT_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    int32_t *slot = slot_scratch;
+    k_append_alloc<<<1, kAllocThreads, 0, st>>>(page_table, seq_len, U, S, Pmax, pool_state,
+                                               free_list, slot);
+    PT_CUDA_TRY(cudaGetLastError());
+    if (kv_dtype == PT_F32 && stats_dtype == PT_F32)
+        return launch_append_rows<PT_F32, PT_F32>(k_new, v_new, k_pool, v_pool, seq_len, slot, U, S, D, Pmax, means, stds, st);
+    if (kv_dtype == PT_BF16 && stats_dtype == PT_F32)
+        return launch_append_rows<PT_BF16, PT_F32>(k_new, v_new, k_pool, v_pool, seq_len, slot, U, S, D, Pmax, means, stds, st);
+    if (kv_dtype == PT_BF16 && stats_dtype == PT_BF16)
+        return launch_append_rows<PT_BF16, PT_BF16>(k_new, v_new, k_pool, v_pool, seq_len, slot, U, S, D, Pmax, means, stds, st);
+    if (kv_dtype == PT_F32 && stats_dtype == PT_BF16)
+        return launch_append_rows<PT_F32, PT_BF16>(k_new, v_new, k_pool, v_pool, seq_len, slot, U, S, D, Pmax, means, stds, st);
+    return PT_ERR_INVALID;
+}
+
+extern "C" int pt_write_rows(const void *k_rows, const void *v_rows, int n_max,
+                             const int32_t *row_begin, const int32_t *n_rows, void *k_pool,
+                             void *v_pool, int kv_dtype, const int32_t *page_table, int U, int S,
+                             int D, int Pmax, void *stream) {
+    if (!k_rows || !v_rows || !row_begin || !n_rows || !k_pool || !v_pool || !page_table ||
+        U < 0 || n_max < 0)
+        return PT_ERR_INVALID;
+    if (U == 0 || n_max == 0) return PT_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    int64_t per_unit = (int64_t)n_max * D;
+    int gx = (int)((per_unit + 255) / 256);
+    if (gx > 1024) gx = 1024;
+    dim3 grid(gx, U);
+    if (kv_dtype == PT_F32)
+        k_write_rows<float><<<grid, 256, 0, st>>>((const float *)k_rows, (const float *)v_rows, n_max,
+                                                  row_begin, n_rows, (float *)k_pool, (float *)v_pool,
+                                                  page_table, S, D, Pmax);
+    else if (kv_dtype == PT_BF16)
+        k_write_rows<uint16_t><<<grid, 256, 0, st>>>((const uint16_t *)k_rows, (const uint16_t *)v_rows,
+                                                     n_max, row_begin, n_rows, (uint16_t *)k_pool,
+                                                     (uint16_t *)v_pool, page_table, S, D, Pmax);
+    else
+        return PT_ERR_INVALID;
+    PT_CUDA_TRY(cudaGetLastError());
+    return PT_OK;
+}

@@ -1,0 +1,155 @@
+"""Batched decode engine: the B200 hot path of attention.py:110-147 over all units.
+
+One decode step for every (sequence, kv-head) unit of a :class:`PagedKvCache`:
+
+    [append K/V row  (K1b: pt_append)]      kvcache.py:185-208
+    score            (K2: pt_score)          scoring.py:108-124 -> bf16 -> ordered keys
+    select           (K3: pt_topk)           select.py:87-115 + page-table translation
+    attend           (K4: pt_attend)         attention.py:94-107 for the G heads of a group
+
+All launches go on the current CUDA stream with device-resident buffers and no
+host synchronisation, so a step can be captured once and replayed as a CUDA graph
+(:meth:`DecodeEngine.capture`).  ``dense`` runs K4 over every page (attention.py:78-91),
+the speed-up denominator.
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import _device as dev
+from . import _lib
+from .kvcache import PagedKvCache
+
+__all__ = ["DecodeEngine"]
+
+
+class DecodeEngine:
+    def __init__(
+        self,
+        cache: PagedKvCache,
+        group_size: int,
+        k: int,
+        lam: float = 0.5,
+        scale: float | None = None,
+        keep_scores: bool = False,
+        keep_logical: bool = False,
+    ) -> None:
+        if k < 1:
+            raise ValueError("k must be at least 1")
+        if group_size < 1:
+            raise ValueError("group_size must be positive")
+        self.cache = cache
+        self.G = group_size
+        self.k = int(k)
+        self.lam = float(lam)
+        D = cache.layout.head_dim
+        self.scale = 1.0 / math.sqrt(D) if scale is None else float(scale)
+        U, Pmax, d = cache.num_units, cache.Pmax, cache.device
+        self.U, self.D = U, D
+        self.keys = torch.zeros(U, Pmax, dtype=torch.int16, device=d)  # u16 bit patterns
+        self.scores = torch.zeros(U, Pmax, dtype=torch.float32, device=d) if keep_scores else None
+        self.sel = torch.zeros(U, self.k, dtype=torch.int32, device=d)
+        self.sel_logical = (torch.zeros(U, self.k, dtype=torch.int32, device=d)
+                            if keep_logical else None)
+        self.n_sel = torch.zeros(U, dtype=torch.int32, device=d)
+        self.kth = torch.zeros(U, dtype=torch.int32, device=d)
+        self.kplus1 = torch.zeros(U, dtype=torch.int32, device=d)
+        self.out = torch.zeros(U * self.G, D, dtype=torch.float32, device=d)
+        self.lse = torch.zeros(U * self.G, dtype=torch.float32, device=d)
+        self.dense_out = torch.zeros_like(self.out)
+        self.dense_lse = torch.zeros_like(self.lse)
+        wsb = _lib.load().pt_attend_workspace_bytes(U, self.G, D, max(self.k, Pmax))
+        self.ws = torch.zeros(wsb, dtype=torch.uint8, device=d)
+        self.tickets = torch.zeros(U, dtype=torch.int32, device=d)
+        self.dense_tickets = torch.zeros(U, dtype=torch.int32, device=d)
+        self.graph: torch.cuda.CUDAGraph | None = None
+
+    # ------------------------------------------------------------------
+    def _q(self, q: torch.Tensor) -> tuple[torch.Tensor, int]:
+        """Queries as [U*G, D] (i.e. [batch, Hq, D] with contiguous GQA grouping)."""
+        q2 = q.reshape(-1, self.D)
+        if q2.shape[0] != self.U * self.G:
+            raise ValueError(f"{q2.shape[0]} query heads do not form {self.U} groups of {self.G}")
+        if not q2.is_cuda or not q2.is_contiguous():
+            raise ValueError("queries must be a contiguous device tensor")
+        return q2, dev.dtype_code(q2.dtype)
+
+    def score(self, q: torch.Tensor, norms: torch.Tensor | None = None, stream=None) -> None:
+        q2, qc = self._q(q)
+        c = self.cache
+        _lib.call("pt_score", q2.data_ptr(), qc, dev.ptr(norms), c.means.data_ptr(), c.stats_code,
+                  c.stds.data_ptr(), c.seq_lens.data_ptr(), self.U, self.G, self.D,
+                  c.layout.page_size, c.Pmax, self.lam, self.keys.data_ptr(),
+                  dev.ptr(self.scores), dev.stream_handle(stream))
+
+    def select(self, stream=None) -> None:
+        c = self.cache
+        _lib.call("pt_topk", self.keys.data_ptr(), c.seq_lens.data_ptr(), c.page_table.data_ptr(),
+                  self.U, c.layout.page_size, c.Pmax, self.k, self.sel.data_ptr(),
+                  dev.ptr(self.sel_logical), self.n_sel.data_ptr(), self.kth.data_ptr(),
+                  self.kplus1.data_ptr(), dev.stream_handle(stream))
+
+    def attend(self, q: torch.Tensor, stream=None, nsplit: int = 0) -> None:
+        q2, qc = self._q(q)
+        c = self.cache
+        _lib.call("pt_attend", q2.data_ptr(), qc, c.k_pool.data_ptr(), c.v_pool.data_ptr(),
+                  c.kv_code, self.sel.data_ptr(), self.k, self.n_sel.data_ptr(),
+                  c.page_table.data_ptr(), c.seq_lens.data_ptr(), self.U, self.G, self.D,
+                  c.layout.page_size, c.Pmax, None, self.scale, self.out.data_ptr(),
+                  self.lse.data_ptr(), self.ws.data_ptr(), self.ws.numel(),
+                  self.tickets.data_ptr(), nsplit, dev.stream_handle(stream))
+
+    def dense(self, q: torch.Tensor, stream=None, nsplit: int = 0):
+        """Dense paged decode over every page of every unit (the speed-up denominator)."""
+        q2, qc = self._q(q)
+        c = self.cache
+        _lib.call("pt_attend", q2.data_ptr(), qc, c.k_pool.data_ptr(), c.v_pool.data_ptr(),
+                  c.kv_code, c.page_table.data_ptr(), c.Pmax, None, c.page_table.data_ptr(),
+                  c.seq_lens.data_ptr(), self.U, self.G, self.D, c.layout.page_size, c.Pmax,
+                  None, self.scale, self.dense_out.data_ptr(), self.dense_lse.data_ptr(),
+                  self.ws.data_ptr(), self.ws.numel(), self.dense_tickets.data_ptr(), nsplit,
+                  dev.stream_handle(stream))
+        return self.dense_out, self.dense_lse
+
+    def step(self, q: torch.Tensor, k_new: torch.Tensor | None = None,
+             v_new: torch.Tensor | None = None, stream=None):
+        """One decode step: [append] -> score -> select -> attend.  Returns (out, lse)."""
+        if k_new is not None:
+            self.cache.append_batch(k_new, v_new, stream=stream)
+        self.score(q, stream=stream)
+        self.select(stream=stream)
+        self.attend(q, stream=stream)
+        return self.out, self.lse
+
+    # ------------------------------------------------------------------
+    def capture(self, q: torch.Tensor, k_new: torch.Tensor | None = None,
+                v_new: torch.Tensor | None = None) -> torch.cuda.CUDAGraph:
+        """Capture one step (static input buffers q/k_new/v_new) as a CUDA graph.
+
+        With appends, each replay advances every unit by one token (the host mirror of
+        the sequence lengths is advanced by :meth:`replay`).
+        """
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                if k_new is not None:
+                    self.cache.append_batch(k_new, v_new)
+                    self.cache._seq_host -= 1  # replay() accounts for the captured append
+                self.score(q)
+                self.select()
+                self.attend(q)
+        torch.cuda.current_stream().wait_stream(s)
+        self.graph = g
+        self._graph_appends = k_new is not None
+        return g
+
+    def replay(self) -> None:
+        assert self.graph is not None, "capture() first"
+        self.graph.replay()
+        if self._graph_appends:
+            self.cache._seq_host += 1
