@@ -1,0 +1,501 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 UNIQUE sparse decode step (BASELINE.json metric).
+
+Workload (N=1): BASELINE.json configs[2] -- Llama-3.1-8B attention shape, batch 32,
+128K context, 32 q / 8 kv heads, d=128, page 16, k = 2048 tokens (128 pages), bf16
+KV pool, f32 page stats (exact reference statistics).  One step = one decode token
+per sequence through the full hot path: append the new K/V row (K1b, stats of the
+tail page recomputed) -> score every page (K2) -> top-k pages (K3) -> split-KV sparse
+attention over the selected pages (K4), replayed as a CUDA graph.  Multi-GPU: one
+process per GPU, each rank owns its own batch of 32 sequences (units shard with no
+data-path collective; "scaling": "weak"); NCCL only for the barrier / max-time reduce
+and the optional output all-gather reported beside the line.
+
+Prints ONE JSON line on rank 0.  `--impl reference` times the reference CPU path
+(the oracle port of attention.py:110-147, bit-identical to the reference's compiled
+backend) on the host cores instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "sparse decode attn tokens/s @128K ctx (batch 32, k=2048 tokens, 32q/8kv d128 page16)"
+UNIT = "tokens/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--batch", type=int, default=32, help="sequences per GPU")
+    ap.add_argument("--ctx", type=int, default=131072)
+    ap.add_argument("--q-heads", type=int, default=32)
+    ap.add_argument("--kv-heads", type=int, default=8)
+    ap.add_argument("--head-dim", type=int, default=128)
+    ap.add_argument("--page", type=int, default=16)
+    ap.add_argument("--budget", type=int, default=2048, help="token budget k*S")
+    ap.add_argument("--stats-dtype", default="f32", choices=["f32", "bf16"])
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--profile", action="store_true",
+                    help="few eager steps, no graph/cpu/dense (for ncu launch lists)")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (NVML) during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {
+        0x0000000000000002: "applications_clocks_setting",
+        0x0000000000000004: "sw_power_cap",
+        0x0000000000000008: "hw_slowdown",
+        0x0000000000000020: "sw_thermal_slowdown",
+        0x0000000000000040: "hw_thermal_slowdown",
+        0x0000000000000080: "hw_power_brake_slowdown",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons = [], set()
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:  # pragma: no cover - no NVML
+            self.max_mhz = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        return {
+            "sm_mhz": statistics.median(self.samples) if self.samples else None,
+            "sm_max_mhz": self.max_mhz,
+            "reasons": sorted(self.reasons),
+            "samples": len(self.samples),
+        }
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# algorithmic bytes
+# ---------------------------------------------------------------------------
+def step_bytes(U, G, D, P, kp, S, e_kv, e_stats, N_tok):
+    score = U * (P * D * e_stats + 4 * P + G * D * e_kv + 2 * P)
+    topk = U * (2 * P + 8 * kp)  # keys read + page-table entries read + ids written
+    T = kp * S
+    attn = U * (2 * T * D * e_kv + G * D * e_kv + 4 * kp) + U * G * D * 4
+    append = U * (S * D * e_kv + 3 * D * e_kv + D * e_stats + 8)
+    dense = 2 * U * N_tok * D * e_kv + U * G * D * 4
+    return dict(score=score, topk=topk, attend=attn, append=append, dense=dense)
+
+
+def build_cache(args, device, seed):
+    import torch
+
+    import paper_2605_27740_b200 as pt
+
+    H, D, S = args.kv_heads, args.head_dim, args.page
+    B = args.batch
+    U = B * H
+    spare = (args.warmup + args.steps) * 4 + 64  # appends during warm-up/timed/extra loops
+    P_cap = -(-(args.ctx + spare) // S)
+    layout = pt.CacheLayout(num_kv_heads=H, head_dim=D, page_size=S, max_pages=U * P_cap)
+    sdt = torch.float32 if args.stats_dtype == "f32" else torch.bfloat16
+    cache = pt.PagedKvCache(layout, batch=B, dtype=torch.bfloat16, stats_dtype=sdt,
+                            max_pages_per_head=P_cap, device=device)
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    chunk = 8192
+    done = 0
+    while done < args.ctx:
+        n = min(chunk, args.ctx - done)
+        kk = torch.randn(U, n, D, generator=g, device=device, dtype=torch.float32).to(torch.bfloat16)
+        vv = torch.randn(U, n, D, generator=g, device=device, dtype=torch.float32).to(torch.bfloat16)
+        cache.extend_units(kk, vv)
+        done += n
+        del kk, vv
+    torch.cuda.synchronize()
+    return cache
+
+
+def cpu_baseline(cache, q_bf16, args, budget_s, nthreads):
+    """Reference decode_step (oracle port, bit-identical to the compiled backend) on host
+    cores over a bounded sample of whole sequences of the same workload."""
+    from oracle import oracle as O
+
+    H, D, S = args.kv_heads, args.head_dim, args.page
+    G = args.q_heads // args.kv_heads
+    kp = -(-args.budget // S)
+    import torch
+
+    seqs = 2
+    units = list(range(seqs * H))
+    tab = cache.page_table[: len(units)].cpu().numpy()
+    seq = cache.seq_lens[: len(units)].cpu().numpy()
+    P = int(-(-seq.max() // S))
+    pids = np.unique(tab[:, :P][tab[:, :P] >= 0])
+    remap = -np.ones(cache.layout.max_pages, dtype=np.int64)
+    remap[pids] = np.arange(pids.size)
+    idx = torch.from_numpy(pids).to(cache.device)
+    kpool = cache.k_pool[idx].to(torch.float32).cpu().numpy()
+    vpool = cache.v_pool[idx].to(torch.float32).cpu().numpy()
+    tab2 = np.where(tab >= 0, remap[np.maximum(tab, 0)], -1).astype(np.int32)
+    import paper_2605_27740_b200._device as dev
+
+    means = dev.untile_means(cache.means, cache.num_units, cache.Pmax, D, cache.stats_dtype)
+    means = means[: len(units)].to(torch.float32).cpu().numpy()
+    stds = cache.stds[: len(units)].cpu().numpy()
+    q = q_bf16.reshape(cache.num_units, G, D)[: len(units)].to(torch.float32).cpu().numpy()
+    reps, t0 = 0, time.perf_counter()
+    res = None
+    while True:
+        res = O.decode_units(q, kpool, vpool, tab2, seq, means, stds, kp, 0.5,
+                             1.0 / math.sqrt(D), S, nthreads=nthreads)
+        reps += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = (time.perf_counter() - t0) / reps
+    return {
+        "value": seqs / dt,
+        "unit": UNIT,
+        "cores": nthreads,
+        "kind": "port",
+        "sample": f"{seqs} sequences x {H} kv-heads (128K ctx, k={kp} pages, bf16 values upcast "
+                  f"to f32) per rep, {reps} reps in {time.perf_counter() - t0:.1f}s; "
+                  "oracle/pagetopk_oracle.c (bit-identical to _kernels_cy), OpenMP over units",
+        "_res": res,
+        "_units": len(units),
+        "_pids": pids,
+    }
+
+
+def main():
+    args = parse()
+    import torch
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    device = torch.device("cuda", local if torch.cuda.is_available() else 0)
+    G = args.q_heads // args.kv_heads
+    H, D, S = args.kv_heads, args.head_dim, args.page
+    kp = -(-args.budget // S)
+    U = args.batch * H
+    config = {
+        "workload": "BASELINE configs[2]: Llama-3.1-8B attn shape, 32q/8kv d128, batch "
+                    f"{args.batch}/GPU, ctx {args.ctx}, page {S}, k={args.budget} tokens "
+                    f"({kp} pages), bf16 KV, {args.stats_dtype} page stats",
+        "global_batch": args.batch * world,
+        "seq_len": args.ctx,
+        "parallelism": f"units (batch x kv-head) sharded over {world} GPU(s), no data-path collective",
+        "l2": "inputs larger than L2 (~1.3 GB touched per step vs 126 MB L2); 4 rotating query sets",
+    }
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        from oracle import oracle as O
+
+        ncores = O.max_threads()
+        # the oracle sample needs the same cache contents: build a 2-sequence cache on the GPU
+        # when one is present, else generate on the host (identical distribution).
+        if torch.cuda.is_available():
+            a2 = argparse.Namespace(**vars(args))
+            a2.batch = 2
+            cache = build_cache(a2, device, seed=1234 + rank)
+            qg = torch.Generator(device=device)
+            qg.manual_seed(7)
+            q = torch.randn(cache.num_units * G, D, generator=qg, device=device).to(torch.bfloat16)
+            budget = args.cpu_seconds
+            vals = []
+            for _ in range(args.warmup and 1):
+                cpu_baseline(cache, q, a2, 0.5, ncores)
+            for _ in range(max(1, min(args.steps, 3))):
+                vals.append(cpu_baseline(cache, q, a2, budget / 3, ncores))
+            v = statistics.median([x["value"] for x in vals])
+            cb = {k: vals[0][k] for k in ("unit", "cores", "kind", "sample")}
+            cb["value"] = v
+        else:
+            print(json.dumps({"impl": "reference", "unavailable": "no CUDA device to build the "
+                              "shared workload"}))
+            return
+        line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+                "steps": len(vals), "warmup": 1, "ms_per_step": 1000.0 * 32 / v,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic N(0,1) (reference workload distribution)", "config": config,
+                "cpu_baseline": cb,
+                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    import paper_2605_27740_b200 as pt
+
+    cache = build_cache(args, device, seed=1234 + rank)
+    eng = pt.DecodeEngine(cache, G, kp)
+    qg = torch.Generator(device=device)
+    qg.manual_seed(7 + rank)
+    NQ = 4
+    qs = [torch.randn(U * G, D, generator=qg, device=device).to(torch.bfloat16) for _ in range(NQ)]
+    kn = torch.randn(U, D, generator=qg, device=device).to(torch.bfloat16)
+    vn = torch.randn(U, D, generator=qg, device=device).to(torch.bfloat16)
+    stream = torch.cuda.current_stream()
+
+    if args.profile:
+        for i in range(max(args.steps, 1)):
+            eng.step(qs[i % NQ], kn, vn)
+        torch.cuda.synchronize()
+        if rank == 0:
+            print(json.dumps({"profile": "done", "steps": args.steps}))
+        return
+
+    # warm-up (eager, configures kernel attributes), then capture NQ graphs
+    for i in range(max(args.warmup, 3)):
+        eng.step(qs[i % NQ], kn, vn)
+    torch.cuda.synchronize()
+    cache.check_errors()
+    graphs = []
+    for i in range(NQ):
+        gph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gph):
+            cache.append_batch(kn, vn)
+            eng.score(qs[i])
+            eng.select()
+            eng.attend(qs[i])
+        cache._seq_host -= 1
+        graphs.append(gph)
+    for i in range(args.warmup):
+        graphs[i % NQ].replay()
+        cache._seq_host += 1
+    torch.cuda.synchronize()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- timed region: K graph replays -------------------------------------------
+    sampler = ClockSampler(local)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    with sampler:
+        e0.record(stream)
+        for i in range(args.steps):
+            graphs[i % NQ].replay()
+        e1.record(stream)
+        barrier()
+    cache._seq_host += args.steps
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], device=device)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_per_step = ms_max / args.steps
+    value = world * args.batch / (ms_per_step / 1000.0)
+    cache.check_errors()
+
+    # ---- per-kernel breakdown (CUDA events on the launching stream) -----------------
+    reps = max(20, min(args.steps, 100))
+    names = ["append", "score", "select", "attend"]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(reps)]
+    for r in range(reps):
+        q = qs[r % NQ]
+        ev = evs[r]
+        ev[0].record(stream)
+        cache.append_batch(kn, vn)
+        ev[1].record(stream)
+        eng.score(q)
+        ev[2].record(stream)
+        eng.select()
+        ev[3].record(stream)
+        eng.attend(q)
+        ev[4].record(stream)
+    torch.cuda.synchronize()
+    cache.check_errors()
+    brk = {n: statistics.median([evs[r][i].elapsed_time(evs[r][i + 1]) * 1000 for r in range(reps)])
+           for i, n in enumerate(names)}
+
+    # ---- dense denominator: same GPU, every page of every unit ------------------------
+    dense_us = None
+    if not args.no_dense:
+        for i in range(3):
+            eng.dense(qs[i % NQ])
+        dreps = 20
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d0.record(stream)
+        for i in range(dreps):
+            eng.dense(qs[i % NQ])
+        d1.record(stream)
+        torch.cuda.synchronize()
+        dense_us = d0.elapsed_time(d1) * 1000 / dreps
+
+    # ---- e2e: public API with pinned host buffers, H2D inputs + D2H result per step ----
+    q_host = [x.cpu().pin_memory() for x in qs]
+    kn_h, vn_h = kn.cpu().pin_memory(), vn.cpu().pin_memory()
+    out_h = torch.empty(U * G, D, dtype=torch.float32).pin_memory()
+    q_dev = torch.empty_like(qs[0])
+    kn_d, vn_d = torch.empty_like(kn), torch.empty_like(vn)
+    e2e_steps = max(20, min(args.steps, 100))
+    for i in range(3 + e2e_steps):
+        if i == 3:
+            barrier()
+            t0 = time.perf_counter()
+        q_dev.copy_(q_host[i % NQ], non_blocking=True)
+        kn_d.copy_(kn_h, non_blocking=True)
+        vn_d.copy_(vn_h, non_blocking=True)
+        out, _ = eng.step(q_dev, kn_d, vn_d)
+        out_h.copy_(out, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    te = torch.tensor([e2e_s], device=device)
+    if dist is not None:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = world * args.batch / float(te.item())
+    cache.check_errors()
+    h2d = q_host[0].numel() * 2 + kn_h.numel() * 2 * 2
+    d2h = out_h.numel() * 4
+
+    # ---- optional output all-gather (NCCL over NVLink), reported beside the line ------
+    allgather_us = None
+    if dist is not None:
+        outs = [torch.empty_like(eng.out) for _ in range(world)]
+        for _ in range(3):
+            dist.all_gather(outs, eng.out)
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(20):
+            dist.all_gather(outs, eng.out)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        allgather_us = a0.elapsed_time(a1) * 1000 / 20
+
+    # ---- roofline of the dominant kernel + whole step ----------------------------------
+    peaks, peak_kind = measured_peaks()
+    e_st = 4 if args.stats_dtype == "f32" else 2
+    P = -(-args.ctx // S)
+    by = step_bytes(U, G, D, P, kp, S, 2, e_st, args.ctx)
+    dom = max(("score", "attend"), key=lambda n: brk[n])
+    dom_bytes = by[dom]
+    achieved = dom_bytes / (brk[dom] * 1e-6) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(dom)
+        except Exception:
+            traffic = None
+    step_total = by["append"] + by["score"] + by["topk"] + by["attend"]
+
+    cb = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        from oracle import oracle as O
+
+        nth = O.max_threads()
+        r = cpu_baseline(cache, qs[0], args, args.cpu_seconds, nth)
+        cb = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": UNIT,
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_per_step,
+            "us_per_step": ms_per_step * 1000,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "bf16",
+            "data": "synthetic N(0,1) K/V/q (reference workload distribution), generated on device",
+            "config": config,
+            "gpu_launches": 5 * args.steps,
+            "breakdown_us": brk,
+            "step_bytes": step_total,
+            "step_hbm_gbs": step_total / (ms_per_step * 1e-3) / 1e9,
+            "step_frac_of_hbm": step_total / (ms_per_step * 1e-3) / 1e9 / peaks["hbm_gbs"],
+            "roofline": {
+                "kernel": dom,
+                "bound": "hbm",
+                "achieved": achieved,
+                "peak": peaks["hbm_gbs"],
+                "peak_kind": peak_kind,
+                "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"],
+                "bytes_per_launch": dom_bytes,
+                "traffic": traffic,
+            },
+            "dense_us_per_step": dense_us,
+            "x_over_dense": (dense_us / (brk["score"] + brk["select"] + brk["attend"]))
+            if dense_us else None,
+            "x_over_dense_attn_only": (dense_us / brk["attend"]) if dense_us else None,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1000},
+            "clocks": sampler.summary(),
+            "allgather_us": allgather_us,
+            "cpu_baseline": cb,
+        }
+        print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

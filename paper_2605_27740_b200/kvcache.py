@@ -248,26 +248,20 @@ class PagedKvCache:
     # Appends
 
     def _host_alloc(self, counts: np.ndarray) -> list[np.ndarray]:
-        """Host-side _alloc_page for `counts[u]` new pages per unit, in unit order."""
-        st = self.pool_state.cpu().numpy().copy()
+        """Host-side _alloc_page (kvcache.py:154-176) for `counts[u]` new pages per unit,
+        in unit order: the free list is popped from its end first, then the bump pointer."""
+        st = self.pool_state.cpu().numpy()
         bump, nfree, maxp = int(st[0]), int(st[1]), int(st[2])
-        free = self.free_list_dev[:nfree].cpu().numpy().tolist()
         need = int(counts.sum())
-        if need > len(free) + (maxp - bump):
+        if need > nfree + (maxp - bump):
             raise CapacityError(f"page pool exhausted ({maxp} pages)")
-        out = []
-        for u in range(len(counts)):
-            pids = []
-            for _ in range(int(counts[u])):
-                if free:
-                    pids.append(free.pop())
-                else:
-                    pids.append(bump)
-                    bump += 1
-            out.append(np.asarray(pids, dtype=np.int64))
-        self.pool_state[0] = bump
-        self.pool_state[1] = len(free)
-        return out
+        from_free = min(need, nfree)
+        popped = self.free_list_dev[nfree - from_free : nfree].cpu().numpy()[::-1]
+        pids = np.concatenate([popped.astype(np.int64),
+                               np.arange(bump, bump + need - from_free, dtype=np.int64)])
+        self.pool_state[0] = bump + need - from_free
+        self.pool_state[1] = nfree - from_free
+        return np.split(pids, np.cumsum(counts)[:-1])
 
     def extend_units(self, keys: torch.Tensor, values: torch.Tensor, n_rows=None) -> None:
         """Batched extend (kvcache.py:210-233) for every unit at once.
@@ -288,17 +282,12 @@ class PagedKvCache:
         if np.any(P1 > self.Pmax):
             raise CapacityError(f"page table capacity exhausted ({self.Pmax} pages per head)")
         new_pids = self._host_alloc(P1 - P0)
-        rows_idx, cols_idx, vals = [], [], []
-        for u in range(U):
-            if len(new_pids[u]):
-                rows_idx.append(np.full(len(new_pids[u]), u))
-                cols_idx.append(np.arange(P0[u], P1[u]))
-                vals.append(new_pids[u])
         d = self.device
-        if vals:
-            r = torch.from_numpy(np.concatenate(rows_idx)).to(d)
-            c = torch.from_numpy(np.concatenate(cols_idx)).to(d)
-            v = torch.from_numpy(np.concatenate(vals).astype(np.int32)).to(d)
+        cnt = P1 - P0
+        if cnt.sum():
+            r = torch.from_numpy(np.repeat(np.arange(U), cnt)).to(d)
+            c = torch.from_numpy(np.concatenate([np.arange(a, b) for a, b in zip(P0, P1)])).to(d)
+            v = torch.from_numpy(np.concatenate(new_pids).astype(np.int32)).to(d)
             self.page_table[r, c] = v
         kk = dev.to_device(keys, self.dtype, d)
         vv = dev.to_device(values, self.dtype, d)

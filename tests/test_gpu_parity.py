@@ -1,0 +1,362 @@
+"""GPU parity: the sm_100a kernels against the CPU oracle on identical inputs.
+
+Stage-isolated checks feed the oracle exactly what the GPU consumed (its stats, its
+keys) so integer/index results must be bit-identical; end-to-end checks run the
+oracle's restatement of attention.py:110-147 on the cache contents read back.
+Tolerances (BASELINE.json north_star): f32 outputs 1e-5, bf16 2e-2 abs; page stats,
+scores, keys and selections bit-exact.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+def _pt():
+    import paper_2605_27740_b200 as pt
+
+    return pt
+
+
+def make_cache(rng, B, H, D, S, lens, dtype="f32", stats="f32", spare=8):
+    pt = _pt()
+    U = B * H
+    lens = np.broadcast_to(np.asarray(lens), (U,)).astype(np.int64)
+    Pcap = int(-(-lens.max() // S)) + spare
+    layout = pt.CacheLayout(num_kv_heads=H, head_dim=D, page_size=S, max_pages=U * Pcap)
+    tdt = torch.float32 if dtype == "f32" else torch.bfloat16
+    sdt = torch.float32 if stats == "f32" else torch.bfloat16
+    cache = pt.PagedKvCache(layout, batch=B, dtype=tdt, stats_dtype=sdt, max_pages_per_head=Pcap)
+    nmax = int(lens.max())
+    K = rng.standard_normal((U, nmax, D)).astype(np.float32)
+    V = rng.standard_normal((U, nmax, D)).astype(np.float32)
+    cache.extend_units(torch.from_numpy(K), torch.from_numpy(V), lens)
+    return cache
+
+
+def readback(cache):
+    kpool = cache.k_pool.to(torch.float32).cpu().numpy()
+    vpool = cache.v_pool.to(torch.float32).cpu().numpy()
+    table = cache.page_table.cpu().numpy()
+    seq = cache.seq_lens.cpu().numpy()
+    return kpool, vpool, table, seq
+
+
+def gpu_stats(cache):
+    from paper_2605_27740_b200 import _device as dev
+
+    m = dev.untile_means(cache.means, cache.num_units, cache.Pmax, cache.layout.head_dim,
+                         cache.stats_dtype).to(torch.float32).cpu().numpy()
+    return m, cache.stds.cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# K1: page statistics
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("D,S", [(128, 16), (64, 32), (16, 8), (256, 8), (96, 64)])
+def test_page_stats_bit_exact(cuda, oracle, dtype, D, S):
+    rng = np.random.default_rng(100 + D + S)
+    lens = rng.integers(1, 40 * S, size=6)
+    cache = make_cache(rng, 2, 3, D, S, lens, dtype=dtype)
+    kpool, _, table, seq = readback(cache)
+    means, stds = oracle.build_stats(kpool, table, seq, S)
+    gm, gs = gpu_stats(cache)
+    for u in range(cache.num_units):
+        P = cache.num_pages(u)
+        np.testing.assert_array_equal(gm[u, :P], means[u, :P])
+        np.testing.assert_array_equal(gs[u, :P], stds[u, :P])
+
+
+def test_compute_page_stats_golden(cuda):
+    pt = _pt()
+    s = pt.compute_page_stats(np.array([[1.0, 0.0, 0.0, 0.0], [0.0, 1.0, 0.0, 0.0]]))
+    np.testing.assert_array_equal(s.mean, np.float32([0.5, 0.5, 0.0, 0.0]))
+    assert s.std == float(np.float32(np.sqrt(0.5)))  # SPEC.md:59 (padded dims add zero variance)
+    one = pt.compute_page_stats(np.full((1, 4), 3.5, np.float32))
+    assert one.std == 0.0 and one.count == 1
+
+
+# ---------------------------------------------------------------------------
+# K2: scoring (f32 scores and ordered bf16 keys, bit-exact)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("G", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("qdt", ["f32", "bf16"])
+def test_scores_bit_exact(cuda, oracle, G, qdt):
+    pt = _pt()
+    rng = np.random.default_rng(7 + G)
+    B, H, D, S = 2, 2, 128, 16
+    lens = rng.integers(S, 300 * S, size=B * H)
+    cache = make_cache(rng, B, H, D, S, lens, dtype="bf16")
+    eng = pt.DecodeEngine(cache, G, 8, keep_scores=True)
+    q = torch.from_numpy(rng.standard_normal((B * H * G, D)).astype(np.float32)).cuda()
+    if qdt == "bf16":
+        q = q.to(torch.bfloat16)
+    eng.score(q)
+    torch.cuda.synchronize()
+    gm, gs = gpu_stats(cache)
+    qh = q.to(torch.float32).cpu().numpy().reshape(-1, G, D)
+    for u in range(cache.num_units):
+        P = cache.num_pages(u)
+        norms = oracle.query_norms(qh[u])
+        want = oracle.fused_scores(qh[u], norms, gm[u, :P], gs[u, :P], 0.5)
+        got = eng.scores[u, :P].cpu().numpy()
+        np.testing.assert_array_equal(got, want)
+        keys = eng.keys[u, :P].cpu().numpy().view(np.uint16)
+        np.testing.assert_array_equal(keys, oracle.encode_ordered(oracle.f32_to_bf16(want)))
+
+
+def test_scores_bf16_stats_bit_exact(cuda, oracle):
+    pt = _pt()
+    rng = np.random.default_rng(11)
+    cache = make_cache(rng, 1, 2, 128, 16, [5000, 3001], dtype="bf16", stats="bf16")
+    eng = pt.DecodeEngine(cache, 4, 8, keep_scores=True)
+    q = torch.from_numpy(rng.standard_normal((8, 128)).astype(np.float32)).cuda().to(torch.bfloat16)
+    eng.score(q)
+    torch.cuda.synchronize()
+    gm, gs = gpu_stats(cache)  # bf16 means upcast -- what the kernel consumed
+    qh = q.to(torch.float32).cpu().numpy().reshape(2, 4, 128)
+    for u in range(2):
+        P = cache.num_pages(u)
+        want = oracle.fused_scores(qh[u], oracle.query_norms(qh[u]), gm[u, :P], gs[u, :P], 0.5)
+        np.testing.assert_array_equal(eng.scores[u, :P].cpu().numpy(), want)
+
+
+# ---------------------------------------------------------------------------
+# K3: top-k selection (integer work, bit-exact)
+# ---------------------------------------------------------------------------
+def _topk_run(keys_u16: np.ndarray, k: int, S: int = 1):
+    """Run pt_topk on one unit with an identity page table; returns logical ids etc."""
+    from paper_2605_27740_b200 import _device as dev
+    from paper_2605_27740_b200 import _lib
+
+    P = keys_u16.shape[0]
+    Pmax = dev.round_up(max(P, 1), 32)
+    d = torch.device("cuda")
+    keys = torch.zeros(Pmax, dtype=torch.int16, device=d)
+    keys[:P] = torch.from_numpy(keys_u16.view(np.int16)).to(d)
+    table = torch.arange(Pmax, dtype=torch.int32, device=d) + 1000
+    seq = torch.tensor([P * S], dtype=torch.int32, device=d)
+    sel = torch.zeros(k, dtype=torch.int32, device=d)
+    lg = torch.zeros(k, dtype=torch.int32, device=d)
+    meta = torch.zeros(3, dtype=torch.int32, device=d)
+    _lib.call("pt_topk", keys.data_ptr(), seq.data_ptr(), table.data_ptr(), 1, S, Pmax, k,
+              sel.data_ptr(), lg.data_ptr(), meta.data_ptr(), meta.data_ptr() + 4,
+              meta.data_ptr() + 8, dev.stream_handle())
+    m = meta.cpu().numpy()
+    n = int(m[0])
+    return sel.cpu().numpy()[:n], lg.cpu().numpy()[:n], int(m[1]), int(m[2])
+
+
+@pytest.mark.parametrize("P", [2, 64, 1024, 4096, 8192, 16384, 23553, 32768])
+def test_topk_matches_oracle(cuda, oracle, P):
+    rng = np.random.default_rng(P)
+    for trial in range(12):
+        k = int(rng.integers(1, min(P, 300)))
+        if trial % 4 == 0:
+            vals = rng.integers(-6, 7, P).astype(np.float32)  # dense ties
+        else:
+            vals = (rng.standard_normal(P) * rng.choice([0.05, 1.0, 30.0])).astype(np.float32)
+        keys = oracle.encode_ordered(oracle.f32_to_bf16(vals))
+        if k >= P:
+            continue
+        sel, lg, kth, kp1 = _topk_run(keys, k)
+        ids, thr, kplus1, _ = oracle.radix_select_desc(keys, k)
+        np.testing.assert_array_equal(np.sort(lg), np.sort(ids))
+        np.testing.assert_array_equal(sel, lg + 1000)  # physical translation
+        assert np.all(np.diff(lg) > 0)  # emitted in ascending logical order
+        assert (kth, kp1) == (thr, kplus1)
+
+
+def test_topk_take_all_and_ties_lowest_index(cuda, oracle):
+    keys = oracle.encode_ordered(oracle.f32_to_bf16(np.float32([3, 1, 4, 1, 5])))
+    sel, lg, kth, kp1 = _topk_run(keys, 2)
+    assert set(lg.tolist()) == {2, 4} and kth == keys[2] and kp1 == keys[0]
+    sel, lg, kth, kp1 = _topk_run(keys, 9)  # P <= k: everything, kplus1 None
+    assert sorted(lg.tolist()) == [0, 1, 2, 3, 4] and kp1 == -1 and kth == keys.min()
+    flat = oracle.encode_ordered(oracle.f32_to_bf16(np.ones(100, np.float32)))
+    _, lg, _, _ = _topk_run(flat, 10)
+    assert lg.tolist() == list(range(10))
+
+
+# ---------------------------------------------------------------------------
+# K4: attention over the selected pages
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("G,D,S", [(4, 128, 16), (1, 64, 32), (8, 128, 16), (2, 256, 8), (4, 24, 8)])
+def test_attend_matches_oracle(cuda, oracle, G, D, S):
+    pt = _pt()
+    rng = np.random.default_rng(G * 1000 + D + S)
+    B, H = 2, 2
+    lens = rng.integers(S * 3, S * 200, size=B * H)
+    cache = make_cache(rng, B, H, D, S, lens)
+    eng = pt.DecodeEngine(cache, G, 24)
+    q = torch.from_numpy(rng.standard_normal((B * H * G, D)).astype(np.float32)).cuda()
+    eng.step(q)
+    torch.cuda.synchronize()
+    kpool, vpool, table, seq = readback(cache)
+    sel = eng.sel.cpu().numpy()
+    nsel = eng.n_sel.cpu().numpy()
+    qh = q.cpu().numpy().reshape(-1, G, D)
+    out = eng.out.cpu().numpy().reshape(-1, G, D)
+    lse = eng.lse.cpu().numpy().reshape(-1, G)
+    for u in range(cache.num_units):
+        P = cache.num_pages(u)
+        tail = table[u, P - 1]
+        rows = []
+        for pid in sel[u, : nsel[u]]:
+            r = seq[u] - (P - 1) * S if pid == tail else S
+            rows.append((pid, r))
+        gk = np.concatenate([kpool[p, :r] for p, r in rows])
+        gv = np.concatenate([vpool[p, :r] for p, r in rows])
+        for g in range(G):
+            o, l = oracle.stream_attention(qh[u, g], gk, gv, 1.0 / math.sqrt(D), S)
+            np.testing.assert_allclose(out[u, g], o, rtol=1e-5, atol=2e-6)
+            assert lse[u, g] == pytest.approx(l, rel=1e-5)
+
+
+def test_dense_matches_oracle(cuda, oracle):
+    pt = _pt()
+    rng = np.random.default_rng(5)
+    D, S, G = 128, 16, 4
+    cache = make_cache(rng, 1, 2, D, S, [3000, 4096 + 7])
+    eng = pt.DecodeEngine(cache, G, 8)
+    q = torch.from_numpy(rng.standard_normal((8, D)).astype(np.float32)).cuda()
+    out, lse = eng.dense(q)
+    torch.cuda.synchronize()
+    kpool, vpool, table, seq = readback(cache)
+    o, l = oracle.dense_units(q.cpu().numpy().reshape(2, G, D), kpool, vpool, table, seq,
+                              1.0 / math.sqrt(D), S)
+    np.testing.assert_allclose(out.cpu().numpy().reshape(2, G, D), o, rtol=1e-5, atol=2e-6)
+    np.testing.assert_allclose(lse.cpu().numpy().reshape(2, G), l, rtol=1e-5)
+
+
+# ---------------------------------------------------------------------------
+# End to end: the batched decode step vs the reference decode_step restatement
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("dtype,tol", [("f32", 1e-5), ("bf16", 2e-2)])
+@pytest.mark.parametrize("B,H,G,D,S,N,k", [
+    (1, 8, 1, 128, 16, 4096, 32),      # cfg1 (8 heads, f32 reference path)
+    (1, 1, 8, 128, 16, 4096, 32),      # cfg1 with 8 q / 1 kv
+    (1, 8, 4, 128, 16, 32768, 128),    # cfg2: Llama-3.1-8B shape, 32K, k=2048 tokens
+    (2, 16, 1, 64, 32, 60000, 16),     # cfg4 shape (2 of 64 sequences), ragged tail page
+    (2, 2, 4, 128, 64, 20000, 8),      # page 64
+])
+def test_decode_step_end_to_end(cuda, oracle, dtype, tol, B, H, G, D, S, N, k):
+    pt = _pt()
+    rng = np.random.default_rng(N + k)
+    lens = N - rng.integers(0, S, size=B * H)
+    cache = make_cache(rng, B, H, D, S, lens, dtype=dtype)
+    eng = pt.DecodeEngine(cache, G, k)
+    q = torch.from_numpy(rng.standard_normal((B * H * G, D)).astype(np.float32)).cuda()
+    if dtype == "bf16":
+        q = q.to(torch.bfloat16)
+    out, lse = eng.step(q)
+    torch.cuda.synchronize()
+    kpool, vpool, table, seq = readback(cache)
+    means, stds = oracle.build_stats(kpool, table, seq, S)
+    ref = oracle.decode_units(q.to(torch.float32).cpu().numpy().reshape(-1, G, D), kpool, vpool,
+                              table, seq, means, stds, k, 0.5, 1.0 / math.sqrt(D), S)
+    sel = eng.sel.cpu().numpy()
+    nsel = eng.n_sel.cpu().numpy()
+    for u in range(cache.num_units):
+        assert nsel[u] == ref["n_sel"][u]
+        assert set(sel[u, : nsel[u]].tolist()) == set(ref["sel"][u, : nsel[u]].tolist())
+    np.testing.assert_array_equal(eng.kth.cpu().numpy(), ref["kth"])
+    np.testing.assert_array_equal(eng.kplus1.cpu().numpy(), ref["kplus1"])
+    np.testing.assert_allclose(out.cpu().numpy().reshape(-1, G, D), ref["out"], rtol=tol, atol=tol)
+    np.testing.assert_allclose(lse.cpu().numpy().reshape(-1, G), ref["lse"], rtol=tol)
+
+
+def test_append_batch_and_graph_replay(cuda, oracle):
+    pt = _pt()
+    rng = np.random.default_rng(3)
+    B, H, G, D, S = 2, 2, 4, 128, 16
+    cache = make_cache(rng, B, H, D, S, [33, 47, 16, 1], dtype="bf16", spare=4)
+    U = B * H
+    eng = pt.DecodeEngine(cache, G, 4)
+    q = torch.from_numpy(rng.standard_normal((U * G, D)).astype(np.float32)).cuda().to(torch.bfloat16)
+    kn = torch.from_numpy(rng.standard_normal((U, D)).astype(np.float32)).cuda().to(torch.bfloat16)
+    vn = torch.from_numpy(rng.standard_normal((U, D)).astype(np.float32)).cuda().to(torch.bfloat16)
+    for _ in range(20):  # crosses page boundaries: device-side allocation
+        eng.step(q, kn, vn)
+    torch.cuda.synchronize()
+    cache.check_errors()
+    assert [cache.seq_len(u) for u in range(U)] == [53, 67, 36, 21]
+    kpool, _, table, seq = readback(cache)
+    means, stds = oracle.build_stats(kpool, table, seq, S)
+    gm, gs = gpu_stats(cache)
+    for u in range(U):
+        P = cache.num_pages(u)
+        np.testing.assert_array_equal(gm[u, :P], means[u, :P])
+        np.testing.assert_array_equal(gs[u, :P], stds[u, :P])
+        np.testing.assert_array_equal(kpool[table[u, P - 1], (seq[u] - 1) % S],
+                                      kn[u].to(torch.float32).cpu().numpy())
+    # physical ids are unique across units
+    used = np.concatenate([table[u, : cache.num_pages(u)] for u in range(U)])
+    assert len(np.unique(used)) == len(used)
+    # a captured graph replays the same step
+    out_eager = eng.step(q)[0].clone()
+    eng.capture(q)
+    eng.replay()
+    torch.cuda.synchronize()
+    torch.testing.assert_close(eng.out, out_eager, rtol=0, atol=0)
+
+
+def test_append_capacity_error(cuda):
+    pt = _pt()
+    layout = pt.CacheLayout(num_kv_heads=1, head_dim=16, page_size=8, max_pages=2)
+    cache = pt.PagedKvCache(layout, max_pages_per_head=32)
+    x = np.zeros((16, 16), np.float32)
+    cache.extend(0, x, x)
+    with pytest.raises(pt.CapacityError, match="exhausted"):
+        cache.append(0, np.zeros(16), np.zeros(16))
+    kn = torch.zeros(1, 16, device="cuda")
+    cache.append_batch(kn, kn)
+    torch.cuda.synchronize()
+    with pytest.raises(pt.CapacityError):
+        cache.check_errors()
+    assert cache.seq_len(0) == 16
+
+
+# ---------------------------------------------------------------------------
+# The reference backend contract over host buffers (backend.py:14-58)
+# ---------------------------------------------------------------------------
+def test_backend_contract_vs_oracle(cuda, oracle):
+    from paper_2605_27740_b200 import backend
+
+    rng = np.random.default_rng(404)
+    for _ in range(15):
+        g, p, d = int(rng.integers(1, 6)), int(rng.integers(1, 300)), int(rng.integers(4, 96))
+        q = rng.standard_normal((g, d)).astype(np.float32)
+        norms = np.linalg.norm(q.astype(np.float64), axis=1).astype(np.float32)
+        means = rng.standard_normal((p, d)).astype(np.float32)
+        stds = np.abs(rng.standard_normal(p)).astype(np.float32)
+        np.testing.assert_array_equal(backend.fused_scores(q, norms, means, stds, 0.5),
+                                      oracle.fused_scores(q, norms, means, stds, 0.5))
+    for _ in range(15):
+        p = int(rng.integers(2, 3000))
+        k = int(rng.integers(1, p))
+        s = (rng.standard_normal(p) * rng.choice([0.01, 1.0, 100.0])).astype(np.float32)
+        keys = oracle.encode_ordered(oracle.f32_to_bf16(s))
+        ids, thr, kp1, passes = backend.radix_select_desc(keys, k)
+        ids0, thr0, kp10, _ = oracle.radix_select_desc(keys, k)
+        np.testing.assert_array_equal(np.sort(ids), np.sort(ids0))
+        assert (thr, kp1, passes) == (thr0, kp10, 3)
+    for _ in range(15):
+        nb, block, d = int(rng.integers(1, 40)), int(rng.integers(1, 9)), int(rng.integers(4, 64))
+        n = nb * block
+        q = rng.standard_normal(d).astype(np.float32)
+        K = rng.standard_normal((n, d)).astype(np.float32)
+        V = rng.standard_normal((n, d)).astype(np.float32)
+        bias = rng.uniform(-3, 0, nb).astype(np.float32)
+        out, lse = backend.stream_attention(q, K, V, 0.3, block, bias)
+        o0, l0 = oracle.stream_attention(q, K, V, 0.3, block, bias)
+        np.testing.assert_allclose(out, o0, rtol=2e-5, atol=2e-6)
+        assert lse == pytest.approx(l0, rel=1e-5)
