@@ -132,11 +132,12 @@ PT_API int pt_topk(const uint16_t *keys, const int32_t *seq_len, const int32_t *
  * seq_len - (P-1)*S rows, others S.  bias f32 [U][sel_stride] per page or NULL.
  * n_sel == NULL selects dense mode (attention.py:78-91): every page of the unit, i.e.
  * pass sel = page_table, sel_stride = Pmax.
+ * num_phys_pages: pool extent (for the TMA tensor maps of the bf16 tensor-core path).
  * out f32 [U*G][D], lse f32 [U*G].  workspace: pt_attend_workspace_bytes();
  * tickets int32 [U] zero-initialised once (self-resetting).  nsplit 0 = automatic. */
 PT_API size_t pt_attend_workspace_bytes(int U, int G, int D, int sel_stride);
 PT_API int pt_attend(const void *q, int q_dtype, const void *k_pool, const void *v_pool, int kv_dtype,
-              const int32_t *sel, int sel_stride, const int32_t *n_sel,
+              int num_phys_pages, const int32_t *sel, int sel_stride, const int32_t *n_sel,
               const int32_t *page_table, const int32_t *seq_len, int U, int G, int D, int S,
               int Pmax, const float *bias, float scale, float *out, float *lse, void *workspace,
               size_t workspace_bytes, int32_t *tickets, int nsplit, void *stream);

@@ -46,7 +46,7 @@ _PROTOS = {
     "pt_score": (_i, [_vp, _i, _vp, _vp, _i, _vp, _vp, _i, _i, _i, _i, _i, _f, _vp, _vp, _vp]),
     "pt_topk": (_i, [_vp, _vp, _vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pt_attend_workspace_bytes": (_sz, [_i, _i, _i, _i]),
-    "pt_attend": (_i, [_vp, _i, _vp, _vp, _i, _vp, _i, _vp, _vp, _vp, _i, _i, _i, _i, _i, _vp,
+    "pt_attend": (_i, [_vp, _i, _vp, _vp, _i, _i, _vp, _i, _vp, _vp, _vp, _i, _i, _i, _i, _i, _vp,
                        _f, _vp, _vp, _vp, _sz, _vp, _i, _vp]),
     "pt_tile_means": (_i, [_vp, _i, _i, _i, _i, _vp, _i, _vp]),
 }

@@ -101,7 +101,8 @@ def sparse_attention(q, cache: PagedKvCache, head: int, selection: TopKSelection
     pt_row = cache.page_table[head]
     seq = cache.seq_lens[head : head + 1]
     _lib.call("pt_attend", qt.data_ptr(), _lib.PT_F32, cache.k_pool.data_ptr(),
-              cache.v_pool.data_ptr(), cache.kv_code, sel.data_ptr(), sel.numel(),
+              cache.v_pool.data_ptr(), cache.kv_code, cache.layout.max_pages, sel.data_ptr(),
+              sel.numel(),
               n_sel.data_ptr(), pt_row.data_ptr(), seq.data_ptr(), 1, 1, D, S, cache.Pmax, None,
               float(scale), out.data_ptr(), lse.data_ptr(), ws.data_ptr(), ws.numel(),
               tickets.data_ptr(), 0, dev.stream_handle())

@@ -1,0 +1,33 @@
+// attend_mma.cu -- tensor-core (mma.sync + TMA) K4 instantiations for bf16 KV (attend.cuh).
+#include "attend.cuh"
+
+namespace pt {
+
+template <int D, int MT>
+static int launch_one(const CUtensorMap &tk, const CUtensorMap &tv, const AttnParams &prm, int U,
+                      int nsplit, int NW, size_t smem, cudaStream_t st) {
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+        PT_CUDA_TRY(cudaFuncSetAttribute(k_attend_mma<D, MT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured = smem;
+    }
+    dim3 grid(nsplit, U);
+    k_attend_mma<D, MT><<<grid, NW * 32, smem, st>>>(tk, tv, prm);
+    PT_CUDA_TRY(cudaGetLastError());
+    return PT_OK;
+}
+
+int launch_attend_mma(const CUtensorMap &tk, const CUtensorMap &tv, const AttnParams &prm, int U,
+                      int nsplit, int NW, size_t smem, cudaStream_t st) {
+    const int D = prm.D, S = prm.S;
+#define PT_MMA(D_, MT_) \
+    if (D == D_ && S == 16 * MT_) return launch_one<D_, MT_>(tk, tv, prm, U, nsplit, NW, smem, st);
+    PT_MMA(64, 1) PT_MMA(64, 2) PT_MMA(64, 4)
+    PT_MMA(128, 1) PT_MMA(128, 2) PT_MMA(128, 4)
+    PT_MMA(256, 1) PT_MMA(256, 2) PT_MMA(256, 4)
+#undef PT_MMA
+    return PT_ERR_UNSUPPORTED;
+}
+
+}  // namespace pt

@@ -191,7 +191,7 @@ extern "C" int pt_stream_attention_host(const float *q, const float *keys, const
     PT_CUDA_TRY(cudaMemcpyAsync(dns.p, &n_pages, 4, cudaMemcpyHostToDevice, st));
     if (block_bias)
         PT_CUDA_TRY(cudaMemcpyAsync(db.p, pbias.data(), (size_t)npages * 4, cudaMemcpyHostToDevice, st));
-    rc = pt_attend(dq.p, PT_F32, dkp.p, dvp.p, PT_F32, (const int32_t *)dt.p, (int)npages,
+    rc = pt_attend(dq.p, PT_F32, dkp.p, dvp.p, PT_F32, (int)npages, (const int32_t *)dt.p, (int)npages,
                    (const int32_t *)dns.p, (const int32_t *)dt.p, (const int32_t *)dsl.p, 1, 1, Dp,
                    Sp, Pmax, block_bias ? (const float *)db.p : nullptr, scale, (float *)dout.p,
                    (float *)dlse.p, dws.p, wsb, (int32_t *)dtk.p, 0, st);

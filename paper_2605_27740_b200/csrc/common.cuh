@@ -118,7 +118,7 @@ __device__ __forceinline__ float warp_max(float v) {
 // identity-initialised -- pinned against numpy in tests/test_oracle_golden.py).
 // X is any accessor `double operator()(int i)`.
 template <class X>
-__device__ __forceinline__ double np_pairwise_leaf(const X &x, int off, int n) {
+__device__ __noinline__ double np_pairwise_leaf(const X &x, int off, int n) {
     if (n < 8) {
         double res = 0.0;
         for (int i = 0; i < n; i++) res = __dadd_rn(res, x(off + i));
@@ -138,7 +138,7 @@ __device__ __forceinline__ double np_pairwise_leaf(const X &x, int off, int n) {
 }
 
 template <int DEPTH, class X>
-__device__ __forceinline__ double np_pairwise(const X &x, int off, int n) {
+__device__ __noinline__ double np_pairwise(const X &x, int off, int n) {
     if constexpr (DEPTH == 0) {
         return np_pairwise_leaf(x, off, n);  // caller guarantees n <= 128 * 2^DEPTH
     } else {

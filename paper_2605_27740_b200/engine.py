@@ -96,7 +96,7 @@ class DecodeEngine:
         q2, qc = self._q(q)
         c = self.cache
         _lib.call("pt_attend", q2.data_ptr(), qc, c.k_pool.data_ptr(), c.v_pool.data_ptr(),
-                  c.kv_code, self.sel.data_ptr(), self.k, self.n_sel.data_ptr(),
+                  c.kv_code, c.layout.max_pages, self.sel.data_ptr(), self.k, self.n_sel.data_ptr(),
                   c.page_table.data_ptr(), c.seq_lens.data_ptr(), self.U, self.G, self.D,
                   c.layout.page_size, c.Pmax, None, self.scale, self.out.data_ptr(),
                   self.lse.data_ptr(), self.ws.data_ptr(), self.ws.numel(),
@@ -107,7 +107,7 @@ class DecodeEngine:
         q2, qc = self._q(q)
         c = self.cache
         _lib.call("pt_attend", q2.data_ptr(), qc, c.k_pool.data_ptr(), c.v_pool.data_ptr(),
-                  c.kv_code, c.page_table.data_ptr(), c.Pmax, None, c.page_table.data_ptr(),
+                  c.kv_code, c.layout.max_pages, c.page_table.data_ptr(), c.Pmax, None, c.page_table.data_ptr(),
                   c.seq_lens.data_ptr(), self.U, self.G, self.D, c.layout.page_size, c.Pmax,
                   None, self.scale, self.dense_out.data_ptr(), self.dense_lse.data_ptr(),
                   self.ws.data_ptr(), self.ws.numel(), self.dense_tickets.data_ptr(), nsplit,

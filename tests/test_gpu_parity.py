@@ -360,3 +360,33 @@ def test_backend_contract_vs_oracle(cuda, oracle):
         o0, l0 = oracle.stream_attention(q, K, V, 0.3, block, bias)
         np.testing.assert_allclose(out, o0, rtol=2e-5, atol=2e-6)
         assert lse == pytest.approx(l0, rel=1e-5)
+
+
+@pytest.mark.parametrize("G,D,S", [(4, 128, 16), (8, 128, 32), (1, 64, 16), (2, 256, 16), (4, 128, 64)])
+def test_attend_tensor_core_path_vs_simt(cuda, oracle, G, D, S, monkeypatch):
+    """bf16 KV: the TMA + mma.sync kernel against the CUDA-core kernel and the oracle."""
+    pt = _pt()
+    rng = np.random.default_rng(G + D + S)
+    B, H = 2, 2
+    lens = rng.integers(S * 2, S * 150, size=B * H)
+    cache = make_cache(rng, B, H, D, S, lens, dtype="bf16")
+    eng = pt.DecodeEngine(cache, G, 40)
+    q = torch.from_numpy(rng.standard_normal((B * H * G, D)).astype(np.float32)).cuda()
+    q = q.to(torch.bfloat16)
+    out_tc = eng.step(q)[0].clone()
+    lse_tc = eng.lse.clone()
+    monkeypatch.setenv("PT_ATTEND_SIMT", "1")
+    eng.attend(q)
+    torch.cuda.synchronize()
+    out_simt, lse_simt = eng.out.clone(), eng.lse.clone()
+    monkeypatch.delenv("PT_ATTEND_SIMT")
+    torch.testing.assert_close(out_tc, out_simt, rtol=0, atol=2e-2)
+    torch.testing.assert_close(lse_tc, lse_simt, rtol=0, atol=2e-2)
+    # dense over every page, tensor-core path, vs the oracle
+    out_d, lse_d = eng.dense(q)
+    torch.cuda.synchronize()
+    kpool, vpool, table, seq = readback(cache)
+    o, l = oracle.dense_units(q.to(torch.float32).cpu().numpy().reshape(-1, G, D), kpool, vpool,
+                              table, seq, 1.0 / math.sqrt(D), S)
+    np.testing.assert_allclose(out_d.cpu().numpy().reshape(-1, G, D), o, rtol=0, atol=2e-2)
+    np.testing.assert_allclose(lse_d.cpu().numpy().reshape(-1, G), l, rtol=0, atol=2e-2)
