@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--nsplit", type=int, default=0, help="attention splits per unit (0 = auto)")
+    ap.add_argument("--sweep-nsplit", action="store_true")
+    ap.add_argument("--sweep", action="store_true", help="time kernel variants / tuning knobs")
     ap.add_argument("--profile", action="store_true",
                     help="few eager steps, no graph/cpu/dense (for ncu launch lists)")
     return ap.parse_args()
@@ -315,9 +318,8 @@ def main():
         gph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(gph):
             cache.append_batch(kn, vn)
-            eng.score(qs[i])
-            eng.select()
-            eng.attend(qs[i])
+            eng.score_select(qs[i])
+            eng.attend(qs[i], nsplit=args.nsplit)
         cache._seq_host -= 1
         graphs.append(gph)
     for i in range(args.warmup):
@@ -352,24 +354,81 @@ def main():
 
     # ---- per-kernel breakdown (CUDA events on the launching stream) -----------------
     reps = max(20, min(args.steps, 100))
-    names = ["append", "score", "select", "attend"]
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(reps)]
+    names = ["append", "score_select", "attend"]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(reps)]
     for r in range(reps):
         q = qs[r % NQ]
         ev = evs[r]
         ev[0].record(stream)
         cache.append_batch(kn, vn)
         ev[1].record(stream)
-        eng.score(q)
+        eng.score_select(q)
         ev[2].record(stream)
-        eng.select()
+        eng.attend(q, nsplit=args.nsplit)
         ev[3].record(stream)
-        eng.attend(q)
-        ev[4].record(stream)
     torch.cuda.synchronize()
     cache.check_errors()
     brk = {n: statistics.median([evs[r][i].elapsed_time(evs[r][i + 1]) * 1000 for r in range(reps)])
            for i, n in enumerate(names)}
+    # the unfused stages, for reference (scoring alone is the HBM-heaviest kernel)
+    ev2 = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(reps)]
+    for r in range(reps):
+        ev2[r][0].record(stream)
+        eng.score(qs[r % NQ])
+        ev2[r][1].record(stream)
+        eng.select()
+        ev2[r][2].record(stream)
+    torch.cuda.synchronize()
+    brk["score_only"] = statistics.median([ev2[r][0].elapsed_time(ev2[r][1]) * 1000 for r in range(reps)])
+    brk["select_only"] = statistics.median([ev2[r][1].elapsed_time(ev2[r][2]) * 1000 for r in range(reps)])
+    tune = None
+    if args.sweep:
+        tune = {}
+        def timeit(fn, reps=20):
+            for _ in range(3):
+                fn()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            for r in range(reps):
+                fn()
+            a1.record(stream)
+            torch.cuda.synchronize()
+            return a0.elapsed_time(a1) * 1000 / reps
+        for nst in ("2", "3", "4"):
+            for ch in ("2", "4", "5", "8", "16"):
+                os.environ["PT_ATTEND_NSTAGE"], os.environ["PT_ATTEND_CHUNK"] = nst, ch
+                try:
+                    tune[f"attend_stream_nst{nst}_c{ch}"] = timeit(lambda: eng.attend(qs[0]))
+                except Exception as e:  # noqa: BLE001
+                    tune[f"attend_stream_nst{nst}_c{ch}"] = str(e)[:60]
+        os.environ.pop("PT_ATTEND_NSTAGE"); os.environ.pop("PT_ATTEND_CHUNK")
+        os.environ["PT_ATTEND_SPLIT"] = "1"
+        tune["attend_split_auto"] = timeit(lambda: eng.attend(qs[0]))
+        os.environ.pop("PT_ATTEND_SPLIT")
+        for nst in ("2", "3"):
+            os.environ["PT_SCORE_NST"] = nst
+            tune[f"score_stream_nst{nst}"] = timeit(lambda: eng.score(qs[0]))
+        os.environ.pop("PT_SCORE_NST")
+        os.environ["PT_SCORE_CTA"] = "1"
+        tune["score_cta"] = timeit(lambda: eng.score(qs[0]))
+        os.environ.pop("PT_SCORE_CTA")
+        tune["select"] = timeit(lambda: eng.select())
+        eng.fused_select = True
+        tune["score_select_fused_cta"] = timeit(lambda: eng.score_select(qs[0]))
+        eng.fused_select = False
+    nsplit_sweep = None
+    if args.sweep_nsplit:
+        nsplit_sweep = {}
+        for ns in (1, 2, 3, 4, 6, 8, 12, 16, 32):
+            for _ in range(3):
+                eng.attend(qs[0], nsplit=ns)
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            for r in range(20):
+                eng.attend(qs[r % NQ], nsplit=ns)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            nsplit_sweep[ns] = a0.elapsed_time(a1) * 1000 / 20
 
     # ---- dense denominator: same GPU, every page of every unit ------------------------
     dense_us = None
@@ -430,8 +489,9 @@ def main():
     e_st = 4 if args.stats_dtype == "f32" else 2
     P = -(-args.ctx // S)
     by = step_bytes(U, G, D, P, kp, S, 2, e_st, args.ctx)
-    dom = max(("score", "attend"), key=lambda n: brk[n])
-    dom_bytes = by[dom]
+    kbytes = {"score_select": by["score"] + by["topk"], "attend": by["attend"]}
+    dom = max(("score_select", "attend"), key=lambda n: brk[n])
+    dom_bytes = kbytes[dom]
     achieved = dom_bytes / (brk[dom] * 1e-6) / 1e9
     traffic = None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
@@ -466,7 +526,9 @@ def main():
             "dtype": "bf16",
             "data": "synthetic N(0,1) K/V/q (reference workload distribution), generated on device",
             "config": config,
-            "gpu_launches": 5 * args.steps,
+            "gpu_launches": 4 * args.steps,
+            "nsplit_sweep_us": nsplit_sweep,
+            "tune_us": tune,
             "breakdown_us": brk,
             "step_bytes": step_total,
             "step_hbm_gbs": step_total / (ms_per_step * 1e-3) / 1e9,
@@ -483,8 +545,7 @@ def main():
                 "traffic": traffic,
             },
             "dense_us_per_step": dense_us,
-            "x_over_dense": (dense_us / (brk["score"] + brk["select"] + brk["attend"]))
-            if dense_us else None,
+            "x_over_dense": (dense_us / (brk["score_select"] + brk["attend"])) if dense_us else None,
             "x_over_dense_attn_only": (dense_us / brk["attend"]) if dense_us else None,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1000},

@@ -113,10 +113,23 @@ PT_API int pt_write_rows(const void *k_rows, const void *v_rows, int n_max, cons
 /* K2. scoring.py:108-124 + _kernels_cy.pyx:19-43 + bf16.py:18-33 + select.py:51-57:
  * q [U*G][D] (q_dtype); norms f32 [U*G] or NULL (computed as scoring.py:39-47);
  * score = max_g fl(fl(sum_d q*mean) + fl(fl(lam*norm_g)*std)), sequential d order;
- * writes keys u16 [U][Pmax] and optionally scores f32 [U][Pmax]. */
+ * writes keys u16 [U][Pmax] and optionally scores f32 [U][Pmax].
+ * lamnorm_ws: f32 [U*8] device scratch enabling the streaming kernel (NULL: CTA kernel). */
 PT_API int pt_score(const void *q, int q_dtype, const float *norms, const void *means, int stats_dtype,
              const float *stds, const int32_t *seq_len, int U, int G, int D, int S, int Pmax,
-             float lam, uint16_t *keys, float *scores, void *stream);
+             float lam, uint16_t *keys, float *scores, float *lamnorm_ws, void *stream);
+
+/* K2+K3 fused: pt_score followed by pt_topk in ONE launch -- the last CTA to finish a unit's
+ * pages selects that unit's top-k while other CTAs keep scoring (same outputs as the two
+ * separate calls).  counters: int32 [U] zero-initialised once (self-resetting).  Returns
+ * PT_ERR_UNSUPPORTED when the unit's keys exceed the kernel's shared-memory envelope; the
+ * caller then uses pt_score + pt_topk. */
+PT_API int pt_score_select(const void *q, int q_dtype, const float *norms, const void *means,
+                           int stats_dtype, const float *stds, const int32_t *seq_len,
+                           const int32_t *page_table, int U, int G, int D, int S, int Pmax,
+                           float lam, int k, uint16_t *keys, float *scores, int32_t *sel,
+                           int32_t *sel_logical, int32_t *n_sel, int32_t *kth, int32_t *kplus1,
+                           int32_t *counters, void *stream);
 
 /* K3. select.py:87-115 + _kernels_cy.pyx:46-126: per unit, k highest keys, ties to the
  * lowest logical index; P <= k takes every page.  sel: int32 [U][k] physical ids in

@@ -5,6 +5,8 @@
 namespace pt {
 int launch_attend_mma(const CUtensorMap &tk, const CUtensorMap &tv, const AttnParams &prm, int U,
                       int nsplit, int NW, size_t smem, cudaStream_t st);
+int launch_attend_stream(const CUtensorMap &tk, const CUtensorMap &tv, const StreamParams &p,
+                         int D, int S, int grid, int NW, size_t smem, cudaStream_t st);
 int launch_attend_simt_f32(const AttnParams &prm, int gp, int dpl, int U, int nsplit, int NW,
                            size_t smem, cudaStream_t st);
 int launch_attend_simt_bf16(const AttnParams &prm, int gp, int dpl, int U, int nsplit, int NW,
@@ -50,10 +52,16 @@ static bool make_pool_tmap(CUtensorMap *tm, const void *base, int D, int S, int6
     return r == CUDA_SUCCESS;
 }
 
-// PT_ATTEND_SIMT=1 forces the CUDA-core kernel (used by the parity tests to pin both paths)
+// PT_ATTEND_SIMT=1 forces the CUDA-core kernel (used by the parity tests to pin both paths);
+// PT_ATTEND_SPLIT=1 forces the (split, unit) grid instead of the streaming kernel;
+// PT_ATTEND_NSTAGE / PT_ATTEND_CHUNK override the streaming ring depth / chunk size.
 static bool simt_forced() {
     const char *e = getenv("PT_ATTEND_SIMT");
     return e && e[0] == '1';
+}
+static int env_int(const char *name, int dflt) {
+    const char *e = getenv(name);
+    return (e && *e) ? atoi(e) : dflt;
 }
 
 extern "C" int pt_attend(const void *q, int q_dtype, const void *k_pool, const void *v_pool,
@@ -68,35 +76,79 @@ extern "C" int pt_attend(const void *q, int q_dtype, const void *k_pool, const v
     const int E = kv_dtype == PT_F32 ? 4 : 2;
     const bool mma = kv_dtype == PT_BF16 && G <= 8 && (D == 64 || D == 128 || D == 256) &&
                      (S == 16 || S == 32 || S == 64) && num_phys_pages > 0 && !simt_forced();
+    // sparse selections on the tensor-core path: persistent streaming kernel
+    if (mma && n_sel != nullptr && U > 0 && env_int("PT_ATTEND_SPLIT", 0) == 0) {
+        const int stage_bytes = 2 * S * D * 2;
+        const int NW = 4;
+        int nstage = env_int("PT_ATTEND_NSTAGE", 0);
+        if (nstage <= 0) {
+            nstage = 3;
+            while (nstage > 2 && attn_stream_smem(NW, nstage, stage_bytes) > 110 * 1024) nstage--;
+        }
+        const size_t smem = attn_stream_smem(NW, nstage, stage_bytes);
+        if (smem <= 220 * 1024) {
+            const int ctas_per_sm = smem <= 110 * 1024 ? 2 : 1;
+            const int grid = 148 * ctas_per_sm;
+            const int W = grid * NW;
+            int C = env_int("PT_ATTEND_CHUNK", 0);
+            if (C <= 0) {  // ~6 chunks per warp for balance
+                const long long pages = (long long)U * sel_stride;
+                C = (int)((pages + (long long)W * 6 - 1) / ((long long)W * 6));
+            }
+            if (C < 1) C = 1;
+            if (C > 32) C = 32;
+            const int CPU = (sel_stride + C - 1) / C;
+            if (CPU <= kAttnMaxSplits && (CPU == 1 || (workspace && tickets &&
+                workspace_bytes >= pt_attend_workspace_bytes(U, G, D, sel_stride)))) {
+                CUtensorMap tk, tv;
+                if (!make_pool_tmap(&tk, k_pool, D, S, num_phys_pages) ||
+                    !make_pool_tmap(&tv, v_pool, D, S, num_phys_pages))
+                    return PT_ERR_UNSUPPORTED;
+                StreamParams sp;
+                sp.q = q; sp.sel = sel; sp.n_sel = n_sel; sp.page_table = page_table;
+                sp.seq_len = seq_len; sp.bias = bias; sp.out = out; sp.lse = lse;
+                sp.ws = static_cast<float *>(workspace); sp.tickets = tickets;
+                sp.q_dtype = q_dtype; sp.sel_stride = sel_stride; sp.U = U; sp.G = G;
+                sp.Pmax = Pmax; sp.C = C; sp.CPU = CPU; sp.nstage = nstage; sp.scale = scale;
+                return launch_attend_stream(tk, tv, sp, D, S, grid, NW, smem,
+                                            (cudaStream_t)stream);
+            }
+        }
+    }
     if (!mma && (gp_of(G) < 0 || dpl_of(D) < 0 || (D * E) % 16 || D % dpl_of(D)))
         return PT_ERR_UNSUPPORTED;
     if (U == 0) return PT_OK;
     // warps per CTA and ring depth: keep >= 2 CTAs per SM where the page size allows
     const size_t stage = (size_t)2 * S * D * E;
     const int gpl = mma ? kMmaGP : gp_of(G);
-    auto smem_of = [&](int nw, int nst) {
+    const int kMaxPps = 512;  // bounds the per-warp page-id lists of the mma kernel
+    auto smem_of = [&](int nw, int nst, int pps_) {
         const size_t ring = (size_t)nw * nst * stage;
         const size_t merge = (size_t)nw * gpl * (D + 2) * 4;
-        const size_t hdr = mma ? attn_mma_hdr_bytes(nw, nst) : attn_hdr_bytes(nw, nst, gpl);
+        const size_t hdr = mma ? attn_mma_hdr_bytes(nw, nst, pps_) : attn_hdr_bytes(nw, nst, gpl);
         return hdr + (ring > merge ? ring : merge);
     };
     int NW = 4, nstage = 3;
-    while (smem_of(NW, nstage) > 110 * 1024 && nstage > 2) nstage--;
-    while (smem_of(NW, nstage) > 110 * 1024 && NW > 2) NW--;
-    while (smem_of(NW, nstage) > 220 * 1024 && NW > 1) NW--;
-    if (smem_of(NW, nstage) > 220 * 1024) return PT_ERR_UNSUPPORTED;
-    const size_t smem = smem_of(NW, nstage);
-    const int ctas_per_sm = smem <= 110 * 1024 ? 2 : 1;
+    while (smem_of(NW, nstage, kMaxPps) > 110 * 1024 && nstage > 2) nstage--;
+    while (smem_of(NW, nstage, kMaxPps) > 110 * 1024 && NW > 2) NW--;
+    while (smem_of(NW, nstage, kMaxPps) > 220 * 1024 && NW > 1) NW--;
+    if (smem_of(NW, nstage, kMaxPps) > 220 * 1024) return PT_ERR_UNSUPPORTED;
+    const int ctas_per_sm = smem_of(NW, nstage, kMaxPps) <= 110 * 1024 ? 2 : 1;
     if (nsplit <= 0) {
-        const int target = 148 * ctas_per_sm * 2;
+        // enough CTAs for ~4 waves of the resident slots
+        const int target = 148 * ctas_per_sm * 4;
         nsplit = (target + U - 1) / U;
     }
-    int max_useful = (sel_stride + NW - 1) / NW;
+    const int max_useful = (sel_stride + NW - 1) / NW;
     if (nsplit > max_useful) nsplit = max_useful;
     if (nsplit > kAttnMaxSplits) nsplit = kAttnMaxSplits;
+    const int min_split = (sel_stride + kMaxPps - 1) / kMaxPps;
+    if (nsplit < min_split) nsplit = min_split;
     if (nsplit < 1) nsplit = 1;
+    if (nsplit > kAttnMaxSplits) return PT_ERR_UNSUPPORTED;
     const int pps = (sel_stride + nsplit - 1) / nsplit;
     nsplit = (sel_stride + pps - 1) / pps;
+    const size_t smem = smem_of(NW, nstage, pps);
     if (nsplit > 1) {
         if (!workspace || !tickets ||
             workspace_bytes < pt_attend_workspace_bytes(U, G, D, sel_stride))

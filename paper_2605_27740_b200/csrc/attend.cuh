@@ -388,8 +388,10 @@ __device__ __forceinline__ uint32_t swz(int t, int chunk16, int S) {
 
 constexpr int kMmaGP = 8;  // heads padded to the MMA N
 
-__host__ __device__ __forceinline__ size_t attn_mma_hdr_bytes(int NW, int nstage) {
-    const size_t b = (size_t)NW * nstage * 8;
+// [mbarriers][per-warp page-id lists][pad to 1024][stage rings]
+__host__ __device__ __forceinline__ int attn_mma_maxc(int pps, int NW) { return (pps + NW - 1) / NW; }
+__host__ __device__ __forceinline__ size_t attn_mma_hdr_bytes(int NW, int nstage, int pps) {
+    const size_t b = (size_t)NW * nstage * 8 + (size_t)NW * attn_mma_maxc(pps, NW) * 4;
     return (b + 1023) & ~(size_t)1023;
 }
 
@@ -418,14 +420,19 @@ __global__ void __launch_bounds__(128) k_attend_mma(const __grid_constant__ CUte
     const int nstage = prm.nstage;
 
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem) + warp * nstage;
-    char *ring = smem + attn_mma_hdr_bytes(NW, nstage);
+    const int maxc = attn_mma_maxc(prm.pps, NW);
+    int32_t *my_pids = reinterpret_cast<int32_t *>(smem + (size_t)NW * nstage * 8) + warp * maxc;
+    char *ring = smem + attn_mma_hdr_bytes(NW, nstage, prm.pps);
     char *my_stages = ring + (size_t)warp * nstage * STAGE_BYTES;
     const int rem = last - first - warp;
     const int my_count = rem > 0 ? (rem + NW - 1) / NW : 0;
     const int32_t *selu = prm.sel + u * (int64_t)prm.sel_stride;
+    // this warp's page ids, fetched once (no dependent global load on the TMA issue path)
+    for (int i = lane; i < my_count; i += 32) my_pids[i] = selu[first + warp + i * NW];
+    __syncwarp();
 
     auto issue = [&](int i) {
-        const int pid = selu[first + warp + i * NW];
+        const int pid = my_pids[i];
         const int st = i % nstage;
         char *ks = my_stages + (size_t)st * STAGE_BYTES;
         mbar_arrive_expect_tx(&bars[st], STAGE_BYTES);
@@ -452,10 +459,11 @@ __global__ void __launch_bounds__(128) k_attend_mma(const __grid_constant__ CUte
         uint32_t b0 = 0, b1 = 0;
         if (gq < G) {
             const int64_t row = (u * G + gq) * (int64_t)D;
-            if (prm.q_dtype == PT_BF16) {
-                const uint16_t *qp = static_cast<const uint16_t *>(prm.q) + row;
-                b0 = (uint32_t)qp[d0] | ((uint32_t)qp[d0 + 1] << 16);
-                b1 = (uint32_t)qp[d0 + 8] | ((uint32_t)qp[d0 + 9] << 16);
+            if (prm.q_dtype == PT_BF16) {  // d0 is even: one 32-bit load per bf16 pair
+                const uint32_t *qp =
+                    reinterpret_cast<const uint32_t *>(static_cast<const uint16_t *>(prm.q) + row);
+                b0 = __ldg(qp + (d0 >> 1));
+                b1 = __ldg(qp + ((d0 + 8) >> 1));
             } else {
                 const float *qp = static_cast<const float *>(prm.q) + row;
                 b0 = pack_bf16(qp[d0], qp[d0 + 1]);
@@ -475,7 +483,7 @@ __global__ void __launch_bounds__(128) k_attend_mma(const __grid_constant__ CUte
     for (int i = 0; i < my_count; i++) {
         const int st = i % nstage;
         const int j = first + warp + i * NW;
-        const int pid = selu[j];
+        const int pid = my_pids[i];
         const int rows = (pid == tail_pid) ? tail_rows : S;
         const float b2 = prm.bias ? prm.bias[u * prm.sel_stride + j] * kLog2e : 0.f;
         mbar_wait(&bars[st], (uint32_t)((i / nstage) & 1));
@@ -557,6 +565,327 @@ __global__ void __launch_bounds__(128) k_attend_mma(const __grid_constant__ CUte
     }
     __syncthreads();
     cta_finish(prm, macc, mml, NW, kMmaGP, u, s, nsplit_u);
+}
+
+
+// ===========================================================================
+// Streaming variant of the tensor-core kernel (the sparse decode path).
+//
+// The short per-unit page lists of a sparse step (k = 128 pages) make per-CTA set-up and
+// merge costs dominate a grid of (split, unit) CTAs.  Here every warp of a persistent grid
+// owns a static list of chunks (C <= 32 consecutive selected pages of one unit; chunk c of
+// the warp = gw + t * W) and streams all their pages through ONE continuous TMA ring: the
+// producer lane runs `nstage` pages ahead across chunk boundaries, the page ids of the
+// current and next chunk sit in registers (one id per lane), q for the next unit is
+// fetched while the current chunk computes.  Each finished chunk writes its partial
+// (m, l, acc) -- or the final output when the unit has a single chunk -- and the last chunk
+// of a unit to finish (atomic ticket, self-resetting) merges the unit's partials.
+// ===========================================================================
+struct StreamParams {
+    const void *q;
+    const int32_t *sel;
+    const int32_t *n_sel;
+    const int32_t *page_table;
+    const int32_t *seq_len;
+    const float *bias;
+    float *out, *lse, *ws;
+    int32_t *tickets;
+    int q_dtype, sel_stride, U, G, Pmax, C, CPU, nstage;
+    float scale;
+};
+
+struct ChunkInfo {
+    int u, j, np;        // unit, chunk index in unit, pages in this chunk (0: none)
+    int nch;             // non-empty chunks of the unit
+    int tail_pid, tail_rows;
+    int pid;             // this lane's page id (lane < np)
+    float bias2;         // this lane's page bias (log2 domain)
+};
+
+template <int D, int MT>
+__device__ __forceinline__ ChunkInfo load_chunk(const StreamParams &p, int c, int lane) {
+    constexpr int S = 16 * MT;
+    ChunkInfo ci;
+    ci.u = c / p.CPU;
+    ci.j = c - ci.u * p.CPU;
+    const int ns = p.n_sel[ci.u];
+    ci.np = max(0, min(p.C, ns - ci.j * p.C));
+    ci.nch = (ns + p.C - 1) / p.C;
+    const int n = p.seq_len[ci.u];
+    const int P = (n + S - 1) / S;
+    ci.tail_pid = P > 0 ? p.page_table[(int64_t)ci.u * p.Pmax + P - 1] : -1;
+    ci.tail_rows = n - (P - 1) * S;
+    const int64_t off = (int64_t)ci.u * p.sel_stride + ci.j * p.C + lane;
+    ci.pid = lane < ci.np ? p.sel[off] : 0;
+    ci.bias2 = (p.bias && lane < ci.np) ? p.bias[off] * kLog2e : 0.f;
+    return ci;
+}
+
+template <int D>
+__device__ __forceinline__ void load_qfrag(const StreamParams &p, int u, int lane,
+                                           uint32_t (&qb)[D / 16][2]) {
+    const int gq = lane >> 2;
+#pragma unroll
+    for (int ks = 0; ks < D / 16; ks++) {
+        const int d0 = ks * 16 + 2 * (lane & 3);
+        uint32_t b0 = 0, b1 = 0;
+        if (gq < p.G) {
+            const int64_t row = ((int64_t)u * p.G + gq) * D;
+            if (p.q_dtype == PT_BF16) {
+                const uint32_t *qp =
+                    reinterpret_cast<const uint32_t *>(static_cast<const uint16_t *>(p.q) + row);
+                b0 = __ldg(qp + (d0 >> 1));
+                b1 = __ldg(qp + ((d0 + 8) >> 1));
+            } else {
+                const float *qp = static_cast<const float *>(p.q) + row;
+                b0 = pack_bf16(qp[d0], qp[d0 + 1]);
+                b1 = pack_bf16(qp[d0 + 8], qp[d0 + 9]);
+            }
+        }
+        qb[ks][0] = b0;
+        qb[ks][1] = b1;
+    }
+}
+
+// One staged page through QK -> online softmax -> PV (the k_attend_mma inner loop).
+template <int D, int MT>
+__device__ __forceinline__ void mma_page(uint32_t kbase, uint32_t vbase, int rows, float b2,
+                                         float qscale, const uint32_t (&qb)[D / 16][2],
+                                         float (&acc)[D / 16][4], float (&m_run)[2],
+                                         float (&l_run)[2], int lane) {
+    constexpr int S = 16 * MT;
+    constexpr int KS = D / 16;
+    const int r8 = lane & 7, mat = lane >> 3;
+#pragma unroll
+    for (int mt = 0; mt < MT; mt++) {
+        if (mt * 16 >= rows) break;
+        float sc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int ks = 0; ks < KS; ks++) {
+            uint32_t a[4];
+            const int t = mt * 16 + r8 + ((mat & 1) << 3);
+            ldsm_x4(kbase + swz(t, ks * 2 + (mat >> 1), S), a);
+            mma_bf16(sc, a, qb[ks][0], qb[ks][1]);
+        }
+        const int t0 = mt * 16 + (lane >> 2);
+        const bool v0 = t0 < rows, v1 = t0 + 8 < rows;
+        sc[0] = v0 ? fmaf(sc[0], qscale, b2) : -INFINITY;
+        sc[1] = v0 ? fmaf(sc[1], qscale, b2) : -INFINITY;
+        sc[2] = v1 ? fmaf(sc[2], qscale, b2) : -INFINITY;
+        sc[3] = v1 ? fmaf(sc[3], qscale, b2) : -INFINITY;
+        float p[4], carry[2];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            float mx = fmaxf(sc[h], sc[h + 2]);
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+            const float m_new = fmaxf(m_run[h], mx);
+            carry[h] = exp2f(m_run[h] - m_new);
+            p[h] = exp2f(sc[h] - m_new);
+            p[h + 2] = exp2f(sc[h + 2] - m_new);
+            float ls = p[h] + p[h + 2];
+            ls += __shfl_xor_sync(0xffffffffu, ls, 4);
+            ls += __shfl_xor_sync(0xffffffffu, ls, 8);
+            ls += __shfl_xor_sync(0xffffffffu, ls, 16);
+            l_run[h] = l_run[h] * carry[h] + ls;
+            m_run[h] = m_new;
+        }
+        const uint32_t pb0 = movm_t(pack_bf16(p[0], p[1]));
+        const uint32_t pb1 = movm_t(pack_bf16(p[2], p[3]));
+#pragma unroll
+        for (int dm = 0; dm < KS; dm++) {
+            acc[dm][0] *= carry[0];
+            acc[dm][1] *= carry[1];
+            acc[dm][2] *= carry[0];
+            acc[dm][3] *= carry[1];
+            uint32_t a[4];
+            const int t = mt * 16 + r8 + ((mat >> 1) << 3);
+            ldsm_x4_t(vbase + swz(t, dm * 2 + (mat & 1), S), a);
+            mma_bf16(acc[dm], a, pb0, pb1);
+        }
+    }
+}
+
+__host__ __device__ __forceinline__ size_t attn_stream_smem(int NW, int nstage, int stage_bytes) {
+    return 1024 + (size_t)NW * nstage * stage_bytes;  // [mbarriers | pad][rings]
+}
+
+template <int D, int MT>
+__global__ void __launch_bounds__(128) k_attend_stream(const __grid_constant__ CUtensorMap tmk,
+                                                       const __grid_constant__ CUtensorMap tmv,
+                                                       const StreamParams prm) {
+    constexpr int S = 16 * MT;
+    constexpr int KS = D / 16;
+    constexpr uint32_t PAGE_BYTES = S * D * 2;
+    constexpr uint32_t STAGE_BYTES = 2 * PAGE_BYTES;
+    extern __shared__ __align__(1024) char smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
+    const int nstage = prm.nstage;
+    const int W = gridDim.x * NW;
+    const int gw = blockIdx.x * NW + warp;
+    const int total = prm.U * prm.CPU;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem) + warp * nstage;
+    char *my_stages = smem + 1024 + (size_t)warp * nstage * STAGE_BYTES;
+    if (lane == 0) {
+        for (int i = 0; i < nstage; i++) mbar_init(&bars[i], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+
+    // chunk cursor helpers: the warp's chunks are gw, gw + W, ...; skip empty ones
+    auto next_nonempty = [&](int c) -> int {
+        while (c < total) {
+            const int u = c / prm.CPU, j = c - u * prm.CPU;
+            if (j * prm.C < prm.n_sel[u]) return c;
+            c += W;
+        }
+        return total;
+    };
+    int c_cur = next_nonempty(gw);
+    if (c_cur >= total) return;
+    int c_nxt = next_nonempty(c_cur + W);
+    ChunkInfo cur = load_chunk<D, MT>(prm, c_cur, lane);
+    ChunkInfo nxt;
+    if (c_nxt < total) nxt = load_chunk<D, MT>(prm, c_nxt, lane);
+    else nxt.np = 0;
+
+    // producer: page index within the stream; (which, off) = chunk (0 cur / 1 nxt) + page
+    int prod_i = 0;          // pages issued so far (ring position)
+    int prod_off = 0;        // page offset inside the producer's chunk
+    int prod_which = 0;      // 0: producer is in `cur`, 1: in `nxt`
+    auto produce = [&](int limit_i) {
+        // issue pages while the ring has room (prod_i < limit_i) and pages remain in cur/nxt
+        while (prod_i < limit_i) {
+            const ChunkInfo &pc = prod_which == 0 ? cur : nxt;
+            if (prod_off >= pc.np) {
+                if (prod_which == 0 && nxt.np > 0) { prod_which = 1; prod_off = 0; continue; }
+                break;
+            }
+            const int pid = __shfl_sync(0xffffffffu, pc.pid, prod_off);
+            if (lane == 0) {
+                const int st = prod_i % nstage;
+                char *ks = my_stages + (size_t)st * STAGE_BYTES;
+                mbar_arrive_expect_tx(&bars[st], STAGE_BYTES);
+#pragma unroll
+                for (int b = 0; b < D / 64; b++) {
+                    tma_load_2d(ks + b * S * 128, &tmk, b * 64, pid * S, &bars[st]);
+                    tma_load_2d(ks + PAGE_BYTES + b * S * 128, &tmv, b * 64, pid * S, &bars[st]);
+                }
+            }
+            prod_i++;
+            prod_off++;
+        }
+    };
+
+    uint32_t qb[KS][2];
+    load_qfrag<D>(prm, cur.u, lane, qb);
+    const float qscale = prm.scale * kLog2e;
+    int cons_i = 0;
+    produce(nstage);
+
+    float *wacc = prm.ws;                                               // [U*CPU][G][D]
+    float *wml = prm.ws + (size_t)prm.U * prm.CPU * prm.G * D;          // [U*CPU][G][2]
+    __shared__ int last_flag[4];
+    const int g0 = 2 * (lane & 3);
+    while (true) {
+        float acc[KS][4];
+#pragma unroll
+        for (int i = 0; i < KS; i++) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+        float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};
+        for (int pg = 0; pg < cur.np; pg++) {
+            const int st = cons_i % nstage;
+            const int pid = __shfl_sync(0xffffffffu, cur.pid, pg);
+            const float b2 = __shfl_sync(0xffffffffu, cur.bias2, pg);
+            const int rows = (pid == cur.tail_pid) ? cur.tail_rows : S;
+            mbar_wait(&bars[st], (uint32_t)((cons_i / nstage) & 1));
+            const uint32_t kbase = smem_u32(my_stages + (size_t)st * STAGE_BYTES);
+            mma_page<D, MT>(kbase, kbase + PAGE_BYTES, rows, b2, qscale, qb, acc, m_run, l_run, lane);
+            __syncwarp();
+            cons_i++;
+            produce(cons_i + nstage);
+        }
+        // ---- chunk epilogue: final output (single-chunk unit) or partial + ticket ----
+        const int u = cur.u;
+        if (cur.nch == 1) {
+            const float inv0 = 1.f / l_run[0], inv1 = 1.f / l_run[1];
+#pragma unroll
+            for (int dm = 0; dm < KS; dm++) {
+                const int d = dm * 16 + (lane >> 2);
+                if (g0 < prm.G) {
+                    prm.out[((int64_t)u * prm.G + g0) * D + d] = acc[dm][0] * inv0;
+                    prm.out[((int64_t)u * prm.G + g0) * D + d + 8] = acc[dm][2] * inv0;
+                }
+                if (g0 + 1 < prm.G) {
+                    prm.out[((int64_t)u * prm.G + g0 + 1) * D + d] = acc[dm][1] * inv1;
+                    prm.out[((int64_t)u * prm.G + g0 + 1) * D + d + 8] = acc[dm][3] * inv1;
+                }
+            }
+            if (lane < 4) {
+                if (g0 < prm.G) prm.lse[u * prm.G + g0] = (m_run[0] + log2f(l_run[0])) * kLn2;
+                if (g0 + 1 < prm.G) prm.lse[u * prm.G + g0 + 1] = (m_run[1] + log2f(l_run[1])) * kLn2;
+            }
+        } else {
+            const int64_t slot = (int64_t)u * prm.CPU + cur.j;
+#pragma unroll
+            for (int dm = 0; dm < KS; dm++) {
+                const int d = dm * 16 + (lane >> 2);
+                if (g0 < prm.G) {
+                    wacc[(slot * prm.G + g0) * D + d] = acc[dm][0];
+                    wacc[(slot * prm.G + g0) * D + d + 8] = acc[dm][2];
+                }
+                if (g0 + 1 < prm.G) {
+                    wacc[(slot * prm.G + g0 + 1) * D + d] = acc[dm][1];
+                    wacc[(slot * prm.G + g0 + 1) * D + d + 8] = acc[dm][3];
+                }
+            }
+            if (lane < 4) {
+                if (g0 < prm.G) {
+                    wml[(slot * prm.G + g0) * 2] = m_run[0];
+                    wml[(slot * prm.G + g0) * 2 + 1] = l_run[0];
+                }
+                if (g0 + 1 < prm.G) {
+                    wml[(slot * prm.G + g0 + 1) * 2] = m_run[1];
+                    wml[(slot * prm.G + g0 + 1) * 2 + 1] = l_run[1];
+                }
+            }
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence();
+                last_flag[warp] = (atomicAdd(&prm.tickets[u], 1) == cur.nch - 1);
+            }
+            __syncwarp();
+            if (last_flag[warp]) {
+                __threadfence();
+                for (int i = lane; i < prm.G * D; i += 32) {
+                    const int g = i / D, d = i - g * D;
+                    float mt = -INFINITY;
+                    for (int w = 0; w < cur.nch; w++)
+                        mt = fmaxf(mt, __ldcg(&wml[(((int64_t)u * prm.CPU + w) * prm.G + g) * 2]));
+                    float lt = 0.f, a = 0.f;
+                    for (int w = 0; w < cur.nch; w++) {
+                        const int64_t sl = ((int64_t)u * prm.CPU + w) * prm.G + g;
+                        const float f = exp2f(__ldcg(&wml[sl * 2]) - mt);
+                        lt += __ldcg(&wml[sl * 2 + 1]) * f;
+                        a += __ldcg(&wacc[sl * D + d]) * f;
+                    }
+                    prm.out[((int64_t)u * prm.G + g) * D + d] = a / lt;
+                    if (d == 0) prm.lse[u * prm.G + g] = (mt + log2f(lt)) * kLn2;
+                }
+                if (lane == 0) prm.tickets[u] = 0;
+            }
+        }
+        // ---- advance: nxt becomes cur; fetch the following chunk ----
+        if (nxt.np == 0) break;
+        const int prev_u = cur.u;
+        cur = nxt;
+        prod_which = 0;  // the producer's chunk `nxt` is now `cur` (prod_off already counts it)
+        c_nxt = next_nonempty(c_nxt + W);
+        if (c_nxt < total) nxt = load_chunk<D, MT>(prm, c_nxt, lane);
+        else nxt.np = 0;
+        if (cur.u != prev_u) load_qfrag<D>(prm, cur.u, lane, qb);
+        produce(cons_i + nstage);
+    }
 }
 
 }  // namespace pt

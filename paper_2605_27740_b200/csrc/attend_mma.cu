@@ -30,4 +30,29 @@ int launch_attend_mma(const CUtensorMap &tk, const CUtensorMap &tv, const AttnPa
     return PT_ERR_UNSUPPORTED;
 }
 
+template <int D, int MT>
+static int launch_stream_one(const CUtensorMap &tk, const CUtensorMap &tv, const StreamParams &p,
+                             int grid, int NW, size_t smem, cudaStream_t st) {
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+        PT_CUDA_TRY(cudaFuncSetAttribute(k_attend_stream<D, MT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured = smem;
+    }
+    k_attend_stream<D, MT><<<grid, NW * 32, smem, st>>>(tk, tv, p);
+    PT_CUDA_TRY(cudaGetLastError());
+    return PT_OK;
+}
+
+int launch_attend_stream(const CUtensorMap &tk, const CUtensorMap &tv, const StreamParams &p,
+                         int D, int S, int grid, int NW, size_t smem, cudaStream_t st) {
+#define PT_STR(D_, MT_) \
+    if (D == D_ && S == 16 * MT_) return launch_stream_one<D_, MT_>(tk, tv, p, grid, NW, smem, st);
+    PT_STR(64, 1) PT_STR(64, 2) PT_STR(64, 4)
+    PT_STR(128, 1) PT_STR(128, 2) PT_STR(128, 4)
+    PT_STR(256, 1) PT_STR(256, 2) PT_STR(256, 4)
+#undef PT_STR
+    return PT_ERR_UNSUPPORTED;
+}
+
 }  // namespace pt

@@ -14,12 +14,13 @@
 //
 // Memory layout: the page-interleaved tile layout of the means (common.cuh) makes each
 // warp-wide step one contiguous 512-byte, 128-bit-per-lane load with lane = page.
-#include "common.cuh"
+#include <stdlib.h>
+
+#include "select.cuh"
 
 namespace pt {
 
-constexpr int kScoreThreads = 256;
-constexpr int kScoreMaxD = 512;
+constexpr int kScoreMaxD = 256;
 
 template <int SDT>
 struct MeanVec;
@@ -43,30 +44,83 @@ struct MeanVec<PT_BF16> {
 
 // Q products are exact in f32 when both factors are bf16 values (8-bit significands):
 // then fma(q, m, acc) == fl(acc + q*m) and one FFMA replaces FMUL+FADD.
+//
+// Memory pipeline: a CTA owns TILES page tiles (32 pages each) of one unit.  At entry one
+// thread issues every byte the CTA will read as 1-D bulk copies (cp.async.bulk, SASS
+// UBLKCP) -- the tile layout makes each (tile, d-range) a single contiguous block --
+// split into NST d-range stages with one mbarrier each, so compute on the first dims
+// starts while the rest is in flight (64 KB in flight per CTA, 3 CTAs per SM).  Threads
+// then read their page's 16-byte chunks from shared memory (lane-contiguous, no bank
+// conflicts) in the reference's sequential d order.
+constexpr int kScoreStages = 4;
+
+struct ScoreParams {
+    const void *q;
+    const float *norms_in;
+    const void *means;
+    const float *stds;
+    const int32_t *seq_len;
+    uint16_t *keys;
+    float *scores;
+    // fused selection (counters == nullptr: scoring only)
+    int32_t *counters;
+    const int32_t *page_table;
+    int32_t *sel, *sel_logical, *n_sel, *kth, *kplus1;
+    int D, S, Pmax, k;
+    float lam;
+};
+
+constexpr int kFusedThreads = 128;  // the fused selection runs with the 4-tile CTA
+
 template <int QDT, int SDT, int G>
-__global__ void __launch_bounds__(kScoreThreads)
-    k_score(const void *__restrict__ q, const float *__restrict__ norms_in,
-            const void *__restrict__ means, const float *__restrict__ stds,
-            const int32_t *__restrict__ seq_len, int D, int S, int Pmax, float lam,
-            uint16_t *__restrict__ keys, float *__restrict__ scores) {
+__global__ void __launch_bounds__(128) k_score(const ScoreParams prm) {
+    const void *__restrict__ q = prm.q;
+    const float *__restrict__ norms_in = prm.norms_in;
+    const void *__restrict__ means = prm.means;
+    const float *__restrict__ stds = prm.stds;
+    const int D = prm.D, S = prm.S, Pmax = prm.Pmax;
+    const float lam = prm.lam;
+    uint16_t *__restrict__ keys = prm.keys;
+    float *__restrict__ scores = prm.scores;
     constexpr int V = MeanVec<SDT>::V;
+    constexpr int ES = SDT == PT_F32 ? 4 : 2;
     constexpr bool kExactProduct = (QDT == PT_BF16 && SDT == PT_BF16);
+    extern __shared__ __align__(128) char tiles[];
     __shared__ __align__(16) float qs[G][kScoreMaxD];
     __shared__ float lam_norm[G];
+    __shared__ uint64_t bars[kScoreStages];
     const int64_t u = blockIdx.y;
     const int tid = threadIdx.x;
-    const int n = seq_len[u];
+    const int TILES = blockDim.x >> 5;
+    const int n = prm.seq_len[u];
     const int P = (n + S - 1) / S;
-    const int64_t p0 = (int64_t)blockIdx.x * kScoreThreads;
+    const int64_t p0 = (int64_t)blockIdx.x * blockDim.x;
     if (p0 >= P) return;
-
-    for (int i = tid; i < G * D; i += kScoreThreads) {
+    const int nch = D / V;                                   // 16-byte chunks per page row
+    const int cps = (nch + kScoreStages - 1) / kScoreStages; // chunks per stage
+    const int nst = (nch + cps - 1) / cps;
+    const int tile_bytes = 32 * D * ES;
+    const int ntiles = min(TILES, (int)((P - p0 + 31) >> 5));
+    const char *gbase = static_cast<const char *>(means) +
+                        (u * Pmax * D + (p0 >> 5) * 32 * (int64_t)D) * ES;
+    if (tid == 0) {  // first thing: put every byte of this CTA in flight
+        for (int st = 0; st < nst; st++) mbar_init(&bars[st], 1);
+        fence_mbar_init();
+        for (int st = 0; st < nst; st++) {
+            const int c0 = st * cps, c1 = min(nch, c0 + cps);
+            const uint32_t bytes = (uint32_t)(c1 - c0) * 512;
+            mbar_arrive_expect_tx(&bars[st], bytes * ntiles);
+            for (int t = 0; t < ntiles; t++)
+                bulk_g2s(tiles + t * tile_bytes + c0 * 512, gbase + (int64_t)t * tile_bytes + c0 * 512,
+                         bytes, &bars[st]);
+        }
+    }
+    for (int i = tid; i < G * D; i += blockDim.x) {
         const int g = i / D, d = i % D;
-        const float v = load_elem<QDT>(q, (u * G + g) * (int64_t)D + d);
-        qs[g][d] = v;
+        qs[g][d] = load_elem<QDT>(q, (u * G + g) * (int64_t)D + d);
     }
     __syncthreads();
-    if (tid < G) {
+    if (tid < G) {  // overlaps the copies in flight
         const float nrm = norms_in ? norms_in[u * G + tid]
                                    : __double2float_rn(__dsqrt_rn(np_sum(SquaresOfF32{qs[tid]}, D)));
         lam_norm[tid] = __fmul_rn(lam, nrm);
@@ -74,38 +128,262 @@ __global__ void __launch_bounds__(kScoreThreads)
     __syncthreads();
 
     const int64_t p = p0 + tid;
-    if (p >= P) return;
-    const char *mp = static_cast<const char *>(means) +
-                     ((u * Pmax * D + (p >> 5) * 32 * (int64_t)D + (p & 31) * V) *
-                      (SDT == PT_F32 ? 4 : 2));
-    const int64_t chunk_stride = 32 * V * (SDT == PT_F32 ? 4 : 2);  // bytes between d-chunks
+    const bool live = p < P;
+    const char *mp = tiles + (tid >> 5) * tile_bytes + (tid & 31) * 16;
     float acc[G];
 #pragma unroll
     for (int g = 0; g < G; g++) acc[g] = 0.0f;
-    const int nchunk = D / V;
-#pragma unroll 8
-    for (int c = 0; c < nchunk; c++) {
-        float m[V];
-        MeanVec<SDT>::load(mp + c * chunk_stride, m);
+    for (int st = 0; st < nst; st++) {
+        mbar_wait(&bars[st], 0);  // every thread waits: no copy outlives the CTA
+        if (!live) continue;
+        const int c0 = st * cps, c1 = min(nch, c0 + cps);
+#pragma unroll 4
+        for (int c = c0; c < c1; c++) {
+            float m[V];
+            if constexpr (SDT == PT_F32) {
+                const float4 v = *reinterpret_cast<const float4 *>(mp + c * 512);
+                m[0] = v.x; m[1] = v.y; m[2] = v.z; m[3] = v.w;
+            } else {
+                const uint4 v = *reinterpret_cast<const uint4 *>(mp + c * 512);
+                m[0] = bf16_lo(v.x); m[1] = bf16_hi(v.x); m[2] = bf16_lo(v.y); m[3] = bf16_hi(v.y);
+                m[4] = bf16_lo(v.z); m[5] = bf16_hi(v.z); m[6] = bf16_lo(v.w); m[7] = bf16_hi(v.w);
+            }
 #pragma unroll
-        for (int j = 0; j < V; j++) {
-            const int d = c * V + j;
+            for (int j = 0; j < V; j++) {
+                const int d = c * V + j;
 #pragma unroll
-            for (int g = 0; g < G; g++) {
-                if constexpr (kExactProduct) acc[g] = __fmaf_rn(qs[g][d], m[j], acc[g]);
-                else acc[g] = __fadd_rn(acc[g], __fmul_rn(qs[g][d], m[j]));
+                for (int g = 0; g < G; g++) {
+                    if constexpr (kExactProduct) acc[g] = __fmaf_rn(qs[g][d], m[j], acc[g]);
+                    else acc[g] = __fadd_rn(acc[g], __fmul_rn(qs[g][d], m[j]));
+                }
             }
         }
     }
-    const float sd = stds[u * Pmax + p];
-    float best = -INFINITY;
+    if (live) {
+        const float sd = stds[u * Pmax + p];
+        float best = -INFINITY;
 #pragma unroll
-    for (int g = 0; g < G; g++) {
-        const float a = __fadd_rn(acc[g], __fmul_rn(lam_norm[g], sd));
-        if (a > best) best = a;
+        for (int g = 0; g < G; g++) {
+            const float a = __fadd_rn(acc[g], __fmul_rn(lam_norm[g], sd));
+            if (a > best) best = a;
+        }
+        keys[u * Pmax + p] = encode_ordered(f32_to_bf16_rne(best));
+        if (scores) scores[u * Pmax + p] = best;
     }
-    keys[u * Pmax + p] = encode_ordered(f32_to_bf16_rne(best));
-    if (scores) scores[u * Pmax + p] = best;
+    if (prm.counters == nullptr) return;
+
+    // ---- fused selection: the last CTA to finish scoring unit u selects its top-k ----
+    // (select.py:87-115 via select.cuh) while other CTAs keep streaming other units.
+    __shared__ int is_last;
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        const int nblk = (P + blockDim.x - 1) / blockDim.x;
+        is_last = (atomicAdd(&prm.counters[u], 1) == nblk - 1);
+    }
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    if (tid == 0) prm.counters[u] = 0;  // self-resetting for graph replay
+    uint16_t *sk = reinterpret_cast<uint16_t *>(tiles);  // page tiles are consumed: reuse
+    const uint4 *src = reinterpret_cast<const uint4 *>(keys + u * (int64_t)Pmax);
+    for (int i = tid; i < (P + 7) / 8; i += blockDim.x)
+        reinterpret_cast<uint4 *>(sk)[i] = __ldcg(src + i);
+    __syncthreads();
+    __shared__ SelectShared<kFusedThreads> ssh;
+    const int k = prm.k;
+    select_block<kFusedThreads>(sk, P, k, prm.page_table + u * Pmax, prm.sel + u * (int64_t)k,
+                                prm.sel_logical ? prm.sel_logical + u * (int64_t)k : nullptr,
+                                prm.n_sel + u, prm.kth + u, prm.kplus1 + u, ssh);
+}
+
+
+// ===========================================================================
+// Streaming scoring kernel (default path).
+//
+// A persistent grid of warps; warp gw scores the 32-page tiles T = gw, gw + W, ... of the
+// unit-major tile space (so units complete progressively).  Each warp streams its tiles
+// through its own ring of NST shared-memory stages; one stage holds, for one tile:
+//   [32 pages x D means (tile layout: 16-byte chunk c of page l at c*512 + l*16)]
+//   [the unit's G query rows][lam*||q_g|| padded to 8][the 32 page stds]
+// all filled by 1-D bulk copies (cp.async.bulk -> UBLKCP) on one mbarrier, issued by lane 0
+// NST tiles ahead.  Lane l = page l of the tile walks its mean vector in the reference's
+// sequential d order (bit-identical scores).  No per-tile prologue: the q rows, norms and
+// stds ride along with the tile, and the per-unit page counts sit in shared memory.
+// ===========================================================================
+struct StreamScoreParams {
+    const void *q;
+    const float *lamnorm;   // [U][8]: fl(lam * norm_g), padded
+    const void *means;
+    const float *stds;
+    const int32_t *seq_len;
+    uint16_t *keys;
+    float *scores;
+    int U, D, S, Pmax, nst;
+};
+
+__host__ __device__ __forceinline__ int score_stage_bytes(int D, int es, int G, int qes) {
+    const int tile = 32 * D * es;
+    const int qb = (G * D * qes + 15) & ~15;
+    return (tile + qb + 32 + 128 + 127) & ~127;
+}
+
+template <int QDT, int SDT, int G>
+__global__ void __launch_bounds__(128, 1) k_score_stream(const StreamScoreParams prm) {
+    constexpr int V = MeanVec<SDT>::V;
+    constexpr int ES = SDT == PT_F32 ? 4 : 2;
+    constexpr int QES = QDT == PT_F32 ? 4 : 2;
+    constexpr bool kExactProduct = (QDT == PT_BF16 && SDT == PT_BF16);
+    extern __shared__ __align__(128) char smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
+    const int D = prm.D, S = prm.S, Pmax = prm.Pmax, U = prm.U, NST = prm.nst;
+    const int TPU = Pmax >> 5;
+    const long long total = (long long)U * TPU;
+    const int W = gridDim.x * NW;
+    const int gw = blockIdx.x * NW + warp;
+    const int tile_bytes = 32 * D * ES;
+    const int q_bytes = G * D * QES;
+    const int q_off = tile_bytes, ln_off = tile_bytes + ((q_bytes + 15) & ~15);
+    const int sd_off = ln_off + 32;
+    const int stage_bytes = score_stage_bytes(D, ES, G, QES);
+    int *Ps = reinterpret_cast<int *>(smem);                               // [U] pages per unit
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + ((U * 4 + 15) & ~15)) + warp * NST;
+    const size_t hdr = (((size_t)U * 4 + 15) & ~15) + (size_t)NW * NST * 8;
+    char *ring = smem + ((hdr + 127) & ~(size_t)127) + (size_t)warp * NST * stage_bytes;
+    for (int i = threadIdx.x; i < U; i += blockDim.x) Ps[i] = (prm.seq_len[i] + S - 1) / S;
+    if (lane == 0) {
+        for (int i = 0; i < NST; i++) mbar_init(&bars[i], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    auto next_tile = [&](long long T) -> long long {
+        while (T < total) {
+            const int u = (int)(T / TPU), t = (int)(T - (long long)u * TPU);
+            if (t * 32 < Ps[u]) return T;
+            T += W;
+        }
+        return total;
+    };
+    auto issue = [&](long long T, int slot) {  // lane 0 only
+        const int u = (int)(T / TPU), t = (int)(T - (long long)u * TPU);
+        char *st = ring + (size_t)slot * stage_bytes;
+        const uint32_t qcopy = (uint32_t)((q_bytes + 15) & ~15);
+        mbar_arrive_expect_tx(&bars[slot], (uint32_t)tile_bytes + qcopy + 32 + 128);
+        bulk_g2s(st, static_cast<const char *>(prm.means) + ((int64_t)u * Pmax + (int64_t)t * 32) * D * ES,
+                 (uint32_t)tile_bytes, &bars[slot]);
+        bulk_g2s(st + q_off, static_cast<const char *>(prm.q) + (int64_t)u * q_bytes, qcopy, &bars[slot]);
+        bulk_g2s(st + ln_off, prm.lamnorm + (int64_t)u * 8, 32, &bars[slot]);
+        bulk_g2s(st + sd_off, prm.stds + (int64_t)u * Pmax + t * 32, 128, &bars[slot]);
+    };
+
+    long long Tp = next_tile(gw);  // producer cursor
+    long long Tc = Tp;             // consumer cursor
+    int issued = 0;
+    if (lane == 0) {
+        for (int i = 0; i < NST && Tp < total; i++) {
+            issue(Tp, i);
+            issued++;
+            Tp = next_tile(Tp + W);
+        }
+    }
+    issued = __shfl_sync(0xffffffffu, issued, 0);
+    Tp = __shfl_sync(0xffffffffu, Tp, 0);
+    int consumed = 0;
+    while (Tc < total) {
+        const int slot = consumed % NST;
+        const int u = (int)(Tc / TPU), t = (int)(Tc - (long long)u * TPU);
+        mbar_wait(&bars[slot], (uint32_t)((consumed / NST) & 1));
+        const char *st = ring + (size_t)slot * stage_bytes;
+        const char *mp = st + lane * 16;
+        const char *qp = st + q_off;
+        const float *ln = reinterpret_cast<const float *>(st + ln_off);
+        float acc[G];
+#pragma unroll
+        for (int g = 0; g < G; g++) acc[g] = 0.0f;
+        const int nch = D / V;
+#pragma unroll 2
+        for (int c = 0; c < nch; c++) {
+            float m[V];
+            if constexpr (SDT == PT_F32) {
+                const float4 v = *reinterpret_cast<const float4 *>(mp + c * 512);
+                m[0] = v.x; m[1] = v.y; m[2] = v.z; m[3] = v.w;
+            } else {
+                const uint4 v = *reinterpret_cast<const uint4 *>(mp + c * 512);
+                m[0] = bf16_lo(v.x); m[1] = bf16_hi(v.x); m[2] = bf16_lo(v.y); m[3] = bf16_hi(v.y);
+                m[4] = bf16_lo(v.z); m[5] = bf16_hi(v.z); m[6] = bf16_lo(v.w); m[7] = bf16_hi(v.w);
+            }
+#pragma unroll
+            for (int g = 0; g < G; g++) {
+                float qv[V];
+                if constexpr (QDT == PT_F32) {
+#pragma unroll
+                    for (int j = 0; j < V; j += 4) {
+                        const float4 w = *reinterpret_cast<const float4 *>(qp + (g * D + c * V + j) * 4);
+                        qv[j] = w.x; qv[j + 1] = w.y; qv[j + 2] = w.z; qv[j + 3] = w.w;
+                    }
+                } else {
+                    if constexpr (V == 4) {
+                        const uint2 w = *reinterpret_cast<const uint2 *>(qp + (g * D + c * V) * 2);
+                        qv[0] = bf16_lo(w.x); qv[1] = bf16_hi(w.x); qv[2] = bf16_lo(w.y); qv[3] = bf16_hi(w.y);
+                    } else {
+                        const uint4 w = *reinterpret_cast<const uint4 *>(qp + (g * D + c * V) * 2);
+                        qv[0] = bf16_lo(w.x); qv[1] = bf16_hi(w.x); qv[2] = bf16_lo(w.y); qv[3] = bf16_hi(w.y);
+                        qv[4] = bf16_lo(w.z); qv[5] = bf16_hi(w.z); qv[6] = bf16_lo(w.w); qv[7] = bf16_hi(w.w);
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < V; j++) {
+                    if constexpr (kExactProduct) acc[g] = __fmaf_rn(qv[j], m[j], acc[g]);
+                    else acc[g] = __fadd_rn(acc[g], __fmul_rn(qv[j], m[j]));
+                }
+            }
+        }
+        const float sd = reinterpret_cast<const float *>(st + sd_off)[lane];
+        float best = -INFINITY;
+#pragma unroll
+        for (int g = 0; g < G; g++) {
+            const float a = __fadd_rn(acc[g], __fmul_rn(ln[g], sd));
+            if (a > best) best = a;
+        }
+        const int p = t * 32 + lane;
+        if (p < Ps[u]) {
+            prm.keys[(int64_t)u * Pmax + p] = encode_ordered(f32_to_bf16_rne(best));
+            if (prm.scores) prm.scores[(int64_t)u * Pmax + p] = best;
+        }
+        __syncwarp();  // every lane is done with this stage
+        consumed++;
+        if (lane == 0 && Tp < total) {
+            issue(Tp, slot);
+            Tp = next_tile(Tp + W);
+        }
+        Tp = __shfl_sync(0xffffffffu, Tp, 0);
+        Tc = next_tile(Tc + W);
+    }
+}
+
+// lam * ||q_g|| for every (unit, g), numpy's float64 order (scoring.py:45), padded to 8
+template <int QDT>
+__global__ void k_lam_norms(const void *__restrict__ q, const float *__restrict__ norms_in,
+                            int rows, int G, int D, float lam, float *__restrict__ out) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    float nrm;
+    if (norms_in) {
+        nrm = norms_in[r];
+    } else {
+        struct Sq {
+            const void *q;
+            int64_t base;
+            __device__ double operator()(int i) const {
+                const double v = (double)load_elem<QDT>(q, base + i);
+                return __dmul_rn(v, v);
+            }
+        } sq{q, (int64_t)r * D};
+        nrm = __double2float_rn(__dsqrt_rn(np_sum(sq, D)));
+    }
+    const int u = r / G, g = r - u * G;
+    out[(int64_t)u * 8 + g] = __fmul_rn(lam, nrm);
 }
 
 // row-major f32 means [U][P][D] -> tiled stats layout (stats dtype)
@@ -128,16 +406,34 @@ __global__ void k_tile_means(const float *__restrict__ src, int U, int P, int D,
 
 using namespace pt;
 
+// tiles per CTA: 64 KB of page means per CTA (3 CTAs per SM)
+static int score_tiles(int D, int es) {
+    const int tile = 32 * D * es;
+    int t = 65536 / tile;
+    return t < 1 ? 1 : (t > 4 ? 4 : t);
+}
+
 template <int QDT, int SDT>
-static int launch_score(const void *q, const float *norms, const void *means, const float *stds,
-                        const int32_t *seq_len, int U, int G, int D, int S, int Pmax, float lam,
-                        uint16_t *keys, float *scores, cudaStream_t st) {
-    dim3 grid((Pmax + kScoreThreads - 1) / kScoreThreads, U);
+static int launch_score(ScoreParams prm, int U, int G, cudaStream_t st) {
+    const int es = SDT == PT_F32 ? 4 : 2;
+    const int tiles = score_tiles(prm.D, es);
+    const int threads = 32 * tiles;
+    const size_t smem = (size_t)tiles * 32 * prm.D * es;
+    if (prm.counters && (threads != kFusedThreads || (size_t)(prm.Pmax + 8) * 2 > smem))
+        return PT_ERR_UNSUPPORTED;  // caller falls back to pt_score + pt_topk
+    dim3 grid((prm.Pmax + threads - 1) / threads, U);
 #define PT_SCORE_CASE(G_)                                                                      \
-    case G_:                                                                                   \
-        k_score<QDT, SDT, G_><<<grid, kScoreThreads, 0, st>>>(q, norms, means, stds, seq_len, D, \
-                                                              S, Pmax, lam, keys, scores);     \
-        break;
+    case G_: {                                                                                 \
+        static size_t configured = 0;                                                          \
+        if (smem > 48 * 1024 && smem > configured) {                                           \
+            PT_CUDA_TRY(cudaFuncSetAttribute(k_score<QDT, SDT, G_>,                            \
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                                             (int)smem));                                      \
+            configured = smem;                                                                 \
+        }                                                                                      \
+        k_score<QDT, SDT, G_><<<grid, threads, smem, st>>>(prm);                               \
+        break;                                                                                 \
+    }
     switch (G) {
         PT_SCORE_CASE(1)
         PT_SCORE_CASE(2)
@@ -154,25 +450,105 @@ static int launch_score(const void *q, const float *norms, const void *means, co
     return PT_OK;
 }
 
+static int dispatch_score(const ScoreParams &prm, int q_dtype, int stats_dtype, int U, int G,
+                          cudaStream_t st) {
+    if (q_dtype == PT_F32 && stats_dtype == PT_F32) return launch_score<PT_F32, PT_F32>(prm, U, G, st);
+    if (q_dtype == PT_BF16 && stats_dtype == PT_F32) return launch_score<PT_BF16, PT_F32>(prm, U, G, st);
+    if (q_dtype == PT_BF16 && stats_dtype == PT_BF16) return launch_score<PT_BF16, PT_BF16>(prm, U, G, st);
+    if (q_dtype == PT_F32 && stats_dtype == PT_BF16) return launch_score<PT_F32, PT_BF16>(prm, U, G, st);
+    return PT_ERR_INVALID;
+}
+
+template <int QDT, int SDT>
+static int launch_score_stream(const StreamScoreParams &sp, int G, size_t smem, cudaStream_t st) {
+#define PT_SS_CASE(G_)                                                                         \
+    case G_: {                                                                                 \
+        static size_t configured = 0;                                                          \
+        if (smem > configured) {                                                               \
+            PT_CUDA_TRY(cudaFuncSetAttribute(k_score_stream<QDT, SDT, G_>,                     \
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                                             (int)smem));                                      \
+            configured = smem;                                                                 \
+        }                                                                                      \
+        k_score_stream<QDT, SDT, G_><<<148, 128, smem, st>>>(sp);                              \
+        break;                                                                                 \
+    }
+    switch (G) {
+        PT_SS_CASE(1)
+        PT_SS_CASE(2)
+        PT_SS_CASE(3)
+        PT_SS_CASE(4)
+        PT_SS_CASE(5)
+        PT_SS_CASE(6)
+        PT_SS_CASE(7)
+        PT_SS_CASE(8)
+        default: return PT_ERR_UNSUPPORTED;
+    }
+#undef PT_SS_CASE
+    PT_CUDA_TRY(cudaGetLastError());
+    return PT_OK;
+}
+
 extern "C" int pt_score(const void *q, int q_dtype, const float *norms, const void *means,
                         int stats_dtype, const float *stds, const int32_t *seq_len, int U, int G,
                         int D, int S, int Pmax, float lam, uint16_t *keys, float *scores,
-                        void *stream) {
+                        float *lamnorm_ws, void *stream) {
     if (!q || !means || !stds || !seq_len || !keys || U < 0 || S < 1 || Pmax % 32 || G < 1)
         return PT_ERR_INVALID;
     const int V = stats_dtype == PT_F32 ? 4 : 8;
     if (D < 1 || D > kScoreMaxD || D % V) return PT_ERR_UNSUPPORTED;
     if (U == 0) return PT_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    if (q_dtype == PT_F32 && stats_dtype == PT_F32)
-        return launch_score<PT_F32, PT_F32>(q, norms, means, stds, seq_len, U, G, D, S, Pmax, lam, keys, scores, st);
-    if (q_dtype == PT_BF16 && stats_dtype == PT_F32)
-        return launch_score<PT_BF16, PT_F32>(q, norms, means, stds, seq_len, U, G, D, S, Pmax, lam, keys, scores, st);
-    if (q_dtype == PT_BF16 && stats_dtype == PT_BF16)
-        return launch_score<PT_BF16, PT_BF16>(q, norms, means, stds, seq_len, U, G, D, S, Pmax, lam, keys, scores, st);
-    if (q_dtype == PT_F32 && stats_dtype == PT_BF16)
-        return launch_score<PT_F32, PT_BF16>(q, norms, means, stds, seq_len, U, G, D, S, Pmax, lam, keys, scores, st);
-    return PT_ERR_INVALID;
+    const int es = stats_dtype == PT_F32 ? 4 : 2, qes = q_dtype == PT_F32 ? 4 : 2;
+    const int nst_env = getenv("PT_SCORE_NST") ? atoi(getenv("PT_SCORE_NST")) : 0;
+    if (lamnorm_ws && G <= 8 && (G * D * qes) % 16 == 0 && !getenv("PT_SCORE_CTA")) {
+        const size_t stage = (size_t)score_stage_bytes(D, es, G, qes);
+        const size_t hdr = ((((size_t)U * 4 + 15) & ~(size_t)15) + 4 * 4 * 8 + 127) & ~(size_t)127;
+        int nst = nst_env > 0 ? nst_env : 3;
+        while (nst > 2 && hdr + 4 * nst * stage > 225 * 1024) nst--;
+        const size_t smem = hdr + 4 * nst * stage;
+        if (smem <= 225 * 1024) {
+            const int rows = U * G;
+            if (q_dtype == PT_F32)
+                k_lam_norms<PT_F32><<<(rows + 127) / 128, 128, 0, st>>>(q, norms, rows, G, D, lam, lamnorm_ws);
+            else
+                k_lam_norms<PT_BF16><<<(rows + 127) / 128, 128, 0, st>>>(q, norms, rows, G, D, lam, lamnorm_ws);
+            PT_CUDA_TRY(cudaGetLastError());
+            StreamScoreParams sp{q, lamnorm_ws, means, stds, seq_len, keys, scores, U, D, S, Pmax, nst};
+            if (q_dtype == PT_F32 && stats_dtype == PT_F32) return launch_score_stream<PT_F32, PT_F32>(sp, G, smem, st);
+            if (q_dtype == PT_BF16 && stats_dtype == PT_F32) return launch_score_stream<PT_BF16, PT_F32>(sp, G, smem, st);
+            if (q_dtype == PT_BF16 && stats_dtype == PT_BF16) return launch_score_stream<PT_BF16, PT_BF16>(sp, G, smem, st);
+            if (q_dtype == PT_F32 && stats_dtype == PT_BF16) return launch_score_stream<PT_F32, PT_BF16>(sp, G, smem, st);
+            return PT_ERR_INVALID;
+        }
+    }
+    ScoreParams prm{};
+    prm.q = q; prm.norms_in = norms; prm.means = means; prm.stds = stds; prm.seq_len = seq_len;
+    prm.keys = keys; prm.scores = scores; prm.counters = nullptr;
+    prm.D = D; prm.S = S; prm.Pmax = Pmax; prm.lam = lam; prm.k = 0;
+    return dispatch_score(prm, q_dtype, stats_dtype, U, G, st);
+}
+
+extern "C" int pt_score_select(const void *q, int q_dtype, const float *norms, const void *means,
+                               int stats_dtype, const float *stds, const int32_t *seq_len,
+                               const int32_t *page_table, int U, int G, int D, int S, int Pmax,
+                               float lam, int k, uint16_t *keys, float *scores, int32_t *sel,
+                               int32_t *sel_logical, int32_t *n_sel, int32_t *kth,
+                               int32_t *kplus1, int32_t *counters, void *stream) {
+    if (!q || !means || !stds || !seq_len || !page_table || !keys || !sel || !n_sel || !kth ||
+        !kplus1 || !counters || U < 0 || S < 1 || Pmax % 32 || G < 1)
+        return PT_ERR_INVALID;
+    if (k < 1) return PT_ERR_K;
+    const int V = stats_dtype == PT_F32 ? 4 : 8;
+    if (D < 1 || D > kScoreMaxD || D % V) return PT_ERR_UNSUPPORTED;
+    if (U == 0) return PT_OK;
+    ScoreParams prm{};
+    prm.q = q; prm.norms_in = norms; prm.means = means; prm.stds = stds; prm.seq_len = seq_len;
+    prm.keys = keys; prm.scores = scores; prm.counters = counters; prm.page_table = page_table;
+    prm.sel = sel; prm.sel_logical = sel_logical; prm.n_sel = n_sel; prm.kth = kth;
+    prm.kplus1 = kplus1;
+    prm.D = D; prm.S = S; prm.Pmax = Pmax; prm.lam = lam; prm.k = k;
+    return dispatch_score(prm, q_dtype, stats_dtype, U, G, (cudaStream_t)stream);
 }
 
 extern "C" int pt_tile_means(const float *src, int U, int P, int D, int Pmax, void *dst,

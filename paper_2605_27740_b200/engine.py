@@ -3,8 +3,8 @@
 One decode step for every (sequence, kv-head) unit of a :class:`PagedKvCache`:
 
     [append K/V row  (K1b: pt_append)]      kvcache.py:185-208
-    score            (K2: pt_score)          scoring.py:108-124 -> bf16 -> ordered keys
-    select           (K3: pt_topk)           select.py:87-115 + page-table translation
+    score + select   (K2+K3: pt_score_select) scoring.py:108-124 -> bf16 -> ordered keys ->
+                                              select.py:87-115 + page-table translation
     attend           (K4: pt_attend)         attention.py:94-107 for the G heads of a group
 
 All launches go on the current CUDA stream with device-resident buffers and no
@@ -64,6 +64,11 @@ class DecodeEngine:
         wsb = _lib.load().pt_attend_workspace_bytes(U, self.G, D, max(self.k, Pmax))
         self.ws = torch.zeros(wsb, dtype=torch.uint8, device=d)
         self.tickets = torch.zeros(U, dtype=torch.int32, device=d)
+        self.score_counters = torch.zeros(U, dtype=torch.int32, device=d)
+        self.lamnorm = torch.zeros(U * 8, dtype=torch.float32, device=d)
+        # K2 streaming kernel + K3 (two launches) is the default; the one-launch fused
+        # score+select CTA kernel (pt_score_select) is kept as an alternative
+        self.fused_select = False
         self.dense_tickets = torch.zeros(U, dtype=torch.int32, device=d)
         self.graph: torch.cuda.CUDAGraph | None = None
 
@@ -83,7 +88,7 @@ class DecodeEngine:
         _lib.call("pt_score", q2.data_ptr(), qc, dev.ptr(norms), c.means.data_ptr(), c.stats_code,
                   c.stds.data_ptr(), c.seq_lens.data_ptr(), self.U, self.G, self.D,
                   c.layout.page_size, c.Pmax, self.lam, self.keys.data_ptr(),
-                  dev.ptr(self.scores), dev.stream_handle(stream))
+                  dev.ptr(self.scores), self.lamnorm.data_ptr(), dev.stream_handle(stream))
 
     def select(self, stream=None) -> None:
         c = self.cache
@@ -114,13 +119,34 @@ class DecodeEngine:
                   dev.stream_handle(stream))
         return self.dense_out, self.dense_lse
 
+    def score_select(self, q: torch.Tensor, norms: torch.Tensor | None = None, stream=None) -> None:
+        """K2 + K3 fused into one launch (pt_score_select); falls back to two launches when
+        a unit's keys exceed the fused kernel's shared-memory envelope."""
+        if self.fused_select:
+            q2, qc = self._q(q)
+            c = self.cache
+            rc = _lib.load().pt_score_select(
+                q2.data_ptr(), qc, dev.ptr(norms), c.means.data_ptr(), c.stats_code,
+                c.stds.data_ptr(), c.seq_lens.data_ptr(), c.page_table.data_ptr(), self.U,
+                self.G, self.D, c.layout.page_size, c.Pmax, self.lam, self.k,
+                self.keys.data_ptr(), dev.ptr(self.scores), self.sel.data_ptr(),
+                dev.ptr(self.sel_logical), self.n_sel.data_ptr(), self.kth.data_ptr(),
+                self.kplus1.data_ptr(), self.score_counters.data_ptr(),
+                dev.stream_handle(stream))
+            if rc == _lib.PT_OK:
+                return
+            if rc != _lib.PT_ERR_UNSUPPORTED:
+                _lib.check(rc, "pt_score_select")
+            self.fused_select = False
+        self.score(q, norms, stream=stream)
+        self.select(stream=stream)
+
     def step(self, q: torch.Tensor, k_new: torch.Tensor | None = None,
              v_new: torch.Tensor | None = None, stream=None):
-        """One decode step: [append] -> score -> select -> attend.  Returns (out, lse)."""
+        """One decode step: [append] -> score+select -> attend.  Returns (out, lse)."""
         if k_new is not None:
             self.cache.append_batch(k_new, v_new, stream=stream)
-        self.score(q, stream=stream)
-        self.select(stream=stream)
+        self.score_select(q, stream=stream)
         self.attend(q, stream=stream)
         return self.out, self.lse
 
@@ -140,8 +166,7 @@ class DecodeEngine:
                 if k_new is not None:
                     self.cache.append_batch(k_new, v_new)
                     self.cache._seq_host -= 1  # replay() accounts for the captured append
-                self.score(q)
-                self.select()
+                self.score_select(q)
                 self.attend(q)
         torch.cuda.current_stream().wait_stream(s)
         self.graph = g

@@ -364,7 +364,8 @@ def test_backend_contract_vs_oracle(cuda, oracle):
 
 @pytest.mark.parametrize("G,D,S", [(4, 128, 16), (8, 128, 32), (1, 64, 16), (2, 256, 16), (4, 128, 64)])
 def test_attend_tensor_core_path_vs_simt(cuda, oracle, G, D, S, monkeypatch):
-    """bf16 KV: the TMA + mma.sync kernel against the CUDA-core kernel and the oracle."""
+    """bf16 KV: the TMA + mma.sync kernels (streaming and split grids) against the CUDA-core
+    kernel and the oracle."""
     pt = _pt()
     rng = np.random.default_rng(G + D + S)
     B, H = 2, 2
@@ -375,6 +376,21 @@ def test_attend_tensor_core_path_vs_simt(cuda, oracle, G, D, S, monkeypatch):
     q = q.to(torch.bfloat16)
     out_tc = eng.step(q)[0].clone()
     lse_tc = eng.lse.clone()
+    for env in ({"PT_ATTEND_SPLIT": "1"}, {"PT_ATTEND_CHUNK": "3", "PT_ATTEND_NSTAGE": "2"},
+                {"PT_ATTEND_CHUNK": "32"}):
+        for kk, vv in env.items():
+            monkeypatch.setenv(kk, vv)
+        eng.attend(q)
+        torch.cuda.synchronize()
+        torch.testing.assert_close(eng.out, out_tc, rtol=0, atol=1e-5)
+        for kk in env:
+            monkeypatch.delenv(kk)
+    monkeypatch.setenv("PT_SCORE_CTA", "1")  # the CTA scoring kernel gives identical keys
+    keys_stream = eng.keys.clone()
+    eng.score(q)
+    torch.cuda.synchronize()
+    assert torch.equal(eng.keys, keys_stream)
+    monkeypatch.delenv("PT_SCORE_CTA")
     monkeypatch.setenv("PT_ATTEND_SIMT", "1")
     eng.attend(q)
     torch.cuda.synchronize()
@@ -390,3 +406,27 @@ def test_attend_tensor_core_path_vs_simt(cuda, oracle, G, D, S, monkeypatch):
                               table, seq, 1.0 / math.sqrt(D), S)
     np.testing.assert_allclose(out_d.cpu().numpy().reshape(-1, G, D), o, rtol=0, atol=2e-2)
     np.testing.assert_allclose(lse_d.cpu().numpy().reshape(-1, G), l, rtol=0, atol=2e-2)
+
+
+@pytest.mark.parametrize("lens,k,fused", [([4096 * 16 + 5, 333, 16 * 16, 7 * 16 + 1], 16, True),
+                                          ([20000 * 16, 2048 * 16 - 3, 9, 100 * 16], 128, True),
+                                          ([40000 * 16, 3, 9, 100 * 16], 64, False)])
+def test_fused_score_select_equals_two_launches(cuda, lens, k, fused):
+    """pt_score_select (last-CTA selection) == pt_score followed by pt_topk, bit for bit."""
+    pt = _pt()
+    rng = np.random.default_rng(len(lens) + k)
+    cache = make_cache(rng, 2, 2, 128, 16, lens, dtype="bf16")
+    eng = pt.DecodeEngine(cache, 4, k, keep_logical=True)
+    q = torch.from_numpy(rng.standard_normal((16, 128)).astype(np.float32)).cuda().to(torch.bfloat16)
+    for _ in range(2):  # second call checks the self-resetting counters
+        eng.fused_select = True
+        eng.score_select(q)
+        torch.cuda.synchronize()
+        assert eng.fused_select == fused  # beyond the smem envelope: two-launch fallback
+        fused_out = [t.clone() for t in (eng.sel, eng.sel_logical, eng.n_sel, eng.kth, eng.kplus1)]
+        eng.score(q)
+        eng.select()
+        torch.cuda.synchronize()
+        sep = (eng.sel, eng.sel_logical, eng.n_sel, eng.kth, eng.kplus1)
+        for a, b in zip(fused_out, sep):
+            assert torch.equal(a, b)
