@@ -394,14 +394,14 @@ def main():
             a1.record(stream)
             torch.cuda.synchronize()
             return a0.elapsed_time(a1) * 1000 / reps
-        for nst in ("2", "3", "4"):
-            for ch in ("2", "4", "5", "8", "16"):
-                os.environ["PT_ATTEND_NSTAGE"], os.environ["PT_ATTEND_CHUNK"] = nst, ch
+        for nst in ("2", "3", "4", "6"):
+            for ctas in ("1", "2"):
+                os.environ["PT_ATTEND_NSTAGE"], os.environ["PT_ATTEND_CTAS"] = nst, ctas
                 try:
-                    tune[f"attend_stream_nst{nst}_c{ch}"] = timeit(lambda: eng.attend(qs[0]))
+                    tune[f"attend_stream_nst{nst}_ctas{ctas}"] = timeit(lambda: eng.attend(qs[0]))
                 except Exception as e:  # noqa: BLE001
-                    tune[f"attend_stream_nst{nst}_c{ch}"] = str(e)[:60]
-        os.environ.pop("PT_ATTEND_NSTAGE"); os.environ.pop("PT_ATTEND_CHUNK")
+                    tune[f"attend_stream_nst{nst}_ctas{ctas}"] = str(e)[:60]
+        os.environ.pop("PT_ATTEND_NSTAGE"); os.environ.pop("PT_ATTEND_CTAS")
         os.environ["PT_ATTEND_SPLIT"] = "1"
         tune["attend_split_auto"] = timeit(lambda: eng.attend(qs[0]))
         os.environ.pop("PT_ATTEND_SPLIT")

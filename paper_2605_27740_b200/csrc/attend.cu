@@ -76,43 +76,38 @@ extern "C" int pt_attend(const void *q, int q_dtype, const void *k_pool, const v
     const int E = kv_dtype == PT_F32 ? 4 : 2;
     const bool mma = kv_dtype == PT_BF16 && G <= 8 && (D == 64 || D == 128 || D == 256) &&
                      (S == 16 || S == 32 || S == 64) && num_phys_pages > 0 && !simt_forced();
-    // sparse selections on the tensor-core path: persistent streaming kernel
-    if (mma && n_sel != nullptr && U > 0 && env_int("PT_ATTEND_SPLIT", 0) == 0) {
+    // sparse selections on the tensor-core path: persistent streaming kernel (one wave of
+    // warps, balanced contiguous ranges of the concatenated page lists)
+    if (mma && n_sel != nullptr && U > 0 && U <= 8192 && env_int("PT_ATTEND_SPLIT", 0) == 0) {
         const int stage_bytes = 2 * S * D * 2;
         const int NW = 4;
         int nstage = env_int("PT_ATTEND_NSTAGE", 0);
-        if (nstage <= 0) {
-            nstage = 3;
-            while (nstage > 2 && attn_stream_smem(NW, nstage, stage_bytes) > 110 * 1024) nstage--;
-        }
-        const size_t smem = attn_stream_smem(NW, nstage, stage_bytes);
-        if (smem <= 220 * 1024) {
-            const int ctas_per_sm = smem <= 110 * 1024 ? 2 : 1;
-            const int grid = 148 * ctas_per_sm;
-            const int W = grid * NW;
-            int C = env_int("PT_ATTEND_CHUNK", 0);
-            if (C <= 0) {  // ~6 chunks per warp for balance
-                const long long pages = (long long)U * sel_stride;
-                C = (int)((pages + (long long)W * 6 - 1) / ((long long)W * 6));
-            }
-            if (C < 1) C = 1;
-            if (C > 32) C = 32;
-            const int CPU = (sel_stride + C - 1) / C;
-            if (CPU <= kAttnMaxSplits && (CPU == 1 || (workspace && tickets &&
-                workspace_bytes >= pt_attend_workspace_bytes(U, G, D, sel_stride)))) {
-                CUtensorMap tk, tv;
-                if (!make_pool_tmap(&tk, k_pool, D, S, num_phys_pages) ||
-                    !make_pool_tmap(&tv, v_pool, D, S, num_phys_pages))
-                    return PT_ERR_UNSUPPORTED;
-                StreamParams sp;
-                sp.q = q; sp.sel = sel; sp.n_sel = n_sel; sp.page_table = page_table;
-                sp.seq_len = seq_len; sp.bias = bias; sp.out = out; sp.lse = lse;
-                sp.ws = static_cast<float *>(workspace); sp.tickets = tickets;
-                sp.q_dtype = q_dtype; sp.sel_stride = sel_stride; sp.U = U; sp.G = G;
-                sp.Pmax = Pmax; sp.C = C; sp.CPU = CPU; sp.nstage = nstage; sp.scale = scale;
-                return launch_attend_stream(tk, tv, sp, D, S, grid, NW, smem,
-                                            (cudaStream_t)stream);
-            }
+        if (nstage <= 0) nstage = 3;
+        const int ctas_per_sm = env_int("PT_ATTEND_CTAS", 2);
+        const int grid = 148 * ctas_per_sm;
+        const int W = grid * NW;
+        const long long pages_ub = (long long)U * sel_stride;  // bound; exact count on device
+        int L = (int)((pages_ub + W - 1) / W);
+        // at most kAttnMaxSplits partial slots per unit
+        const int lmin = (sel_stride + kAttnMaxSplits - 3) / (kAttnMaxSplits - 2);
+        if (L < lmin) L = lmin;
+        if (L < 1) L = 1;
+        const size_t smem = attn_stream_hdr(U, NW, L, nstage) + (size_t)NW * nstage * stage_bytes;
+        if (L <= 4096 && smem <= 225 * 1024 &&
+            workspace && tickets &&
+            workspace_bytes >= pt_attend_workspace_bytes(U, G, D, sel_stride)) {
+            CUtensorMap tk, tv;
+            if (!make_pool_tmap(&tk, k_pool, D, S, num_phys_pages) ||
+                !make_pool_tmap(&tv, v_pool, D, S, num_phys_pages))
+                return PT_ERR_UNSUPPORTED;
+            StreamParams sp;
+            sp.q = q; sp.sel = sel; sp.n_sel = n_sel; sp.page_table = page_table;
+            sp.seq_len = seq_len; sp.bias = bias; sp.out = out; sp.lse = lse;
+            sp.ws = static_cast<float *>(workspace); sp.tickets = tickets;
+            sp.q_dtype = q_dtype; sp.sel_stride = sel_stride; sp.U = U; sp.G = G;
+            sp.Pmax = Pmax; sp.L = L; sp.maxparts = kAttnMaxSplits; sp.nstage = nstage;
+            sp.scale = scale;
+            return launch_attend_stream(tk, tv, sp, D, S, grid, NW, smem, (cudaStream_t)stream);
         }
     }
     if (!mma && (gp_of(G) < 0 || dpl_of(D) < 0 || (D * E) % 16 || D % dpl_of(D)))

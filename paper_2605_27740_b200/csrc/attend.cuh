@@ -571,15 +571,15 @@ __global__ void __launch_bounds__(128) k_attend_mma(const __grid_constant__ CUte
 // ===========================================================================
 // Streaming variant of the tensor-core kernel (the sparse decode path).
 //
-// The short per-unit page lists of a sparse step (k = 128 pages) make per-CTA set-up and
-// merge costs dominate a grid of (split, unit) CTAs.  Here every warp of a persistent grid
-// owns a static list of chunks (C <= 32 consecutive selected pages of one unit; chunk c of
-// the warp = gw + t * W) and streams all their pages through ONE continuous TMA ring: the
-// producer lane runs `nstage` pages ahead across chunk boundaries, the page ids of the
-// current and next chunk sit in registers (one id per lane), q for the next unit is
-// fetched while the current chunk computes.  Each finished chunk writes its partial
-// (m, l, acc) -- or the final output when the unit has a single chunk -- and the last chunk
-// of a unit to finish (atomic ticket, self-resetting) merges the unit's partials.
+// The short per-unit page lists of a sparse step (k = 128 pages) make per-CTA set-up,
+// merge and wave-quantisation costs dominate a grid of (split, unit) CTAs.  Here the
+// selected pages of ALL units are concatenated (unit-major, offsets = prefix sum of n_sel)
+// and cut into W equal contiguous ranges, one per warp of a persistent grid (one wave).
+// Each warp streams its range through ONE continuous TMA ring -- the producer lane runs
+// `nstage` pages ahead across unit boundaries, page ids come from a per-warp list staged
+// in shared memory -- and emits one result per unit segment it touches: the final output
+// when it owns the whole unit, else a partial (m, l, acc) into slot (warp - first warp of
+// the unit); the last partial of a unit to land (atomic ticket, self-resetting) merges them.
 // ===========================================================================
 struct StreamParams {
     const void *q;
@@ -590,36 +590,9 @@ struct StreamParams {
     const float *bias;
     float *out, *lse, *ws;
     int32_t *tickets;
-    int q_dtype, sel_stride, U, G, Pmax, C, CPU, nstage;
+    int q_dtype, sel_stride, U, G, Pmax, L, maxparts, nstage;
     float scale;
 };
-
-struct ChunkInfo {
-    int u, j, np;        // unit, chunk index in unit, pages in this chunk (0: none)
-    int nch;             // non-empty chunks of the unit
-    int tail_pid, tail_rows;
-    int pid;             // this lane's page id (lane < np)
-    float bias2;         // this lane's page bias (log2 domain)
-};
-
-template <int D, int MT>
-__device__ __forceinline__ ChunkInfo load_chunk(const StreamParams &p, int c, int lane) {
-    constexpr int S = 16 * MT;
-    ChunkInfo ci;
-    ci.u = c / p.CPU;
-    ci.j = c - ci.u * p.CPU;
-    const int ns = p.n_sel[ci.u];
-    ci.np = max(0, min(p.C, ns - ci.j * p.C));
-    ci.nch = (ns + p.C - 1) / p.C;
-    const int n = p.seq_len[ci.u];
-    const int P = (n + S - 1) / S;
-    ci.tail_pid = P > 0 ? p.page_table[(int64_t)ci.u * p.Pmax + P - 1] : -1;
-    ci.tail_rows = n - (P - 1) * S;
-    const int64_t off = (int64_t)ci.u * p.sel_stride + ci.j * p.C + lane;
-    ci.pid = lane < ci.np ? p.sel[off] : 0;
-    ci.bias2 = (p.bias && lane < ci.np) ? p.bias[off] * kLog2e : 0.f;
-    return ci;
-}
 
 template <int D>
 __device__ __forceinline__ void load_qfrag(const StreamParams &p, int u, int lane,
@@ -707,8 +680,53 @@ __device__ __forceinline__ void mma_page(uint32_t kbase, uint32_t vbase, int row
     }
 }
 
-__host__ __device__ __forceinline__ size_t attn_stream_smem(int NW, int nstage, int stage_bytes) {
-    return 1024 + (size_t)NW * nstage * stage_bytes;  // [mbarriers | pad][rings]
+
+// smem: [unit offsets (U+1) | per-warp page lists (L ints) | mbarriers | pad] [rings]
+__host__ __device__ __forceinline__ size_t attn_stream_hdr(int U, int NW, int L, int nstage) {
+    const size_t b = (size_t)(U + 1) * 4 + (size_t)NW * L * 4 + (size_t)NW * nstage * 8 + 8;
+    return (b + 1023) & ~(size_t)1023;
+}
+
+// merge the nparts partials of unit u (one warp): lanes own d = lane + 32 i, so every
+// load is coalesced; the per-part scale factors are computed once per head.
+template <int D>
+__device__ __noinline__ void merge_unit(const StreamParams &p, int u, int nparts, int lane) {
+    const float *wacc = p.ws;
+    const float *wml = p.ws + (size_t)p.U * p.maxparts * p.G * D;
+    for (int g = 0; g < p.G; g++) {
+        float mw[2], lw[2];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int w = lane + 32 * h;
+            const int64_t sl = ((int64_t)u * p.maxparts + w) * p.G + g;
+            mw[h] = w < nparts ? __ldcg(&wml[sl * 2]) : -INFINITY;
+            lw[h] = w < nparts ? __ldcg(&wml[sl * 2 + 1]) : 0.f;
+        }
+        float mt = fmaxf(mw[0], mw[1]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, o));
+        float f[2], lt = 0.f;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            f[h] = exp2f(mw[h] - mt);
+            lt += lw[h] * f[h];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) lt += __shfl_xor_sync(0xffffffffu, lt, o);
+        const float inv = 1.f / lt;
+        float a[D / 32];
+#pragma unroll
+        for (int i = 0; i < D / 32; i++) a[i] = 0.f;
+        for (int w = 0; w < nparts; w++) {
+            const float fw = __shfl_sync(0xffffffffu, f[w >> 5], w & 31);
+            const float *src = wacc + (((int64_t)u * p.maxparts + w) * p.G + g) * D;
+#pragma unroll
+            for (int i = 0; i < D / 32; i++) a[i] = fmaf(__ldcg(src + lane + 32 * i), fw, a[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < D / 32; i++) p.out[((int64_t)u * p.G + g) * D + lane + 32 * i] = a[i] * inv;
+        if (lane == 0) p.lse[u * p.G + g] = (mt + log2f(lt)) * kLn2;
+    }
 }
 
 template <int D, int MT>
@@ -721,93 +739,122 @@ __global__ void __launch_bounds__(128) k_attend_stream(const __grid_constant__ C
     constexpr uint32_t STAGE_BYTES = 2 * PAGE_BYTES;
     extern __shared__ __align__(1024) char smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
-    const int nstage = prm.nstage;
-    const int W = gridDim.x * NW;
+    const int nstage = prm.nstage, U = prm.U, L = prm.L;
     const int gw = blockIdx.x * NW + warp;
-    const int total = prm.U * prm.CPU;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem) + warp * nstage;
-    char *my_stages = smem + 1024 + (size_t)warp * nstage * STAGE_BYTES;
+    int *off = reinterpret_cast<int *>(smem);                        // [U + 1]
+    int *plist = off + (U + 1) + warp * L;                           // this warp's page ids
+    uint64_t *bars = reinterpret_cast<uint64_t *>(
+                         smem + (((size_t)(U + 1) * 4 + (size_t)NW * L * 4 + 7) & ~(size_t)7)) +
+                     warp * nstage;
+    char *my_stages = smem + attn_stream_hdr(U, NW, L, nstage) + (size_t)warp * nstage * STAGE_BYTES;
+
+    // exclusive prefix sum of n_sel (every CTA; one warp, U is small)
+    if (warp == 0) {
+        int carry = 0;
+        for (int base = 0; base < U; base += 32) {
+            const int u = base + lane;
+            int v = u < U ? prm.n_sel[u] : 0, inc = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int x = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += x;
+            }
+            if (u < U) off[u] = carry + inc - v;
+            carry += __shfl_sync(0xffffffffu, inc, 31);
+        }
+        if (lane == 0) off[U] = carry;
+    }
     if (lane == 0) {
         for (int i = 0; i < nstage; i++) mbar_init(&bars[i], 1);
         fence_mbar_init();
     }
+    __syncthreads();
+    const int T = off[U];
+    const int a = min(gw * L, T), b = min(a + L, T);
+    if (a >= b) return;
+    // first unit of the range: largest u with off[u] <= a
+    int u = 0;
+    {
+        int lo = 0, hi = U - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (off[mid] <= a) lo = mid; else hi = mid - 1;
+        }
+        u = lo;
+        while (u < U - 1 && off[u + 1] <= a) u++;
+    }
+    // stage this warp's page ids (positions a..b-1)
+    {
+        int uu = u;
+        for (int i = a + lane; i < b; i += 32) {
+            while (uu < U - 1 && off[uu + 1] <= i) uu++;
+            plist[i - a] = prm.sel[(int64_t)uu * prm.sel_stride + (i - off[uu])];
+        }
+    }
     __syncwarp();
 
-    // chunk cursor helpers: the warp's chunks are gw, gw + W, ...; skip empty ones
-    auto next_nonempty = [&](int c) -> int {
-        while (c < total) {
-            const int u = c / prm.CPU, j = c - u * prm.CPU;
-            if (j * prm.C < prm.n_sel[u]) return c;
-            c += W;
-        }
-        return total;
-    };
-    int c_cur = next_nonempty(gw);
-    if (c_cur >= total) return;
-    int c_nxt = next_nonempty(c_cur + W);
-    ChunkInfo cur = load_chunk<D, MT>(prm, c_cur, lane);
-    ChunkInfo nxt;
-    if (c_nxt < total) nxt = load_chunk<D, MT>(prm, c_nxt, lane);
-    else nxt.np = 0;
-
-    // producer: page index within the stream; (which, off) = chunk (0 cur / 1 nxt) + page
-    int prod_i = 0;          // pages issued so far (ring position)
-    int prod_off = 0;        // page offset inside the producer's chunk
-    int prod_which = 0;      // 0: producer is in `cur`, 1: in `nxt`
-    auto produce = [&](int limit_i) {
-        // issue pages while the ring has room (prod_i < limit_i) and pages remain in cur/nxt
-        while (prod_i < limit_i) {
-            const ChunkInfo &pc = prod_which == 0 ? cur : nxt;
-            if (prod_off >= pc.np) {
-                if (prod_which == 0 && nxt.np > 0) { prod_which = 1; prod_off = 0; continue; }
-                break;
-            }
-            const int pid = __shfl_sync(0xffffffffu, pc.pid, prod_off);
-            if (lane == 0) {
+    const int n_pos = b - a;
+    int prod_i = 0;
+    int cons_i = 0;
+    // producer: lane 0 keeps up to nstage pages in flight
+    auto fill = [&]() {
+        if (lane == 0) {
+            while (prod_i < n_pos && prod_i < cons_i + nstage) {
+                const int pid = plist[prod_i];
                 const int st = prod_i % nstage;
                 char *ks = my_stages + (size_t)st * STAGE_BYTES;
                 mbar_arrive_expect_tx(&bars[st], STAGE_BYTES);
 #pragma unroll
-                for (int b = 0; b < D / 64; b++) {
-                    tma_load_2d(ks + b * S * 128, &tmk, b * 64, pid * S, &bars[st]);
-                    tma_load_2d(ks + PAGE_BYTES + b * S * 128, &tmv, b * 64, pid * S, &bars[st]);
+                for (int bb = 0; bb < D / 64; bb++) {
+                    tma_load_2d(ks + bb * S * 128, &tmk, bb * 64, pid * S, &bars[st]);
+                    tma_load_2d(ks + PAGE_BYTES + bb * S * 128, &tmv, bb * 64, pid * S, &bars[st]);
                 }
+                prod_i++;
             }
-            prod_i++;
-            prod_off++;
         }
     };
-
-    uint32_t qb[KS][2];
-    load_qfrag<D>(prm, cur.u, lane, qb);
+    fill();
     const float qscale = prm.scale * kLog2e;
-    int cons_i = 0;
-    produce(nstage);
-
-    float *wacc = prm.ws;                                               // [U*CPU][G][D]
-    float *wml = prm.ws + (size_t)prm.U * prm.CPU * prm.G * D;          // [U*CPU][G][2]
+    float *wacc = prm.ws;
+    float *wml = prm.ws + (size_t)U * prm.maxparts * prm.G * D;
     __shared__ int last_flag[4];
     const int g0 = 2 * (lane & 3);
-    while (true) {
+    uint32_t qb[KS][2];
+    load_qfrag<D>(prm, u, lane, qb);
+    int pos = a;
+    while (pos < b) {
+        // segment of unit u: [pos, seg_end)
+        const int seg_end = min(b, off[u + 1]);
+        const int n = prm.seq_len[u];
+        const int P = (n + S - 1) / S;
+        const int tail_pid = prm.page_table[(int64_t)u * prm.Pmax + P - 1];
+        const int tail_rows = n - (P - 1) * S;
+        // q of the next (non-empty) unit is fetched while this segment computes
+        uint32_t qn[KS][2];
+        const bool more = seg_end < b;
+        int nu = u + 1;
+        while (nu < U - 1 && off[nu + 1] <= seg_end) nu++;
+        if (more) load_qfrag<D>(prm, nu, lane, qn);
         float acc[KS][4];
 #pragma unroll
         for (int i = 0; i < KS; i++) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
         float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};
-        for (int pg = 0; pg < cur.np; pg++) {
+        for (; pos < seg_end; pos++) {
             const int st = cons_i % nstage;
-            const int pid = __shfl_sync(0xffffffffu, cur.pid, pg);
-            const float b2 = __shfl_sync(0xffffffffu, cur.bias2, pg);
-            const int rows = (pid == cur.tail_pid) ? cur.tail_rows : S;
+            const int pid = plist[cons_i];
+            const int rows = (pid == tail_pid) ? tail_rows : S;
+            const float b2 =
+                prm.bias ? prm.bias[(int64_t)u * prm.sel_stride + (pos - off[u])] * kLog2e : 0.f;
             mbar_wait(&bars[st], (uint32_t)((cons_i / nstage) & 1));
             const uint32_t kbase = smem_u32(my_stages + (size_t)st * STAGE_BYTES);
             mma_page<D, MT>(kbase, kbase + PAGE_BYTES, rows, b2, qscale, qb, acc, m_run, l_run, lane);
             __syncwarp();
             cons_i++;
-            produce(cons_i + nstage);
+            fill();
         }
-        // ---- chunk epilogue: final output (single-chunk unit) or partial + ticket ----
-        const int u = cur.u;
-        if (cur.nch == 1) {
+        // ---- segment epilogue ----
+        const int ustart = off[u], uend = off[u + 1];
+        if (ustart >= a && uend <= b) {  // this warp owns the whole unit: final output
             const float inv0 = 1.f / l_run[0], inv1 = 1.f / l_run[1];
 #pragma unroll
             for (int dm = 0; dm < KS; dm++) {
@@ -826,7 +873,9 @@ __global__ void __launch_bounds__(128) k_attend_stream(const __grid_constant__ C
                 if (g0 + 1 < prm.G) prm.lse[u * prm.G + g0 + 1] = (m_run[1] + log2f(l_run[1])) * kLn2;
             }
         } else {
-            const int64_t slot = (int64_t)u * prm.CPU + cur.j;
+            const int wfirst = ustart / L, wlast = (uend - 1) / L;
+            const int nparts = wlast - wfirst + 1;
+            const int64_t slot = (int64_t)u * prm.maxparts + (gw - wfirst);
 #pragma unroll
             for (int dm = 0; dm < KS; dm++) {
                 const int d = dm * 16 + (lane >> 2);
@@ -852,40 +901,21 @@ __global__ void __launch_bounds__(128) k_attend_stream(const __grid_constant__ C
             __syncwarp();
             if (lane == 0) {
                 __threadfence();
-                last_flag[warp] = (atomicAdd(&prm.tickets[u], 1) == cur.nch - 1);
+                last_flag[warp] = (atomicAdd(&prm.tickets[u], 1) == nparts - 1);
             }
             __syncwarp();
             if (last_flag[warp]) {
                 __threadfence();
-                for (int i = lane; i < prm.G * D; i += 32) {
-                    const int g = i / D, d = i - g * D;
-                    float mt = -INFINITY;
-                    for (int w = 0; w < cur.nch; w++)
-                        mt = fmaxf(mt, __ldcg(&wml[(((int64_t)u * prm.CPU + w) * prm.G + g) * 2]));
-                    float lt = 0.f, a = 0.f;
-                    for (int w = 0; w < cur.nch; w++) {
-                        const int64_t sl = ((int64_t)u * prm.CPU + w) * prm.G + g;
-                        const float f = exp2f(__ldcg(&wml[sl * 2]) - mt);
-                        lt += __ldcg(&wml[sl * 2 + 1]) * f;
-                        a += __ldcg(&wacc[sl * D + d]) * f;
-                    }
-                    prm.out[((int64_t)u * prm.G + g) * D + d] = a / lt;
-                    if (d == 0) prm.lse[u * prm.G + g] = (mt + log2f(lt)) * kLn2;
-                }
+                merge_unit<D>(prm, u, nparts, lane);
                 if (lane == 0) prm.tickets[u] = 0;
             }
         }
-        // ---- advance: nxt becomes cur; fetch the following chunk ----
-        if (nxt.np == 0) break;
-        const int prev_u = cur.u;
-        cur = nxt;
-        prod_which = 0;  // the producer's chunk `nxt` is now `cur` (prod_off already counts it)
-        c_nxt = next_nonempty(c_nxt + W);
-        if (c_nxt < total) nxt = load_chunk<D, MT>(prm, c_nxt, lane);
-        else nxt.np = 0;
-        if (cur.u != prev_u) load_qfrag<D>(prm, cur.u, lane, qb);
-        produce(cons_i + nstage);
+        if (!more) break;
+        u = nu;
+#pragma unroll
+        for (int ks = 0; ks < KS; ks++) { qb[ks][0] = qn[ks][0]; qb[ks][1] = qn[ks][1]; }
     }
+
 }
 
 }  // namespace pt

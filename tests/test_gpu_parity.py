@@ -376,8 +376,8 @@ def test_attend_tensor_core_path_vs_simt(cuda, oracle, G, D, S, monkeypatch):
     q = q.to(torch.bfloat16)
     out_tc = eng.step(q)[0].clone()
     lse_tc = eng.lse.clone()
-    for env in ({"PT_ATTEND_SPLIT": "1"}, {"PT_ATTEND_CHUNK": "3", "PT_ATTEND_NSTAGE": "2"},
-                {"PT_ATTEND_CHUNK": "32"}):
+    for env in ({"PT_ATTEND_SPLIT": "1"}, {"PT_ATTEND_NSTAGE": "2", "PT_ATTEND_CTAS": "1"},
+                {"PT_ATTEND_NSTAGE": "4"}):
         for kk, vv in env.items():
             monkeypatch.setenv(kk, vv)
         eng.attend(q)
