@@ -405,14 +405,20 @@ def main():
         os.environ["PT_ATTEND_SPLIT"] = "1"
         tune["attend_split_auto"] = timeit(lambda: eng.attend(qs[0]))
         os.environ.pop("PT_ATTEND_SPLIT")
-        for nst in ("2", "3"):
-            os.environ["PT_SCORE_NST"] = nst
-            tune[f"score_stream_nst{nst}"] = timeit(lambda: eng.score(qs[0]))
-        os.environ.pop("PT_SCORE_NST")
+        for nst in ("2", "3", "4"):
+            for cps in ("4", "8", "16"):
+                os.environ["PT_SCORE_NST"], os.environ["PT_SCORE_CPS"] = nst, cps
+                tune[f"score_stream_nst{nst}_cps{cps}"] = timeit(lambda: eng.score(qs[0]))
+        os.environ.pop("PT_SCORE_NST"); os.environ.pop("PT_SCORE_CPS")
         os.environ["PT_SCORE_CTA"] = "1"
         tune["score_cta"] = timeit(lambda: eng.score(qs[0]))
         os.environ.pop("PT_SCORE_CTA")
         tune["select"] = timeit(lambda: eng.select())
+        # same byte count, contiguous pages instead of the selected (scattered) ones
+        saved = eng.sel.clone()
+        eng.sel.copy_(cache.page_table[:, : eng.k])
+        tune["attend_contiguous_pages"] = timeit(lambda: eng.attend(qs[0]))
+        eng.sel.copy_(saved)
         eng.fused_select = True
         tune["score_select_fused_cta"] = timeit(lambda: eng.score_select(qs[0]))
         eng.fused_select = False

@@ -201,15 +201,16 @@ __global__ void __launch_bounds__(128) k_score(const ScoreParams prm) {
 // ===========================================================================
 // Streaming scoring kernel (default path).
 //
-// A persistent grid of warps; warp gw scores the 32-page tiles T = gw, gw + W, ... of the
-// unit-major tile space (so units complete progressively).  Each warp streams its tiles
-// through its own ring of NST shared-memory stages; one stage holds, for one tile:
-//   [32 pages x D means (tile layout: 16-byte chunk c of page l at c*512 + l*16)]
-//   [the unit's G query rows][lam*||q_g|| padded to 8][the 32 page stds]
-// all filled by 1-D bulk copies (cp.async.bulk -> UBLKCP) on one mbarrier, issued by lane 0
-// NST tiles ahead.  Lane l = page l of the tile walks its mean vector in the reference's
-// sequential d order (bit-identical scores).  No per-tile prologue: the q rows, norms and
-// stds ride along with the tile, and the per-unit page counts sit in shared memory.
+// A persistent grid of warps (3 CTAs x 4 warps per SM); warp gw scores the 32-page tiles
+// T = gw, gw + W, ... of the unit-major tile space.  Each warp streams its tiles through
+// its own ring of NST small shared-memory stages, one stage = one contiguous d-range of a
+// tile (CPS 16-byte chunks of all 32 pages = CPS*512 bytes, a single cp.async.bulk ->
+// UBLKCP), with lane 0 running NST stages ahead.  The first stage of a tile also brings the
+// tile header -- the unit's G query rows, lam*||q_g|| (padded to 8) and the 32 page stds --
+// into one of NHDR header slots; the query rows are widened once per tile into a per-warp
+// f32 buffer read by broadcast.  Lane l = page l walks its mean vector in the reference's
+// sequential d order (bit-identical scores).  Bytes in flight are decoupled from registers,
+// and 12 warps per SM hide the dependent FADD chains.
 // ===========================================================================
 struct StreamScoreParams {
     const void *q;
@@ -219,37 +220,61 @@ struct StreamScoreParams {
     const int32_t *seq_len;
     uint16_t *keys;
     float *scores;
-    int U, D, S, Pmax, nst;
+    int U, D, S, Pmax, nst, cps;
 };
 
-__host__ __device__ __forceinline__ int score_stage_bytes(int D, int es, int G, int qes) {
-    const int tile = 32 * D * es;
-    const int qb = (G * D * qes + 15) & ~15;
-    return (tile + qb + 32 + 128 + 127) & ~127;
+constexpr int kScoreStreamWarps = 4;
+constexpr int kScoreStreamCtas = 3;  // per SM
+
+struct ScoreStreamLayout {  // per-warp shared-memory carve-up (bytes)
+    int stage, hdr, nhdr, qf, per_warp, hdr_q, hdr_ln, hdr_sd;
+};
+
+__host__ __device__ __forceinline__ ScoreStreamLayout score_stream_layout(int D, int es, int G,
+                                                                           int qes, int nst,
+                                                                           int cps) {
+    ScoreStreamLayout L;
+    const int nch = D / (16 / es);
+    const int spt = (nch + cps - 1) / cps;
+    L.stage = cps * 512;
+    L.hdr_q = 0;
+    L.hdr_ln = (G * D * qes + 15) & ~15;
+    L.hdr_sd = L.hdr_ln + 32;
+    L.hdr = (L.hdr_sd + 128 + 127) & ~127;
+    L.nhdr = nst / spt + 2;
+    L.qf = (G * D * 4 + 127) & ~127;
+    L.per_warp = nst * L.stage + L.nhdr * L.hdr + L.qf;
+    return L;
 }
 
 template <int QDT, int SDT, int G>
-__global__ void __launch_bounds__(128, 1) k_score_stream(const StreamScoreParams prm) {
+__global__ void __launch_bounds__(kScoreStreamWarps * 32, kScoreStreamCtas)
+    k_score_stream(const StreamScoreParams prm) {
     constexpr int V = MeanVec<SDT>::V;
     constexpr int ES = SDT == PT_F32 ? 4 : 2;
     constexpr int QES = QDT == PT_F32 ? 4 : 2;
     constexpr bool kExactProduct = (QDT == PT_BF16 && SDT == PT_BF16);
     extern __shared__ __align__(128) char smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
-    const int D = prm.D, S = prm.S, Pmax = prm.Pmax, U = prm.U, NST = prm.nst;
+    const int D = prm.D, S = prm.S, Pmax = prm.Pmax, U = prm.U, NST = prm.nst, CPS = prm.cps;
+    const int nch = D / V;
+    const int SPT = (nch + CPS - 1) / CPS;  // stages per tile
     const int TPU = Pmax >> 5;
     const long long total = (long long)U * TPU;
     const int W = gridDim.x * NW;
     const int gw = blockIdx.x * NW + warp;
+    const ScoreStreamLayout Ly = score_stream_layout(D, ES, G, QES, NST, CPS);
     const int tile_bytes = 32 * D * ES;
     const int q_bytes = G * D * QES;
-    const int q_off = tile_bytes, ln_off = tile_bytes + ((q_bytes + 15) & ~15);
-    const int sd_off = ln_off + 32;
-    const int stage_bytes = score_stage_bytes(D, ES, G, QES);
-    int *Ps = reinterpret_cast<int *>(smem);                               // [U] pages per unit
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + ((U * 4 + 15) & ~15)) + warp * NST;
-    const size_t hdr = (((size_t)U * 4 + 15) & ~15) + (size_t)NW * NST * 8;
-    char *ring = smem + ((hdr + 127) & ~(size_t)127) + (size_t)warp * NST * stage_bytes;
+    // [Ps: U ints][mbarriers NW*NST][pad 128][warp regions: rings | headers | qf]
+    int *Ps = reinterpret_cast<int *>(smem);
+    const size_t ps_bytes = ((size_t)U * 4 + 15) & ~(size_t)15;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + ps_bytes) + warp * NST;
+    const size_t hdr0 = (ps_bytes + (size_t)NW * NST * 8 + 127) & ~(size_t)127;
+    char *wbase = smem + hdr0 + (size_t)warp * Ly.per_warp;
+    char *ring = wbase;
+    char *hdrs = wbase + NST * Ly.stage;
+    float *qf = reinterpret_cast<float *>(hdrs + Ly.nhdr * Ly.hdr);
     for (int i = threadIdx.x; i < U; i += blockDim.x) Ps[i] = (prm.seq_len[i] + S - 1) / S;
     if (lane == 0) {
         for (int i = 0; i < NST; i++) mbar_init(&bars[i], 1);
@@ -265,81 +290,97 @@ __global__ void __launch_bounds__(128, 1) k_score_stream(const StreamScoreParams
         }
         return total;
     };
-    auto issue = [&](long long T, int slot) {  // lane 0 only
-        const int u = (int)(T / TPU), t = (int)(T - (long long)u * TPU);
-        char *st = ring + (size_t)slot * stage_bytes;
-        const uint32_t qcopy = (uint32_t)((q_bytes + 15) & ~15);
-        mbar_arrive_expect_tx(&bars[slot], (uint32_t)tile_bytes + qcopy + 32 + 128);
-        bulk_g2s(st, static_cast<const char *>(prm.means) + ((int64_t)u * Pmax + (int64_t)t * 32) * D * ES,
-                 (uint32_t)tile_bytes, &bars[slot]);
-        bulk_g2s(st + q_off, static_cast<const char *>(prm.q) + (int64_t)u * q_bytes, qcopy, &bars[slot]);
-        bulk_g2s(st + ln_off, prm.lamnorm + (int64_t)u * 8, 32, &bars[slot]);
-        bulk_g2s(st + sd_off, prm.stds + (int64_t)u * Pmax + t * 32, 128, &bars[slot]);
-    };
-
-    long long Tp = next_tile(gw);  // producer cursor
-    long long Tc = Tp;             // consumer cursor
-    int issued = 0;
-    if (lane == 0) {
-        for (int i = 0; i < NST && Tp < total; i++) {
-            issue(Tp, i);
+    // producer state (lane 0 drives; kept uniform across the warp)
+    long long pT = next_tile(gw);
+    int p_part = 0, p_tile_seq = 0, issued = 0;
+    auto fill = [&](int consumed) {
+        while (pT < total && issued < consumed + NST) {
+            if (lane == 0) {
+                const int slot = issued % NST;
+                const int u = (int)(pT / TPU), t = (int)(pT - (long long)u * TPU);
+                const int c0 = p_part * CPS, c1 = min(nch, c0 + CPS);
+                const uint32_t bytes = (uint32_t)(c1 - c0) * 512;
+                uint32_t tx = bytes;
+                const uint32_t qcopy = (uint32_t)((q_bytes + 15) & ~15);
+                if (p_part == 0) tx += qcopy + 32 + 128;
+                mbar_arrive_expect_tx(&bars[slot], tx);
+                bulk_g2s(ring + slot * Ly.stage,
+                         static_cast<const char *>(prm.means) +
+                             ((int64_t)u * Pmax + (int64_t)t * 32) * D * ES + c0 * 512,
+                         bytes, &bars[slot]);
+                if (p_part == 0) {
+                    char *h = hdrs + (p_tile_seq % Ly.nhdr) * Ly.hdr;
+                    bulk_g2s(h + Ly.hdr_q, static_cast<const char *>(prm.q) + (int64_t)u * q_bytes,
+                             qcopy, &bars[slot]);
+                    bulk_g2s(h + Ly.hdr_ln, prm.lamnorm + (int64_t)u * 8, 32, &bars[slot]);
+                    bulk_g2s(h + Ly.hdr_sd, prm.stds + (int64_t)u * Pmax + t * 32, 128, &bars[slot]);
+                }
+            }
             issued++;
-            Tp = next_tile(Tp + W);
+            if (++p_part == SPT) {
+                p_part = 0;
+                p_tile_seq++;
+                pT = next_tile(pT + W);
+            }
         }
-    }
-    issued = __shfl_sync(0xffffffffu, issued, 0);
-    Tp = __shfl_sync(0xffffffffu, Tp, 0);
-    int consumed = 0;
-    while (Tc < total) {
-        const int slot = consumed % NST;
-        const int u = (int)(Tc / TPU), t = (int)(Tc - (long long)u * TPU);
-        mbar_wait(&bars[slot], (uint32_t)((consumed / NST) & 1));
-        const char *st = ring + (size_t)slot * stage_bytes;
-        const char *mp = st + lane * 16;
-        const char *qp = st + q_off;
-        const float *ln = reinterpret_cast<const float *>(st + ln_off);
+    };
+    fill(0);
+    int consumed = 0, tile_seq = 0;
+    for (long long T = next_tile(gw); T < total; T = next_tile(T + W), tile_seq++) {
+        const int u = (int)(T / TPU), t = (int)(T - (long long)u * TPU);
+        const char *h = hdrs + (tile_seq % Ly.nhdr) * Ly.hdr;
         float acc[G];
 #pragma unroll
         for (int g = 0; g < G; g++) acc[g] = 0.0f;
-        const int nch = D / V;
-#pragma unroll 2
-        for (int c = 0; c < nch; c++) {
-            float m[V];
-            if constexpr (SDT == PT_F32) {
-                const float4 v = *reinterpret_cast<const float4 *>(mp + c * 512);
-                m[0] = v.x; m[1] = v.y; m[2] = v.z; m[3] = v.w;
-            } else {
-                const uint4 v = *reinterpret_cast<const uint4 *>(mp + c * 512);
-                m[0] = bf16_lo(v.x); m[1] = bf16_hi(v.x); m[2] = bf16_lo(v.y); m[3] = bf16_hi(v.y);
-                m[4] = bf16_lo(v.z); m[5] = bf16_hi(v.z); m[6] = bf16_lo(v.w); m[7] = bf16_hi(v.w);
+        for (int part = 0; part < SPT; part++) {
+            const int slot = consumed % NST;
+            mbar_wait(&bars[slot], (uint32_t)((consumed / NST) & 1));
+            if (part == 0) {  // widen this tile's query rows once
+                for (int i = lane; i < G * D; i += 32) {
+                    if constexpr (QDT == PT_F32) qf[i] = reinterpret_cast<const float *>(h + Ly.hdr_q)[i];
+                    else qf[i] = bf16_bits_to_f32(reinterpret_cast<const uint16_t *>(h + Ly.hdr_q)[i]);
+                }
+                __syncwarp();
             }
+            const char *mp = ring + slot * Ly.stage + lane * 16;
+            const int c0 = part * CPS, c1 = min(nch, c0 + CPS);
+#pragma unroll 2
+            for (int c = c0; c < c1; c++) {
+                float m[V];
+                if constexpr (SDT == PT_F32) {
+                    const float4 v = *reinterpret_cast<const float4 *>(mp + (c - c0) * 512);
+                    m[0] = v.x; m[1] = v.y; m[2] = v.z; m[3] = v.w;
+                } else {
+                    const uint4 v = *reinterpret_cast<const uint4 *>(mp + (c - c0) * 512);
+                    m[0] = bf16_lo(v.x); m[1] = bf16_hi(v.x); m[2] = bf16_lo(v.y); m[3] = bf16_hi(v.y);
+                    m[4] = bf16_lo(v.z); m[5] = bf16_hi(v.z); m[6] = bf16_lo(v.w); m[7] = bf16_hi(v.w);
+                }
 #pragma unroll
-            for (int g = 0; g < G; g++) {
-                float qv[V];
-                if constexpr (QDT == PT_F32) {
+                for (int g = 0; g < G; g++) {
 #pragma unroll
                     for (int j = 0; j < V; j += 4) {
-                        const float4 w = *reinterpret_cast<const float4 *>(qp + (g * D + c * V + j) * 4);
-                        qv[j] = w.x; qv[j + 1] = w.y; qv[j + 2] = w.z; qv[j + 3] = w.w;
+                        const float4 w = *reinterpret_cast<const float4 *>(qf + g * D + c * V + j);
+                        if constexpr (kExactProduct) {
+                            acc[g] = __fmaf_rn(w.x, m[j], acc[g]);
+                            acc[g] = __fmaf_rn(w.y, m[j + 1], acc[g]);
+                            acc[g] = __fmaf_rn(w.z, m[j + 2], acc[g]);
+                            acc[g] = __fmaf_rn(w.w, m[j + 3], acc[g]);
+                        } else {
+                            acc[g] = __fadd_rn(acc[g], __fmul_rn(w.x, m[j]));
+                            acc[g] = __fadd_rn(acc[g], __fmul_rn(w.y, m[j + 1]));
+                            acc[g] = __fadd_rn(acc[g], __fmul_rn(w.z, m[j + 2]));
+                            acc[g] = __fadd_rn(acc[g], __fmul_rn(w.w, m[j + 3]));
+                        }
                     }
-                } else {
-                    if constexpr (V == 4) {
-                        const uint2 w = *reinterpret_cast<const uint2 *>(qp + (g * D + c * V) * 2);
-                        qv[0] = bf16_lo(w.x); qv[1] = bf16_hi(w.x); qv[2] = bf16_lo(w.y); qv[3] = bf16_hi(w.y);
-                    } else {
-                        const uint4 w = *reinterpret_cast<const uint4 *>(qp + (g * D + c * V) * 2);
-                        qv[0] = bf16_lo(w.x); qv[1] = bf16_hi(w.x); qv[2] = bf16_lo(w.y); qv[3] = bf16_hi(w.y);
-                        qv[4] = bf16_lo(w.z); qv[5] = bf16_hi(w.z); qv[6] = bf16_lo(w.w); qv[7] = bf16_hi(w.w);
-                    }
-                }
-#pragma unroll
-                for (int j = 0; j < V; j++) {
-                    if constexpr (kExactProduct) acc[g] = __fmaf_rn(qv[j], m[j], acc[g]);
-                    else acc[g] = __fadd_rn(acc[g], __fmul_rn(qv[j], m[j]));
                 }
             }
+            __syncwarp();  // stage fully read
+            consumed++;
+            if (part == SPT - 1) break;  // the refill below happens after the epilogue reads
+            fill(consumed);
         }
-        const float sd = reinterpret_cast<const float *>(st + sd_off)[lane];
+        const float *ln = reinterpret_cast<const float *>(h + Ly.hdr_ln);
+        const float sd = reinterpret_cast<const float *>(h + Ly.hdr_sd)[lane];
         float best = -INFINITY;
 #pragma unroll
         for (int g = 0; g < G; g++) {
@@ -351,14 +392,8 @@ __global__ void __launch_bounds__(128, 1) k_score_stream(const StreamScoreParams
             prm.keys[(int64_t)u * Pmax + p] = encode_ordered(f32_to_bf16_rne(best));
             if (prm.scores) prm.scores[(int64_t)u * Pmax + p] = best;
         }
-        __syncwarp();  // every lane is done with this stage
-        consumed++;
-        if (lane == 0 && Tp < total) {
-            issue(Tp, slot);
-            Tp = next_tile(Tp + W);
-        }
-        Tp = __shfl_sync(0xffffffffu, Tp, 0);
-        Tc = next_tile(Tc + W);
+        __syncwarp();  // header + qf reads done
+        fill(consumed);
     }
 }
 
@@ -461,6 +496,7 @@ static int dispatch_score(const ScoreParams &prm, int q_dtype, int stats_dtype, 
 
 template <int QDT, int SDT>
 static int launch_score_stream(const StreamScoreParams &sp, int G, size_t smem, cudaStream_t st) {
+    const int grid = 148 * kScoreStreamCtas;
 #define PT_SS_CASE(G_)                                                                         \
     case G_: {                                                                                 \
         static size_t configured = 0;                                                          \
@@ -470,7 +506,7 @@ static int launch_score_stream(const StreamScoreParams &sp, int G, size_t smem, 
                                              (int)smem));                                      \
             configured = smem;                                                                 \
         }                                                                                      \
-        k_score_stream<QDT, SDT, G_><<<148, 128, smem, st>>>(sp);                              \
+        k_score_stream<QDT, SDT, G_><<<grid, kScoreStreamWarps * 32, smem, st>>>(sp);          \
         break;                                                                                 \
     }
     switch (G) {
@@ -502,19 +538,23 @@ extern "C" int pt_score(const void *q, int q_dtype, const float *norms, const vo
     const int es = stats_dtype == PT_F32 ? 4 : 2, qes = q_dtype == PT_F32 ? 4 : 2;
     const int nst_env = getenv("PT_SCORE_NST") ? atoi(getenv("PT_SCORE_NST")) : 0;
     if (lamnorm_ws && G <= 8 && (G * D * qes) % 16 == 0 && !getenv("PT_SCORE_CTA")) {
-        const size_t stage = (size_t)score_stage_bytes(D, es, G, qes);
-        const size_t hdr = ((((size_t)U * 4 + 15) & ~(size_t)15) + 4 * 4 * 8 + 127) & ~(size_t)127;
         int nst = nst_env > 0 ? nst_env : 3;
-        while (nst > 2 && hdr + 4 * nst * stage > 225 * 1024) nst--;
-        const size_t smem = hdr + 4 * nst * stage;
-        if (smem <= 225 * 1024) {
+        int cps = getenv("PT_SCORE_CPS") ? atoi(getenv("PT_SCORE_CPS")) : 8;
+        const int nch = D / V;
+        if (cps > nch) cps = nch;
+        if (cps < 1) cps = 1;
+        const ScoreStreamLayout Ly = score_stream_layout(D, es, G, qes, nst, cps);
+        const size_t ps_bytes = ((size_t)U * 4 + 15) & ~(size_t)15;
+        const size_t hdr0 = (ps_bytes + (size_t)kScoreStreamWarps * nst * 8 + 127) & ~(size_t)127;
+        const size_t smem = hdr0 + (size_t)kScoreStreamWarps * Ly.per_warp;
+        if (smem * kScoreStreamCtas <= 226 * 1024) {
             const int rows = U * G;
             if (q_dtype == PT_F32)
                 k_lam_norms<PT_F32><<<(rows + 127) / 128, 128, 0, st>>>(q, norms, rows, G, D, lam, lamnorm_ws);
             else
                 k_lam_norms<PT_BF16><<<(rows + 127) / 128, 128, 0, st>>>(q, norms, rows, G, D, lam, lamnorm_ws);
             PT_CUDA_TRY(cudaGetLastError());
-            StreamScoreParams sp{q, lamnorm_ws, means, stds, seq_len, keys, scores, U, D, S, Pmax, nst};
+            StreamScoreParams sp{q, lamnorm_ws, means, stds, seq_len, keys, scores, U, D, S, Pmax, nst, cps};
             if (q_dtype == PT_F32 && stats_dtype == PT_F32) return launch_score_stream<PT_F32, PT_F32>(sp, G, smem, st);
             if (q_dtype == PT_BF16 && stats_dtype == PT_F32) return launch_score_stream<PT_BF16, PT_F32>(sp, G, smem, st);
             if (q_dtype == PT_BF16 && stats_dtype == PT_BF16) return launch_score_stream<PT_BF16, PT_BF16>(sp, G, smem, st);
