@@ -414,6 +414,10 @@ def main():
         tune["score_cta"] = timeit(lambda: eng.score(qs[0]))
         os.environ.pop("PT_SCORE_CTA")
         tune["select"] = timeit(lambda: eng.select())
+        for nt in ("256", "1024"):
+            os.environ["PT_TOPK_THREADS"] = nt
+            tune[f"select_nt{nt}"] = timeit(lambda: eng.select())
+        os.environ.pop("PT_TOPK_THREADS")
         # same byte count, contiguous pages instead of the selected (scattered) ones
         saved = eng.sel.clone()
         eng.sel.copy_(cache.page_table[:, : eng.k])

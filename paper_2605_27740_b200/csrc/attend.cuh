@@ -687,44 +687,57 @@ __host__ __device__ __forceinline__ size_t attn_stream_hdr(int U, int NW, int L,
     return (b + 1023) & ~(size_t)1023;
 }
 
-// merge the nparts partials of unit u (one warp): lanes own d = lane + 32 i, so every
-// load is coalesced; the per-part scale factors are computed once per head.
+// merge the nparts partials of unit u (one warp).  All (m, l) pairs are fetched at once
+// (lane w holds part w), the per-part scale factors come from warp reductions, and the
+// accumulator loads are issued 8 parts at a time (lanes own d = lane + 32 i: coalesced).
 template <int D>
 __device__ __noinline__ void merge_unit(const StreamParams &p, int u, int nparts, int lane) {
     const float *wacc = p.ws;
     const float *wml = p.ws + (size_t)p.U * p.maxparts * p.G * D;
-    for (int g = 0; g < p.G; g++) {
-        float mw[2], lw[2];
+    constexpr int DI = D / 32;
+    float mw[2][8], lw[2][8];
 #pragma unroll
-        for (int h = 0; h < 2; h++) {
-            const int w = lane + 32 * h;
+    for (int h = 0; h < 2; h++) {
+        const int w = lane + 32 * h;
+#pragma unroll
+        for (int g = 0; g < 8; g++) {
+            const bool ok = w < nparts && g < p.G;
             const int64_t sl = ((int64_t)u * p.maxparts + w) * p.G + g;
-            mw[h] = w < nparts ? __ldcg(&wml[sl * 2]) : -INFINITY;
-            lw[h] = w < nparts ? __ldcg(&wml[sl * 2 + 1]) : 0.f;
+            mw[h][g] = ok ? __ldcg(&wml[sl * 2]) : -INFINITY;
+            lw[h][g] = ok ? __ldcg(&wml[sl * 2 + 1]) : 0.f;
         }
-        float mt = fmaxf(mw[0], mw[1]);
+    }
+    for (int g = 0; g < p.G; g++) {
+        float mt = fmaxf(mw[0][g], mw[1][g]);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, o));
-        float f[2], lt = 0.f;
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-            f[h] = exp2f(mw[h] - mt);
-            lt += lw[h] * f[h];
-        }
+        const float f0 = exp2f(mw[0][g] - mt), f1 = exp2f(mw[1][g] - mt);
+        float lt = lw[0][g] * f0 + lw[1][g] * f1;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) lt += __shfl_xor_sync(0xffffffffu, lt, o);
-        const float inv = 1.f / lt;
-        float a[D / 32];
+        float a[DI];
 #pragma unroll
-        for (int i = 0; i < D / 32; i++) a[i] = 0.f;
-        for (int w = 0; w < nparts; w++) {
-            const float fw = __shfl_sync(0xffffffffu, f[w >> 5], w & 31);
-            const float *src = wacc + (((int64_t)u * p.maxparts + w) * p.G + g) * D;
+        for (int i = 0; i < DI; i++) a[i] = 0.f;
+        for (int w0 = 0; w0 < nparts; w0 += 8) {
+            float v[8][DI];
 #pragma unroll
-            for (int i = 0; i < D / 32; i++) a[i] = fmaf(__ldcg(src + lane + 32 * i), fw, a[i]);
+            for (int j = 0; j < 8; j++) {
+                const int w = w0 + j;
+                const float *src = wacc + (((int64_t)u * p.maxparts + w) * p.G + g) * D + lane;
+#pragma unroll
+                for (int i = 0; i < DI; i++) v[j][i] = w < nparts ? __ldcg(src + 32 * i) : 0.f;
+            }
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                const int w = w0 + j;
+                const float fw = __shfl_sync(0xffffffffu, (w & 32) ? f1 : f0, w & 31);
+#pragma unroll
+                for (int i = 0; i < DI; i++) a[i] = fmaf(v[j][i], w < nparts ? fw : 0.f, a[i]);
+            }
         }
+        const float inv = 1.f / lt;
 #pragma unroll
-        for (int i = 0; i < D / 32; i++) p.out[((int64_t)u * p.G + g) * D + lane + 32 * i] = a[i] * inv;
+        for (int i = 0; i < DI; i++) p.out[((int64_t)u * p.G + g) * D + lane + 32 * i] = a[i] * inv;
         if (lane == 0) p.lse[u * p.G + g] = (mt + log2f(lt)) * kLn2;
     }
 }
@@ -748,25 +761,29 @@ __global__ void __launch_bounds__(128) k_attend_stream(const __grid_constant__ C
                      warp * nstage;
     char *my_stages = smem + attn_stream_hdr(U, NW, L, nstage) + (size_t)warp * nstage * STAGE_BYTES;
 
-    // exclusive prefix sum of n_sel (every CTA; one warp, U is small)
+    // exclusive prefix sum of n_sel (every CTA): one coalesced load round, then a
+    // shared-memory scan by warp 0
+    for (int i = threadIdx.x; i < U; i += blockDim.x) off[i] = prm.n_sel[i];
+    if (lane == 0) {
+        for (int i = 0; i < nstage; i++) mbar_init(&bars[i], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
     if (warp == 0) {
         int carry = 0;
         for (int base = 0; base < U; base += 32) {
-            const int u = base + lane;
-            int v = u < U ? prm.n_sel[u] : 0, inc = v;
+            const int uu = base + lane;
+            const int v = uu < U ? off[uu] : 0;
+            int inc = v;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const int x = __shfl_up_sync(0xffffffffu, inc, o);
                 if (lane >= o) inc += x;
             }
-            if (u < U) off[u] = carry + inc - v;
+            if (uu < U) off[uu] = carry + inc - v;
             carry += __shfl_sync(0xffffffffu, inc, 31);
         }
         if (lane == 0) off[U] = carry;
-    }
-    if (lane == 0) {
-        for (int i = 0; i < nstage; i++) mbar_init(&bars[i], 1);
-        fence_mbar_init();
     }
     __syncthreads();
     const int T = off[U];
@@ -821,20 +838,34 @@ __global__ void __launch_bounds__(128) k_attend_stream(const __grid_constant__ C
     const int g0 = 2 * (lane & 3);
     uint32_t qb[KS][2];
     load_qfrag<D>(prm, u, lane, qb);
+    // tail page of a unit: (physical id, rows); lane 0 loads, shuffled to the warp
+    auto tail_of = [&](int uu, int &tpid, int &trows) {
+        int n = 0, pid = -1;
+        if (lane == 0) {
+            n = prm.seq_len[uu];
+            const int P = (n + S - 1) / S;
+            pid = prm.page_table[(int64_t)uu * prm.Pmax + P - 1];
+        }
+        n = __shfl_sync(0xffffffffu, n, 0);
+        tpid = __shfl_sync(0xffffffffu, pid, 0);
+        trows = n - ((n + S - 1) / S - 1) * S;
+    };
+    int tail_pid, tail_rows;
+    tail_of(u, tail_pid, tail_rows);
     int pos = a;
     while (pos < b) {
         // segment of unit u: [pos, seg_end)
         const int seg_end = min(b, off[u + 1]);
-        const int n = prm.seq_len[u];
-        const int P = (n + S - 1) / S;
-        const int tail_pid = prm.page_table[(int64_t)u * prm.Pmax + P - 1];
-        const int tail_rows = n - (P - 1) * S;
-        // q of the next (non-empty) unit is fetched while this segment computes
+        // q and tail page of the next (non-empty) unit are fetched while this one computes
         uint32_t qn[KS][2];
         const bool more = seg_end < b;
         int nu = u + 1;
         while (nu < U - 1 && off[nu + 1] <= seg_end) nu++;
-        if (more) load_qfrag<D>(prm, nu, lane, qn);
+        int ntail_pid = -1, ntail_rows = 0;
+        if (more) {
+            load_qfrag<D>(prm, nu, lane, qn);
+            tail_of(nu, ntail_pid, ntail_rows);
+        }
         float acc[KS][4];
 #pragma unroll
         for (int i = 0; i < KS; i++) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
@@ -912,6 +943,8 @@ __global__ void __launch_bounds__(128) k_attend_stream(const __grid_constant__ C
         }
         if (!more) break;
         u = nu;
+        tail_pid = ntail_pid;
+        tail_rows = ntail_rows;
 #pragma unroll
         for (int ks = 0; ks < KS; ks++) { qb[ks][0] = qn[ks][0]; qb[ks][1] = qn[ks][1]; }
     }

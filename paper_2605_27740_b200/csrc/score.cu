@@ -16,6 +16,7 @@
 // warp-wide step one contiguous 512-byte, 128-bit-per-lane load with lane = page.
 #include <stdlib.h>
 
+#include "score_stream.cuh"
 #include "select.cuh"
 
 namespace pt {
@@ -191,211 +192,14 @@ __global__ void __launch_bounds__(128) k_score(const ScoreParams prm) {
         reinterpret_cast<uint4 *>(sk)[i] = __ldcg(src + i);
     __syncthreads();
     __shared__ SelectShared<kFusedThreads> ssh;
+    __shared__ int sbins[kSelectBins];
     const int k = prm.k;
-    select_block<kFusedThreads>(sk, P, k, prm.page_table + u * Pmax, prm.sel + u * (int64_t)k,
+    select_block<kFusedThreads>(sk, sbins, P, k, prm.page_table + u * Pmax, prm.sel + u * (int64_t)k,
                                 prm.sel_logical ? prm.sel_logical + u * (int64_t)k : nullptr,
                                 prm.n_sel + u, prm.kth + u, prm.kplus1 + u, ssh);
 }
 
 
-// ===========================================================================
-// Streaming scoring kernel (default path).
-//
-// A persistent grid of warps (3 CTAs x 4 warps per SM); warp gw scores the 32-page tiles
-// T = gw, gw + W, ... of the unit-major tile space.  Each warp streams its tiles through
-// its own ring of NST small shared-memory stages, one stage = one contiguous d-range of a
-// tile (CPS 16-byte chunks of all 32 pages = CPS*512 bytes, a single cp.async.bulk ->
-// UBLKCP), with lane 0 running NST stages ahead.  The first stage of a tile also brings the
-// tile header -- the unit's G query rows, lam*||q_g|| (padded to 8) and the 32 page stds --
-// into one of NHDR header slots; the query rows are widened once per tile into a per-warp
-// f32 buffer read by broadcast.  Lane l = page l walks its mean vector in the reference's
-// sequential d order (bit-identical scores).  Bytes in flight are decoupled from registers,
-// and 12 warps per SM hide the dependent FADD chains.
-// ===========================================================================
-struct StreamScoreParams {
-    const void *q;
-    const float *lamnorm;   // [U][8]: fl(lam * norm_g), padded
-    const void *means;
-    const float *stds;
-    const int32_t *seq_len;
-    uint16_t *keys;
-    float *scores;
-    int U, D, S, Pmax, nst, cps;
-};
-
-constexpr int kScoreStreamWarps = 4;
-constexpr int kScoreStreamCtas = 3;  // per SM
-
-struct ScoreStreamLayout {  // per-warp shared-memory carve-up (bytes)
-    int stage, hdr, nhdr, qf, per_warp, hdr_q, hdr_ln, hdr_sd;
-};
-
-__host__ __device__ __forceinline__ ScoreStreamLayout score_stream_layout(int D, int es, int G,
-                                                                           int qes, int nst,
-                                                                           int cps) {
-    ScoreStreamLayout L;
-    const int nch = D / (16 / es);
-    const int spt = (nch + cps - 1) / cps;
-    L.stage = cps * 512;
-    L.hdr_q = 0;
-    L.hdr_ln = (G * D * qes + 15) & ~15;
-    L.hdr_sd = L.hdr_ln + 32;
-    L.hdr = (L.hdr_sd + 128 + 127) & ~127;
-    L.nhdr = nst / spt + 2;
-    L.qf = (G * D * 4 + 127) & ~127;
-    L.per_warp = nst * L.stage + L.nhdr * L.hdr + L.qf;
-    return L;
-}
-
-template <int QDT, int SDT, int G>
-__global__ void __launch_bounds__(kScoreStreamWarps * 32, kScoreStreamCtas)
-    k_score_stream(const StreamScoreParams prm) {
-    constexpr int V = MeanVec<SDT>::V;
-    constexpr int ES = SDT == PT_F32 ? 4 : 2;
-    constexpr int QES = QDT == PT_F32 ? 4 : 2;
-    constexpr bool kExactProduct = (QDT == PT_BF16 && SDT == PT_BF16);
-    extern __shared__ __align__(128) char smem[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
-    const int D = prm.D, S = prm.S, Pmax = prm.Pmax, U = prm.U, NST = prm.nst, CPS = prm.cps;
-    const int nch = D / V;
-    const int SPT = (nch + CPS - 1) / CPS;  // stages per tile
-    const int TPU = Pmax >> 5;
-    const long long total = (long long)U * TPU;
-    const int W = gridDim.x * NW;
-    const int gw = blockIdx.x * NW + warp;
-    const ScoreStreamLayout Ly = score_stream_layout(D, ES, G, QES, NST, CPS);
-    const int tile_bytes = 32 * D * ES;
-    const int q_bytes = G * D * QES;
-    // [Ps: U ints][mbarriers NW*NST][pad 128][warp regions: rings | headers | qf]
-    int *Ps = reinterpret_cast<int *>(smem);
-    const size_t ps_bytes = ((size_t)U * 4 + 15) & ~(size_t)15;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + ps_bytes) + warp * NST;
-    const size_t hdr0 = (ps_bytes + (size_t)NW * NST * 8 + 127) & ~(size_t)127;
-    char *wbase = smem + hdr0 + (size_t)warp * Ly.per_warp;
-    char *ring = wbase;
-    char *hdrs = wbase + NST * Ly.stage;
-    float *qf = reinterpret_cast<float *>(hdrs + Ly.nhdr * Ly.hdr);
-    for (int i = threadIdx.x; i < U; i += blockDim.x) Ps[i] = (prm.seq_len[i] + S - 1) / S;
-    if (lane == 0) {
-        for (int i = 0; i < NST; i++) mbar_init(&bars[i], 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-
-    auto next_tile = [&](long long T) -> long long {
-        while (T < total) {
-            const int u = (int)(T / TPU), t = (int)(T - (long long)u * TPU);
-            if (t * 32 < Ps[u]) return T;
-            T += W;
-        }
-        return total;
-    };
-    // producer state (lane 0 drives; kept uniform across the warp)
-    long long pT = next_tile(gw);
-    int p_part = 0, p_tile_seq = 0, issued = 0;
-    auto fill = [&](int consumed) {
-        while (pT < total && issued < consumed + NST) {
-            if (lane == 0) {
-                const int slot = issued % NST;
-                const int u = (int)(pT / TPU), t = (int)(pT - (long long)u * TPU);
-                const int c0 = p_part * CPS, c1 = min(nch, c0 + CPS);
-                const uint32_t bytes = (uint32_t)(c1 - c0) * 512;
-                uint32_t tx = bytes;
-                const uint32_t qcopy = (uint32_t)((q_bytes + 15) & ~15);
-                if (p_part == 0) tx += qcopy + 32 + 128;
-                mbar_arrive_expect_tx(&bars[slot], tx);
-                bulk_g2s(ring + slot * Ly.stage,
-                         static_cast<const char *>(prm.means) +
-                             ((int64_t)u * Pmax + (int64_t)t * 32) * D * ES + c0 * 512,
-                         bytes, &bars[slot]);
-                if (p_part == 0) {
-                    char *h = hdrs + (p_tile_seq % Ly.nhdr) * Ly.hdr;
-                    bulk_g2s(h + Ly.hdr_q, static_cast<const char *>(prm.q) + (int64_t)u * q_bytes,
-                             qcopy, &bars[slot]);
-                    bulk_g2s(h + Ly.hdr_ln, prm.lamnorm + (int64_t)u * 8, 32, &bars[slot]);
-                    bulk_g2s(h + Ly.hdr_sd, prm.stds + (int64_t)u * Pmax + t * 32, 128, &bars[slot]);
-                }
-            }
-            issued++;
-            if (++p_part == SPT) {
-                p_part = 0;
-                p_tile_seq++;
-                pT = next_tile(pT + W);
-            }
-        }
-    };
-    fill(0);
-    int consumed = 0, tile_seq = 0;
-    for (long long T = next_tile(gw); T < total; T = next_tile(T + W), tile_seq++) {
-        const int u = (int)(T / TPU), t = (int)(T - (long long)u * TPU);
-        const char *h = hdrs + (tile_seq % Ly.nhdr) * Ly.hdr;
-        float acc[G];
-#pragma unroll
-        for (int g = 0; g < G; g++) acc[g] = 0.0f;
-        for (int part = 0; part < SPT; part++) {
-            const int slot = consumed % NST;
-            mbar_wait(&bars[slot], (uint32_t)((consumed / NST) & 1));
-            if (part == 0) {  // widen this tile's query rows once
-                for (int i = lane; i < G * D; i += 32) {
-                    if constexpr (QDT == PT_F32) qf[i] = reinterpret_cast<const float *>(h + Ly.hdr_q)[i];
-                    else qf[i] = bf16_bits_to_f32(reinterpret_cast<const uint16_t *>(h + Ly.hdr_q)[i]);
-                }
-                __syncwarp();
-            }
-            const char *mp = ring + slot * Ly.stage + lane * 16;
-            const int c0 = part * CPS, c1 = min(nch, c0 + CPS);
-#pragma unroll 2
-            for (int c = c0; c < c1; c++) {
-                float m[V];
-                if constexpr (SDT == PT_F32) {
-                    const float4 v = *reinterpret_cast<const float4 *>(mp + (c - c0) * 512);
-                    m[0] = v.x; m[1] = v.y; m[2] = v.z; m[3] = v.w;
-                } else {
-                    const uint4 v = *reinterpret_cast<const uint4 *>(mp + (c - c0) * 512);
-                    m[0] = bf16_lo(v.x); m[1] = bf16_hi(v.x); m[2] = bf16_lo(v.y); m[3] = bf16_hi(v.y);
-                    m[4] = bf16_lo(v.z); m[5] = bf16_hi(v.z); m[6] = bf16_lo(v.w); m[7] = bf16_hi(v.w);
-                }
-#pragma unroll
-                for (int g = 0; g < G; g++) {
-#pragma unroll
-                    for (int j = 0; j < V; j += 4) {
-                        const float4 w = *reinterpret_cast<const float4 *>(qf + g * D + c * V + j);
-                        if constexpr (kExactProduct) {
-                            acc[g] = __fmaf_rn(w.x, m[j], acc[g]);
-                            acc[g] = __fmaf_rn(w.y, m[j + 1], acc[g]);
-                            acc[g] = __fmaf_rn(w.z, m[j + 2], acc[g]);
-                            acc[g] = __fmaf_rn(w.w, m[j + 3], acc[g]);
-                        } else {
-                            acc[g] = __fadd_rn(acc[g], __fmul_rn(w.x, m[j]));
-                            acc[g] = __fadd_rn(acc[g], __fmul_rn(w.y, m[j + 1]));
-                            acc[g] = __fadd_rn(acc[g], __fmul_rn(w.z, m[j + 2]));
-                            acc[g] = __fadd_rn(acc[g], __fmul_rn(w.w, m[j + 3]));
-                        }
-                    }
-                }
-            }
-            __syncwarp();  // stage fully read
-            consumed++;
-            if (part == SPT - 1) break;  // the refill below happens after the epilogue reads
-            fill(consumed);
-        }
-        const float *ln = reinterpret_cast<const float *>(h + Ly.hdr_ln);
-        const float sd = reinterpret_cast<const float *>(h + Ly.hdr_sd)[lane];
-        float best = -INFINITY;
-#pragma unroll
-        for (int g = 0; g < G; g++) {
-            const float a = __fadd_rn(acc[g], __fmul_rn(ln[g], sd));
-            if (a > best) best = a;
-        }
-        const int p = t * 32 + lane;
-        if (p < Ps[u]) {
-            prm.keys[(int64_t)u * Pmax + p] = encode_ordered(f32_to_bf16_rne(best));
-            if (prm.scores) prm.scores[(int64_t)u * Pmax + p] = best;
-        }
-        __syncwarp();  // header + qf reads done
-        fill(consumed);
-    }
-}
 
 // lam * ||q_g|| for every (unit, g), numpy's float64 order (scoring.py:45), padded to 8
 template <int QDT>
@@ -494,36 +298,10 @@ static int dispatch_score(const ScoreParams &prm, int q_dtype, int stats_dtype, 
     return PT_ERR_INVALID;
 }
 
-template <int QDT, int SDT>
-static int launch_score_stream(const StreamScoreParams &sp, int G, size_t smem, cudaStream_t st) {
-    const int grid = 148 * kScoreStreamCtas;
-#define PT_SS_CASE(G_)                                                                         \
-    case G_: {                                                                                 \
-        static size_t configured = 0;                                                          \
-        if (smem > configured) {                                                               \
-            PT_CUDA_TRY(cudaFuncSetAttribute(k_score_stream<QDT, SDT, G_>,                     \
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,     \
-                                             (int)smem));                                      \
-            configured = smem;                                                                 \
-        }                                                                                      \
-        k_score_stream<QDT, SDT, G_><<<grid, kScoreStreamWarps * 32, smem, st>>>(sp);          \
-        break;                                                                                 \
-    }
-    switch (G) {
-        PT_SS_CASE(1)
-        PT_SS_CASE(2)
-        PT_SS_CASE(3)
-        PT_SS_CASE(4)
-        PT_SS_CASE(5)
-        PT_SS_CASE(6)
-        PT_SS_CASE(7)
-        PT_SS_CASE(8)
-        default: return PT_ERR_UNSUPPORTED;
-    }
-#undef PT_SS_CASE
-    PT_CUDA_TRY(cudaGetLastError());
-    return PT_OK;
-}
+namespace pt {
+int launch_score_stream_q32(const StreamScoreParams &sp, int sdt, int G, int D, cudaStream_t st);
+int launch_score_stream_q16(const StreamScoreParams &sp, int sdt, int G, int D, cudaStream_t st);
+}  // namespace pt
 
 extern "C" int pt_score(const void *q, int q_dtype, const float *norms, const void *means,
                         int stats_dtype, const float *stds, const int32_t *seq_len, int U, int G,
@@ -536,31 +314,18 @@ extern "C" int pt_score(const void *q, int q_dtype, const float *norms, const vo
     if (U == 0) return PT_OK;
     cudaStream_t st = (cudaStream_t)stream;
     const int es = stats_dtype == PT_F32 ? 4 : 2, qes = q_dtype == PT_F32 ? 4 : 2;
-    const int nst_env = getenv("PT_SCORE_NST") ? atoi(getenv("PT_SCORE_NST")) : 0;
-    if (lamnorm_ws && G <= 8 && (G * D * qes) % 16 == 0 && !getenv("PT_SCORE_CTA")) {
-        int nst = nst_env > 0 ? nst_env : 3;
-        int cps = getenv("PT_SCORE_CPS") ? atoi(getenv("PT_SCORE_CPS")) : 8;
-        const int nch = D / V;
-        if (cps > nch) cps = nch;
-        if (cps < 1) cps = 1;
-        const ScoreStreamLayout Ly = score_stream_layout(D, es, G, qes, nst, cps);
-        const size_t ps_bytes = ((size_t)U * 4 + 15) & ~(size_t)15;
-        const size_t hdr0 = (ps_bytes + (size_t)kScoreStreamWarps * nst * 8 + 127) & ~(size_t)127;
-        const size_t smem = hdr0 + (size_t)kScoreStreamWarps * Ly.per_warp;
-        if (smem * kScoreStreamCtas <= 226 * 1024) {
-            const int rows = U * G;
-            if (q_dtype == PT_F32)
-                k_lam_norms<PT_F32><<<(rows + 127) / 128, 128, 0, st>>>(q, norms, rows, G, D, lam, lamnorm_ws);
-            else
-                k_lam_norms<PT_BF16><<<(rows + 127) / 128, 128, 0, st>>>(q, norms, rows, G, D, lam, lamnorm_ws);
-            PT_CUDA_TRY(cudaGetLastError());
-            StreamScoreParams sp{q, lamnorm_ws, means, stds, seq_len, keys, scores, U, D, S, Pmax, nst, cps};
-            if (q_dtype == PT_F32 && stats_dtype == PT_F32) return launch_score_stream<PT_F32, PT_F32>(sp, G, smem, st);
-            if (q_dtype == PT_BF16 && stats_dtype == PT_F32) return launch_score_stream<PT_BF16, PT_F32>(sp, G, smem, st);
-            if (q_dtype == PT_BF16 && stats_dtype == PT_BF16) return launch_score_stream<PT_BF16, PT_BF16>(sp, G, smem, st);
-            if (q_dtype == PT_F32 && stats_dtype == PT_BF16) return launch_score_stream<PT_F32, PT_BF16>(sp, G, smem, st);
-            return PT_ERR_INVALID;
-        }
+    if (lamnorm_ws && G <= 8 && (D == 64 || D == 128) && !getenv("PT_SCORE_CTA") &&
+        (long long)U * (Pmax / 32) < (1LL << 31)) {
+        const int rows = U * G;
+        if (q_dtype == PT_F32)
+            k_lam_norms<PT_F32><<<(rows + 127) / 128, 128, 0, st>>>(q, norms, rows, G, D, lam, lamnorm_ws);
+        else
+            k_lam_norms<PT_BF16><<<(rows + 127) / 128, 128, 0, st>>>(q, norms, rows, G, D, lam, lamnorm_ws);
+        PT_CUDA_TRY(cudaGetLastError());
+        StreamScoreParams sp{q, lamnorm_ws, means, stds, seq_len, keys, scores, U, S, Pmax};
+        const int rc = q_dtype == PT_F32 ? launch_score_stream_q32(sp, stats_dtype, G, D, st)
+                                         : launch_score_stream_q16(sp, stats_dtype, G, D, st);
+        if (rc != PT_ERR_UNSUPPORTED) return rc;
     }
     ScoreParams prm{};
     prm.q = q; prm.norms_in = norms; prm.means = means; prm.stds = stds; prm.seq_len = seq_len;

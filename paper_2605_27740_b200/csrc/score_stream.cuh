@@ -1,0 +1,241 @@
+// score_stream.cuh -- K2 streaming scoring kernel (default path), fully specialised on
+// (query dtype, stats dtype, G, D) so every index is a compile-time constant.
+//
+// Restates, per page p of unit u (see score.cu for the reference citations):
+//   acc_g = fl(... fl(fl(0 + fl(q[g,0]*m[p,0])) + fl(q[g,1]*m[p,1])) ...)  (sequential d)
+//   score = max_g fl(acc_g + fl(fl(lam*norm_g) * std_p));  key = ordered(bf16_rne(score))
+// bit-identical to _kernels_cy.pyx:19-43 (non-FMA x86 build).
+//
+// Structure: a persistent grid (3 CTAs x 4 warps per SM); warp gw owns the 32-page tiles
+// T = gw, gw + W, ... of the unit-major tile space, so units complete progressively.  Each
+// warp streams its tiles through a private ring of NST = 3 stages; one stage = CPS 16-byte
+// chunks of all 32 pages of a tile = one contiguous block of CPS*512 bytes in the
+// page-interleaved means layout, fetched by a single cp.async.bulk (UBLKCP) on the stage's
+// mbarrier.  The first stage of a tile also fetches the tile header (the unit's G query
+// rows, lam*||q_g|| padded to 8, the 32 page stds) into one of NHDR header slots.  The query
+// rows are widened once per tile into a head-pair-interleaved f32 buffer so each 16-byte
+// broadcast read yields (q_g[d], q_g+1[d], q_g[d+1], q_g+1[d+1]); products of two heads are
+// formed by one FMUL2 and accumulated by scalar FADDs (two roundings, as the reference --
+// an f32x2 add after an f32x2 mul would be contracted to FFMA2 by ptxas).  With bf16 x bf16
+// operands the products are exact in f32, so FFMA2 is bit-identical and used.
+#pragma once
+#include "common.cuh"
+
+namespace pt {
+
+struct StreamScoreParams {
+    const void *q;
+    const float *lamnorm;  // [U][8]: fl(lam * norm_g), padded
+    const void *means;
+    const float *stds;
+    const int32_t *seq_len;
+    uint16_t *keys;
+    float *scores;
+    int U, S, Pmax;
+};
+
+constexpr int kSSWarps = 4;
+constexpr int kSSCtas = 3;  // per SM
+constexpr int kSSNst = 3;   // ring stages per warp
+
+__device__ __forceinline__ float2 ss_mul2(float m, float2 q) {
+    unsigned long long r;
+    const float2 mm = make_float2(m, m);
+    asm("mul.rn.f32x2 %0, %1, %2;"
+        : "=l"(r)
+        : "l"(*reinterpret_cast<const unsigned long long *>(&mm)),
+          "l"(*reinterpret_cast<const unsigned long long *>(&q)));
+    return *reinterpret_cast<float2 *>(&r);
+}
+__device__ __forceinline__ float2 ss_fma2(float m, float2 q, float2 acc) {
+    unsigned long long r;
+    const float2 mm = make_float2(m, m);
+    asm("fma.rn.f32x2 %0, %1, %2, %3;"
+        : "=l"(r)
+        : "l"(*reinterpret_cast<const unsigned long long *>(&mm)),
+          "l"(*reinterpret_cast<const unsigned long long *>(&q)),
+          "l"(*reinterpret_cast<const unsigned long long *>(&acc)));
+    return *reinterpret_cast<float2 *>(&r);
+}
+
+template <int QDT, int SDT, int G, int D>
+struct SSCfg {
+    static constexpr int ES = SDT == PT_F32 ? 4 : 2;
+    static constexpr int QES = QDT == PT_F32 ? 4 : 2;
+    static constexpr int V = 16 / ES;            // means per 16-byte chunk
+    static constexpr int NCH = D / V;            // chunks per page row
+    static constexpr int CPS = NCH < 8 ? NCH : 8;
+    static constexpr int SPT = NCH / CPS;        // stages per tile
+    static constexpr int GP2 = (G + 1) / 2;      // head pairs
+    static constexpr int STAGE = CPS * 512;
+    static constexpr int HDR_LN = (G * D * QES + 15) & ~15;
+    static constexpr int HDR_SD = HDR_LN + 32;
+    static constexpr int HDR = (HDR_SD + 128 + 127) & ~127;
+    static constexpr int NHDR = kSSNst / SPT + 2;
+    static constexpr int QF = (GP2 * 2 * D * 4 + 127) & ~127;
+    static constexpr int PER_WARP = kSSNst * STAGE + NHDR * HDR + QF;
+    static constexpr uint32_t QCOPY = (uint32_t)((G * D * QES + 15) & ~15);
+    static_assert(NCH % CPS == 0, "chunks per stage must divide the row");
+};
+
+__host__ __device__ __forceinline__ size_t ss_hdr_bytes(int U) {
+    const size_t ps = ((size_t)U * 4 + 15) & ~(size_t)15;
+    return (ps + (size_t)kSSWarps * kSSNst * 8 + 127) & ~(size_t)127;
+}
+
+template <int QDT, int SDT, int G, int D>
+__global__ void __launch_bounds__(kSSWarps * 32, kSSCtas) k_score_stream(const StreamScoreParams prm) {
+    using C = SSCfg<QDT, SDT, G, D>;
+    constexpr bool kExactProduct = (QDT == PT_BF16 && SDT == PT_BF16);
+    constexpr int NST = kSSNst;
+    extern __shared__ __align__(128) char smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int S = prm.S, Pmax = prm.Pmax, U = prm.U;
+    const int TPU = Pmax >> 5;
+    const int W = gridDim.x * kSSWarps;
+    const int gw = blockIdx.x * kSSWarps + warp;
+    int *Ps = reinterpret_cast<int *>(smem);
+    uint64_t *bars =
+        reinterpret_cast<uint64_t *>(smem + (((size_t)U * 4 + 15) & ~(size_t)15)) + warp * NST;
+    char *wbase = smem + ss_hdr_bytes(U) + (size_t)warp * C::PER_WARP;
+    char *ring = wbase;
+    char *hdrs = wbase + NST * C::STAGE;
+    float *qf = reinterpret_cast<float *>(hdrs + C::NHDR * C::HDR);
+    for (int i = threadIdx.x; i < U; i += blockDim.x) Ps[i] = (prm.seq_len[i] + S - 1) / S;
+    if (lane == 0) {
+        for (int i = 0; i < NST; i++) mbar_init(&bars[i], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    // tile cursors (u, t): advance by W tiles, skipping tiles past a unit's last page
+    auto settle = [&](int &u, int &t) {
+        while (u < U) {
+            while (t >= TPU) { t -= TPU; ++u; }
+            if (u >= U || t * 32 < Ps[u]) return;
+            t += W;
+        }
+    };
+    int pu = gw / TPU, pt = gw - (gw / TPU) * TPU;  // producer
+    settle(pu, pt);
+    int cu = pu, ct = pt;                            // consumer
+    int p_part = 0, p_seq = 0, issued = 0;
+    auto fill = [&](int consumed) {
+        while (pu < U && issued < consumed + NST) {
+            if (lane == 0) {
+                const int slot = issued % NST;
+                const char *gsrc = static_cast<const char *>(prm.means) +
+                                   ((int64_t)pu * Pmax + (int64_t)pt * 32) * D * C::ES;
+                uint32_t tx = C::STAGE;
+                if (p_part == 0) tx += C::QCOPY + 32 + 128;
+                mbar_arrive_expect_tx(&bars[slot], tx);
+                bulk_g2s(ring + slot * C::STAGE, gsrc + p_part * C::STAGE, C::STAGE, &bars[slot]);
+                if (p_part == 0) {
+                    char *h = hdrs + (p_seq % C::NHDR) * C::HDR;
+                    bulk_g2s(h, static_cast<const char *>(prm.q) + (int64_t)pu * G * D * C::QES,
+                             C::QCOPY, &bars[slot]);
+                    bulk_g2s(h + C::HDR_LN, prm.lamnorm + (int64_t)pu * 8, 32, &bars[slot]);
+                    bulk_g2s(h + C::HDR_SD, prm.stds + (int64_t)pu * Pmax + pt * 32, 128, &bars[slot]);
+                }
+            }
+            issued++;
+            if (++p_part == C::SPT) {
+                p_part = 0;
+                p_seq++;
+                pt += W;
+                settle(pu, pt);
+            }
+        }
+    };
+    fill(0);
+    int consumed = 0, seq = 0;
+    float2 *qf2 = reinterpret_cast<float2 *>(qf);
+    while (cu < U) {
+        const char *h = hdrs + (seq % C::NHDR) * C::HDR;
+        float2 acc[C::GP2];
+#pragma unroll
+        for (int g = 0; g < C::GP2; g++) acc[g] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int part = 0; part < C::SPT; part++) {
+            const int slot = consumed % NST;
+            mbar_wait(&bars[slot], (uint32_t)((consumed / NST) & 1));
+            if (part == 0) {  // widen this tile's query rows, head-pair interleaved
+#pragma unroll
+                for (int pr = 0; pr < C::GP2; pr++) {
+#pragma unroll
+                    for (int d = lane; d < D; d += 32) {
+                        float a, b = 0.f;
+                        if constexpr (QDT == PT_F32) {
+                            const float *qh = reinterpret_cast<const float *>(h);
+                            a = qh[(2 * pr) * D + d];
+                            if (2 * pr + 1 < G) b = qh[(2 * pr + 1) * D + d];
+                        } else {
+                            const uint16_t *qh = reinterpret_cast<const uint16_t *>(h);
+                            a = bf16_bits_to_f32(qh[(2 * pr) * D + d]);
+                            if (2 * pr + 1 < G) b = bf16_bits_to_f32(qh[(2 * pr + 1) * D + d]);
+                        }
+                        qf2[pr * D + d] = make_float2(a, b);
+                    }
+                }
+                __syncwarp();
+            }
+            const char *mp = ring + slot * C::STAGE + lane * 16;
+#pragma unroll
+            for (int c = 0; c < C::CPS; c++) {
+                const int cc = part * C::CPS + c;  // chunk index within the page row
+                float m[C::V];
+                if constexpr (SDT == PT_F32) {
+                    const float4 v = *reinterpret_cast<const float4 *>(mp + c * 512);
+                    m[0] = v.x; m[1] = v.y; m[2] = v.z; m[3] = v.w;
+                } else {
+                    const uint4 v = *reinterpret_cast<const uint4 *>(mp + c * 512);
+                    m[0] = bf16_lo(v.x); m[1] = bf16_hi(v.x); m[2] = bf16_lo(v.y); m[3] = bf16_hi(v.y);
+                    m[4] = bf16_lo(v.z); m[5] = bf16_hi(v.z); m[6] = bf16_lo(v.w); m[7] = bf16_hi(v.w);
+                }
+#pragma unroll
+                for (int pr = 0; pr < C::GP2; pr++) {
+#pragma unroll
+                    for (int j = 0; j < C::V; j += 2) {
+                        const float4 w =
+                            *reinterpret_cast<const float4 *>(qf2 + pr * D + cc * C::V + j);
+                        if constexpr (kExactProduct) {
+                            acc[pr] = ss_fma2(m[j], make_float2(w.x, w.y), acc[pr]);
+                            acc[pr] = ss_fma2(m[j + 1], make_float2(w.z, w.w), acc[pr]);
+                        } else {
+                            const float2 p0 = ss_mul2(m[j], make_float2(w.x, w.y));
+                            acc[pr].x = __fadd_rn(acc[pr].x, p0.x);
+                            acc[pr].y = __fadd_rn(acc[pr].y, p0.y);
+                            const float2 p1 = ss_mul2(m[j + 1], make_float2(w.z, w.w));
+                            acc[pr].x = __fadd_rn(acc[pr].x, p1.x);
+                            acc[pr].y = __fadd_rn(acc[pr].y, p1.y);
+                        }
+                    }
+                }
+            }
+            __syncwarp();  // stage fully read
+            consumed++;
+            if (part < C::SPT - 1) fill(consumed);
+        }
+        const float *ln = reinterpret_cast<const float *>(h + C::HDR_LN);
+        const float sd = reinterpret_cast<const float *>(h + C::HDR_SD)[lane];
+        float best = -INFINITY;
+#pragma unroll
+        for (int g = 0; g < G; g++) {
+            const float ag = (g & 1) ? acc[g >> 1].y : acc[g >> 1].x;
+            const float a = __fadd_rn(ag, __fmul_rn(ln[g], sd));
+            if (a > best) best = a;
+        }
+        const int p = ct * 32 + lane;
+        if (p < Ps[cu]) {
+            prm.keys[(int64_t)cu * Pmax + p] = encode_ordered(f32_to_bf16_rne(best));
+            if (prm.scores) prm.scores[(int64_t)cu * Pmax + p] = best;
+        }
+        __syncwarp();  // header + qf reads done before their slots are refilled
+        fill(consumed);
+        seq++;
+        ct += W;
+        settle(cu, ct);
+    }
+}
+
+}  // namespace pt

@@ -4,9 +4,8 @@
 //
 // Restates select.py:87-115 + _kernels_cy.pyx:46-126.  The reference finds the threshold
 // key (the k-th largest) with two 8-bit radix histogram rounds; here the same key is found
-// by a 16-step bisection over the key space with block-wide counts (each thread owns a
-// contiguous segment of keys; SIMD u16 compares, no atomics -- scores cluster in one or two
-// radix buckets, which makes histogram atomics contend).  Given the threshold:
+// with one histogram over the keys' actual range (or a bisection when that range is wide).
+// Given the threshold:
 //   selected = keys > thr  +  the first (k - #>thr) keys == thr in ascending LOGICAL index
 //   (the reference's tie rule) -- an ordered compaction by block-wide
 //   exclusive scans over the contiguous segments;
@@ -68,27 +67,24 @@ __device__ __forceinline__ void block_exscan2(int a, int b, int &ea, int &eb, in
     tb = sb;
 }
 
-// number of u16 keys >= t among this thread's words i = tid, tid + NT, ... (strided:
-// bank-conflict free; the count is order independent).  Packed-pair compare without the
-// emulated SIMD intrinsics: hi >= t and lo >= t tested on the two halves.
-template <int NT>
-__device__ __forceinline__ int count_ge(const uint32_t *w, int nw, uint32_t t) {
-    int c = 0;
-    for (int i = threadIdx.x; i < nw; i += NT) {
-        const uint32_t x = w[i];
-        c += ((x & 0xFFFFu) >= t) + ((x >> 16) >= t);
-    }
-    return c;
-}
-
 // Select for one unit.  `skeys` (shared, 16-byte aligned, room for P + 1 keys) holds the
-// unit's P keys.  Writes out/out_l [k]; thread 0 writes n_sel, kth, kplus1.
+// unit's P keys; `bins` (shared, kSelectBins ints) is histogram scratch.  Writes
+// out/out_l [k]; thread 0 writes n_sel, kth, kplus1.
+//
+// Threshold search: one pass for the key range [mn, mx]; when it spans <= kSelectBins
+// values (always, in practice: scores cluster in a few dozen bf16 values) a single
+// shared-memory histogram of (key - mn) and a descending block scan over the bins give the
+// k-th largest key; otherwise a bisection over [mn, mx] with block-wide counts.
+constexpr int kSelectBins = 4096;
+
 template <int NT>
-__device__ void select_block(uint16_t *skeys, int P, int k, const int32_t *__restrict__ map,
-                             int32_t *__restrict__ out, int32_t *__restrict__ out_l,
-                             int32_t *__restrict__ n_sel, int32_t *__restrict__ kth,
-                             int32_t *__restrict__ kplus1, SelectShared<NT> &sh) {
+__device__ void select_block(uint16_t *skeys, int *bins, int P, int k,
+                             const int32_t *__restrict__ map, int32_t *__restrict__ out,
+                             int32_t *__restrict__ out_l, int32_t *__restrict__ n_sel,
+                             int32_t *__restrict__ kth, int32_t *__restrict__ kplus1,
+                             SelectShared<NT> &sh) {
     const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
     if (P <= k) {  // _take_all
         int mn = 0xFFFF;
         for (int i = tid; i < P; i += NT) {
@@ -98,7 +94,7 @@ __device__ void select_block(uint16_t *skeys, int P, int k, const int32_t *__res
         }
         mn = __reduce_min_sync(0xffffffffu, mn);
         __syncthreads();
-        if ((tid & 31) == 0) sh.warp_a[tid >> 5] = mn;
+        if (lane == 0) sh.warp_a[warp] = mn;
         __syncthreads();
         if (tid == 0) {
             int m = 0xFFFF;
@@ -109,25 +105,81 @@ __device__ void select_block(uint16_t *skeys, int P, int k, const int32_t *__res
         }
         return;
     }
-    // pad the key array to an even count with 0 (key 0 never counts for t >= 1 and is
-    // excluded explicitly below), segments of whole 32-bit words
-    if (tid == 0 && (P & 1)) skeys[P] = 0;
+    if (tid == 0 && (P & 1)) skeys[P] = skeys[P - 1];  // pad: duplicate (counted only below)
     __syncthreads();
     const uint32_t *w = reinterpret_cast<const uint32_t *>(skeys);
-    const int nw = (P + 1) >> 1;
-    const int wseg = (nw + NT - 1) / NT;
-    const int w0 = min(tid * wseg, nw), w1 = min(w0 + wseg, nw);
-    // bisection: thr = max t with #(keys >= t) >= k   (t = 0 always qualifies; the odd-P
-    // padding key 0 never counts for the probed t >= 1)
-    int lo = 0, hi = 0x10000;
-    while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        const int tot = block_sum<NT>(count_ge<NT>(w, nw, (uint32_t)mid), sh);
-        if (tot >= k) lo = mid; else hi = mid;
+    const int nw = P >> 1;  // full words; an odd tail key is handled separately
+    // ---- key range ----
+    int mn = 0xFFFF, mx = 0;
+    for (int i = tid; i < nw; i += NT) {
+        const uint32_t x = w[i];
+        const int lo = x & 0xFFFF, hi = x >> 16;
+        mn = min(mn, min(lo, hi));
+        mx = max(mx, max(lo, hi));
     }
-    const int thr = lo;
-    // per-segment counts of > thr and == thr (in logical order: key index 2*word + half)
-    const int i0 = min(2 * w0, P), i1 = min(2 * w1, P);
+    if ((P & 1) && tid == 0) { mn = min(mn, (int)skeys[P - 1]); mx = max(mx, (int)skeys[P - 1]); }
+    mn = __reduce_min_sync(0xffffffffu, mn);
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    __syncthreads();
+    if (lane == 0) { sh.warp_a[warp] = mn; sh.warp_b[warp] = mx; }
+    __syncthreads();
+    mn = 0xFFFF;
+    mx = 0;
+#pragma unroll
+    for (int i = 0; i < NT / 32; i++) { mn = min(mn, sh.warp_a[i]); mx = max(mx, sh.warp_b[i]); }
+    const int R = mx - mn + 1;
+    int thr;
+    if (R <= kSelectBins) {
+        // ---- one-pass histogram of (key - mn) ----
+        for (int i = tid; i < R; i += NT) bins[i] = 0;
+        __syncthreads();
+        for (int i = tid; i < nw; i += NT) {
+            const uint32_t x = w[i];
+            atomicAdd(&bins[(int)(x & 0xFFFF) - mn], 1);
+            atomicAdd(&bins[(int)(x >> 16) - mn], 1);
+        }
+        if ((P & 1) && tid == 0) atomicAdd(&bins[(int)skeys[P - 1] - mn], 1);
+        __syncthreads();
+        // descending segments of bins: thread t owns [top_t - seg + 1, top_t]
+        const int seg = (R + NT - 1) / NT;
+        const int top = R - 1 - tid * seg;
+        int s = 0;
+        for (int j = 0; j < seg; j++) {
+            const int bb = top - j;
+            if (bb >= 0) s += bins[bb];
+        }
+        int above, dummy, tot, dummy2;
+        block_exscan2<NT>(s, 0, above, dummy, tot, dummy2, sh);
+        __syncthreads();
+        if (above < k && above + s >= k) {  // the crossing segment
+            int cum = above;
+            for (int j = 0; j < seg; j++) {
+                const int bb = top - j;
+                cum += bins[bb];
+                if (cum >= k) { sh.warp_a[0] = mn + bb; break; }
+            }
+        }
+        __syncthreads();
+        thr = sh.warp_a[0];
+    } else {
+        // ---- bisection over [mn, mx]: thr = max t with #(keys >= t) >= k ----
+        int lo = mn, hi = mx + 1;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            int c = 0;
+            for (int i = tid; i < nw; i += NT) {
+                const uint32_t x = w[i];
+                c += ((int)(x & 0xFFFF) >= mid) + ((int)(x >> 16) >= mid);
+            }
+            if ((P & 1) && tid == 0) c += (int)skeys[P - 1] >= mid;
+            const int tot = block_sum<NT>(c, sh);
+            if (tot >= k) lo = mid; else hi = mid;
+        }
+        thr = lo;
+    }
+    // ---- ordered compaction over contiguous per-thread segments (logical order) ----
+    const int kseg = (P + NT - 1) / NT;
+    const int i0 = min(tid * kseg, P), i1 = min(i0 + kseg, P);
     int gt = 0, eq = 0, below = -1;
     for (int i = i0; i < i1; i++) {
         const int key = skeys[i];
@@ -154,7 +206,7 @@ __device__ void select_block(uint16_t *skeys, int P, int k, const int32_t *__res
     }
     below = __reduce_max_sync(0xffffffffu, below);
     __syncthreads();
-    if ((tid & 31) == 0) sh.warp_a[tid >> 5] = below;
+    if (lane == 0) sh.warp_a[warp] = below;
     __syncthreads();
     if (tid == 0) {
         int m = -1;

@@ -77,41 +77,41 @@ __global__ void __launch_bounds__(kStatsWarps * 32)
 // Phase 1 (one CTA): deterministic physical-page allocation in unit order, the
 // batched form of _alloc_page (kvcache.py:154-176): free list popped from its end
 // first (list.pop()), then the bump pointer; exhaustion -> error flag, unit skipped.
-constexpr int kAllocThreads = 1024;
-
-__global__ void __launch_bounds__(kAllocThreads)
-    k_append_alloc(int32_t *__restrict__ page_table, const int32_t *__restrict__ seq_len, int U,
-                   int S, int Pmax, int32_t *__restrict__ pool_state,
-                   const int32_t *__restrict__ free_list, int32_t *__restrict__ slot) {
-    __shared__ int warp_tot[kAllocThreads / 32];
-    __shared__ int carry;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+// Single-launch append.  CTA 0 first runs the unit-order allocation scan above for every
+// unit (k_append_alloc's body), publishes it with a release flag, and the other CTAs
+// acquire it before touching their units (CTA 0 never waits, so there is no deadlock even
+// when the grid exceeds the resident capacity; the last CTA to finish re-arms the flag).
+// Then one warp per unit writes the new K/V row and recomputes the tail page's stats from
+// a shared-memory copy of the page rows (one load round instead of 2*rows dependent ones).
+__device__ void alloc_block(int32_t *__restrict__ page_table, const int32_t *__restrict__ seq_len,
+                            int U, int S, int Pmax, int32_t *__restrict__ pool_state,
+                            const int32_t *__restrict__ free_list, int32_t *__restrict__ slot,
+                            int *warp_tot, int *carry) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
     const int bump0 = pool_state[0], free0 = pool_state[1], max_pages = pool_state[2];
-    if (tid == 0) carry = 0;
+    if (tid == 0) *carry = 0;
     __syncthreads();
-    for (int base = 0; base < U; base += kAllocThreads) {
+    for (int base = 0; base < U; base += blockDim.x) {
         const int u = base + tid;
         int n = 0, need = 0;
         if (u < U) {
             n = seq_len[u];
             need = (n % S == 0) ? 1 : 0;
         }
-        // block exclusive scan of need
-        unsigned m = __ballot_sync(0xffffffffu, need);
-        int wpre = __popc(m & ((1u << lane) - 1u));
+        const unsigned m = __ballot_sync(0xffffffffu, need);
+        const int wpre = __popc(m & ((1u << lane) - 1u));
         if (lane == 0) warp_tot[warp] = __popc(m);
         __syncthreads();
-        int before = carry;
-        for (int w = 0; w < warp; w++) before += warp_tot[w];
-        int chunk_total = 0;
-        for (int w = 0; w < kAllocThreads / 32; w++) chunk_total += warp_tot[w];
+        int before = *carry, chunk_total = 0;
+        for (int w = 0; w < nwarps; w++) {
+            if (w < warp) before += warp_tot[w];
+            chunk_total += warp_tot[w];
+        }
         const int rank = before + wpre;
         if (u < U) {
             int target;
             if (need) {
-                int pid;
-                if (rank < free0) pid = free_list[free0 - 1 - rank];
-                else pid = bump0 + (rank - free0);
+                const int pid = rank < free0 ? free_list[free0 - 1 - rank] : bump0 + (rank - free0);
                 const int lp = n / S;
                 if (pid >= max_pages || lp >= Pmax) {
                     target = -1;
@@ -126,48 +126,106 @@ __global__ void __launch_bounds__(kAllocThreads)
             slot[u] = target;
         }
         __syncthreads();
-        if (tid == 0) carry += chunk_total;
+        if (tid == 0) *carry += chunk_total;
         __syncthreads();
     }
     if (tid == 0) {
-        const int tot = carry;
+        const int tot = *carry;
         const int from_free = tot < free0 ? tot : free0;
-        int bump = bump0 + (tot - from_free);
+        const int bump = bump0 + (tot - from_free);
         pool_state[1] = free0 - from_free;
         pool_state[0] = bump < max_pages ? bump : max_pages;
     }
 }
 
-// Phase 2: one warp per unit writes the K/V row and recomputes the touched page.
 template <int DT, int SDT, int DJ>
-__global__ void __launch_bounds__(kStatsWarps * 32)
-    k_append_rows(const void *__restrict__ k_new, const void *__restrict__ v_new,
-                  void *__restrict__ k_pool, void *__restrict__ v_pool,
-                  int32_t *__restrict__ seq_len, const int32_t *__restrict__ slot, int U, int S,
-                  int D, int Pmax, void *__restrict__ means, float *__restrict__ stds) {
-    __shared__ double var_smem[kStatsWarps][kMaxD];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t u = (int64_t)blockIdx.x * kStatsWarps + warp;
-    if (u >= U) return;
-    const int pid = slot[u];
-    if (pid < 0) return;
-    const int n = seq_len[u];
-    const int row = n % S;
-    const int64_t dst = ((int64_t)pid * S + row) * D;
-    for (int d = lane; d < D; d += 32) {
-        if constexpr (DT == PT_F32) {
-            static_cast<float *>(k_pool)[dst + d] = static_cast<const float *>(k_new)[u * D + d];
-            static_cast<float *>(v_pool)[dst + d] = static_cast<const float *>(v_new)[u * D + d];
-        } else {
-            static_cast<uint16_t *>(k_pool)[dst + d] = static_cast<const uint16_t *>(k_new)[u * D + d];
-            static_cast<uint16_t *>(v_pool)[dst + d] = static_cast<const uint16_t *>(v_new)[u * D + d];
+__global__ void __launch_bounds__(256)
+    k_append(const void *__restrict__ k_new, const void *__restrict__ v_new,
+             void *__restrict__ k_pool, void *__restrict__ v_pool,
+             int32_t *__restrict__ page_table, int32_t *__restrict__ seq_len, int U, int S, int D,
+             int Pmax, void *__restrict__ means, float *__restrict__ stds,
+             int32_t *__restrict__ pool_state, const int32_t *__restrict__ free_list,
+             int32_t *__restrict__ slot) {
+    extern __shared__ __align__(16) char asmem[];
+    __shared__ int warp_tot[8];
+    __shared__ int carry;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpc = blockDim.x >> 5;
+    int *flag = slot + U, *done = slot + U + 1;
+    if (blockIdx.x == 0) {
+        alloc_block(page_table, seq_len, U, S, Pmax, pool_state, free_list, slot, warp_tot, &carry);
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) atomicExch(flag, 1);
+    } else {
+        if (threadIdx.x == 0) {
+            while (atomicAdd(flag, 0) == 0) __nanosleep(64);
+            __threadfence();
+        }
+        __syncthreads();
+    }
+    const int64_t u = (int64_t)blockIdx.x * wpc + warp;
+    const size_t per_warp = (size_t)S * D * 4 + (size_t)D * 8;
+    float *rows_s = reinterpret_cast<float *>(asmem + warp * per_warp);
+    double *var_s = reinterpret_cast<double *>(asmem + warp * per_warp + (size_t)S * D * 4);
+    if (u < U) {
+        const int pid = __ldcg(&slot[u]);
+        if (pid >= 0) {
+            const int n = seq_len[u];
+            const int row = n % S;
+            const int64_t base = (int64_t)pid * S * D;
+            // stage the page's existing rows (one load round) and the new row
+            for (int i = lane; i < row * D; i += 32) rows_s[i] = load_elem<DT>(k_pool, base + i);
+            for (int d = lane; d < D; d += 32) {
+                const float kv = load_elem<DT>(k_new, u * D + d);
+                rows_s[row * D + d] = kv;
+                if constexpr (DT == PT_F32) {
+                    static_cast<float *>(k_pool)[base + (int64_t)row * D + d] = static_cast<const float *>(k_new)[u * D + d];
+                    static_cast<float *>(v_pool)[base + (int64_t)row * D + d] = static_cast<const float *>(v_new)[u * D + d];
+                } else {
+                    static_cast<uint16_t *>(k_pool)[base + (int64_t)row * D + d] = static_cast<const uint16_t *>(k_new)[u * D + d];
+                    static_cast<uint16_t *>(v_pool)[base + (int64_t)row * D + d] = static_cast<const uint16_t *>(v_new)[u * D + d];
+                }
+            }
+            __syncwarp();
+            const int cnt = row + 1;
+            double mean[DJ];
+#pragma unroll
+            for (int j = 0; j < DJ; j++) {
+                const int d = lane + 32 * j;
+                double sacc = 0.0;
+                if (d < D)
+                    for (int r = 0; r < cnt; r++) sacc = __dadd_rn(sacc, (double)rows_s[r * D + d]);
+                mean[j] = __ddiv_rn(sacc, (double)cnt);
+            }
+            constexpr int V = StatsTile<SDT>::V;
+#pragma unroll
+            for (int j = 0; j < DJ; j++) {
+                const int d = lane + 32 * j;
+                if (d < D) {
+                    double sacc = 0.0;
+                    for (int r = 0; r < cnt; r++) {
+                        const double t = __dsub_rn((double)rows_s[r * D + d], mean[j]);
+                        sacc = __dadd_rn(sacc, __dmul_rn(t, t));
+                    }
+                    var_s[d] = __ddiv_rn(sacc, (double)cnt);
+                    store_elem<SDT>(means, mean_offset(u, n / S, d, D, Pmax, V), __double2float_rn(mean[j]));
+                }
+            }
+            __syncwarp();
+            if (lane == 0) {
+                stds[u * Pmax + n / S] = __double2float_rn(__dsqrt_rn(np_sum(DoubleArray{var_s}, D)));
+                seq_len[u] = n + 1;
+            }
         }
     }
-    __syncwarp();
-    __threadfence_block();
-    page_stats_warp<DT, SDT, DJ>(k_pool, pid, row + 1, S, D, u, n / S, Pmax, means, stds,
-                                 var_smem[warp]);
-    if (lane == 0) seq_len[u] = n + 1;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(done, 1) == (int)gridDim.x - 1) {  // re-arm for the next append
+            atomicExch(flag, 0);
+            atomicExch(done, 0);
+        }
+    }
 }
 
 // extend (kvcache.py:210-233): scatter dense staged rows into mapped pages
@@ -248,17 +306,31 @@ extern "C" int pt_page_stats(const void *k_pool, int kv_dtype, const int32_t *pa
 }
 
 template <int DT, int SDT>
-static int launch_append_rows(const void *kn, const void *vn, void *kp, void *vp, int32_t *sl,
-                              const int32_t *slot, int U, int S, int D, int Pmax, void *means,
-                              float *stds, cudaStream_t st) {
-    const int blocks = (U + kStatsWarps - 1) / kStatsWarps;
+static int launch_append(const void *kn, const void *vn, void *kp, void *vp, int32_t *ptab,
+                         int32_t *sl, int U, int S, int D, int Pmax, void *means, float *stds,
+                         int32_t *pool_state, const int32_t *free_list, int32_t *slot,
+                         cudaStream_t st) {
+    const size_t per_warp = (size_t)S * D * 4 + (size_t)D * 8;
+    int wpc = (int)((200 * 1024) / per_warp);
+    if (wpc > 8) wpc = 8;
+    if (wpc < 1) return PT_ERR_UNSUPPORTED;
+    const size_t smem = per_warp * wpc;
+    const int grid = (U + wpc - 1) / wpc;
     const int dj = (D + 31) / 32;
-#define PT_APP_CASE(DJ_)                                                                  \
-    case DJ_:                                                                             \
-        k_append_rows<DT, SDT, DJ_><<<blocks, kStatsWarps * 32, 0, st>>>(kn, vn, kp, vp, sl, \
-                                                                         slot, U, S, D, Pmax, \
-                                                                         means, stds);     \
-        break;
+#define PT_APP_CASE(DJ_)                                                                      \
+    case DJ_: {                                                                               \
+        static size_t configured = 0;                                                         \
+        if (smem > configured) {                                                              \
+            PT_CUDA_TRY(cudaFuncSetAttribute(k_append<DT, SDT, DJ_>,                          \
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                                             (int)smem));                                     \
+            configured = smem;                                                                \
+        }                                                                                     \
+        k_append<DT, SDT, DJ_><<<grid, wpc * 32, smem, st>>>(kn, vn, kp, vp, ptab, sl, U, S, D, \
+                                                            Pmax, means, stds, pool_state,    \
+                                                            free_list, slot);                 \
+        break;                                                                                \
+    }
     switch (dj) {
         PT_APP_CASE(1)
         PT_APP_CASE(2)
@@ -285,17 +357,14 @@ extern "C" int pt_append(const void *k_new, const void *v_new, void *k_pool, voi
     if (U == 0) return PT_OK;
     cudaStream_t st = (cudaStream_t)stream;
     int32_t *slot = slot_scratch;
-    k_append_alloc<<<1, kAllocThreads, 0, st>>>(page_table, seq_len, U, S, Pmax, pool_state,
-                                               free_list, slot);
-    PT_CUDA_TRY(cudaGetLastError());
     if (kv_dtype == PT_F32 && stats_dtype == PT_F32)
-        return launch_append_rows<PT_F32, PT_F32>(k_new, v_new, k_pool, v_pool, seq_len, slot, U, S, D, Pmax, means, stds, st);
+        return launch_append<PT_F32, PT_F32>(k_new, v_new, k_pool, v_pool, page_table, seq_len, U, S, D, Pmax, means, stds, pool_state, free_list, slot, st);
     if (kv_dtype == PT_BF16 && stats_dtype == PT_F32)
-        return launch_append_rows<PT_BF16, PT_F32>(k_new, v_new, k_pool, v_pool, seq_len, slot, U, S, D, Pmax, means, stds, st);
+        return launch_append<PT_BF16, PT_F32>(k_new, v_new, k_pool, v_pool, page_table, seq_len, U, S, D, Pmax, means, stds, pool_state, free_list, slot, st);
     if (kv_dtype == PT_BF16 && stats_dtype == PT_BF16)
-        return launch_append_rows<PT_BF16, PT_BF16>(k_new, v_new, k_pool, v_pool, seq_len, slot, U, S, D, Pmax, means, stds, st);
+        return launch_append<PT_BF16, PT_BF16>(k_new, v_new, k_pool, v_pool, page_table, seq_len, U, S, D, Pmax, means, stds, pool_state, free_list, slot, st);
     if (kv_dtype == PT_F32 && stats_dtype == PT_BF16)
-        return launch_append_rows<PT_F32, PT_BF16>(k_new, v_new, k_pool, v_pool, seq_len, slot, U, S, D, Pmax, means, stds, st);
+        return launch_append<PT_F32, PT_BF16>(k_new, v_new, k_pool, v_pool, page_table, seq_len, U, S, D, Pmax, means, stds, pool_state, free_list, slot, st);
     return PT_ERR_INVALID;
 }
 

@@ -5,12 +5,13 @@
 // the lowest-logical-index tie rule, page-table translation in the epilogue).  The decode
 // engine normally runs this fused into the tail of the scoring kernel (score.cu); this
 // entry point serves pages beyond that kernel's shared-memory envelope and the C ABI.
+#include <stdlib.h>
+
 #include "select.cuh"
 
 namespace pt {
 
-constexpr int kTopkThreads = 512;
-
+template <int kTopkThreads>
 __global__ void __launch_bounds__(kTopkThreads)
     k_topk(const uint16_t *__restrict__ keys_g, const int32_t *__restrict__ seq_len,
            const int32_t *__restrict__ page_table, int S, int Pmax, int k,
@@ -18,6 +19,7 @@ __global__ void __launch_bounds__(kTopkThreads)
            int32_t *__restrict__ n_sel, int32_t *__restrict__ kth, int32_t *__restrict__ kplus1) {
     extern __shared__ __align__(16) uint16_t skeys[];
     __shared__ SelectShared<kTopkThreads> sh;
+    __shared__ int bins[kSelectBins];
     const int64_t u = blockIdx.x;
     const int n = seq_len[u];
     const int P = (n + S - 1) / S;
@@ -29,7 +31,7 @@ __global__ void __launch_bounds__(kTopkThreads)
     for (int i = threadIdx.x; i < (P + 7) / 8; i += kTopkThreads)
         reinterpret_cast<uint4 *>(skeys)[i] = __ldg(src + i);
     __syncthreads();
-    select_block<kTopkThreads>(skeys, P, k, page_table + u * Pmax, sel + u * (int64_t)k,
+    select_block<kTopkThreads>(skeys, bins, P, k, page_table + u * Pmax, sel + u * (int64_t)k,
                                sel_logical ? sel_logical + u * (int64_t)k : nullptr, n_sel + u,
                                kth + u, kplus1 + u, sh);
 }
@@ -50,13 +52,23 @@ extern "C" int pt_topk(const uint16_t *keys, const int32_t *seq_len, const int32
     if (U == 0) return PT_OK;
     const size_t smem = topk_smem_bytes(Pmax);
     if (smem > 200 * 1024) return PT_ERR_UNSUPPORTED;
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-        PT_CUDA_TRY(cudaFuncSetAttribute(k_topk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        configured = smem;
-    }
-    k_topk<<<U, kTopkThreads, smem, (cudaStream_t)stream>>>(keys, seq_len, page_table, S, Pmax, k, sel,
-                                                           sel_logical, n_sel, kth, kplus1);
+    // PT_TOPK_THREADS (256 / 512 / 1024) overrides the block size (tuning)
+    const char *e = getenv("PT_TOPK_THREADS");
+    const int nt = e ? atoi(e) : 512;
+    cudaStream_t st = (cudaStream_t)stream;
+#define PT_TOPK(NT_)                                                                           \
+    if (nt == NT_) {                                                                           \
+        static size_t configured = 0;                                                          \
+        if (smem > configured) { /* static bins + dynamic keys may exceed 48 KB */              \
+            PT_CUDA_TRY(cudaFuncSetAttribute(k_topk<NT_>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                             (int)smem));                                      \
+            configured = smem;                                                                 \
+        }                                                                                      \
+        k_topk<NT_><<<U, NT_, smem, st>>>(keys, seq_len, page_table, S, Pmax, k, sel, sel_logical, \
+                                          n_sel, kth, kplus1);                                 \
+    } else
+    PT_TOPK(256) PT_TOPK(1024) PT_TOPK(512)
+#undef PT_TOPK
     PT_CUDA_TRY(cudaGetLastError());
     return PT_OK;
 }
