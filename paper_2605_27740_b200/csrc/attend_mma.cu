@@ -7,7 +7,7 @@ template <int D, int MT>
 static int launch_one(const CUtensorMap &tk, const CUtensorMap &tv, const AttnParams &prm, int U,
                       int nsplit, int NW, size_t smem, cudaStream_t st) {
     static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
+    if (smem > configured) {
         PT_CUDA_TRY(cudaFuncSetAttribute(k_attend_mma<D, MT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured = smem;
@@ -34,7 +34,7 @@ template <int D, int MT>
 static int launch_stream_one(const CUtensorMap &tk, const CUtensorMap &tv, const StreamParams &p,
                              int grid, int NW, size_t smem, cudaStream_t st) {
     static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
+    if (smem > configured) {
         PT_CUDA_TRY(cudaFuncSetAttribute(k_attend_stream<D, MT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured = smem;

@@ -7,7 +7,7 @@ template <int GP, int DPL>
 static int launch_one(const AttnParams &prm, int U, int nsplit, int NW, size_t smem,
                       cudaStream_t st) {
     static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
+    if (smem > configured) {
         PT_CUDA_TRY(cudaFuncSetAttribute(k_attend<PT_F32, GP, DPL>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured = smem;

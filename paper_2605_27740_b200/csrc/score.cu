@@ -264,7 +264,7 @@ static int launch_score(ScoreParams prm, int U, int G, cudaStream_t st) {
 #define PT_SCORE_CASE(G_)                                                                      \
     case G_: {                                                                                 \
         static size_t configured = 0;                                                          \
-        if (smem > 48 * 1024 && smem > configured) {                                           \
+        if (smem > configured) { /* dynamic + static may pass 48 KB */                    \
             PT_CUDA_TRY(cudaFuncSetAttribute(k_score<QDT, SDT, G_>,                            \
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,     \
                                              (int)smem));                                      \

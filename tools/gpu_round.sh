@@ -1,0 +1,23 @@
+#!/bin/bash
+# One GPU-box pass: parity suite, smoke, bench (both arms), ncu launch list + full captures.
+# Usage (from the build container): gpurun --timeout 2400 -- 'bash tools/gpu_round.sh [tag]'
+set -u
+TAG=${1:-r01}
+OUT=gpurun_out/$TAG
+mkdir -p $OUT
+nvidia-smi > $OUT/nvidia-smi.txt 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $OUT/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke exit $?" >> $OUT/smoke.log
+timeout 600 python bench.py ${BENCH_ARGS:-} > $OUT/bench.json 2> $OUT/bench.err
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_ref.json 2> $OUT/bench_ref.err
+if [ -z "${SKIP_NCU:-}" ]; then
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:^k_ -c 400 --csv \
+    --log-file $OUT/launches.csv python bench.py --profile --steps 20 --warmup 3 > $OUT/launches.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_score_stream -s 2 -c 1 \
+    -o $OUT/prof_score python bench.py --profile --steps 4 > $OUT/ncu_score.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_attend -s 2 -c 1 \
+    -o $OUT/prof_attend python bench.py --profile --steps 4 > $OUT/ncu_attend.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_topk -s 2 -c 1 \
+    -o $OUT/prof_topk python bench.py --profile --steps 4 > $OUT/ncu_topk.log 2>&1
+fi
+echo done
