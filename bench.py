@@ -317,9 +317,7 @@ def main():
     for i in range(NQ):
         gph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(gph):
-            cache.append_batch(kn, vn)
-            eng.score_select(qs[i])
-            eng.attend(qs[i], nsplit=args.nsplit)
+            eng.step(qs[i], kn, vn)
         cache._seq_host -= 1
         graphs.append(gph)
     for i in range(args.warmup):
@@ -354,18 +352,20 @@ def main():
 
     # ---- per-kernel breakdown (CUDA events on the launching stream) -----------------
     reps = max(20, min(args.steps, 100))
-    names = ["append", "score_select", "attend"]
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(reps)]
+    names = ["append", "lam_norms", "score", "select_attend"]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(reps)]
     for r in range(reps):
         q = qs[r % NQ]
         ev = evs[r]
         ev[0].record(stream)
         cache.append_batch(kn, vn)
         ev[1].record(stream)
-        eng.score_select(q)
+        eng.lam_norms(q)
         ev[2].record(stream)
-        eng.attend(q, nsplit=args.nsplit)
+        eng.score_prenorm(q)
         ev[3].record(stream)
+        eng.select_attend(q)
+        ev[4].record(stream)
     torch.cuda.synchronize()
     cache.check_errors()
     brk = {n: statistics.median([evs[r][i].elapsed_time(evs[r][i + 1]) * 1000 for r in range(reps)])
@@ -381,6 +381,14 @@ def main():
     torch.cuda.synchronize()
     brk["score_only"] = statistics.median([ev2[r][0].elapsed_time(ev2[r][1]) * 1000 for r in range(reps)])
     brk["select_only"] = statistics.median([ev2[r][1].elapsed_time(ev2[r][2]) * 1000 for r in range(reps)])
+    # the unfused attention kernel over the same selection (pt_attend), for reference
+    ev3 = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(reps)]
+    for r in range(reps):
+        ev3[r][0].record(stream)
+        eng.attend(qs[r % NQ], nsplit=args.nsplit)
+        ev3[r][1].record(stream)
+    torch.cuda.synchronize()
+    brk["attend_only"] = statistics.median([ev3[r][0].elapsed_time(ev3[r][1]) * 1000 for r in range(reps)])
     tune = None
     if args.sweep:
         tune = {}
@@ -499,8 +507,8 @@ def main():
     e_st = 4 if args.stats_dtype == "f32" else 2
     P = -(-args.ctx // S)
     by = step_bytes(U, G, D, P, kp, S, 2, e_st, args.ctx)
-    kbytes = {"score_select": by["score"] + by["topk"], "attend": by["attend"]}
-    dom = max(("score_select", "attend"), key=lambda n: brk[n])
+    kbytes = {"score": by["score"], "select_attend": by["topk"] + by["attend"]}
+    dom = max(("score", "select_attend"), key=lambda n: brk[n])
     dom_bytes = kbytes[dom]
     achieved = dom_bytes / (brk[dom] * 1e-6) / 1e9
     traffic = None
@@ -536,7 +544,7 @@ def main():
             "dtype": "bf16",
             "data": "synthetic N(0,1) K/V/q (reference workload distribution), generated on device",
             "config": config,
-            "gpu_launches": 4 * args.steps,
+            "gpu_launches": 4 * args.steps,  # append | lam-norms (parallel branches), score, select+attend
             "nsplit_sweep_us": nsplit_sweep,
             "tune_us": tune,
             "breakdown_us": brk,
@@ -555,8 +563,8 @@ def main():
                 "traffic": traffic,
             },
             "dense_us_per_step": dense_us,
-            "x_over_dense": (dense_us / (brk["score_select"] + brk["attend"])) if dense_us else None,
-            "x_over_dense_attn_only": (dense_us / brk["attend"]) if dense_us else None,
+            "x_over_dense": (dense_us / (brk["score"] + brk["select_attend"])) if dense_us else None,
+            "x_over_dense_attn_only": (dense_us / brk["attend_only"]) if dense_us else None,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1000},
             "clocks": sampler.summary(),

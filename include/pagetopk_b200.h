@@ -96,7 +96,7 @@ PT_API int pt_page_stats(const void *k_pool, int kv_dtype, const int32_t *page_t
  * (free list first, then bump; deterministic in unit order, kvcache.py:154-176); the
  * touched page's stats are recomputed exactly.  pool_state int32[4] =
  * {bump_next, free_count, max_pages, error_flag}; error_flag set to PT_ERR_CAPACITY
- * when the pool is exhausted (that unit is left unchanged).  slot_scratch: int32 [U + 2]
+ * when the pool is exhausted (that unit is left unchanged).  slot_scratch: int32 [U + 4]
  * device scratch, zero-initialised once (per-unit target page + the launch's internal
  * allocation flag; self-resetting).  One launch. */
 PT_API int pt_append(const void *k_new, const void *v_new, void *k_pool, void *v_pool, int kv_dtype,
@@ -115,10 +115,25 @@ PT_API int pt_write_rows(const void *k_rows, const void *v_rows, int n_max, cons
  * q [U*G][D] (q_dtype); norms f32 [U*G] or NULL (computed as scoring.py:39-47);
  * score = max_g fl(fl(sum_d q*mean) + fl(fl(lam*norm_g)*std)), sequential d order;
  * writes keys u16 [U][Pmax] and optionally scores f32 [U][Pmax].
- * lamnorm_ws: f32 [U*8] device scratch enabling the streaming kernel (NULL: CTA kernel). */
+ * lamnorm_ws: f32 [U*8] device scratch enabling the streaming kernel (NULL: CTA kernel).
+ * tile_max: u16 [U][Pmax/32] or NULL -- the largest key of every 32-page tile (a lower
+ * bound for the k-th largest key that lets pt_select_attend skip most keys). */
 PT_API int pt_score(const void *q, int q_dtype, const float *norms, const void *means, int stats_dtype,
              const float *stds, const int32_t *seq_len, int U, int G, int D, int S, int Pmax,
-             float lam, uint16_t *keys, float *scores, float *lamnorm_ws, void *stream);
+             float lam, uint16_t *keys, float *scores, float *lamnorm_ws, uint16_t *tile_max,
+             void *stream);
+
+/* K2 split in two launches so the first can run concurrently with the append:
+ * pt_lam_norms writes fl(lam * ||q_g||) (norms NULL: computed in numpy's float64 order,
+ * scoring.py:39-47) into lamnorm f32 [U][8]; pt_score_prenorm is pt_score's streaming
+ * kernel reading it (same keys / scores / tile_max, bit for bit).  pt_score_prenorm
+ * returns PT_ERR_UNSUPPORTED outside that kernel's envelope (G <= 8, D in {64, 128}). */
+PT_API int pt_lam_norms(const void *q, int q_dtype, const float *norms, int U, int G, int D,
+                        float lam, float *lamnorm, void *stream);
+PT_API int pt_score_prenorm(const void *q, int q_dtype, const float *lamnorm, const void *means,
+                            int stats_dtype, const float *stds, const int32_t *seq_len, int U,
+                            int G, int D, int S, int Pmax, uint16_t *keys, float *scores,
+                            uint16_t *tile_max, void *stream);
 
 /* K2+K3 fused: pt_score followed by pt_topk in ONE launch -- the last CTA to finish a unit's
  * pages selects that unit's top-k while other CTAs keep scoring (same outputs as the two
@@ -155,6 +170,29 @@ PT_API int pt_attend(const void *q, int q_dtype, const void *k_pool, const void 
               const int32_t *page_table, const int32_t *seq_len, int U, int G, int D, int S,
               int Pmax, const float *bias, float scale, float *out, float *lse, void *workspace,
               size_t workspace_bytes, int32_t *tickets, int nsplit, void *stream);
+
+/* K3+K4 fused (the engine's default after pt_score): per unit, the selection of pt_topk
+ * (same outputs: sel [U][k], sel_logical or NULL, n_sel, kth, kplus1) followed by the
+ * sparse attention of pt_attend over exactly those pages (sel_stride = k, no bias), in
+ * ONE launch -- the selected ids stay in shared memory and feed the TMA producer.
+ * Replaces the select.py:105-107 -> attention.py:143-146 pair of calls of decode_step
+ * (attention.py:137-146).  bf16 KV, G <= 8, D in {64,128,256}, S in {16,32,64}; returns
+ * PT_ERR_UNSUPPORTED outside that envelope (the caller runs pt_topk + pt_attend).
+ * tile_max: pt_score's per-tile maxima or NULL (they let the selection skip the keys below
+ * the k-th largest tile maximum).  Emission order equals pt_topk's (ascending logical). */
+PT_API int pt_select_attend(const uint16_t *keys, const uint16_t *tile_max,
+                            const int32_t *seq_len, const int32_t *page_table,
+                            int U, int S, int Pmax, int k, int32_t *sel, int32_t *sel_logical,
+                            int32_t *n_sel, int32_t *kth, int32_t *kplus1, const void *q,
+                            int q_dtype, const void *k_pool, const void *v_pool, int kv_dtype,
+                            int num_phys_pages, int G, int D, float scale, float *out, float *lse,
+                            void *workspace, size_t workspace_bytes, int32_t *tickets, void *stream);
+
+/* Tuning aid: per-CTA phase timestamps (%globaltimer ns; 10 per CTA: entry, keys staged,
+ * selection done, first page landed, stream done, exit, then inside the selection: range,
+ * threshold, compaction, translation) of the last pt_select_attend launch made with
+ * PT_SA_PROF=1 in the environment.  n <= 10 * 4096. */
+PT_API int pt_debug_sa_prof(unsigned long long *host, int n);
 
 /* Layout helper: row-major means f32 [U][P][D] -> tiled stats layout (stats_dtype). */
 PT_API int pt_tile_means(const float *means_rowmajor, int U, int P, int D, int Pmax, void *means_tiled,

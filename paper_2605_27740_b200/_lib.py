@@ -43,13 +43,20 @@ _PROTOS = {
     "pt_append": (_i, [_vp, _vp, _vp, _vp, _i, _vp, _vp, _i, _i, _i, _i, _vp, _i, _vp, _vp,
                        _vp, _vp, _vp]),
     "pt_write_rows": (_i, [_vp, _vp, _i, _vp, _vp, _vp, _vp, _i, _vp, _i, _i, _i, _i, _vp]),
-    "pt_score": (_i, [_vp, _i, _vp, _vp, _i, _vp, _vp, _i, _i, _i, _i, _i, _f, _vp, _vp, _vp, _vp]),
+    "pt_score": (_i, [_vp, _i, _vp, _vp, _i, _vp, _vp, _i, _i, _i, _i, _i, _f, _vp, _vp, _vp, _vp,
+                      _vp]),
+    "pt_lam_norms": (_i, [_vp, _i, _vp, _i, _i, _i, _f, _vp, _vp]),
+    "pt_score_prenorm": (_i, [_vp, _i, _vp, _vp, _i, _vp, _vp, _i, _i, _i, _i, _i, _vp, _vp, _vp,
+                              _vp]),
     "pt_topk": (_i, [_vp, _vp, _vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pt_score_select": (_i, [_vp, _i, _vp, _vp, _i, _vp, _vp, _vp, _i, _i, _i, _i, _i, _f, _i, _vp,
                              _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pt_attend_workspace_bytes": (_sz, [_i, _i, _i, _i]),
     "pt_attend": (_i, [_vp, _i, _vp, _vp, _i, _i, _vp, _i, _vp, _vp, _vp, _i, _i, _i, _i, _i, _vp,
                        _f, _vp, _vp, _vp, _sz, _vp, _i, _vp]),
+    "pt_select_attend": (_i, [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp,
+                              _vp, _i, _i, _i, _i, _f, _vp, _vp, _vp, _sz, _vp, _vp]),
+    "pt_debug_sa_prof": (_i, [_vp, _i]),
     "pt_tile_means": (_i, [_vp, _i, _i, _i, _i, _vp, _i, _vp]),
 }
 

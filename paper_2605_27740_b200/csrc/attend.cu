@@ -52,6 +52,11 @@ static bool make_pool_tmap(CUtensorMap *tm, const void *base, int D, int S, int6
     return r == CUDA_SUCCESS;
 }
 
+// shared with attend_fused.cu
+bool pt_make_pool_tmap(CUtensorMap *m, const void *pool, int D, int S, int num_pages) {
+    return make_pool_tmap(m, pool, D, S, num_pages);
+}
+
 // PT_ATTEND_SIMT=1 forces the CUDA-core kernel (used by the parity tests to pin both paths);
 // PT_ATTEND_SPLIT=1 forces the (split, unit) grid instead of the streaming kernel;
 // PT_ATTEND_NSTAGE / PT_ATTEND_CHUNK override the streaming ring depth / chunk size.

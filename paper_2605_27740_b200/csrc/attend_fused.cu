@@ -1,0 +1,335 @@
+// attend_fused.cu -- K3 + K4 in one launch: per-unit top-k page selection followed by the
+// tensor-core sparse decode attention over exactly those pages (the decode hot path of
+// attention.py:137-146: select.py:87-115 radix_topk, then sparse_attention for the G heads
+// of the group, attention.py:94-107 / _kernels_cy.pyx:129-172).
+//
+// Why fused: at the headline shape (256 units x 8192 pages, k = 128) a standalone selection
+// kernel is latency-bound (one CTA per unit, ~15 barrier phases) and its launch boundary
+// drains the GPU between two HBM-bound kernels.  Here the CTA that attends a unit first
+// selects its pages -- the keys are read once into shared memory, the selected physical ids
+// stay in shared memory and feed the TMA producer directly -- so the select costs one CTA
+// prologue instead of a kernel, and the sel / n_sel / kth / kplus1 outputs are still written
+// for the caller (bit-identical to pt_topk: same select_block).
+//
+// Grid (nchunk, U), 4 warps.  Every chunk CTA of a unit runs the (deterministic) selection;
+// chunk 0 publishes it.  Chunk c attends the c-th contiguous slice of the emitted list; the
+// warps of the CTA interleave pages (warp w: slice[w], slice[w+4], ...), each through a
+// private nstage-deep ring of TMA tensor copies (one K + one V page per stage), QK / PV on
+// mma.sync m16n8k16 with the G <= 8 heads as N (see attend.cuh for the fragment layouts);
+// warps merge in shared memory, chunks through the workspace (last-arriving CTA, ticket).
+//
+// Shared memory: [region: select scratch (keys + bins) | reused as the stage rings and then
+// the merge buffers] [selected ids, k ints] [mbarriers].
+#include "attend.cuh"
+#include "select.cuh"
+
+namespace pt {
+
+struct SelAttnParams {
+    const uint16_t *keys;
+    const uint16_t *tile_max;
+    const int32_t *seq_len;
+    const int32_t *page_table;
+    int32_t *sel, *sel_logical, *n_sel, *kth, *kplus1;
+    const void *q;
+    float *out, *lse, *ws;
+    int32_t *tickets;
+    int q_dtype, U, G, Pmax, k, nchunk, nstage;
+    int region;  // bytes of the shared region (multiple of 1024)
+    int prof;    // record phase timestamps into g_sa_prof
+    float scale;
+};
+
+constexpr int kSAWarps = 4;
+
+// Optional phase timestamps (%globaltimer, ns) per CTA for tuning: enabled by
+// PT_SA_PROF=1 on the host, read back with pt_debug_sa_prof().  10 stamps per CTA
+// (6 kernel phases + 4 inside the selection).
+constexpr int kSAProfCtas = 4096;
+__device__ unsigned long long g_sa_prof[kSAProfCtas * 10];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+constexpr int kSAThreads = kSAWarps * 32;
+constexpr int kSARegVecs = 16;  // register-resident candidate pass: P <= 128 * 8 * 16 = 16384
+
+__host__ __device__ __forceinline__ size_t sa_keys_bytes(int Pmax) {
+    return (size_t)((Pmax + 8) / 8) * 16;
+}
+
+template <int D, int MT>
+__global__ void __launch_bounds__(kSAThreads) k_select_attend(const __grid_constant__ CUtensorMap tmk,
+                                                              const __grid_constant__ CUtensorMap tmv,
+                                                              const SelAttnParams p) {
+    constexpr int S = 16 * MT;
+    constexpr int KS = D / 16;
+    constexpr int NW = kSAWarps;
+    constexpr uint32_t PAGE_BYTES = S * D * 2;
+    constexpr uint32_t STAGE_BYTES = 2 * PAGE_BYTES;
+    extern __shared__ __align__(1024) char smem[];
+    __shared__ SelectShared<kSAThreads> sh;
+    __shared__ SelectCandShared<kSAThreads> csh;
+    __shared__ int sdummy[3];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t u = blockIdx.y;
+    const int c = blockIdx.x;
+    const int G = p.G, k = p.k, nstage = p.nstage;
+    int *ids = reinterpret_cast<int *>(smem + p.region);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + p.region + (((size_t)k * 4 + 7) & ~(size_t)7)) +
+                     warp * nstage;
+
+    const int n = p.seq_len[u];
+    const int P = (n + S - 1) / S;
+    const bool lead = (c == 0);
+    const int cta = blockIdx.y * gridDim.x + blockIdx.x;
+    const bool prof = p.prof && threadIdx.x == 0 && cta < kSAProfCtas;
+    if (prof) g_sa_prof[cta * 10 + 0] = gtimer();
+    if (P == 0) {
+        if (lead && threadIdx.x == 0) { p.n_sel[u] = 0; p.kth[u] = 0; p.kplus1[u] = -1; }
+        return;
+    }
+    // ---- independent loads first (tail page, query fragments): their latencies overlap the
+    // selection's key loads
+    const int tail_pid = p.page_table[u * p.Pmax + P - 1];
+    const int tail_rows = n - (P - 1) * S;
+    uint32_t qb[KS][2];
+    {
+        const int gq = lane >> 2;
+#pragma unroll
+        for (int ks = 0; ks < KS; ks++) {
+            const int d0 = ks * 16 + 2 * (lane & 3);
+            uint32_t b0 = 0, b1 = 0;
+            if (gq < G) {
+                const int64_t row = (u * G + gq) * (int64_t)D;
+                if (p.q_dtype == PT_BF16) {
+                    const uint32_t *qp =
+                        reinterpret_cast<const uint32_t *>(static_cast<const uint16_t *>(p.q) + row);
+                    b0 = __ldg(qp + (d0 >> 1));
+                    b1 = __ldg(qp + ((d0 + 8) >> 1));
+                } else {
+                    const float *qp = static_cast<const float *>(p.q) + row;
+                    b0 = pack_bf16(qp[d0], qp[d0 + 1]);
+                    b1 = pack_bf16(qp[d0 + 8], qp[d0 + 9]);
+                }
+            }
+            qb[ks][0] = b0;
+            qb[ks][1] = b1;
+        }
+    }
+    if (prof) g_sa_prof[cta * 10 + 1] = gtimer();
+
+    // ---- selection (select.py:87-115): physical ids land in `ids` in emission order ----
+    // register-resident keys (select_regs) when the unit fits and the k-th key lies within
+    // 64 values of the maximum; else the shared-memory select_block
+    const int ns = P < k ? P : k;
+    const uint16_t *krow = p.keys + u * (int64_t)p.Pmax;
+    int32_t *o_sel = lead ? p.sel + u * (int64_t)k : nullptr;
+    int32_t *o_log = (lead && p.sel_logical) ? p.sel_logical + u * (int64_t)k : nullptr;
+    int32_t *o_n = lead ? p.n_sel + u : &sdummy[0];
+    int32_t *o_kth = lead ? p.kth + u : &sdummy[1];
+    int32_t *o_kp1 = lead ? p.kplus1 + u : &sdummy[2];
+    bool selected = false;
+    if (p.tile_max && P <= kSAThreads * 8 * kSARegVecs)
+        selected = select_cand<kSAThreads, kSARegVecs>(
+            krow, p.tile_max + u * (int64_t)(p.Pmax >> 5), P, k, p.page_table + u * p.Pmax, o_sel,
+            o_log, o_n, o_kth, o_kp1, csh, ids, true,
+            prof ? &g_sa_prof[cta * 10 + 6] : nullptr);
+    if (!selected) {
+        uint16_t *skeys = reinterpret_cast<uint16_t *>(smem);
+        int *bins = reinterpret_cast<int *>(smem + sa_keys_bytes(p.Pmax));
+        const uint4 *src = reinterpret_cast<const uint4 *>(krow);
+        constexpr int kMax = 8;
+        const int nv = (P + 7) / 8;
+        for (int i0 = threadIdx.x; i0 < nv; i0 += kMax * kSAThreads) {
+            uint4 v[kMax];
+#pragma unroll
+            for (int j = 0; j < kMax; j++)
+                if (i0 + j * kSAThreads < nv) v[j] = __ldcg(src + i0 + j * kSAThreads);
+#pragma unroll
+            for (int j = 0; j < kMax; j++)
+                if (i0 + j * kSAThreads < nv) reinterpret_cast<uint4 *>(skeys)[i0 + j * kSAThreads] = v[j];
+        }
+        __syncthreads();
+        select_block<kSAThreads>(skeys, bins, P, k, p.page_table + u * p.Pmax, o_sel, o_log, o_n,
+                                 o_kth, o_kp1, sh, ids, true,
+                                 prof ? &g_sa_prof[cta * 10 + 6] : nullptr);
+    }
+    __syncthreads();  // ids complete; the select scratch is dead -> stage rings
+    if (prof) g_sa_prof[cta * 10 + 2] = gtimer();
+
+    // ---- this chunk's slice of the selection ----
+    const int per = (ns + p.nchunk - 1) / p.nchunk;
+    const int first = c * per;
+    if (first >= ns) return;
+    const int last = min(first + per, ns);
+    const int nchunk_u = (ns + per - 1) / per;
+    char *my_stages = smem + (size_t)warp * nstage * STAGE_BYTES;
+    const int rem = last - first - warp;
+    const int my_count = rem > 0 ? (rem + NW - 1) / NW : 0;
+    auto issue = [&](int i) {
+        const int pid = ids[first + warp + i * NW];
+        const int st = i % nstage;
+        char *ks = my_stages + (size_t)st * STAGE_BYTES;
+        mbar_arrive_expect_tx(&bars[st], STAGE_BYTES);
+#pragma unroll
+        for (int b = 0; b < D / 64; b++) {
+            tma_load_2d(ks + b * S * 128, &tmk, b * 64, pid * S, &bars[st]);
+            tma_load_2d(ks + PAGE_BYTES + b * S * 128, &tmv, b * 64, pid * S, &bars[st]);
+        }
+    };
+    if (lane == 0) {
+        for (int i = 0; i < nstage; i++) mbar_init(&bars[i], 1);
+        fence_mbar_init();
+        for (int i = 0; i < min(nstage, my_count); i++) issue(i);
+    }
+    __syncwarp();
+
+    const float qscale = p.scale * kLog2e;
+    float acc[KS][4];
+#pragma unroll
+    for (int i = 0; i < KS; i++) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+    float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};
+    for (int i = 0; i < my_count; i++) {
+        const int st = i % nstage;
+        const int pid = ids[first + warp + i * NW];
+        const int rows = (pid == tail_pid) ? tail_rows : S;
+        mbar_wait(&bars[st], (uint32_t)((i / nstage) & 1));
+        if (prof && i == 0) g_sa_prof[cta * 10 + 3] = gtimer();
+        const uint32_t kbase = smem_u32(my_stages + (size_t)st * STAGE_BYTES);
+        mma_page<D, MT>(kbase, kbase + PAGE_BYTES, rows, 0.f, qscale, qb, acc, m_run, l_run, lane);
+        __syncwarp();
+        if (lane == 0 && i + nstage < my_count) issue(i + nstage);
+    }
+
+    // ---- per-warp partials to shared memory, then the CTA / chunk merge (attend.cuh) ----
+    if (prof) g_sa_prof[cta * 10 + 4] = gtimer();
+    __syncthreads();
+    float *macc = reinterpret_cast<float *>(smem);             // [NW][8][D]
+    float *mml = macc + (size_t)NW * kMmaGP * D;                // [NW][8][2]
+    const int g0 = 2 * (lane & 3);
+#pragma unroll
+    for (int dm = 0; dm < KS; dm++) {
+        const int d = dm * 16 + (lane >> 2);
+        macc[((size_t)warp * kMmaGP + g0) * D + d] = acc[dm][0];
+        macc[((size_t)warp * kMmaGP + g0 + 1) * D + d] = acc[dm][1];
+        macc[((size_t)warp * kMmaGP + g0) * D + d + 8] = acc[dm][2];
+        macc[((size_t)warp * kMmaGP + g0 + 1) * D + d + 8] = acc[dm][3];
+    }
+    if (lane < 4) {
+        mml[(warp * kMmaGP + g0) * 2 + 0] = m_run[0];
+        mml[(warp * kMmaGP + g0) * 2 + 1] = l_run[0];
+        mml[(warp * kMmaGP + g0 + 1) * 2 + 0] = m_run[1];
+        mml[(warp * kMmaGP + g0 + 1) * 2 + 1] = l_run[1];
+    }
+    __syncthreads();
+    AttnParams ap{};
+    ap.out = p.out; ap.lse = p.lse; ap.ws = p.ws; ap.tickets = p.tickets;
+    ap.G = G; ap.D = D; ap.maxs = kAttnMaxSplits;
+    cta_finish(ap, macc, mml, NW, kMmaGP, u, c, nchunk_u);
+    if (prof) g_sa_prof[cta * 10 + 5] = gtimer();
+}
+
+template <int D, int MT>
+static int launch_sa(const CUtensorMap &tk, const CUtensorMap &tv, const SelAttnParams &p,
+                     size_t smem, cudaStream_t st) {
+    static size_t configured = 0;
+    if (smem > configured) {
+        PT_CUDA_TRY(cudaFuncSetAttribute(k_select_attend<D, MT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured = smem;
+    }
+    dim3 grid(p.nchunk, p.U);
+    k_select_attend<D, MT><<<grid, kSAThreads, smem, st>>>(tk, tv, p);
+    PT_CUDA_TRY(cudaGetLastError());
+    return PT_OK;
+}
+
+}  // namespace pt
+
+using namespace pt;
+
+bool pt_make_pool_tmap(CUtensorMap *m, const void *pool, int D, int S, int num_pages);
+
+static int sa_env_int(const char *name, int dflt) {
+    const char *e = getenv(name);
+    return (e && *e) ? atoi(e) : dflt;
+}
+
+// Selection + sparse attention for every unit in one launch.  Same outputs as pt_topk
+// followed by pt_attend (sel_stride = k); PT_ERR_UNSUPPORTED when the shape is outside the
+// fused kernel's envelope (the caller then runs the two-launch path).
+extern "C" int pt_select_attend(const uint16_t *keys, const uint16_t *tile_max,
+                                const int32_t *seq_len,
+                                const int32_t *page_table, int U, int S, int Pmax, int k,
+                                int32_t *sel, int32_t *sel_logical, int32_t *n_sel, int32_t *kth,
+                                int32_t *kplus1, const void *q, int q_dtype, const void *k_pool,
+                                const void *v_pool, int kv_dtype, int num_phys_pages, int G, int D,
+                                float scale, float *out, float *lse, void *workspace,
+                                size_t workspace_bytes, int32_t *tickets, void *stream) {
+    if (!keys || !seq_len || !page_table || !sel || !n_sel || !kth || !kplus1 || !q || !k_pool ||
+        !v_pool || !out || !lse || U < 0 || S < 1 || Pmax % 32 || G < 1)
+        return PT_ERR_INVALID;
+    if (k < 1) return PT_ERR_K;
+    if (U == 0) return PT_OK;
+    if (kv_dtype != PT_BF16 || G > 8 || !(D == 64 || D == 128 || D == 256) ||
+        !(S == 16 || S == 32 || S == 64) || num_phys_pages <= 0 || !workspace || !tickets ||
+        workspace_bytes < pt_attend_workspace_bytes(U, G, D, k) || sa_env_int("PT_NO_FUSED_SA", 0))
+        return PT_ERR_UNSUPPORTED;
+    const int stage = 2 * S * D * 2;
+    int nstage = sa_env_int("PT_SA_NSTAGE", 3);
+    if (nstage < 1) nstage = 1;
+    // chunks per unit: fill the resident CTA slots (2 per SM) without a second wave, and
+    // keep at least one page per warp in a chunk
+    int nchunk = sa_env_int("PT_SA_CHUNKS", 0);
+    if (nchunk <= 0) {
+        nchunk = (148 * 2) / U;
+        if (nchunk < 1) nchunk = 1;
+        const int cap = (k + kSAWarps - 1) / kSAWarps;
+        if (nchunk > cap) nchunk = cap;
+    }
+    if (nchunk > kAttnMaxSplits) nchunk = kAttnMaxSplits;
+    const size_t sel_scratch = sa_keys_bytes(Pmax) + (size_t)kSelectBins * 4;
+    const size_t merge = (size_t)kSAWarps * kMmaGP * (D + 2) * 4;
+    auto smem_of = [&](int nst, size_t *region_out) {
+        const size_t rings = (size_t)kSAWarps * nst * stage;
+        size_t region = rings > sel_scratch ? rings : sel_scratch;
+        if (merge > region) region = merge;
+        region = (region + 1023) & ~(size_t)1023;
+        if (region_out) *region_out = region;
+        return region + (((size_t)k * 4 + 7) & ~(size_t)7) + (size_t)kSAWarps * nst * 8;
+    };
+    // ring depth: keep two CTAs per SM where a 2-deep ring allows, else fit one CTA
+    while (nstage > 2 && smem_of(nstage, nullptr) > 113 * 1024) nstage--;
+    while (nstage > 1 && smem_of(nstage, nullptr) > 225 * 1024) nstage--;
+    size_t region = 0;
+    const size_t smem = smem_of(nstage, &region);
+    if (smem > 225 * 1024) return PT_ERR_UNSUPPORTED;
+    CUtensorMap tk, tv;
+    if (!pt_make_pool_tmap(&tk, k_pool, D, S, num_phys_pages) ||
+        !pt_make_pool_tmap(&tv, v_pool, D, S, num_phys_pages))
+        return PT_ERR_UNSUPPORTED;
+    SelAttnParams p{};
+    p.keys = keys; p.tile_max = tile_max; p.seq_len = seq_len; p.page_table = page_table;
+    p.sel = sel; p.sel_logical = sel_logical; p.n_sel = n_sel; p.kth = kth; p.kplus1 = kplus1;
+    p.q = q; p.out = out; p.lse = lse; p.ws = static_cast<float *>(workspace); p.tickets = tickets;
+    p.q_dtype = q_dtype; p.U = U; p.G = G; p.Pmax = Pmax; p.k = k; p.nchunk = nchunk;
+    p.nstage = nstage; p.region = (int)region; p.scale = scale;
+    p.prof = sa_env_int("PT_SA_PROF", 0);
+    cudaStream_t st = (cudaStream_t)stream;
+#define PT_SA(D_, MT_) \
+    if (D == D_ && S == 16 * MT_) return launch_sa<D_, MT_>(tk, tv, p, smem, st);
+    PT_SA(64, 1) PT_SA(64, 2) PT_SA(64, 4)
+    PT_SA(128, 1) PT_SA(128, 2) PT_SA(128, 4)
+    PT_SA(256, 1) PT_SA(256, 2) PT_SA(256, 4)
+#undef PT_SA
+    return PT_ERR_UNSUPPORTED;
+}
+
+// tuning aid: copy the phase timestamps of the last PT_SA_PROF=1 launch (n <= 10 * 4096)
+extern "C" int pt_debug_sa_prof(unsigned long long *host, int n) {
+    if (!host || n < 0 || n > kSAProfCtas * 10) return PT_ERR_INVALID;
+    PT_CUDA_TRY(cudaMemcpyFromSymbol(host, g_sa_prof, (size_t)n * 8));
+    return PT_OK;
+}

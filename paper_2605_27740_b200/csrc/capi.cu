@@ -85,7 +85,8 @@ extern "C" int pt_fused_scores_host(const float *queries, const float *norms, co
     rc = pt_tile_means((const float *)dm.p, 1, (int)P, Dp, Pmax, dmt.p, PT_F32, st);
     if (rc) return rc;
     rc = pt_score(dq.p, PT_F32, (const float *)dn.p, dmt.p, PT_F32, (const float *)ds.p,
-                  (const int32_t *)dsl.p, 1, G, Dp, 1, Pmax, lam, (uint16_t *)dk.p, (float *)dsc.p, nullptr, st);
+                  (const int32_t *)dsl.p, 1, G, Dp, 1, Pmax, lam, (uint16_t *)dk.p, (float *)dsc.p, nullptr,
+                  nullptr, st);
     if (rc) return rc;
     PT_CUDA_TRY(cudaMemcpyAsync(out, dsc.p, (size_t)P * 4, cudaMemcpyDeviceToHost, st));
     PT_CUDA_TRY(cudaStreamSynchronize(st));

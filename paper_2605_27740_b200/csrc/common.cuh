@@ -23,6 +23,50 @@ __device__ __forceinline__ float load_elem(const void *base, int64_t i) {
     }
 }
 
+// Stage n contiguous elements (rows of length D) from global memory into shared f32 with
+// row stride ld, widening bf16.  Each thread issues up to MAXC 16-byte loads before its
+// first shared store, so a thread's share arrives in one memory round instead of one round
+// per loop iteration (the compiler does not hoist loads across the stores of a runtime-trip
+// loop).  Falls back to element loads when rows are not 16-byte multiples.
+template <int DT, int MAXC>
+__device__ __forceinline__ void stage_rows_f32(float *dst, int ld, const void *src, int n, int D,
+                                               int t, int nt) {
+    constexpr int ES = DT == PT_F32 ? 4 : 2;
+    constexpr int EPC = 16 / ES;
+    if ((D * ES) % 16 != 0 || (reinterpret_cast<uintptr_t>(src) & 15) != 0) {
+        for (int i = t; i < n; i += nt) dst[(i / D) * ld + (i % D)] = load_elem<DT>(src, i);
+        return;
+    }
+    const int C = n / EPC;
+    const uint4 *s4 = static_cast<const uint4 *>(src);
+    for (int c0 = t; c0 < C; c0 += MAXC * nt) {
+        uint4 v[MAXC];
+#pragma unroll
+        for (int j = 0; j < MAXC; j++) {
+            const int c = c0 + j * nt;
+            if (c < C) v[j] = __ldg(s4 + c);
+        }
+#pragma unroll
+        for (int j = 0; j < MAXC; j++) {
+            const int c = c0 + j * nt;
+            if (c >= C) break;
+            const int e = c * EPC, r = e / D, col = e - r * D;
+            float *o = dst + r * ld + col;
+            if constexpr (DT == PT_F32) {
+                o[0] = __uint_as_float(v[j].x); o[1] = __uint_as_float(v[j].y);
+                o[2] = __uint_as_float(v[j].z); o[3] = __uint_as_float(v[j].w);
+            } else {
+                const uint32_t w[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    o[2 * q] = __uint_as_float(w[q] << 16);
+                    o[2 * q + 1] = __uint_as_float(w[q] & 0xFFFF0000u);
+                }
+            }
+        }
+    }
+}
+
 // bf16.py:18-33 -- round to nearest even, NaN quieted (identical to __float2bfloat16_rn
 // for non-NaN inputs; written out so the NaN payload rule matches the reference).
 __device__ __forceinline__ uint16_t f32_to_bf16_rne(float x) {

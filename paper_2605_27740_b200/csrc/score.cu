@@ -69,6 +69,7 @@ struct ScoreParams {
     int32_t *sel, *sel_logical, *n_sel, *kth, *kplus1;
     int D, S, Pmax, k;
     float lam;
+    uint16_t *tile_max;  // [U][Pmax/32] or null
 };
 
 constexpr int kFusedThreads = 128;  // the fused selection runs with the 4-tile CTA
@@ -171,6 +172,11 @@ __global__ void __launch_bounds__(128) k_score(const ScoreParams prm) {
         keys[u * Pmax + p] = encode_ordered(f32_to_bf16_rne(best));
         if (scores) scores[u * Pmax + p] = best;
     }
+    if (prm.tile_max) {  // warp = one 32-page tile (p0 is a multiple of 32)
+        const uint32_t key = live ? (uint32_t)keys[u * Pmax + p] : 0u;
+        const uint32_t m = __reduce_max_sync(0xffffffffu, key);
+        if ((tid & 31) == 0 && p < P) prm.tile_max[u * (Pmax >> 5) + (p >> 5)] = (uint16_t)m;
+    }
     if (prm.counters == nullptr) return;
 
     // ---- fused selection: the last CTA to finish scoring unit u selects its top-k ----
@@ -201,27 +207,40 @@ __global__ void __launch_bounds__(128) k_score(const ScoreParams prm) {
 
 
 
-// lam * ||q_g|| for every (unit, g), numpy's float64 order (scoring.py:45), padded to 8
+// lam * ||q_g|| for every (unit, g), numpy's float64 order (scoring.py:45), padded to 8.
+// A CTA stages kLnRows query rows in shared memory with coalesced loads (one load round),
+// then thread r runs numpy's pairwise float64 sum over row r from shared memory -- the
+// accessor-driven sum over global memory would be a chain of dependent load rounds.
+constexpr int kLnRows = 32;
 template <int QDT>
-__global__ void k_lam_norms(const void *__restrict__ q, const float *__restrict__ norms_in,
-                            int rows, int G, int D, float lam, float *__restrict__ out) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= rows) return;
+__global__ void __launch_bounds__(256) k_lam_norms(const void *__restrict__ q,
+                                                   const float *__restrict__ norms_in, int rows,
+                                                   int G, int D, float lam, float *__restrict__ out) {
+    __shared__ float qs[kLnRows * (kScoreMaxD + 1)];
+    const int r0 = blockIdx.x * kLnRows;
+    const int nr = min(kLnRows, rows - r0);
+    const int ld = D + 1;  // odd stride: thread r's sequential reads hit distinct banks
+    if (!norms_in) {
+        const char *src = static_cast<const char *>(q) + (int64_t)r0 * D * (QDT == PT_F32 ? 4 : 2);
+        stage_rows_f32<QDT, 8>(qs, ld, src, nr * D, D, threadIdx.x, blockDim.x);
+    }
+    __syncthreads();
+    const int r = threadIdx.x;
+    if (r >= nr) return;
     float nrm;
     if (norms_in) {
-        nrm = norms_in[r];
+        nrm = norms_in[r0 + r];
     } else {
         struct Sq {
-            const void *q;
-            int64_t base;
+            const float *row;
             __device__ double operator()(int i) const {
-                const double v = (double)load_elem<QDT>(q, base + i);
+                const double v = (double)row[i];
                 return __dmul_rn(v, v);
             }
-        } sq{q, (int64_t)r * D};
+        } sq{qs + r * ld};
         nrm = __double2float_rn(__dsqrt_rn(np_sum(sq, D)));
     }
-    const int u = r / G, g = r - u * G;
+    const int u = (r0 + r) / G, g = (r0 + r) - u * G;
     out[(int64_t)u * 8 + g] = __fmul_rn(lam, nrm);
 }
 
@@ -306,7 +325,7 @@ int launch_score_stream_q16(const StreamScoreParams &sp, int sdt, int G, int D, 
 extern "C" int pt_score(const void *q, int q_dtype, const float *norms, const void *means,
                         int stats_dtype, const float *stds, const int32_t *seq_len, int U, int G,
                         int D, int S, int Pmax, float lam, uint16_t *keys, float *scores,
-                        float *lamnorm_ws, void *stream) {
+                        float *lamnorm_ws, uint16_t *tile_max, void *stream) {
     if (!q || !means || !stds || !seq_len || !keys || U < 0 || S < 1 || Pmax % 32 || G < 1)
         return PT_ERR_INVALID;
     const int V = stats_dtype == PT_F32 ? 4 : 8;
@@ -318,20 +337,55 @@ extern "C" int pt_score(const void *q, int q_dtype, const float *norms, const vo
         (long long)U * (Pmax / 32) < (1LL << 31)) {
         const int rows = U * G;
         if (q_dtype == PT_F32)
-            k_lam_norms<PT_F32><<<(rows + 127) / 128, 128, 0, st>>>(q, norms, rows, G, D, lam, lamnorm_ws);
+            k_lam_norms<PT_F32><<<(rows + kLnRows - 1) / kLnRows, 256, 0, st>>>(q, norms, rows, G, D, lam, lamnorm_ws);
         else
-            k_lam_norms<PT_BF16><<<(rows + 127) / 128, 128, 0, st>>>(q, norms, rows, G, D, lam, lamnorm_ws);
+            k_lam_norms<PT_BF16><<<(rows + kLnRows - 1) / kLnRows, 256, 0, st>>>(q, norms, rows, G, D, lam, lamnorm_ws);
         PT_CUDA_TRY(cudaGetLastError());
-        StreamScoreParams sp{q, lamnorm_ws, means, stds, seq_len, keys, scores, U, S, Pmax};
+        StreamScoreParams sp{q, lamnorm_ws, means, stds, seq_len, keys, scores, U, S, Pmax, tile_max};
         const int rc = q_dtype == PT_F32 ? launch_score_stream_q32(sp, stats_dtype, G, D, st)
                                          : launch_score_stream_q16(sp, stats_dtype, G, D, st);
         if (rc != PT_ERR_UNSUPPORTED) return rc;
     }
     ScoreParams prm{};
     prm.q = q; prm.norms_in = norms; prm.means = means; prm.stds = stds; prm.seq_len = seq_len;
-    prm.keys = keys; prm.scores = scores; prm.counters = nullptr;
+    prm.keys = keys; prm.scores = scores; prm.counters = nullptr; prm.tile_max = tile_max;
     prm.D = D; prm.S = S; prm.Pmax = Pmax; prm.lam = lam; prm.k = 0;
     return dispatch_score(prm, q_dtype, stats_dtype, U, G, st);
+}
+
+// lam * ||q_g|| of every query row into the padded [U][8] layout of the streaming kernel
+// (scoring.py:39-47 norms, numpy's float64 pairwise order; or lam * the given norms).
+extern "C" int pt_lam_norms(const void *q, int q_dtype, const float *norms, int U, int G, int D,
+                            float lam, float *lamnorm, void *stream) {
+    if (!q || !lamnorm || U < 0 || G < 1 || G > 8 || D < 1 || D > kScoreMaxD) return PT_ERR_INVALID;
+    if (U == 0) return PT_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int rows = U * G;
+    if (q_dtype == PT_F32)
+        k_lam_norms<PT_F32><<<(rows + kLnRows - 1) / kLnRows, 256, 0, st>>>(q, norms, rows, G, D, lam, lamnorm);
+    else
+        k_lam_norms<PT_BF16><<<(rows + kLnRows - 1) / kLnRows, 256, 0, st>>>(q, norms, rows, G, D, lam, lamnorm);
+    PT_CUDA_TRY(cudaGetLastError());
+    return PT_OK;
+}
+
+// K2 with lam * ||q|| precomputed by pt_lam_norms (so the norms launch can run beside the
+// append); streaming kernel only -- PT_ERR_UNSUPPORTED outside its envelope.
+extern "C" int pt_score_prenorm(const void *q, int q_dtype, const float *lamnorm,
+                                const void *means, int stats_dtype, const float *stds,
+                                const int32_t *seq_len, int U, int G, int D, int S, int Pmax,
+                                uint16_t *keys, float *scores, uint16_t *tile_max, void *stream) {
+    if (!q || !lamnorm || !means || !stds || !seq_len || !keys || U < 0 || S < 1 || Pmax % 32 ||
+        G < 1)
+        return PT_ERR_INVALID;
+    if (G > 8 || !(D == 64 || D == 128) || getenv("PT_SCORE_CTA") ||
+        (long long)U * (Pmax / 32) >= (1LL << 31))
+        return PT_ERR_UNSUPPORTED;
+    if (U == 0) return PT_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    StreamScoreParams sp{q, lamnorm, means, stds, seq_len, keys, scores, U, S, Pmax, tile_max};
+    return q_dtype == PT_F32 ? launch_score_stream_q32(sp, stats_dtype, G, D, st)
+                             : launch_score_stream_q16(sp, stats_dtype, G, D, st);
 }
 
 extern "C" int pt_score_select(const void *q, int q_dtype, const float *norms, const void *means,

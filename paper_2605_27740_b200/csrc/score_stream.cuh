@@ -32,6 +32,7 @@ struct StreamScoreParams {
     uint16_t *keys;
     float *scores;
     int U, S, Pmax;
+    uint16_t *tile_max;  // [U][Pmax/32] max key of each 32-page tile, or null
 };
 
 constexpr int kSSWarps = 4;
@@ -226,9 +227,14 @@ __global__ void __launch_bounds__(kSSWarps * 32, kSSCtas) k_score_stream(const S
             if (a > best) best = a;
         }
         const int p = ct * 32 + lane;
+        const uint32_t key = encode_ordered(f32_to_bf16_rne(best));
         if (p < Ps[cu]) {
-            prm.keys[(int64_t)cu * Pmax + p] = encode_ordered(f32_to_bf16_rne(best));
+            prm.keys[(int64_t)cu * Pmax + p] = (uint16_t)key;
             if (prm.scores) prm.scores[(int64_t)cu * Pmax + p] = best;
+        }
+        if (prm.tile_max) {  // the tile's largest key (pads contribute key 0, the minimum)
+            const uint32_t m = __reduce_max_sync(0xffffffffu, p < Ps[cu] ? key : 0u);
+            if (lane == 0) prm.tile_max[(int64_t)cu * TPU + ct] = (uint16_t)m;
         }
         __syncwarp();  // header + qf reads done before their slots are refilled
         fill(consumed);

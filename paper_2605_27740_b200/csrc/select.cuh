@@ -69,7 +69,12 @@ __device__ __forceinline__ void block_exscan2(int a, int b, int &ea, int &eb, in
 
 // Select for one unit.  `skeys` (shared, 16-byte aligned, room for P + 1 keys) holds the
 // unit's P keys; `bins` (shared, kSelectBins ints) is histogram scratch.  Writes
-// out/out_l [k]; thread 0 writes n_sel, kth, kplus1.
+// out/out_l [k]; thread 0 writes n_sel, kth, kplus1.  With `slist` (shared, k ints) the
+// compaction emits logical ids there and the page-table translation runs as one parallel
+// round of loads after it (instead of a dependent global load per selected page inside
+// each thread's serial compaction loop); on return slist holds the selected ids in
+// emission order -- logical, or physical with `slist_physical` (the fused attention
+// kernel streams straight from that list).  `out`/`out_l` may then be null.
 //
 // Threshold search: one pass for the key range [mn, mx]; when it spans <= kSelectBins
 // values (always, in practice: scores cluster in a few dozen bf16 values) a single
@@ -82,14 +87,25 @@ __device__ void select_block(uint16_t *skeys, int *bins, int P, int k,
                              const int32_t *__restrict__ map, int32_t *__restrict__ out,
                              int32_t *__restrict__ out_l, int32_t *__restrict__ n_sel,
                              int32_t *__restrict__ kth, int32_t *__restrict__ kplus1,
-                             SelectShared<NT> &sh) {
+                             SelectShared<NT> &sh, int *slist = nullptr,
+                             bool slist_physical = false, unsigned long long *tp = nullptr) {
+    // tp (tuning aid): thread 0 stamps %globaltimer after each phase
+    auto stamp = [&](int i) {
+        if (tp && threadIdx.x == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+            tp[i] = t;
+        }
+    };
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
     if (P <= k) {  // _take_all
         int mn = 0xFFFF;
         for (int i = tid; i < P; i += NT) {
-            out[i] = map[i];
+            const int pid = (out || (slist && slist_physical)) ? __ldg(map + i) : 0;
+            if (out) out[i] = pid;
             if (out_l) out_l[i] = i;
+            if (slist) slist[i] = slist_physical ? pid : i;
             mn = min(mn, (int)skeys[i]);
         }
         mn = __reduce_min_sync(0xffffffffu, mn);
@@ -109,6 +125,7 @@ __device__ void select_block(uint16_t *skeys, int *bins, int P, int k,
     __syncthreads();
     const uint32_t *w = reinterpret_cast<const uint32_t *>(skeys);
     const int nw = P >> 1;  // full words; an odd tail key is handled separately
+    stamp(0);
     // ---- key range ----
     int mn = 0xFFFF, mx = 0;
     for (int i = tid; i < nw; i += NT) {
@@ -128,8 +145,67 @@ __device__ void select_block(uint16_t *skeys, int *bins, int P, int k,
 #pragma unroll
     for (int i = 0; i < NT / 32; i++) { mn = min(mn, sh.warp_a[i]); mx = max(mx, sh.warp_b[i]); }
     const int R = mx - mn + 1;
-    int thr;
-    if (R <= kSelectBins) {
+    int thr = -1;
+    stamp(1);
+    // ---- fast path: the k-th largest key among the top 64 values below the maximum ----
+    // Lane-private u16 counters (a 32 x 32 word grid per warp, lane = column, so increments
+    // never conflict -- contended shared atomics on the few hot bins of clustered scores
+    // cost ~10 us per unit), summed by 32 warp reductions; falls through when the top 64
+    // values hold fewer than k keys.
+    if constexpr ((NT / 32) * 1024 <= kSelectBins) {
+        if (P / (NT / 32) < 65536 && R > 1) {
+            uint32_t *hw = reinterpret_cast<uint32_t *>(bins) + warp * 1024;
+#pragma unroll 8
+            for (int r = 0; r < 32; r++) hw[r * 32 + lane] = 0u;
+            for (int i = tid; i < nw; i += NT) {
+                const uint32_t x = w[i];
+                const int b0 = mx - (int)(x & 0xFFFF), b1 = mx - (int)(x >> 16);
+                if (b0 < 64) hw[(b0 >> 1) * 32 + lane] += 1u << ((b0 & 1) * 16);
+                if (b1 < 64) hw[(b1 >> 1) * 32 + lane] += 1u << ((b1 & 1) * 16);
+            }
+            if ((P & 1) && tid == 0) {
+                const int b = mx - (int)skeys[P - 1];
+                if (b < 64) hw[(b >> 1) * 32 + lane] += 1u << ((b & 1) * 16);
+            }
+            __syncwarp();
+            uint32_t mine = 0u;  // lane r: this warp's counts of bins 2r (lo) and 2r+1 (hi)
+#pragma unroll 8
+            for (int r = 0; r < 32; r++) {
+                const uint32_t v = __reduce_add_sync(0xffffffffu, hw[r * 32 + lane]);
+                if (lane == r) mine = v;
+            }
+            __syncwarp();
+            hw[lane] = mine;
+            __syncthreads();
+            if (warp == 0) {
+                int c0 = 0, c1 = 0;
+#pragma unroll
+                for (int wi = 0; wi < NT / 32; wi++) {
+                    const uint32_t v = reinterpret_cast<const uint32_t *>(bins)[wi * 1024 + lane];
+                    c0 += (int)(v & 0xFFFFu);
+                    c1 += (int)(v >> 16);
+                }
+                int inc = c0 + c1;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= o) inc += y;
+                }
+                const int pre = inc - c0 - c1;
+                int t = -1;
+                if (pre < k && pre + c0 >= k) t = mx - 2 * lane;
+                else if (pre + c0 < k && inc >= k) t = mx - 2 * lane - 1;
+                t = __reduce_max_sync(0xffffffffu, t);
+                if (lane == 0) sh.warp_a[0] = t;
+            }
+            __syncthreads();
+            thr = sh.warp_a[0];
+            __syncthreads();
+        }
+    }
+    if (thr >= 0) {
+        // threshold found by the fast path
+    } else if (R <= kSelectBins) {
         // ---- one-pass histogram of (key - mn) ----
         for (int i = tid; i < R; i += NT) bins[i] = 0;
         __syncthreads();
@@ -177,31 +253,76 @@ __device__ void select_block(uint16_t *skeys, int *bins, int P, int k,
         }
         thr = lo;
     }
-    // ---- ordered compaction over contiguous per-thread segments (logical order) ----
-    const int kseg = (P + NT - 1) / NT;
-    const int i0 = min(tid * kseg, P), i1 = min(i0 + kseg, P);
+    stamp(2);
+    // ---- ordered compaction (logical order), warp-segmented ----
+    // Warp w owns a contiguous run of key words; each step a warp reads 32 consecutive words
+    // (64 keys, bank-conflict free) and ranks them with ballots, so positions and the
+    // lowest-logical-index tie budget follow the logical order exactly.
+    constexpr int NWARPS = NT / 32;
+    const unsigned lt = (1u << lane) - 1u;
+    const int nwt = (P + 1) >> 1;
+    const int segw = (((nwt + NWARPS - 1) / NWARPS) + 31) & ~31;
+    const int wb = min(warp * segw, nwt), we = min(wb + segw, nwt);
     int gt = 0, eq = 0, below = -1;
-    for (int i = i0; i < i1; i++) {
-        const int key = skeys[i];
-        gt += key > thr;
-        eq += key == thr;
-        if (key < thr) below = max(below, key);
+    for (int i = wb + lane; i < we; i += 32) {
+        const uint32_t x = w[i];
+        const int k0 = x & 0xFFFF, k1 = x >> 16;
+        const bool v1 = 2 * i + 1 < P;
+        gt += (k0 > thr) + (v1 && k1 > thr);
+        eq += (k0 == thr) + (v1 && k1 == thr);
+        if (k0 < thr) below = max(below, k0);
+        if (v1 && k1 < thr) below = max(below, k1);
     }
-    int eq_before, gt_before, eq_tot, gt_tot;
-    block_exscan2<NT>(eq, gt, eq_before, gt_before, eq_tot, gt_tot, sh);
-    const int tie_budget = k - gt_tot;
-    const int take = max(0, min(eq, tie_budget - eq_before));
-    int pos, dummy, tot_sel, dummy2;
-    block_exscan2<NT>(gt + take, 0, pos, dummy, tot_sel, dummy2, sh);
-    int taken = 0;
-    for (int i = i0; i < i1; i++) {
-        const int key = skeys[i];
-        bool s = key > thr;
-        if (key == thr && taken < take) { s = true; taken++; }
-        if (s) {
-            out[pos] = map[i];
-            if (out_l) out_l[pos] = i;
-            pos++;
+    gt = __reduce_add_sync(0xffffffffu, gt);
+    eq = __reduce_add_sync(0xffffffffu, eq);
+    __syncthreads();
+    if (lane == 0) { sh.warp_a[warp] = gt; sh.warp_b[warp] = eq; }
+    __syncthreads();
+    int gt_before = 0, eq_before = 0, gt_tot = 0, eq_tot = 0;
+#pragma unroll
+    for (int wi = 0; wi < NWARPS; wi++) {
+        const int a2 = sh.warp_a[wi], b2 = sh.warp_b[wi];
+        if (wi < warp) { gt_before += a2; eq_before += b2; }
+        gt_tot += a2;
+        eq_tot += b2;
+    }
+    const int tie_budget = k - gt_tot;  // in [1, eq_tot]: thr is the k-th largest key
+    int run_sel = gt_before + min(eq_before, tie_budget);
+    int run_eq = eq_before;
+    for (int base = wb; base < we; base += 32) {
+        const int i = base + lane;
+        const bool v0 = i < we, v1 = v0 && 2 * i + 1 < P;
+        const uint32_t x = v0 ? w[i] : 0u;
+        const int k0 = x & 0xFFFF, k1 = x >> 16;
+        const bool e0 = v0 && k0 == thr, e1 = v1 && k1 == thr;
+        const unsigned be0 = __ballot_sync(0xffffffffu, e0), be1 = __ballot_sync(0xffffffffu, e1);
+        const int t0 = run_eq + __popc(be0 & lt) + __popc(be1 & lt);  // ties before key 2i
+        const bool s0 = (v0 && k0 > thr) || (e0 && t0 < tie_budget);
+        const bool s1 = (v1 && k1 > thr) || (e1 && t0 + (int)e0 < tie_budget);
+        const unsigned bs0 = __ballot_sync(0xffffffffu, s0), bs1 = __ballot_sync(0xffffffffu, s1);
+        const int p0 = run_sel + __popc(bs0 & lt) + __popc(bs1 & lt);
+        if (s0 || s1) {
+            const int p1 = p0 + (int)s0;
+            if (slist) {
+                if (s0) slist[p0] = 2 * i;
+                if (s1) slist[p1] = 2 * i + 1;
+            } else {
+                if (s0) { out[p0] = map[2 * i]; if (out_l) out_l[p0] = 2 * i; }
+                if (s1) { out[p1] = map[2 * i + 1]; if (out_l) out_l[p1] = 2 * i + 1; }
+            }
+        }
+        run_eq += __popc(be0) + __popc(be1);
+        run_sel += __popc(bs0) + __popc(bs1);
+    }
+    stamp(3);
+    if (slist) {
+        __syncthreads();
+        for (int t = tid; t < k; t += NT) {
+            const int li = slist[t];
+            const int pid = __ldg(map + li);
+            if (out) out[t] = pid;
+            if (out_l) out_l[t] = li;
+            if (slist_physical) slist[t] = pid;
         }
     }
     below = __reduce_max_sync(0xffffffffu, below);
@@ -215,6 +336,287 @@ __device__ void select_block(uint16_t *skeys, int *bins, int P, int k,
         *kth = thr;
         *kplus1 = (eq_tot > tie_budget) ? thr : m;
     }
+}
+
+// ---------------------------------------------------------------------------
+// Candidate selection (the fused select+attend prologue).
+//
+// Uses the per-32-page tile maxima written by the scoring kernel: the k-th largest tile
+// maximum L is a lower bound for the k-th largest key (k distinct tiles each hold a key
+// >= L), and for scores of a decode step only ~1-3 % of the keys reach it.  So:
+//   1. L = k-th largest of the ceil(P/32) tile maxima (two 8-way counting rounds relative
+//      to the overall maximum mt, packed 8-bit counters, block reductions);
+//   2. one pass over the keys (register-resident: thread t holds the 16-byte key vectors
+//      t, t+NT, ...) appends every key >= L to a shared candidate list (key << 16 | index);
+//   3. the k-th largest candidate (a 64-bin shared histogram over [L, mt]) is the
+//      threshold thr; keys > thr are selected, ties at thr by ascending logical index
+//      (rank among the tied candidates) -- the reference's rule -- emitted in ascending
+//      logical order: the same list as select_block.
+// Returns false (uniformly) when the shape or the data leave this envelope (fewer tiles
+// than k, L not within 64 values of mt, more than kCandMax candidates); the caller then
+// runs select_block.
+// ---------------------------------------------------------------------------
+constexpr int kCandMax = 2048;
+
+template <int NT>
+struct SelectCandShared {
+    uint32_t red[NT / 32][8];
+    int bins[64];
+    int below, thr, gt, eq;
+    uint32_t cand[kCandMax];
+};
+
+template <int NT, int MAXJ>
+__device__ bool select_cand(const uint16_t *__restrict__ keys_g, const uint16_t *__restrict__ tmax_g,
+                            int P, int k, const int32_t *__restrict__ map,
+                            int32_t *__restrict__ out, int32_t *__restrict__ out_l,
+                            int32_t *__restrict__ n_sel, int32_t *__restrict__ kth,
+                            int32_t *__restrict__ kplus1, SelectCandShared<NT> &sh, int *slist,
+                            bool slist_physical, unsigned long long *tp = nullptr) {
+    auto stamp = [&](int i) {
+        if (tp && threadIdx.x == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+            tp[i] = t;
+        }
+    };
+    constexpr int NWP = NT / 32;
+    constexpr int MAXT = 4;  // tile maxima per thread: ceil(P / 32) <= NT * MAXT
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int ntiles = (P + 31) >> 5;
+    if (P > NT * 8 * MAXJ || P <= k || ntiles < k || ntiles > NT * MAXT) return false;
+    // ---- issue every load up front: keys (registers) and tile maxima ----
+    const uint4 *k4 = reinterpret_cast<const uint4 *>(keys_g);
+    uint4 v[MAXJ];
+#pragma unroll
+    for (int j = 0; j < MAXJ; j++) {
+        const int base = (tid + j * NT) * 8;
+        v[j] = base < P ? __ldcg(k4 + tid + j * NT) : make_uint4(0u, 0u, 0u, 0u);
+    }
+    int tm[MAXT];
+#pragma unroll
+    for (int i = 0; i < MAXT; i++) {
+        const int t = tid + i * NT;
+        tm[i] = t < ntiles ? (int)__ldcg(tmax_g + t) : -1;
+    }
+    if (tid < 64) sh.bins[tid] = 0;
+    if (tid == 0) sh.below = -1;
+    // ---- 1. L = k-th largest tile maximum ----
+    int mt = -1;
+#pragma unroll
+    for (int i = 0; i < MAXT; i++) mt = max(mt, tm[i]);
+    mt = __reduce_max_sync(0xffffffffu, mt);
+    if (lane == 0) sh.red[warp][0] = (uint32_t)mt;
+    __syncthreads();
+    mt = -1;
+#pragma unroll
+    for (int w = 0; w < NWP; w++) mt = max(mt, (int)sh.red[w][0]);
+    __syncthreads();
+    stamp(0);
+    auto round8 = [&](int lo, int shift, int (&tot)[8]) {
+        unsigned long long c = 0ull;
+#pragma unroll
+        for (int i = 0; i < MAXT; i++) {
+            const int d = mt - tm[i] - lo, b = d >> shift;
+            if (tm[i] >= 0 && d >= 0 && b < 8) c += 1ull << (8 * b);
+        }
+#pragma unroll
+        for (int b = 0; b < 8; b++) {
+            const uint32_t x = __reduce_add_sync(0xffffffffu, (uint32_t)((c >> (8 * b)) & 0xFFu));
+            if (lane == 0) sh.red[warp][b] = x;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int b = 0; b < 8; b++) {
+            int t = 0;
+#pragma unroll
+            for (int w = 0; w < NWP; w++) t += (int)sh.red[w][b];
+            tot[b] = t;
+        }
+        __syncthreads();
+    };
+    int ta[8], tb[8];
+    round8(0, 3, ta);
+    int ia = -1, cum = 0, before = 0;
+#pragma unroll
+    for (int b = 0; b < 8; b++) {
+        if (ia < 0 && cum + ta[b] >= k) { ia = b; before = cum; }
+        cum += ta[b];
+    }
+    if (ia < 0) return false;
+    round8(8 * ia, 0, tb);
+    int ib = 7;
+    {
+        int c2 = before;
+        bool done = false;
+#pragma unroll
+        for (int b = 0; b < 8; b++) {
+            if (!done && c2 + tb[b] >= k) { ib = b; done = true; }
+            c2 += tb[b];
+        }
+    }
+    const int L = mt - (8 * ia + ib);  // within 64 values of mt: candidate keys fit 64 bins
+    stamp(1);
+    // ---- 2. candidates: every valid key >= L, and the largest valid key below L ----
+    auto keyof = [&](const uint4 &x, int e) -> int {
+        const uint32_t w = e < 2 ? x.x : e < 4 ? x.y : e < 6 ? x.z : x.w;
+        return (e & 1) ? (int)(w >> 16) : (int)(w & 0xFFFFu);
+    };
+    // per (vector j, thread) candidate counts, scanned in logical order (j-major, then
+    // thread) so the list is written in ascending logical index; two 16-bit counts per word
+    static_assert(MAXJ % 2 == 0 && MAXJ / 2 <= 8, "MAXJ");
+    uint32_t cnt[MAXJ / 2];
+    int below = -1;
+#pragma unroll
+    for (int w = 0; w < MAXJ / 2; w++) cnt[w] = 0u;
+#pragma unroll
+    for (int j = 0; j < MAXJ; j++) {
+        const int base = (tid + j * NT) * 8;
+        if (j * NT * 8 >= P) break;
+        uint32_t c = 0;
+#pragma unroll
+        for (int e = 0; e < 8; e++) {
+            const int key = keyof(v[j], e);
+            const bool ok = base + e < P;
+            c += (ok && key >= L);
+            if (ok && key < L) below = max(below, key);
+        }
+        cnt[j >> 1] += c << (16 * (j & 1));
+    }
+    uint32_t inc[MAXJ / 2];
+#pragma unroll
+    for (int w = 0; w < MAXJ / 2; w++) inc[w] = cnt[w];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+        for (int w = 0; w < MAXJ / 2; w++) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc[w], o);
+            if (lane >= o) inc[w] += y;
+        }
+    }
+    below = __reduce_max_sync(0xffffffffu, below);
+    if (lane == 0) atomicMax(&sh.below, below);
+    if (lane == 31) {
+#pragma unroll
+        for (int w = 0; w < MAXJ / 2; w++) sh.red[warp][w] = inc[w];
+    }
+    __syncthreads();
+    int run = 0;  // candidates in vectors j' < j (all threads)
+#pragma unroll
+    for (int j = 0; j < MAXJ; j++) {
+        if (j * NT * 8 >= P) break;
+        const int sh16 = 16 * (j & 1);
+        int pos = run + (int)(((inc[j >> 1] - cnt[j >> 1]) >> sh16) & 0xFFFFu);
+#pragma unroll
+        for (int w = 0; w < NWP; w++) {
+            const int t = (int)((sh.red[w][j >> 1] >> sh16) & 0xFFFFu);
+            if (w < warp) pos += t;
+            run += t;
+        }
+        if ((cnt[j >> 1] >> sh16) & 0xFFFFu) {
+            const int base = (tid + j * NT) * 8;
+#pragma unroll
+            for (int e = 0; e < 8; e++) {
+                const int key = keyof(v[j], e);
+                if (base + e < P && key >= L) {
+                    if (pos < kCandMax) sh.cand[pos] = ((uint32_t)key << 16) | (uint32_t)(base + e);
+                    pos++;
+                }
+            }
+        }
+    }
+    const int C = run;
+    if (C > kCandMax) return false;  // uniform
+    __syncthreads();
+    stamp(2);
+    // ---- 3. threshold among the candidates: 64-bin histogram of mt - key ----
+    for (int i = tid; i < C; i += NT) atomicAdd(&sh.bins[mt - (int)(sh.cand[i] >> 16)], 1);
+    __syncthreads();
+    if (warp == 0) {
+        const int c0 = sh.bins[2 * lane], c1 = sh.bins[2 * lane + 1];
+        int incl = c0 + c1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int pre = incl - c0 - c1;
+        int b = -1, gt = 0, eq = 0;
+        if (pre < k && pre + c0 >= k) { b = 2 * lane; gt = pre; eq = c0; }
+        else if (pre + c0 < k && incl >= k) { b = 2 * lane + 1; gt = pre + c0; eq = c1; }
+        // largest key below thr among the candidates: the first non-empty bin past b
+        const unsigned hit = __ballot_sync(0xffffffffu, b >= 0);
+        const int src = __ffs(hit) - 1;
+        const int bt = __shfl_sync(0xffffffffu, b, src);
+        const int nb = (c0 > 0 && 2 * lane > bt) ? 2 * lane : (c1 > 0 && 2 * lane + 1 > bt) ? 2 * lane + 1 : 999;
+        const int nbm = __reduce_min_sync(0xffffffffu, nb);
+        if (lane == src) {
+            sh.thr = mt - b;
+            sh.gt = gt;
+            sh.eq = eq;
+            if (nbm < 999) sh.below = mt - nbm;  // a candidate lies below thr
+        }
+    }
+    __syncthreads();
+    const int thr = sh.thr, gt_tot = sh.gt, eq_tot = sh.eq;
+    const int budget = k - gt_tot;  // in [1, eq_tot]
+    stamp(3);
+    // ---- ordered compaction of the (logically ordered) candidates: keys > thr, then the
+    // first `budget` ties -- contiguous per-thread segments and one block scan ----
+    {
+        const int cs = (C + NT - 1) / NT;
+        const int i0 = min(tid * cs, C), i1 = min(i0 + cs, C);
+        int g = 0, q = 0;
+        for (int i = i0; i < i1; i++) {
+            const int key = (int)(sh.cand[i] >> 16);
+            g += key > thr;
+            q += key == thr;
+        }
+        int ig = g, iq = q;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int yg = __shfl_up_sync(0xffffffffu, ig, o);
+            const int yq = __shfl_up_sync(0xffffffffu, iq, o);
+            if (lane >= o) { ig += yg; iq += yq; }
+        }
+        __syncthreads();  // sh.red reuse
+        if (lane == 31) { sh.red[warp][0] = (uint32_t)ig; sh.red[warp][1] = (uint32_t)iq; }
+        __syncthreads();
+        int gb = ig - g, qb = iq - q;
+#pragma unroll
+        for (int w = 0; w < NWP; w++)
+            if (w < warp) { gb += (int)sh.red[w][0]; qb += (int)sh.red[w][1]; }
+        int pos = gb + min(qb, budget);
+        int seen = qb;
+        for (int i = i0; i < i1; i++) {
+            const uint32_t c = sh.cand[i];
+            const int key = (int)(c >> 16), idx = (int)(c & 0xFFFFu);
+            bool sel = key > thr;
+            if (key == thr) { sel = seen < budget; seen++; }
+            if (sel) {
+                if (slist) slist[pos] = idx;
+                else { out[pos] = map[idx]; if (out_l) out_l[pos] = idx; }
+                pos++;
+            }
+        }
+    }
+    if (slist) {
+        __syncthreads();
+        for (int t = tid; t < k; t += NT) {
+            const int li = slist[t];
+            const int pid = __ldg(map + li);
+            if (out) out[t] = pid;
+            if (out_l) out_l[t] = li;
+            if (slist_physical) slist[t] = pid;
+        }
+    }
+    if (tid == 0) {
+        *n_sel = k;
+        *kth = thr;
+        *kplus1 = (eq_tot > budget) ? thr : sh.below;
+    }
+    __syncthreads();
+    return true;
 }
 
 }  // namespace pt

@@ -9,6 +9,8 @@
 // Layout: one warp per page; lane owns dims d = lane + 32*j (a warp load is one
 // contiguous row slice, coalesced); float64 per-dim accumulators live in registers;
 // the D per-dim variances go through shared memory for numpy's pairwise sum.
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace pt {
@@ -74,30 +76,35 @@ __global__ void __launch_bounds__(kStatsWarps * 32)
 // ---------------------------------------------------------------------------
 // decode append (kvcache.py:185-208), batched over units
 // ---------------------------------------------------------------------------
-// Phase 1 (one CTA): deterministic physical-page allocation in unit order, the
-// batched form of _alloc_page (kvcache.py:154-176): free list popped from its end
-// first (list.pop()), then the bump pointer; exhaustion -> error flag, unit skipped.
-// Single-launch append.  CTA 0 first runs the unit-order allocation scan above for every
-// unit (k_append_alloc's body), publishes it with a release flag, and the other CTAs
-// acquire it before touching their units (CTA 0 never waits, so there is no deadlock even
-// when the grid exceeds the resident capacity; the last CTA to finish re-arms the flag).
-// Then one warp per unit writes the new K/V row and recomputes the tail page's stats from
-// a shared-memory copy of the page rows (one load round instead of 2*rows dependent ones).
-__device__ void alloc_block(int32_t *__restrict__ page_table, const int32_t *__restrict__ seq_len,
-                            int U, int S, int Pmax, int32_t *__restrict__ pool_state,
-                            const int32_t *__restrict__ free_list, int32_t *__restrict__ slot,
-                            int *warp_tot, int *carry) {
+// Decode append, one launch (kvcache.py:185-208 for every unit).
+//
+// CTA 0 snapshots every unit's length into shared memory and publishes `flag_read`; if any
+// unit starts a new page it runs the deterministic unit-order allocation -- the batched
+// _alloc_page (kvcache.py:154-176): free list popped from its end (list.pop()), then the
+// bump pointer; exhaustion -> error flag, unit skipped -- and publishes `flag_alloc`.
+// Every warp owns one unit: units continuing their tail page (15 of 16 steps at S = 16)
+// never wait; a unit starting a page waits for the allocation.  The warp writes the new
+// K/V row and recomputes the tail page's stats from a shared-memory copy of its rows (one
+// load round), then -- once CTA 0's snapshot is taken (flag_read; normally long set) --
+// advances its own sequence length.  The last CTA to finish re-arms the flags.  CTA 0
+// never waits, so the scheme cannot deadlock while CTAs are dispatched in index order.
+__device__ __forceinline__ void spin_flag(int *flag, bool acquire) {
+    while (atomicAdd(flag, 0) == 0) __nanosleep(32);
+    if (acquire) __threadfence();  // the allocation's page table / slot writes
+}
+
+__device__ void alloc_scan(int32_t *__restrict__ page_table, const int *__restrict__ sn, int U,
+                           int S, int Pmax, int32_t *__restrict__ pool_state,
+                           const int32_t *__restrict__ free_list, int32_t *__restrict__ slot,
+                           int *warp_tot, int *carry) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
     const int bump0 = pool_state[0], free0 = pool_state[1], max_pages = pool_state[2];
     if (tid == 0) *carry = 0;
     __syncthreads();
     for (int base = 0; base < U; base += blockDim.x) {
         const int u = base + tid;
-        int n = 0, need = 0;
-        if (u < U) {
-            n = seq_len[u];
-            need = (n % S == 0) ? 1 : 0;
-        }
+        const int n = u < U ? sn[u] : 1;
+        const int need = (u < U && n % S == 0) ? 1 : 0;
         const unsigned m = __ballot_sync(0xffffffffu, need);
         const int wpre = __popc(m & ((1u << lane) - 1u));
         if (lane == 0) warp_tot[warp] = __popc(m);
@@ -108,22 +115,16 @@ __device__ void alloc_block(int32_t *__restrict__ page_table, const int32_t *__r
             chunk_total += warp_tot[w];
         }
         const int rank = before + wpre;
-        if (u < U) {
-            int target;
-            if (need) {
-                const int pid = rank < free0 ? free_list[free0 - 1 - rank] : bump0 + (rank - free0);
-                const int lp = n / S;
-                if (pid >= max_pages || lp >= Pmax) {
-                    target = -1;
-                    pool_state[3] = PT_ERR_CAPACITY;
-                } else {
-                    page_table[(int64_t)u * Pmax + lp] = pid;
-                    target = pid;
-                }
+        if (need) {
+            const int pid = rank < free0 ? free_list[free0 - 1 - rank] : bump0 + (rank - free0);
+            const int lp = n / S;
+            if (pid >= max_pages || lp >= Pmax) {
+                slot[u] = -1;
+                pool_state[3] = PT_ERR_CAPACITY;
             } else {
-                target = page_table[(int64_t)u * Pmax + n / S];
+                page_table[(int64_t)u * Pmax + lp] = pid;
+                slot[u] = pid;
             }
-            slot[u] = target;
         }
         __syncthreads();
         if (tid == 0) *carry += chunk_total;
@@ -149,41 +150,64 @@ __global__ void __launch_bounds__(256)
     extern __shared__ __align__(16) char asmem[];
     __shared__ int warp_tot[8];
     __shared__ int carry;
+    __shared__ int is_last;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpc = blockDim.x >> 5;
-    int *flag = slot + U, *done = slot + U + 1;
+    int *flag_alloc = slot + U, *done = slot + U + 1, *flag_read = slot + U + 2;
+    const size_t per_warp = (size_t)S * D * 4 + (size_t)D * 8;
+    const int64_t u = (int64_t)blockIdx.x * wpc + warp;
+    using Bits = typename std::conditional<DT == PT_F32, uint32_t, uint16_t>::type;
+    // this unit's length (read before anyone advances it) and the new K/V row
+    const int n = u < U ? seq_len[u] : 0;
+    Bits kb[DJ], vb[DJ];
+#pragma unroll
+    for (int j = 0; j < DJ; j++) {
+        const int d = lane + 32 * j;
+        if (u < U && d < D) {
+            kb[j] = static_cast<const Bits *>(k_new)[u * D + d];
+            vb[j] = static_cast<const Bits *>(v_new)[u * D + d];
+        }
+    }
     if (blockIdx.x == 0) {
-        alloc_block(page_table, seq_len, U, S, Pmax, pool_state, free_list, slot, warp_tot, &carry);
+        int *sn = reinterpret_cast<int *>(asmem + per_warp * wpc);
+        int any = 0;
+        for (int i = threadIdx.x; i < U; i += blockDim.x) {
+            const int ni = seq_len[i];
+            sn[i] = ni;
+            any |= (ni % S == 0);
+        }
+        any = __syncthreads_or(any);
+        if (threadIdx.x == 0) { __threadfence(); atomicExch(flag_read, 1); }
+        if (any) alloc_scan(page_table, sn, U, S, Pmax, pool_state, free_list, slot, warp_tot, &carry);
         __threadfence();
         __syncthreads();
-        if (threadIdx.x == 0) atomicExch(flag, 1);
-    } else {
-        if (threadIdx.x == 0) {
-            while (atomicAdd(flag, 0) == 0) __nanosleep(64);
-            __threadfence();
-        }
-        __syncthreads();
+        if (threadIdx.x == 0) atomicExch(flag_alloc, 1);
     }
-    const int64_t u = (int64_t)blockIdx.x * wpc + warp;
-    const size_t per_warp = (size_t)S * D * 4 + (size_t)D * 8;
     float *rows_s = reinterpret_cast<float *>(asmem + warp * per_warp);
     double *var_s = reinterpret_cast<double *>(asmem + warp * per_warp + (size_t)S * D * 4);
     if (u < U) {
-        const int pid = __ldcg(&slot[u]);
+        int pid;
+        if (n % S == 0) {  // starts a page: CTA 0's allocation
+            if (lane == 0) spin_flag(flag_alloc, true);
+            __syncwarp();
+            pid = __ldcg(&slot[u]);
+        } else {
+            pid = page_table[u * Pmax + n / S];
+        }
         if (pid >= 0) {
-            const int n = seq_len[u];
             const int row = n % S;
             const int64_t base = (int64_t)pid * S * D;
             // stage the page's existing rows (one load round) and the new row
-            for (int i = lane; i < row * D; i += 32) rows_s[i] = load_elem<DT>(k_pool, base + i);
-            for (int d = lane; d < D; d += 32) {
-                const float kv = load_elem<DT>(k_new, u * D + d);
-                rows_s[row * D + d] = kv;
-                if constexpr (DT == PT_F32) {
-                    static_cast<float *>(k_pool)[base + (int64_t)row * D + d] = static_cast<const float *>(k_new)[u * D + d];
-                    static_cast<float *>(v_pool)[base + (int64_t)row * D + d] = static_cast<const float *>(v_new)[u * D + d];
-                } else {
-                    static_cast<uint16_t *>(k_pool)[base + (int64_t)row * D + d] = static_cast<const uint16_t *>(k_new)[u * D + d];
-                    static_cast<uint16_t *>(v_pool)[base + (int64_t)row * D + d] = static_cast<const uint16_t *>(v_new)[u * D + d];
+            stage_rows_f32<DT, 8>(rows_s, D,
+                                  static_cast<const char *>(k_pool) + base * (DT == PT_F32 ? 4 : 2),
+                                  row * D, D, lane, 32);
+#pragma unroll
+            for (int j = 0; j < DJ; j++) {
+                const int d = lane + 32 * j;
+                if (d < D) {
+                    rows_s[row * D + d] = DT == PT_F32 ? __uint_as_float(kb[j])
+                                                       : bf16_bits_to_f32(kb[j]);
+                    static_cast<Bits *>(k_pool)[base + (int64_t)row * D + d] = kb[j];
+                    static_cast<Bits *>(v_pool)[base + (int64_t)row * D + d] = vb[j];
                 }
             }
             __syncwarp();
@@ -214,15 +238,17 @@ __global__ void __launch_bounds__(256)
             __syncwarp();
             if (lane == 0) {
                 stds[u * Pmax + n / S] = __double2float_rn(__dsqrt_rn(np_sum(DoubleArray{var_s}, D)));
+                spin_flag(flag_read, false);  // CTA 0 has snapshotted every length (no data to acquire)
                 seq_len[u] = n + 1;
             }
         }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();
+        // every flag use of this CTA precedes this atomic in program order: no fence needed
         if (atomicAdd(done, 1) == (int)gridDim.x - 1) {  // re-arm for the next append
-            atomicExch(flag, 0);
+            atomicExch(flag_alloc, 0);
+            atomicExch(flag_read, 0);
             atomicExch(done, 0);
         }
     }
@@ -311,10 +337,11 @@ static int launch_append(const void *kn, const void *vn, void *kp, void *vp, int
                          int32_t *pool_state, const int32_t *free_list, int32_t *slot,
                          cudaStream_t st) {
     const size_t per_warp = (size_t)S * D * 4 + (size_t)D * 8;
-    int wpc = (int)((200 * 1024) / per_warp);
-    if (wpc > 8) wpc = 8;
-    if (wpc < 1) return PT_ERR_UNSUPPORTED;
-    const size_t smem = per_warp * wpc;
+    const size_t snap = (size_t)U * 4;  // CTA 0's snapshot of every unit's length
+    if (snap + per_warp > 200 * 1024) return PT_ERR_UNSUPPORTED;
+    int wpc = (int)((200 * 1024 - snap) / per_warp);
+    if (wpc > 4) wpc = 4;  // spread the latency-bound per-unit warps over more SMs
+    const size_t smem = per_warp * wpc + snap;
     const int grid = (U + wpc - 1) / wpc;
     const int dj = (D + 31) / 32;
 #define PT_APP_CASE(DJ_)                                                                      \

@@ -1,6 +1,6 @@
 // topk.cu -- K3: per-unit top-k page selection (standalone kernel; see select.cuh).
 //
-// One CTA (512 threads) per unit stages the unit's keys once in shared memory and runs the
+// One CTA (128 threads) per unit stages the unit's keys once in shared memory and runs the
 // block selection of select.cuh (bisection for the threshold key, ordered compaction for
 // the lowest-logical-index tie rule, page-table translation in the epilogue).  The decode
 // engine normally runs this fused into the tail of the scoring kernel (score.cu); this
@@ -28,19 +28,32 @@ __global__ void __launch_bounds__(kTopkThreads)
         return;
     }
     const uint4 *src = reinterpret_cast<const uint4 *>(keys_g + u * (int64_t)Pmax);
-    for (int i = threadIdx.x; i < (P + 7) / 8; i += kTopkThreads)
-        reinterpret_cast<uint4 *>(skeys)[i] = __ldg(src + i);
+    {  // all of a thread's 16-byte key loads in flight before its first shared store
+        constexpr int kMax = 4;
+        const int nv = (P + 7) / 8;
+        for (int i0 = threadIdx.x; i0 < nv; i0 += kMax * kTopkThreads) {
+            uint4 v[kMax];
+#pragma unroll
+            for (int j = 0; j < kMax; j++)
+                if (i0 + j * kTopkThreads < nv) v[j] = __ldg(src + i0 + j * kTopkThreads);
+#pragma unroll
+            for (int j = 0; j < kMax; j++)
+                if (i0 + j * kTopkThreads < nv) reinterpret_cast<uint4 *>(skeys)[i0 + j * kTopkThreads] = v[j];
+        }
+    }
     __syncthreads();
     select_block<kTopkThreads>(skeys, bins, P, k, page_table + u * Pmax, sel + u * (int64_t)k,
                                sel_logical ? sel_logical + u * (int64_t)k : nullptr, n_sel + u,
-                               kth + u, kplus1 + u, sh);
+                               kth + u, kplus1 + u, sh,
+                               reinterpret_cast<int *>(skeys + ((Pmax + 8) & ~7)));
 }
 
 }  // namespace pt
 
 using namespace pt;
 
-static size_t topk_smem_bytes(int Pmax) { return (size_t)((Pmax + 8) / 8) * 16; }
+// keys (+1 pad key, 16-byte rounded) then the k-entry logical-id list
+static size_t topk_smem_bytes(int Pmax, int k) { return (size_t)((Pmax + 8) / 8) * 16 + (size_t)k * 4; }
 
 extern "C" int pt_topk(const uint16_t *keys, const int32_t *seq_len, const int32_t *page_table,
                        int U, int S, int Pmax, int k, int32_t *sel, int32_t *sel_logical,
@@ -50,11 +63,12 @@ extern "C" int pt_topk(const uint16_t *keys, const int32_t *seq_len, const int32
         return PT_ERR_INVALID;
     if (k < 1) return PT_ERR_K;
     if (U == 0) return PT_OK;
-    const size_t smem = topk_smem_bytes(Pmax);
+    const size_t smem = topk_smem_bytes(Pmax, k);
     if (smem > 200 * 1024) return PT_ERR_UNSUPPORTED;
-    // PT_TOPK_THREADS (256 / 512 / 1024) overrides the block size (tuning)
+    // PT_TOPK_THREADS (128 / 256 / 512 / 1024) overrides the block size (tuning); 128 keeps
+    // the conflict-free top-64 histogram of select_block in its 16 KB scratch
     const char *e = getenv("PT_TOPK_THREADS");
-    const int nt = e ? atoi(e) : 512;
+    const int nt = e ? atoi(e) : 128;
     cudaStream_t st = (cudaStream_t)stream;
 #define PT_TOPK(NT_)                                                                           \
     if (nt == NT_) {                                                                           \
@@ -67,7 +81,7 @@ extern "C" int pt_topk(const uint16_t *keys, const int32_t *seq_len, const int32
         k_topk<NT_><<<U, NT_, smem, st>>>(keys, seq_len, page_table, S, Pmax, k, sel, sel_logical, \
                                           n_sel, kth, kplus1);                                 \
     } else
-    PT_TOPK(256) PT_TOPK(1024) PT_TOPK(512)
+    PT_TOPK(256) PT_TOPK(512) PT_TOPK(1024) PT_TOPK(128)
 #undef PT_TOPK
     PT_CUDA_TRY(cudaGetLastError());
     return PT_OK;

@@ -50,6 +50,7 @@ class DecodeEngine:
         U, Pmax, d = cache.num_units, cache.Pmax, cache.device
         self.U, self.D = U, D
         self.keys = torch.zeros(U, Pmax, dtype=torch.int16, device=d)  # u16 bit patterns
+        self.tile_max = torch.zeros(U, Pmax // 32, dtype=torch.int16, device=d)  # per 32 pages
         self.scores = torch.zeros(U, Pmax, dtype=torch.float32, device=d) if keep_scores else None
         self.sel = torch.zeros(U, self.k, dtype=torch.int32, device=d)
         self.sel_logical = (torch.zeros(U, self.k, dtype=torch.int32, device=d)
@@ -69,8 +70,11 @@ class DecodeEngine:
         # K2 streaming kernel + K3 (two launches) is the default; the one-launch fused
         # score+select CTA kernel (pt_score_select) is kept as an alternative
         self.fused_select = False
+        # K3 + K4 fused (pt_select_attend) is the default after K2
+        self.fused_attend = True
         self.dense_tickets = torch.zeros(U, dtype=torch.int32, device=d)
         self.graph: torch.cuda.CUDAGraph | None = None
+        self._side = torch.cuda.Stream(device=d)
 
     # ------------------------------------------------------------------
     def _q(self, q: torch.Tensor) -> tuple[torch.Tensor, int]:
@@ -88,7 +92,29 @@ class DecodeEngine:
         _lib.call("pt_score", q2.data_ptr(), qc, dev.ptr(norms), c.means.data_ptr(), c.stats_code,
                   c.stds.data_ptr(), c.seq_lens.data_ptr(), self.U, self.G, self.D,
                   c.layout.page_size, c.Pmax, self.lam, self.keys.data_ptr(),
-                  dev.ptr(self.scores), self.lamnorm.data_ptr(), dev.stream_handle(stream))
+                  dev.ptr(self.scores), self.lamnorm.data_ptr(), self.tile_max.data_ptr(),
+                  dev.stream_handle(stream))
+
+    def lam_norms(self, q: torch.Tensor, norms: torch.Tensor | None = None, stream=None) -> None:
+        """fl(lam * ||q_g||) for every query row (scoring.py:39-47) into the [U][8] scratch read
+        by :meth:`score_prenorm`."""
+        q2, qc = self._q(q)
+        _lib.call("pt_lam_norms", q2.data_ptr(), qc, dev.ptr(norms), self.U, self.G, self.D,
+                  self.lam, self.lamnorm.data_ptr(), dev.stream_handle(stream))
+
+    def score_prenorm(self, q: torch.Tensor, stream=None) -> bool:
+        """K2 reading the norms of :meth:`lam_norms`; False when the shape needs :meth:`score`."""
+        q2, qc = self._q(q)
+        c = self.cache
+        rc = _lib.load().pt_score_prenorm(
+            q2.data_ptr(), qc, self.lamnorm.data_ptr(), c.means.data_ptr(), c.stats_code,
+            c.stds.data_ptr(), c.seq_lens.data_ptr(), self.U, self.G, self.D, c.layout.page_size,
+            c.Pmax, self.keys.data_ptr(), dev.ptr(self.scores), self.tile_max.data_ptr(),
+            dev.stream_handle(stream))
+        if rc == _lib.PT_ERR_UNSUPPORTED:
+            return False
+        _lib.check(rc, "pt_score_prenorm")
+        return True
 
     def select(self, stream=None) -> None:
         c = self.cache
@@ -141,13 +167,49 @@ class DecodeEngine:
         self.score(q, norms, stream=stream)
         self.select(stream=stream)
 
+    def select_attend(self, q: torch.Tensor, stream=None) -> None:
+        """K3 + K4 in one launch (pt_select_attend): per unit, select the top-k pages from the
+        keys of :meth:`score`, then attend over them -- identical outputs to :meth:`select`
+        followed by :meth:`attend`, which run instead outside the fused kernel's envelope."""
+        if self.fused_attend:
+            q2, qc = self._q(q)
+            c = self.cache
+            rc = _lib.load().pt_select_attend(
+                self.keys.data_ptr(), self.tile_max.data_ptr(), c.seq_lens.data_ptr(), c.page_table.data_ptr(), self.U,
+                c.layout.page_size, c.Pmax, self.k, self.sel.data_ptr(),
+                dev.ptr(self.sel_logical), self.n_sel.data_ptr(), self.kth.data_ptr(),
+                self.kplus1.data_ptr(), q2.data_ptr(), qc, c.k_pool.data_ptr(),
+                c.v_pool.data_ptr(), c.kv_code, c.layout.max_pages, self.G, self.D, self.scale,
+                self.out.data_ptr(), self.lse.data_ptr(), self.ws.data_ptr(), self.ws.numel(),
+                self.tickets.data_ptr(), dev.stream_handle(stream))
+            if rc == _lib.PT_OK:
+                return
+            if rc != _lib.PT_ERR_UNSUPPORTED:
+                _lib.check(rc, "pt_select_attend")
+            self.fused_attend = False
+        self.select(stream=stream)
+        self.attend(q, stream=stream)
+
     def step(self, q: torch.Tensor, k_new: torch.Tensor | None = None,
              v_new: torch.Tensor | None = None, stream=None):
-        """One decode step: [append] -> score+select -> attend.  Returns (out, lse)."""
+        """One decode step: [append] -> score -> select+attend.  Returns (out, lse)."""
+        if self.fused_select:
+            if k_new is not None:
+                self.cache.append_batch(k_new, v_new, stream=stream)
+            self.score_select(q, stream=stream)
+            self.attend(q, stream=stream)
+            return self.out, self.lse
+        # the query norms do not depend on the append: run them beside it on a side stream
+        # (a fork/join that CUDA-graph capture records as two parallel branches)
+        main = stream if stream is not None else torch.cuda.current_stream()
+        self._side.wait_stream(main)
+        self.lam_norms(q, stream=self._side)
         if k_new is not None:
-            self.cache.append_batch(k_new, v_new, stream=stream)
-        self.score_select(q, stream=stream)
-        self.attend(q, stream=stream)
+            self.cache.append_batch(k_new, v_new, stream=main)
+        main.wait_stream(self._side)
+        if not self.score_prenorm(q, stream=main):
+            self.score(q, stream=main)
+        self.select_attend(q, stream=main)
         return self.out, self.lse
 
     # ------------------------------------------------------------------
@@ -163,11 +225,9 @@ class DecodeEngine:
         g = torch.cuda.CUDAGraph()
         with torch.cuda.stream(s):
             with torch.cuda.graph(g, stream=s):
+                self.step(q, k_new, v_new)
                 if k_new is not None:
-                    self.cache.append_batch(k_new, v_new)
                     self.cache._seq_host -= 1  # replay() accounts for the captured append
-                self.score_select(q)
-                self.attend(q)
         torch.cuda.current_stream().wait_stream(s)
         self.graph = g
         self._graph_appends = k_new is not None

@@ -223,7 +223,7 @@ class PagedKvCache:
         # {bump_next, free_count, max_pages, error_flag}
         self.pool_state = torch.tensor([0, 0, layout.max_pages, 0], dtype=torch.int32, device=d)
         self.free_list_dev = torch.zeros(layout.max_pages, dtype=torch.int32, device=d)
-        self._slot = torch.zeros(U + 2, dtype=torch.int32, device=d)
+        self._slot = torch.zeros(U + 4, dtype=torch.int32, device=d)  # targets + launch flags
         self._seq_host = np.zeros(U, dtype=np.int64)
         self.table = _DevicePageTable(self)
 

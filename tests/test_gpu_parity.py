@@ -430,3 +430,54 @@ def test_fused_score_select_equals_two_launches(cuda, lens, k, fused):
         sep = (eng.sel, eng.sel_logical, eng.n_sel, eng.kth, eng.kplus1)
         for a, b in zip(fused_out, sep):
             assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("B,H,G,D,S,lens,k", [
+    (2, 2, 4, 128, 16, [4096 * 16 + 5, 333, 16 * 16, 7 * 16 + 1], 16),   # ragged, take-all unit
+    (1, 8, 4, 128, 16, [2048 * 16], 128),                                 # cfg2 shape: many chunks
+    (40, 8, 4, 128, 16, [300 * 16 - 7], 32),                              # U=320 > 296: one chunk
+    (4, 4, 1, 64, 32, [1875 * 32 - 11], 16),                              # cfg4-like head shape
+    (2, 2, 8, 256, 16, [640 * 16 + 3], 40),                               # D=256, G=8
+    (2, 2, 2, 128, 64, [200 * 64 + 1], 8),                                # S=64
+])
+def test_select_attend_equals_two_launches(cuda, oracle, B, H, G, D, S, lens, k):
+    """pt_select_attend (K3+K4 in one launch) == pt_topk + pt_attend: selections bit for bit,
+    outputs within the bf16 tolerance; and both against the oracle."""
+    pt = _pt()
+    rng = np.random.default_rng(B * 1000 + H * 10 + G + D + S)
+    cache = make_cache(rng, B, H, D, S, lens, dtype="bf16")
+    eng = pt.DecodeEngine(cache, G, k, keep_logical=True)
+    U = cache.num_units
+    q = torch.from_numpy(rng.standard_normal((U * G, D)).astype(np.float32)).cuda().to(torch.bfloat16)
+    eng.score(q)
+    for rep in range(2):  # the second pass checks the self-resetting chunk tickets
+        eng.select_attend(q)
+        torch.cuda.synchronize()
+        assert eng.fused_attend, "fused kernel declined a supported shape"
+        fused = [t.clone() for t in (eng.sel, eng.sel_logical, eng.n_sel, eng.kth, eng.kplus1,
+                                     eng.out, eng.lse)]
+        eng.sel.zero_(); eng.n_sel.zero_()
+        eng.select()
+        eng.attend(q)
+        torch.cuda.synchronize()
+        sep = (eng.sel, eng.sel_logical, eng.n_sel, eng.kth, eng.kplus1, eng.out, eng.lse)
+        # ids are emitted in an unspecified order (sets compare, as the reference's)
+        assert torch.equal(fused[0].sort(dim=1).values, sep[0].sort(dim=1).values)
+        assert torch.equal(fused[1].sort(dim=1).values, sep[1].sort(dim=1).values)
+        for a, b in zip(fused[2:5], sep[2:5]):
+            assert torch.equal(a, b)
+        torch.testing.assert_close(fused[5], sep[5], rtol=0, atol=2e-3)
+        torch.testing.assert_close(fused[6], sep[6], rtol=0, atol=2e-3)
+    kpool, vpool, table, seq = readback(cache)
+    means, stds = oracle.build_stats(kpool, table, seq, S)
+    ref = oracle.decode_units(q.to(torch.float32).cpu().numpy().reshape(-1, G, D), kpool, vpool,
+                              table, seq, means, stds, k, 0.5, 1.0 / math.sqrt(D), S)
+    nsel = fused[2].cpu().numpy()
+    sel = fused[0].cpu().numpy()
+    for u in range(U):
+        assert nsel[u] == ref["n_sel"][u]
+        assert set(sel[u, : nsel[u]].tolist()) == set(ref["sel"][u, : nsel[u]].tolist())
+    np.testing.assert_array_equal(fused[3].cpu().numpy(), ref["kth"])
+    np.testing.assert_array_equal(fused[4].cpu().numpy(), ref["kplus1"])
+    np.testing.assert_allclose(fused[5].cpu().numpy().reshape(-1, G, D), ref["out"], rtol=0, atol=2e-2)
+    np.testing.assert_allclose(fused[6].cpu().numpy().reshape(-1, G), ref["lse"], rtol=0, atol=2e-2)

@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--ctx", type=int, default=131072)
     ap.add_argument("--budgets", default="512,1024,2048,4096,8192")
     ap.add_argument("--env", default="", help="extra env sweeps: NAME=v1,v2;NAME2=...")
+    ap.add_argument("--split", default="", help="(split, unit)-grid kernel at these nsplit values")
     a = ap.parse_args()
     ns = argparse.Namespace(batch=a.batch, ctx=a.ctx, q_heads=32, kv_heads=8, head_dim=128,
                             page=16, budget=2048, stats_dtype="f32", warmup=3, steps=10)
@@ -73,6 +74,10 @@ def main():
                     except Exception as e:  # noqa: BLE001
                         res[f"k{kp}"][f"{name}={v}"] = str(e)[:80]
                     os.environ.pop(name)
+        for ns in [int(x) for x in a.split.split(",") if x]:
+            os.environ["PT_ATTEND_SPLIT"] = "1"
+            res[f"k{kp}"][f"split{ns}"] = timeit(lambda: eng.attend(q, nsplit=ns))
+            os.environ.pop("PT_ATTEND_SPLIT")
         del eng
     print(json.dumps(res, indent=1))
 
