@@ -80,6 +80,8 @@ __global__ void __launch_bounds__(kSAThreads) k_select_attend(const __grid_const
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + p.region + (((size_t)k * 4 + 7) & ~(size_t)7)) +
                      warp * nstage;
 
+    pdl_trigger();
+    pdl_wait();
     const int n = p.seq_len[u];
     const int P = (n + S - 1) / S;
     const bool lead = (c == 0);
@@ -241,8 +243,7 @@ static int launch_sa(const CUtensorMap &tk, const CUtensorMap &tv, const SelAttn
         configured = smem;
     }
     dim3 grid(p.nchunk, p.U);
-    k_select_attend<D, MT><<<grid, kSAThreads, smem, st>>>(tk, tv, p);
-    PT_CUDA_TRY(cudaGetLastError());
+    PT_CUDA_TRY(pt_launch(k_select_attend<D, MT>, grid, dim3(kSAThreads), smem, st, tk, tv, p));
     return PT_OK;
 }
 

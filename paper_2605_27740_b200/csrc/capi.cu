@@ -1,3 +1,4 @@
+#include <stdlib.h>
 // capi.cu -- library identity + section A of pagetopk_b200.h: the reference's kernel
 // backend contract (backend.py:14-58; _kernels_cy.pyx:19-172) served from HOST buffers.
 // Each call stages its inputs into device memory, runs the same sm_100a kernels the
@@ -31,6 +32,14 @@ struct DevBuf {
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
 }  // namespace
+
+bool pt_pdl_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("PT_NO_PDL");
+        return !(e && e[0] == '1');
+    }();
+    return on;
+}
 
 extern "C" int pt_version(void) { return 100; }
 

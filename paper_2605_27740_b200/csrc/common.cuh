@@ -215,6 +215,39 @@ struct SquaresOfF32 {
 
 }  // namespace pt
 
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch (PDL): the decode-step kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization so kernel N+1 is dispatched while
+// kernel N drains (its CTAs are scheduled as SM resources free up and block in
+// griddepcontrol.wait until N has completed and its writes are visible).  Every step
+// kernel triggers its dependents first thing and waits before touching global memory, so
+// only launch latency and on-chip set-up overlap -- no data race is possible.  A kernel
+// launched without the attribute treats both instructions as no-ops.  PT_NO_PDL=1 turns
+// the attribute off.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+bool pt_pdl_enabled();  // capi.cu: false when PT_NO_PDL=1
+
+template <typename... KArgs, typename... Args>
+static inline cudaError_t pt_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                    cudaStream_t st, Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pt_pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 #define PT_CUDA_TRY(expr)                                                  \
     do {                                                                   \
         cudaError_t _e = (expr);                                           \

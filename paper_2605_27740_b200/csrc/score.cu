@@ -217,6 +217,8 @@ __global__ void __launch_bounds__(256) k_lam_norms(const void *__restrict__ q,
                                                    const float *__restrict__ norms_in, int rows,
                                                    int G, int D, float lam, float *__restrict__ out) {
     __shared__ float qs[kLnRows * (kScoreMaxD + 1)];
+    pdl_trigger();
+    pdl_wait();
     const int r0 = blockIdx.x * kLnRows;
     const int nr = min(kLnRows, rows - r0);
     const int ld = D + 1;  // odd stride: thread r's sequential reads hit distinct banks
@@ -361,11 +363,11 @@ extern "C" int pt_lam_norms(const void *q, int q_dtype, const float *norms, int 
     if (U == 0) return PT_OK;
     cudaStream_t st = (cudaStream_t)stream;
     const int rows = U * G;
+    const dim3 grid((rows + kLnRows - 1) / kLnRows);
     if (q_dtype == PT_F32)
-        k_lam_norms<PT_F32><<<(rows + kLnRows - 1) / kLnRows, 256, 0, st>>>(q, norms, rows, G, D, lam, lamnorm);
+        PT_CUDA_TRY(pt_launch(k_lam_norms<PT_F32>, grid, dim3(256), 0, st, q, norms, rows, G, D, lam, lamnorm));
     else
-        k_lam_norms<PT_BF16><<<(rows + kLnRows - 1) / kLnRows, 256, 0, st>>>(q, norms, rows, G, D, lam, lamnorm);
-    PT_CUDA_TRY(cudaGetLastError());
+        PT_CUDA_TRY(pt_launch(k_lam_norms<PT_BF16>, grid, dim3(256), 0, st, q, norms, rows, G, D, lam, lamnorm));
     return PT_OK;
 }
 

@@ -102,11 +102,13 @@ __global__ void __launch_bounds__(kSSWarps * 32, kSSCtas) k_score_stream(const S
     char *ring = wbase;
     char *hdrs = wbase + NST * C::STAGE;
     float *qf = reinterpret_cast<float *>(hdrs + C::NHDR * C::HDR);
-    for (int i = threadIdx.x; i < U; i += blockDim.x) Ps[i] = (prm.seq_len[i] + S - 1) / S;
+    pdl_trigger();
     if (lane == 0) {
         for (int i = 0; i < NST; i++) mbar_init(&bars[i], 1);
         fence_mbar_init();
     }
+    pdl_wait();
+    for (int i = threadIdx.x; i < U; i += blockDim.x) Ps[i] = (prm.seq_len[i] + S - 1) / S;
     __syncthreads();
 
     // tile cursors (u, t): advance by W tiles, skipping tiles past a unit's last page

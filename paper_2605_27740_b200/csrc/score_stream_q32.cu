@@ -14,8 +14,8 @@ static int ss_launch(const StreamScoreParams &sp, cudaStream_t st) {
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured = smem;
     }
-    k_score_stream<PT_F32, SDT, G, D><<<148 * kSSCtas, kSSWarps * 32, smem, st>>>(sp);
-    PT_CUDA_TRY(cudaGetLastError());
+    PT_CUDA_TRY(pt_launch(k_score_stream<PT_F32, SDT, G, D>, dim3(148 * kSSCtas), dim3(kSSWarps * 32),
+                          smem, st, sp));
     return PT_OK;
 }
 

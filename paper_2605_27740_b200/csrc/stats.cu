@@ -154,6 +154,8 @@ __global__ void __launch_bounds__(256)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpc = blockDim.x >> 5;
     int *flag_alloc = slot + U, *done = slot + U + 1, *flag_read = slot + U + 2;
     const size_t per_warp = (size_t)S * D * 4 + (size_t)D * 8;
+    pdl_trigger();
+    pdl_wait();
     const int64_t u = (int64_t)blockIdx.x * wpc + warp;
     using Bits = typename std::conditional<DT == PT_F32, uint32_t, uint16_t>::type;
     // this unit's length (read before anyone advances it) and the new K/V row
@@ -353,9 +355,9 @@ static int launch_append(const void *kn, const void *vn, void *kp, void *vp, int
                                              (int)smem));                                     \
             configured = smem;                                                                \
         }                                                                                     \
-        k_append<DT, SDT, DJ_><<<grid, wpc * 32, smem, st>>>(kn, vn, kp, vp, ptab, sl, U, S, D, \
-                                                            Pmax, means, stds, pool_state,    \
-                                                            free_list, slot);                 \
+        PT_CUDA_TRY(pt_launch(k_append<DT, SDT, DJ_>, dim3(grid), dim3(wpc * 32), smem, st,   \
+                              kn, vn, kp, vp, ptab, sl, U, S, D, Pmax, means, stds,           \
+                              pool_state, free_list, slot));                                  \
         break;                                                                                \
     }
     switch (dj) {

@@ -13,11 +13,10 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_r
 if [ -z "${SKIP_NCU:-}" ]; then
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:^k_ -c 400 --csv \
     --log-file $OUT/launches.csv python bench.py --profile --steps 20 --warmup 3 > $OUT/launches.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_score_stream -s 2 -c 1 \
-    -o $OUT/prof_score python bench.py --profile --steps 4 > $OUT/ncu_score.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_attend -s 2 -c 1 \
-    -o $OUT/prof_attend python bench.py --profile --steps 4 > $OUT/ncu_attend.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_topk -s 2 -c 1 \
-    -o $OUT/prof_topk python bench.py --profile --steps 4 > $OUT/ncu_topk.log 2>&1
+python tools/launch_summary.py $OUT/launches.csv > $OUT/launch_summary.txt 2>&1
+for K in k_score_stream k_select_attend k_append; do
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s 3 -c 1 \
+      -o $OUT/prof_$K python bench.py --profile --steps 5 > $OUT/ncu_$K.log 2>&1
+done
 fi
 echo done
