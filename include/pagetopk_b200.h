@@ -111,6 +111,16 @@ PT_API int pt_write_rows(const void *k_rows, const void *v_rows, int n_max, cons
                   const int32_t *n_rows, void *k_pool, void *v_pool, int kv_dtype,
                   const int32_t *page_table, int U, int S, int D, int Pmax, void *stream);
 
+/* K1 fused with the row scatter (the prefill path, kvcache.py:210-233 + :178-183): the
+ * pt_write_rows copy followed by pt_page_stats over every touched page, in ONE launch that
+ * never re-reads the pool (one warp per touched page: old rows of a partial tail page from
+ * the pool, new rows from the staging buffer).  Pages must already be mapped; seq_len is not
+ * read (row_begin / n_rows give the ranges).  Identical results to the two calls. */
+PT_API int pt_extend(const void *k_rows, const void *v_rows, int n_max, const int32_t *row_begin,
+                     const int32_t *n_rows, void *k_pool, void *v_pool, int kv_dtype,
+                     const int32_t *page_table, int U, int S, int D, int Pmax, void *means,
+                     int stats_dtype, float *stds, void *stream);
+
 /* K2. scoring.py:108-124 + _kernels_cy.pyx:19-43 + bf16.py:18-33 + select.py:51-57:
  * q [U*G][D] (q_dtype); norms f32 [U*G] or NULL (computed as scoring.py:39-47);
  * score = max_g fl(fl(sum_d q*mean) + fl(fl(lam*norm_g)*std)), sequential d order;

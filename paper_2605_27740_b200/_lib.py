@@ -43,6 +43,8 @@ _PROTOS = {
     "pt_append": (_i, [_vp, _vp, _vp, _vp, _i, _vp, _vp, _i, _i, _i, _i, _vp, _i, _vp, _vp,
                        _vp, _vp, _vp]),
     "pt_write_rows": (_i, [_vp, _vp, _i, _vp, _vp, _vp, _vp, _i, _vp, _i, _i, _i, _i, _vp]),
+    "pt_extend": (_i, [_vp, _vp, _i, _vp, _vp, _vp, _vp, _i, _vp, _i, _i, _i, _i, _vp, _i, _vp,
+                       _vp]),
     "pt_score": (_i, [_vp, _i, _vp, _vp, _i, _vp, _vp, _i, _i, _i, _i, _i, _f, _vp, _vp, _vp, _vp,
                       _vp]),
     "pt_lam_norms": (_i, [_vp, _i, _vp, _i, _i, _i, _f, _vp, _vp]),

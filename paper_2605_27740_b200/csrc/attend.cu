@@ -121,7 +121,7 @@ extern "C" int pt_attend(const void *q, int q_dtype, const void *k_pool, const v
     // warps per CTA and ring depth: keep >= 2 CTAs per SM where the page size allows
     const size_t stage = (size_t)2 * S * D * E;
     const int gpl = mma ? kMmaGP : gp_of(G);
-    const int kMaxPps = 512;  // bounds the per-warp page-id lists of the mma kernel
+    const int kMaxPps = 2048;  // bounds the per-warp page-id lists of the mma kernel (8 KB)
     auto smem_of = [&](int nw, int nst, int pps_) {
         const size_t ring = (size_t)nw * nst * stage;
         const size_t merge = (size_t)nw * gpl * (D + 2) * 4;

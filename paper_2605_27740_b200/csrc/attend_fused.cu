@@ -233,6 +233,139 @@ __global__ void __launch_bounds__(kSAThreads) k_select_attend(const __grid_const
     if (prof) g_sa_prof[cta * 10 + 5] = gtimer();
 }
 
+// ---------------------------------------------------------------------------
+// Warp-per-unit variant (thousands of short units, small k: cfg4 / short-context cfg5
+// shapes).  A CTA-per-unit grid would pay a full CTA selection + merge for a handful of
+// pages per warp; here each warp owns one unit end to end: warp-level selection
+// (select_warp, keys in registers), then the unit's k pages through the warp's private TMA
+// ring, and the final output written directly (no merge).  Warps are independent: no
+// __syncthreads after the prologue.
+// Shared memory per warp: [ring: nstage stages][ids: kpad ints][mbarriers].
+// ---------------------------------------------------------------------------
+constexpr int kSWMaxV = 8;  // keys per warp in registers: P <= 32 * 8 * 8 = 2048
+
+template <int D, int MT>
+__global__ void __launch_bounds__(128) k_select_attend_warp(const __grid_constant__ CUtensorMap tmk,
+                                                            const __grid_constant__ CUtensorMap tmv,
+                                                            const SelAttnParams p) {
+    constexpr int S = 16 * MT;
+    constexpr int KS = D / 16;
+    constexpr uint32_t PAGE_BYTES = S * D * 2;
+    constexpr uint32_t STAGE_BYTES = 2 * PAGE_BYTES;
+    extern __shared__ __align__(1024) char smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nstage = p.nstage, k = p.k;
+    const size_t per_warp = (size_t)p.region;  // ring + ids + bars, 1024-aligned
+    char *ring = smem + warp * per_warp;
+    int *ids = reinterpret_cast<int *>(ring + (size_t)nstage * STAGE_BYTES);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(ids + ((k + 1) & ~1));
+    pdl_trigger();
+    pdl_wait();
+    const int64_t u = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    if (u >= p.U) return;
+    const int S_ = S;
+    const int n = p.seq_len[u];
+    const int P = (n + S_ - 1) / S_;
+    if (P == 0) {
+        if (lane == 0) { p.n_sel[u] = 0; p.kth[u] = 0; p.kplus1[u] = -1; }
+        return;
+    }
+    const int tail_pid = p.page_table[u * p.Pmax + P - 1];
+    const int tail_rows = n - (P - 1) * S_;
+    uint32_t qb[KS][2];
+    {
+        const int gq = lane >> 2;
+#pragma unroll
+        for (int ks = 0; ks < KS; ks++) {
+            const int d0 = ks * 16 + 2 * (lane & 3);
+            uint32_t b0 = 0, b1 = 0;
+            if (gq < p.G) {
+                const int64_t row = (u * p.G + gq) * (int64_t)D;
+                if (p.q_dtype == PT_BF16) {
+                    const uint32_t *qp =
+                        reinterpret_cast<const uint32_t *>(static_cast<const uint16_t *>(p.q) + row);
+                    b0 = __ldg(qp + (d0 >> 1));
+                    b1 = __ldg(qp + ((d0 + 8) >> 1));
+                } else {
+                    const float *qp = static_cast<const float *>(p.q) + row;
+                    b0 = pack_bf16(qp[d0], qp[d0 + 1]);
+                    b1 = pack_bf16(qp[d0 + 8], qp[d0 + 9]);
+                }
+            }
+            qb[ks][0] = b0;
+            qb[ks][1] = b1;
+        }
+    }
+    select_warp<kSWMaxV>(p.keys + u * (int64_t)p.Pmax, P, k, p.page_table + u * p.Pmax,
+                         p.sel + u * (int64_t)k, p.sel_logical ? p.sel_logical + u * (int64_t)k : nullptr,
+                         p.n_sel + u, p.kth + u, p.kplus1 + u, ids);
+    const int ns = P < k ? P : k;
+    auto issue = [&](int i) {
+        const int pid = ids[i];
+        const int st = i % nstage;
+        char *ks = ring + (size_t)st * STAGE_BYTES;
+        mbar_arrive_expect_tx(&bars[st], STAGE_BYTES);
+#pragma unroll
+        for (int b = 0; b < D / 64; b++) {
+            tma_load_2d(ks + b * S * 128, &tmk, b * 64, pid * S, &bars[st]);
+            tma_load_2d(ks + PAGE_BYTES + b * S * 128, &tmv, b * 64, pid * S, &bars[st]);
+        }
+    };
+    if (lane == 0) {
+        for (int i = 0; i < nstage; i++) mbar_init(&bars[i], 1);
+        fence_mbar_init();
+        for (int i = 0; i < min(nstage, ns); i++) issue(i);
+    }
+    __syncwarp();
+    const float qscale = p.scale * kLog2e;
+    float acc[KS][4];
+#pragma unroll
+    for (int i = 0; i < KS; i++) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+    float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};
+    for (int i = 0; i < ns; i++) {
+        const int st = i % nstage;
+        const int pid = ids[i];
+        const int rows = (pid == tail_pid) ? tail_rows : S;
+        mbar_wait(&bars[st], (uint32_t)((i / nstage) & 1));
+        const uint32_t kbase = smem_u32(ring + (size_t)st * STAGE_BYTES);
+        mma_page<D, MT>(kbase, kbase + PAGE_BYTES, rows, 0.f, qscale, qb, acc, m_run, l_run, lane);
+        __syncwarp();
+        if (lane == 0 && i + nstage < ns) issue(i + nstage);
+    }
+    const int g0 = 2 * (lane & 3);
+    const float inv0 = 1.f / l_run[0], inv1 = 1.f / l_run[1];
+#pragma unroll
+    for (int dm = 0; dm < KS; dm++) {
+        const int d = dm * 16 + (lane >> 2);
+        if (g0 < p.G) {
+            p.out[(u * p.G + g0) * D + d] = acc[dm][0] * inv0;
+            p.out[(u * p.G + g0) * D + d + 8] = acc[dm][2] * inv0;
+        }
+        if (g0 + 1 < p.G) {
+            p.out[(u * p.G + g0 + 1) * D + d] = acc[dm][1] * inv1;
+            p.out[(u * p.G + g0 + 1) * D + d + 8] = acc[dm][3] * inv1;
+        }
+    }
+    if (lane < 4) {
+        if (g0 < p.G) p.lse[u * p.G + g0] = (m_run[0] + log2f(l_run[0])) * kLn2;
+        if (g0 + 1 < p.G) p.lse[u * p.G + g0 + 1] = (m_run[1] + log2f(l_run[1])) * kLn2;
+    }
+}
+
+template <int D, int MT>
+static int launch_saw(const CUtensorMap &tk, const CUtensorMap &tv, const SelAttnParams &p, int nw,
+                      size_t smem, cudaStream_t st) {
+    static size_t configured = 0;
+    if (smem > configured) {
+        PT_CUDA_TRY(cudaFuncSetAttribute(k_select_attend_warp<D, MT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured = smem;
+    }
+    dim3 grid((p.U + nw - 1) / nw);
+    PT_CUDA_TRY(pt_launch(k_select_attend_warp<D, MT>, grid, dim3(nw * 32), smem, st, tk, tv, p));
+    return PT_OK;
+}
+
 template <int D, int MT>
 static int launch_sa(const CUtensorMap &tk, const CUtensorMap &tv, const SelAttnParams &p,
                      size_t smem, cudaStream_t st) {
@@ -307,6 +440,21 @@ extern "C" int pt_select_attend(const uint16_t *keys, const uint16_t *tile_max,
     size_t region = 0;
     const size_t smem = smem_of(nstage, &region);
     if (smem > 225 * 1024) return PT_ERR_UNSUPPORTED;
+    // many short units with a small budget: one warp per unit (no CTA-wide selection/merge)
+    const int want_warp = sa_env_int("PT_SA_WARP", -1);
+    const bool warp_path = want_warp == 1 ||
+                           (want_warp != 0 && U >= 4 * 148 && k <= 64 && Pmax <= 32 * 8 * kSWMaxV);
+    size_t w_per = 0;
+    int w_nst = 3, w_nw = 4;
+    if (warp_path && Pmax <= 32 * 8 * kSWMaxV) {
+        auto per_of = [&](int nst) {
+            return ((size_t)nst * stage + (((size_t)k + 1) & ~(size_t)1) * 4 + (size_t)nst * 8 + 1023) &
+                   ~(size_t)1023;
+        };
+        while (w_nst > 2 && per_of(w_nst) * w_nw > 113 * 1024) w_nst--;
+        while (w_nw > 1 && per_of(w_nst) * w_nw > 225 * 1024) w_nw--;
+        if (per_of(w_nst) * w_nw <= 225 * 1024) w_per = per_of(w_nst);
+    }
     CUtensorMap tk, tv;
     if (!pt_make_pool_tmap(&tk, k_pool, D, S, num_phys_pages) ||
         !pt_make_pool_tmap(&tv, v_pool, D, S, num_phys_pages))
@@ -319,6 +467,17 @@ extern "C" int pt_select_attend(const uint16_t *keys, const uint16_t *tile_max,
     p.nstage = nstage; p.region = (int)region; p.scale = scale;
     p.prof = sa_env_int("PT_SA_PROF", 0);
     cudaStream_t st = (cudaStream_t)stream;
+    if (w_per) {
+        SelAttnParams pw = p;
+        pw.nstage = w_nst;
+        pw.region = (int)w_per;
+#define PT_SAW(D_, MT_) \
+        if (D == D_ && S == 16 * MT_) return launch_saw<D_, MT_>(tk, tv, pw, w_nw, w_per * w_nw, st);
+        PT_SAW(64, 1) PT_SAW(64, 2) PT_SAW(64, 4)
+        PT_SAW(128, 1) PT_SAW(128, 2) PT_SAW(128, 4)
+        PT_SAW(256, 1) PT_SAW(256, 2) PT_SAW(256, 4)
+#undef PT_SAW
+    }
 #define PT_SA(D_, MT_) \
     if (D == D_ && S == 16 * MT_) return launch_sa<D_, MT_>(tk, tv, p, smem, st);
     PT_SA(64, 1) PT_SA(64, 2) PT_SA(64, 4)

@@ -79,7 +79,12 @@ struct SSCfg {
     static_assert(NCH % CPS == 0, "chunks per stage must divide the row");
 };
 
+// page counts of up to kSSPsMax units are cached in shared memory; beyond that (thousands
+// of short sequences) they are read through L1 from seq_len
+constexpr int kSSPsMax = 2048;
+
 __host__ __device__ __forceinline__ size_t ss_hdr_bytes(int U) {
+    if (U > kSSPsMax) U = kSSPsMax;
     const size_t ps = ((size_t)U * 4 + 15) & ~(size_t)15;
     return (ps + (size_t)kSSWarps * kSSNst * 8 + 127) & ~(size_t)127;
 }
@@ -96,8 +101,10 @@ __global__ void __launch_bounds__(kSSWarps * 32, kSSCtas) k_score_stream(const S
     const int W = gridDim.x * kSSWarps;
     const int gw = blockIdx.x * kSSWarps + warp;
     int *Ps = reinterpret_cast<int *>(smem);
+    const bool ps_smem = U <= kSSPsMax;
     uint64_t *bars =
-        reinterpret_cast<uint64_t *>(smem + (((size_t)U * 4 + 15) & ~(size_t)15)) + warp * NST;
+        reinterpret_cast<uint64_t *>(smem + (((size_t)(ps_smem ? U : kSSPsMax) * 4 + 15) & ~(size_t)15)) +
+        warp * NST;
     char *wbase = smem + ss_hdr_bytes(U) + (size_t)warp * C::PER_WARP;
     char *ring = wbase;
     char *hdrs = wbase + NST * C::STAGE;
@@ -108,14 +115,19 @@ __global__ void __launch_bounds__(kSSWarps * 32, kSSCtas) k_score_stream(const S
         fence_mbar_init();
     }
     pdl_wait();
-    for (int i = threadIdx.x; i < U; i += blockDim.x) Ps[i] = (prm.seq_len[i] + S - 1) / S;
+    if (ps_smem)
+        for (int i = threadIdx.x; i < U; i += blockDim.x) Ps[i] = (prm.seq_len[i] + S - 1) / S;
     __syncthreads();
+    auto pages_of = [&](int uu) -> int {
+        return ps_smem ? Ps[uu] : (__ldg(prm.seq_len + uu) + S - 1) / S;
+    };
 
     // tile cursors (u, t): advance by W tiles, skipping tiles past a unit's last page
+    // (a division, not a loop over units: W / TPU is in the hundreds for short contexts)
     auto settle = [&](int &u, int &t) {
         while (u < U) {
-            while (t >= TPU) { t -= TPU; ++u; }
-            if (u >= U || t * 32 < Ps[u]) return;
+            if (t >= TPU) { u += t / TPU; t %= TPU; }
+            if (u >= U || t * 32 < pages_of(u)) return;
             t += W;
         }
     };
@@ -230,12 +242,13 @@ __global__ void __launch_bounds__(kSSWarps * 32, kSSCtas) k_score_stream(const S
         }
         const int p = ct * 32 + lane;
         const uint32_t key = encode_ordered(f32_to_bf16_rne(best));
-        if (p < Ps[cu]) {
+        const int Pc = pages_of(cu);
+        if (p < Pc) {
             prm.keys[(int64_t)cu * Pmax + p] = (uint16_t)key;
             if (prm.scores) prm.scores[(int64_t)cu * Pmax + p] = best;
         }
         if (prm.tile_max) {  // the tile's largest key (pads contribute key 0, the minimum)
-            const uint32_t m = __reduce_max_sync(0xffffffffu, p < Ps[cu] ? key : 0u);
+            const uint32_t m = __reduce_max_sync(0xffffffffu, p < Pc ? key : 0u);
             if (lane == 0) prm.tile_max[(int64_t)cu * TPU + ct] = (uint16_t)m;
         }
         __syncwarp();  // header + qf reads done before their slots are refilled

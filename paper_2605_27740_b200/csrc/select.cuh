@@ -619,4 +619,141 @@ __device__ bool select_cand(const uint16_t *__restrict__ keys_g, const uint16_t 
     return true;
 }
 
+// ---------------------------------------------------------------------------
+// Warp-level selection (the warp-per-unit fused kernel: many short units, small k).
+// One warp selects one unit whose P <= 256 * MAXV keys sit in registers (lane l holds the
+// 16-byte key vectors l, l+32, ...).  Threshold = bisection over [min, max] with warp-wide
+// counts (exact for any key distribution, ~log2(range) rounds); ordered compaction per key
+// vector in logical order (ballot/scan ranks), ties by ascending logical index -- the
+// reference's rule; logical ids land in `ids` (warp-private shared memory) and are translated
+// to physical ids in one parallel round.  Same outputs as select_block.
+// ---------------------------------------------------------------------------
+template <int MAXV>
+__device__ void select_warp(const uint16_t *__restrict__ keys_g, int P, int k,
+                            const int32_t *__restrict__ map, int32_t *__restrict__ out,
+                            int32_t *__restrict__ out_l, int32_t *__restrict__ n_sel,
+                            int32_t *__restrict__ kth, int32_t *__restrict__ kplus1, int *ids) {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const uint4 *k4 = reinterpret_cast<const uint4 *>(keys_g);
+    uint4 v[MAXV];
+#pragma unroll
+    for (int j = 0; j < MAXV; j++) {
+        const int base = (lane + 32 * j) * 8;
+        v[j] = base < P ? __ldcg(k4 + lane + 32 * j) : make_uint4(0u, 0u, 0u, 0u);
+    }
+    auto keyof = [&](const uint4 &x, int e) -> int {
+        const uint32_t w = e < 2 ? x.x : e < 4 ? x.y : e < 6 ? x.z : x.w;
+        return (e & 1) ? (int)(w >> 16) : (int)(w & 0xFFFFu);
+    };
+    int mn = 0xFFFF, mx = 0;
+#pragma unroll
+    for (int j = 0; j < MAXV; j++) {
+        const int base = (lane + 32 * j) * 8;
+#pragma unroll
+        for (int e = 0; e < 8; e++)
+            if (base + e < P) { const int x = keyof(v[j], e); mn = min(mn, x); mx = max(mx, x); }
+    }
+    mn = __reduce_min_sync(0xffffffffu, mn);
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if (P <= k) {  // _take_all (select.py:75-84)
+        for (int i = lane; i < P; i += 32) {
+            const int pid = __ldg(map + i);
+            ids[i] = pid;
+            if (out) out[i] = pid;
+            if (out_l) out_l[i] = i;
+        }
+        if (lane == 0) { *n_sel = P; *kth = mn; *kplus1 = -1; }
+        __syncwarp();
+        return;
+    }
+    auto count_ge = [&](int t) -> int {
+        int c = 0;
+#pragma unroll
+        for (int j = 0; j < MAXV; j++) {
+            const int base = (lane + 32 * j) * 8;
+#pragma unroll
+            for (int e = 0; e < 8; e++) c += (base + e < P) && keyof(v[j], e) >= t;
+        }
+        return __reduce_add_sync(0xffffffffu, c);
+    };
+    // thr = max t with #(keys >= t) >= k
+    int lo = mn, hi = mx + 1;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (count_ge(mid) >= k) lo = mid; else hi = mid;
+    }
+    const int thr = lo;
+    int gt = 0, eq = 0, below = -1;
+#pragma unroll
+    for (int j = 0; j < MAXV; j++) {
+        const int base = (lane + 32 * j) * 8;
+#pragma unroll
+        for (int e = 0; e < 8; e++) {
+            if (base + e >= P) continue;
+            const int x = keyof(v[j], e);
+            gt += x > thr;
+            eq += x == thr;
+            if (x < thr) below = max(below, x);
+        }
+    }
+    const int gt_tot = __reduce_add_sync(0xffffffffu, gt);
+    const int eq_tot = __reduce_add_sync(0xffffffffu, eq);
+    below = __reduce_max_sync(0xffffffffu, below);
+    const int budget = k - gt_tot;
+    int run_sel = 0, run_eq = 0;
+#pragma unroll
+    for (int j = 0; j < MAXV; j++) {
+        if (j * 256 >= P) break;
+        const int base = (lane + 32 * j) * 8;
+        int myeq = 0;
+#pragma unroll
+        for (int e = 0; e < 8; e++) myeq += (base + e < P) && keyof(v[j], e) == thr;
+        int inc = myeq;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        int tie = run_eq + inc - myeq;  // ties before this lane's vector
+        uint32_t selmask = 0u;
+#pragma unroll
+        for (int e = 0; e < 8; e++) {
+            if (base + e >= P) continue;
+            const int x = keyof(v[j], e);
+            bool sl = x > thr;
+            if (x == thr) { sl = tie < budget; tie++; }
+            if (sl) selmask |= 1u << e;
+        }
+        const int mine = __popc(selmask);
+        int sinc = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, sinc, o);
+            if (lane >= o) sinc += y;
+        }
+        int pos = run_sel + sinc - mine;
+#pragma unroll
+        for (int e = 0; e < 8; e++)
+            if (selmask & (1u << e)) ids[pos++] = base + e;
+        run_eq += __shfl_sync(0xffffffffu, inc, 31);
+        run_sel += __shfl_sync(0xffffffffu, sinc, 31);
+    }
+    (void)lt;
+    __syncwarp();
+    for (int t = lane; t < k; t += 32) {
+        const int li = ids[t];
+        const int pid = __ldg(map + li);
+        ids[t] = pid;
+        if (out) out[t] = pid;
+        if (out_l) out_l[t] = li;
+    }
+    if (lane == 0) {
+        *n_sel = k;
+        *kth = thr;
+        *kplus1 = (eq_tot > budget) ? thr : below;
+    }
+    __syncwarp();
+}
+
 }  // namespace pt

@@ -88,6 +88,32 @@ __global__ void __launch_bounds__(kStatsWarps * 32)
 // load round), then -- once CTA 0's snapshot is taken (flag_read; normally long set) --
 // advances its own sequence length.  The last CTA to finish re-arms the flags.  CTA 0
 // never waits, so the scheme cannot deadlock while CTAs are dispatched in index order.
+__host__ __device__ __forceinline__ size_t append_per_warp(int S, int D, int ES) {
+    return (((size_t)S * D * ES + 15) & ~(size_t)15) + (size_t)D * 8;
+}
+
+// raw 16-byte-chunk copy global -> shared of nbytes; every load of a thread is issued before
+// its first store.  Falls back to 2-byte words when not 16-byte aligned.
+template <int MAXC>
+__device__ __forceinline__ void stage_raw(char *dst, const char *src, int nbytes, int lane) {
+    if ((nbytes & 15) == 0 && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+        const int nch = nbytes >> 4;
+        const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+        for (int c0 = lane; c0 < nch; c0 += 32 * MAXC) {
+            uint4 v[MAXC];
+#pragma unroll
+            for (int j = 0; j < MAXC; j++)
+                if (c0 + 32 * j < nch) v[j] = __ldg(s4 + c0 + 32 * j);
+#pragma unroll
+            for (int j = 0; j < MAXC; j++)
+                if (c0 + 32 * j < nch) reinterpret_cast<uint4 *>(dst)[c0 + 32 * j] = v[j];
+        }
+    } else {
+        for (int i = lane; i < nbytes / 2; i += 32)
+            reinterpret_cast<uint16_t *>(dst)[i] = reinterpret_cast<const uint16_t *>(src)[i];
+    }
+}
+
 __device__ __forceinline__ void spin_flag(int *flag, bool acquire) {
     while (atomicAdd(flag, 0) == 0) __nanosleep(32);
     if (acquire) __threadfence();  // the allocation's page table / slot writes
@@ -153,7 +179,8 @@ __global__ void __launch_bounds__(256)
     __shared__ int is_last;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpc = blockDim.x >> 5;
     int *flag_alloc = slot + U, *done = slot + U + 1, *flag_read = slot + U + 2;
-    const size_t per_warp = (size_t)S * D * 4 + (size_t)D * 8;
+    constexpr int ES = DT == PT_F32 ? 4 : 2;
+    const size_t per_warp = append_per_warp(S, D, ES);
     pdl_trigger();
     pdl_wait();
     const int64_t u = (int64_t)blockIdx.x * wpc + warp;
@@ -184,8 +211,15 @@ __global__ void __launch_bounds__(256)
         __syncthreads();
         if (threadIdx.x == 0) atomicExch(flag_alloc, 1);
     }
-    float *rows_s = reinterpret_cast<float *>(asmem + warp * per_warp);
-    double *var_s = reinterpret_cast<double *>(asmem + warp * per_warp + (size_t)S * D * 4);
+    // the tail page's rows stay in their storage format (bf16: half the shared memory of f32,
+    // so short-page-count / many-unit steps keep more warps resident); widened on use
+    Bits *rows_s = reinterpret_cast<Bits *>(asmem + warp * per_warp);
+    double *var_s = reinterpret_cast<double *>(asmem + warp * per_warp +
+                                               (((size_t)S * D * ES + 15) & ~(size_t)15));
+    auto rowval = [&](int i) -> double {
+        return DT == PT_F32 ? (double)__uint_as_float((uint32_t)rows_s[i])
+                            : (double)bf16_bits_to_f32((uint32_t)rows_s[i]);
+    };
     if (u < U) {
         int pid;
         if (n % S == 0) {  // starts a page: CTA 0's allocation
@@ -199,15 +233,13 @@ __global__ void __launch_bounds__(256)
             const int row = n % S;
             const int64_t base = (int64_t)pid * S * D;
             // stage the page's existing rows (one load round) and the new row
-            stage_rows_f32<DT, 8>(rows_s, D,
-                                  static_cast<const char *>(k_pool) + base * (DT == PT_F32 ? 4 : 2),
-                                  row * D, D, lane, 32);
+            stage_raw<8>(reinterpret_cast<char *>(rows_s),
+                         static_cast<const char *>(k_pool) + base * ES, row * D * ES, lane);
 #pragma unroll
             for (int j = 0; j < DJ; j++) {
                 const int d = lane + 32 * j;
                 if (d < D) {
-                    rows_s[row * D + d] = DT == PT_F32 ? __uint_as_float(kb[j])
-                                                       : bf16_bits_to_f32(kb[j]);
+                    rows_s[row * D + d] = kb[j];
                     static_cast<Bits *>(k_pool)[base + (int64_t)row * D + d] = kb[j];
                     static_cast<Bits *>(v_pool)[base + (int64_t)row * D + d] = vb[j];
                 }
@@ -220,7 +252,7 @@ __global__ void __launch_bounds__(256)
                 const int d = lane + 32 * j;
                 double sacc = 0.0;
                 if (d < D)
-                    for (int r = 0; r < cnt; r++) sacc = __dadd_rn(sacc, (double)rows_s[r * D + d]);
+                    for (int r = 0; r < cnt; r++) sacc = __dadd_rn(sacc, rowval(r * D + d));
                 mean[j] = __ddiv_rn(sacc, (double)cnt);
             }
             constexpr int V = StatsTile<SDT>::V;
@@ -230,7 +262,7 @@ __global__ void __launch_bounds__(256)
                 if (d < D) {
                     double sacc = 0.0;
                     for (int r = 0; r < cnt; r++) {
-                        const double t = __dsub_rn((double)rows_s[r * D + d], mean[j]);
+                        const double t = __dsub_rn(rowval(r * D + d), mean[j]);
                         sacc = __dadd_rn(sacc, __dmul_rn(t, t));
                     }
                     var_s[d] = __ddiv_rn(sacc, (double)cnt);
@@ -254,6 +286,125 @@ __global__ void __launch_bounds__(256)
             atomicExch(done, 0);
         }
     }
+}
+
+// ---------------------------------------------------------------------------
+// Fused extend (kvcache.py:210-233 + :178-183 for every touched page): the prefill path.
+// One warp per touched page: the page's rows already in the pool (a partially filled tail)
+// and the new rows from the dense staging buffer land in shared memory as f32 (one round
+// of 16-byte loads); the new K and V rows are stored to the pool from the same registers;
+// mean/std are then computed from shared memory exactly as page_stats_warp (f64, numpy
+// order).  HBM traffic = staging read + pool write + stats write (the pool is not re-read).
+// ---------------------------------------------------------------------------
+template <int DT, int MAXC>
+__device__ __forceinline__ void copy_new_rows(const char *__restrict__ ks, const char *__restrict__ vs,
+                                              char *__restrict__ kd, char *__restrict__ vd,
+                                              float *__restrict__ rows_f32, int nbytes, int lane) {
+    constexpr int EPC = DT == PT_F32 ? 4 : 8;
+    const int nch = nbytes >> 4;
+    const uint4 *k4 = reinterpret_cast<const uint4 *>(ks);
+    const uint4 *v4 = reinterpret_cast<const uint4 *>(vs);
+    for (int c0 = lane; c0 < nch; c0 += 32 * MAXC) {
+        uint4 kv[MAXC], vv[MAXC];
+#pragma unroll
+        for (int j = 0; j < MAXC; j++) {
+            const int c = c0 + 32 * j;
+            if (c < nch) { kv[j] = __ldcs(k4 + c); vv[j] = __ldcs(v4 + c); }
+        }
+#pragma unroll
+        for (int j = 0; j < MAXC; j++) {
+            const int c = c0 + 32 * j;
+            if (c >= nch) break;
+            reinterpret_cast<uint4 *>(kd)[c] = kv[j];
+            reinterpret_cast<uint4 *>(vd)[c] = vv[j];
+            float *o = rows_f32 + c * EPC;
+            if constexpr (DT == PT_F32) {
+                o[0] = __uint_as_float(kv[j].x); o[1] = __uint_as_float(kv[j].y);
+                o[2] = __uint_as_float(kv[j].z); o[3] = __uint_as_float(kv[j].w);
+            } else {
+                const uint32_t w[4] = {kv[j].x, kv[j].y, kv[j].z, kv[j].w};
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    o[2 * q] = __uint_as_float(w[q] << 16);
+                    o[2 * q + 1] = __uint_as_float(w[q] & 0xFFFF0000u);
+                }
+            }
+        }
+    }
+}
+
+template <int DT, int SDT, int DJ>
+__global__ void __launch_bounds__(256)
+    k_extend(const void *__restrict__ k_rows, const void *__restrict__ v_rows, int n_max,
+             const int32_t *__restrict__ row_begin, const int32_t *__restrict__ n_rows,
+             void *__restrict__ k_pool, void *__restrict__ v_pool,
+             const int32_t *__restrict__ page_table, int S, int D, int Pmax,
+             void *__restrict__ means, float *__restrict__ stds) {
+    extern __shared__ __align__(16) char esmem[];
+    constexpr int ES = DT == PT_F32 ? 4 : 2;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpc = blockDim.x >> 5;
+    const int64_t u = blockIdx.y;
+    const int n0 = row_begin[u], nr = n_rows[u], n1 = n0 + nr;
+    if (nr <= 0) return;
+    const int p = n0 / S + blockIdx.x * wpc + warp;
+    if ((int64_t)p * S >= n1) return;
+    const size_t per_warp = (size_t)S * D * 4 + (size_t)D * 8;
+    float *rows_s = reinterpret_cast<float *>(esmem + warp * per_warp);
+    double *var_s = reinterpret_cast<double *>(esmem + warp * per_warp + (size_t)S * D * 4);
+    const int64_t pid = page_table[u * Pmax + p];
+    const int cnt = min(S, n1 - p * S);  // rows in the page after the extend
+    const int r0 = max(0, n0 - p * S);   // rows it already held
+    const char *kp = static_cast<const char *>(k_pool);
+    if (r0 > 0) stage_rows_f32<DT, 8>(rows_s, D, kp + pid * S * D * ES, r0 * D, D, lane, 32);
+    const int64_t srow = u * (int64_t)n_max + ((int64_t)p * S + r0 - n0);
+    const int64_t prow = pid * S + r0;
+    const char *ks = static_cast<const char *>(k_rows) + srow * D * ES;
+    const char *vs = static_cast<const char *>(v_rows) + srow * D * ES;
+    char *kd = static_cast<char *>(k_pool) + prow * D * ES;
+    char *vd = static_cast<char *>(v_pool) + prow * D * ES;
+    if ((D * ES) % 16 == 0) {
+        copy_new_rows<DT, 8>(ks, vs, kd, vd, rows_s + r0 * D, (cnt - r0) * D * ES, lane);
+    } else {
+        for (int i = lane; i < (cnt - r0) * D; i += 32) {
+            if constexpr (DT == PT_F32) {
+                const float a = reinterpret_cast<const float *>(ks)[i];
+                reinterpret_cast<float *>(kd)[i] = a;
+                reinterpret_cast<float *>(vd)[i] = reinterpret_cast<const float *>(vs)[i];
+                rows_s[r0 * D + i] = a;
+            } else {
+                const uint16_t a = reinterpret_cast<const uint16_t *>(ks)[i];
+                reinterpret_cast<uint16_t *>(kd)[i] = a;
+                reinterpret_cast<uint16_t *>(vd)[i] = reinterpret_cast<const uint16_t *>(vs)[i];
+                rows_s[r0 * D + i] = bf16_bits_to_f32(a);
+            }
+        }
+    }
+    __syncwarp();
+    double mean[DJ];
+#pragma unroll
+    for (int j = 0; j < DJ; j++) {
+        const int d = lane + 32 * j;
+        double sacc = 0.0;
+        if (d < D)
+            for (int r = 0; r < cnt; r++) sacc = __dadd_rn(sacc, (double)rows_s[r * D + d]);
+        mean[j] = __ddiv_rn(sacc, (double)cnt);
+    }
+    constexpr int V = StatsTile<SDT>::V;
+#pragma unroll
+    for (int j = 0; j < DJ; j++) {
+        const int d = lane + 32 * j;
+        if (d < D) {
+            double sacc = 0.0;
+            for (int r = 0; r < cnt; r++) {
+                const double t = __dsub_rn((double)rows_s[r * D + d], mean[j]);
+                sacc = __dadd_rn(sacc, __dmul_rn(t, t));
+            }
+            var_s[d] = __ddiv_rn(sacc, (double)cnt);
+            store_elem<SDT>(means, mean_offset(u, p, d, D, Pmax, V), __double2float_rn(mean[j]));
+        }
+    }
+    __syncwarp();
+    if (lane == 0) stds[u * Pmax + p] = __double2float_rn(__dsqrt_rn(np_sum(DoubleArray{var_s}, D)));
 }
 
 // extend (kvcache.py:210-233): scatter dense staged rows into mapped pages
@@ -338,7 +489,7 @@ static int launch_append(const void *kn, const void *vn, void *kp, void *vp, int
                          int32_t *sl, int U, int S, int D, int Pmax, void *means, float *stds,
                          int32_t *pool_state, const int32_t *free_list, int32_t *slot,
                          cudaStream_t st) {
-    const size_t per_warp = (size_t)S * D * 4 + (size_t)D * 8;
+    const size_t per_warp = append_per_warp(S, D, DT == PT_F32 ? 4 : 2);
     const size_t snap = (size_t)U * 4;  // CTA 0's snapshot of every unit's length
     if (snap + per_warp > 200 * 1024) return PT_ERR_UNSUPPORTED;
     int wpc = (int)((200 * 1024 - snap) / per_warp);
@@ -422,4 +573,63 @@ extern "C" int pt_write_rows(const void *k_rows, const void *v_rows, int n_max,
         return PT_ERR_INVALID;
     PT_CUDA_TRY(cudaGetLastError());
     return PT_OK;
+}
+
+template <int DT, int SDT>
+static int launch_extend(const void *kr, const void *vr, int n_max, const int32_t *rb,
+                         const int32_t *nrw, void *kp, void *vp, const int32_t *ptab, int U, int S,
+                         int D, int Pmax, void *means, float *stds, cudaStream_t st) {
+    const size_t per_warp = (size_t)S * D * 4 + (size_t)D * 8;
+    int wpc = (int)((96 * 1024) / per_warp);  // >= 2 CTAs per SM
+    if (wpc > 8) wpc = 8;
+    if (wpc < 1) return PT_ERR_UNSUPPORTED;
+    const size_t smem = per_warp * wpc;
+    const int pages = n_max / S + 2;  // pages one unit's rows can touch
+    dim3 grid((pages + wpc - 1) / wpc, U);
+    const int dj = (D + 31) / 32;
+#define PT_EXT_CASE(DJ_)                                                                      \
+    case DJ_: {                                                                               \
+        static size_t configured = 0;                                                         \
+        if (smem > configured) {                                                              \
+            PT_CUDA_TRY(cudaFuncSetAttribute(k_extend<DT, SDT, DJ_>,                          \
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                                             (int)smem));                                     \
+            configured = smem;                                                                \
+        }                                                                                     \
+        k_extend<DT, SDT, DJ_><<<grid, wpc * 32, smem, st>>>(kr, vr, n_max, rb, nrw, kp, vp,  \
+                                                             ptab, S, D, Pmax, means, stds); \
+        break;                                                                                \
+    }
+    switch (dj) {
+        PT_EXT_CASE(1)
+        PT_EXT_CASE(2)
+        PT_EXT_CASE(3)
+        PT_EXT_CASE(4)
+        PT_EXT_CASE(8)
+        PT_EXT_CASE(16)
+        default: return PT_ERR_UNSUPPORTED;
+    }
+#undef PT_EXT_CASE
+    PT_CUDA_TRY(cudaGetLastError());
+    return PT_OK;
+}
+
+extern "C" int pt_extend(const void *k_rows, const void *v_rows, int n_max,
+                         const int32_t *row_begin, const int32_t *n_rows, void *k_pool,
+                         void *v_pool, int kv_dtype, const int32_t *page_table, int U, int S,
+                         int D, int Pmax, void *means, int stats_dtype, float *stds,
+                         void *stream) {
+    if (!k_rows || !v_rows || !row_begin || !n_rows || !k_pool || !v_pool || !page_table ||
+        !means || !stds || U < 0 || n_max < 0 || S < 1 || Pmax % 32)
+        return PT_ERR_INVALID;
+    if (!stats_dj_ok(D)) return PT_ERR_UNSUPPORTED;
+    if (U == 0 || n_max == 0) return PT_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+#define PT_EXT(DT_, SDT_)                                                                     \
+    if (kv_dtype == DT_ && stats_dtype == SDT_)                                               \
+        return launch_extend<DT_, SDT_>(k_rows, v_rows, n_max, row_begin, n_rows, k_pool,     \
+                                        v_pool, page_table, U, S, D, Pmax, means, stds, st);
+    PT_EXT(PT_F32, PT_F32) PT_EXT(PT_BF16, PT_F32) PT_EXT(PT_BF16, PT_BF16) PT_EXT(PT_F32, PT_BF16)
+#undef PT_EXT
+    return PT_ERR_INVALID;
 }

@@ -224,6 +224,8 @@ class PagedKvCache:
         self.pool_state = torch.tensor([0, 0, layout.max_pages, 0], dtype=torch.int32, device=d)
         self.free_list_dev = torch.zeros(layout.max_pages, dtype=torch.int32, device=d)
         self._slot = torch.zeros(U + 4, dtype=torch.int32, device=d)  # targets + launch flags
+        # extend_units: fused pt_extend (default) or pt_write_rows + pt_page_stats (cross-check)
+        self.split_extend = False
         self._seq_host = np.zeros(U, dtype=np.int64)
         self.table = _DevicePageTable(self)
 
@@ -247,7 +249,7 @@ class PagedKvCache:
     # ------------------------------------------------------------------
     # Appends
 
-    def _host_alloc(self, counts: np.ndarray) -> list[np.ndarray]:
+    def _host_alloc(self, counts: np.ndarray) -> np.ndarray:
         """Host-side _alloc_page (kvcache.py:154-176) for `counts[u]` new pages per unit,
         in unit order: the free list is popped from its end first, then the bump pointer."""
         st = self.pool_state.cpu().numpy()
@@ -261,7 +263,7 @@ class PagedKvCache:
                                np.arange(bump, bump + need - from_free, dtype=np.int64)])
         self.pool_state[0] = bump + need - from_free
         self.pool_state[1] = nfree - from_free
-        return np.split(pids, np.cumsum(counts)[:-1])
+        return pids  # flat, unit-major (counts[u] ids per unit)
 
     def extend_units(self, keys: torch.Tensor, values: torch.Tensor, n_rows=None) -> None:
         """Batched extend (kvcache.py:210-233) for every unit at once.
@@ -284,20 +286,31 @@ class PagedKvCache:
         new_pids = self._host_alloc(P1 - P0)
         d = self.device
         cnt = P1 - P0
-        if cnt.sum():
-            r = torch.from_numpy(np.repeat(np.arange(U), cnt)).to(d)
-            c = torch.from_numpy(np.concatenate([np.arange(a, b) for a, b in zip(P0, P1)])).to(d)
-            v = torch.from_numpy(np.concatenate(new_pids).astype(np.int32)).to(d)
-            self.page_table[r, c] = v
+        total = int(cnt.sum())
+        if total:
+            # (unit, logical page) of every new page, vectorised (no per-unit Python loop)
+            r = np.repeat(np.arange(U), cnt)
+            c = np.arange(total) - np.repeat(np.cumsum(cnt) - cnt, cnt) + np.repeat(P0, cnt)
+            flat = torch.from_numpy((r * self.Pmax + c).astype(np.int64)).to(d)
+            v = torch.from_numpy(new_pids.astype(np.int32)).to(d)
+            self.page_table.view(-1).index_copy_(0, flat, v)
         kk = dev.to_device(keys, self.dtype, d)
         vv = dev.to_device(values, self.dtype, d)
         row_begin = torch.from_numpy(n0.astype(np.int32)).to(d)
         nrows_t = torch.from_numpy(nr.astype(np.int32)).to(d)
         sh = dev.stream_handle()
+        self._seq_host = n1
+        if not self.split_extend:
+            # one launch: rows scattered into their pages and every touched page's stats
+            _lib.call("pt_extend", kk.data_ptr(), vv.data_ptr(), n_max, row_begin.data_ptr(),
+                      nrows_t.data_ptr(), self.k_pool.data_ptr(), self.v_pool.data_ptr(),
+                      self.kv_code, self.page_table.data_ptr(), U, S, D, self.Pmax,
+                      self.means.data_ptr(), self.stats_code, self.stds.data_ptr(), sh)
+            self.seq_lens.copy_(torch.from_numpy(n1.astype(np.int32)))
+            return
         _lib.call("pt_write_rows", kk.data_ptr(), vv.data_ptr(), n_max, row_begin.data_ptr(),
                   nrows_t.data_ptr(), self.k_pool.data_ptr(), self.v_pool.data_ptr(), self.kv_code,
                   self.page_table.data_ptr(), U, S, D, self.Pmax, sh)
-        self._seq_host = n1
         self.seq_lens.copy_(torch.from_numpy(n1.astype(np.int32)))
         first = np.where(nr > 0, n0 // S, np.iinfo(np.int32).max).astype(np.int32)
         page_begin = torch.from_numpy(first).to(d)

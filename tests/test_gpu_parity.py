@@ -439,11 +439,19 @@ def test_fused_score_select_equals_two_launches(cuda, lens, k, fused):
     (4, 4, 1, 64, 32, [1875 * 32 - 11], 16),                              # cfg4-like head shape
     (2, 2, 8, 256, 16, [640 * 16 + 3], 40),                               # D=256, G=8
     (2, 2, 2, 128, 64, [200 * 64 + 1], 8),                                # S=64
+    (80, 8, 4, 128, 16, [100 * 16 - 3], 16),                              # warp-per-unit path
+    (40, 16, 1, 64, 32, [60 * 32 + 7], 16),                               # warp path, cfg4 heads
 ])
-def test_select_attend_equals_two_launches(cuda, oracle, B, H, G, D, S, lens, k):
+@pytest.mark.parametrize("force_warp", [False, True])
+def test_select_attend_equals_two_launches(cuda, oracle, B, H, G, D, S, lens, k, force_warp,
+                                           monkeypatch):
     """pt_select_attend (K3+K4 in one launch) == pt_topk + pt_attend: selections bit for bit,
     outputs within the bf16 tolerance; and both against the oracle."""
     pt = _pt()
+    if force_warp:
+        if int(np.max(lens)) // S + 1 > 2048:
+            pytest.skip("warp path holds at most 2048 keys per unit")
+        monkeypatch.setenv("PT_SA_WARP", "1")
     rng = np.random.default_rng(B * 1000 + H * 10 + G + D + S)
     cache = make_cache(rng, B, H, D, S, lens, dtype="bf16")
     eng = pt.DecodeEngine(cache, G, k, keep_logical=True)
@@ -481,3 +489,50 @@ def test_select_attend_equals_two_launches(cuda, oracle, B, H, G, D, S, lens, k)
     np.testing.assert_array_equal(fused[4].cpu().numpy(), ref["kplus1"])
     np.testing.assert_allclose(fused[5].cpu().numpy().reshape(-1, G, D), ref["out"], rtol=0, atol=2e-2)
     np.testing.assert_allclose(fused[6].cpu().numpy().reshape(-1, G), ref["lse"], rtol=0, atol=2e-2)
+
+
+@pytest.mark.parametrize("dtype,stats,D,S", [("bf16", "f32", 128, 16), ("f32", "f32", 64, 32),
+                                             ("bf16", "bf16", 128, 64), ("f32", "f32", 20, 8)])
+def test_fused_extend_equals_write_rows_plus_stats(cuda, oracle, dtype, stats, D, S):
+    """pt_extend (one launch) == pt_write_rows + pt_page_stats, bit for bit, over ragged
+    extends that start inside partially filled tail pages; and the stats equal the oracle's."""
+    pt = _pt()
+    rng = np.random.default_rng(D + S)
+    B, H = 2, 3
+    U = B * H
+    caches = []
+    for split in (False, True):
+        layout = pt.CacheLayout(num_kv_heads=H, head_dim=D, page_size=S, max_pages=U * 64)
+        tdt = torch.float32 if dtype == "f32" else torch.bfloat16
+        sdt = torch.float32 if stats == "f32" else torch.bfloat16
+        c = pt.PagedKvCache(layout, batch=B, dtype=tdt, stats_dtype=sdt, max_pages_per_head=64)
+        c.split_extend = split
+        caches.append(c)
+    r2 = np.random.default_rng(7)
+    for chunk in range(4):
+        n = int(r2.integers(1, 3 * S + 5))
+        K = rng.standard_normal((U, n, D)).astype(np.float32)
+        V = rng.standard_normal((U, n, D)).astype(np.float32)
+        rows = r2.integers(0, n + 1, size=U)
+        for c in caches:
+            c.extend_units(torch.from_numpy(K), torch.from_numpy(V), rows)
+    torch.cuda.synchronize()
+    a, b = caches
+    assert torch.equal(a.seq_lens, b.seq_lens)
+    assert torch.equal(a.page_table, b.page_table)
+    for u in range(U):
+        P = a.num_pages(u)
+        pids = a.page_table[u, :P].long()
+        assert torch.equal(a.k_pool[pids], b.k_pool[pids])
+        assert torch.equal(a.v_pool[pids], b.v_pool[pids])
+    ma, sa = gpu_stats(a)
+    mb, sb = gpu_stats(b)
+    kpool, _, table, seq = readback(a)
+    means, stds = oracle.build_stats(kpool, table, seq, S)
+    for u in range(U):
+        P = a.num_pages(u)
+        np.testing.assert_array_equal(ma[u, :P], mb[u, :P])
+        np.testing.assert_array_equal(sa[u, :P], sb[u, :P])
+        if stats == "f32":
+            np.testing.assert_array_equal(ma[u, :P], means[u, :P])
+            np.testing.assert_array_equal(sa[u, :P], stds[u, :P])
