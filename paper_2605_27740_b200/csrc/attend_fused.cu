@@ -53,7 +53,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 constexpr int kSAThreads = kSAWarps * 32;
-constexpr int kSARegVecs = 16;  // register-resident candidate pass: P <= 128 * 8 * 16 = 16384
 
 __host__ __device__ __forceinline__ size_t sa_keys_bytes(int Pmax) {
     return (size_t)((Pmax + 8) / 8) * 16;
@@ -123,8 +122,8 @@ __global__ void __launch_bounds__(kSAThreads) k_select_attend(const __grid_const
     if (prof) g_sa_prof[cta * 10 + 1] = gtimer();
 
     // ---- selection (select.py:87-115): physical ids land in `ids` in emission order ----
-    // register-resident keys (select_regs) when the unit fits and the k-th key lies within
-    // 64 values of the maximum; else the shared-memory select_block
+    // candidate selection (select_cand: tile-maximum lower bound or bisection, then the
+    // candidates only); select_block for take-all and massive ties
     const int ns = P < k ? P : k;
     const uint16_t *krow = p.keys + u * (int64_t)p.Pmax;
     int32_t *o_sel = lead ? p.sel + u * (int64_t)k : nullptr;
@@ -132,15 +131,10 @@ __global__ void __launch_bounds__(kSAThreads) k_select_attend(const __grid_const
     int32_t *o_n = lead ? p.n_sel + u : &sdummy[0];
     int32_t *o_kth = lead ? p.kth + u : &sdummy[1];
     int32_t *o_kp1 = lead ? p.kplus1 + u : &sdummy[2];
-    bool selected = false;
-    if (p.tile_max && P <= kSAThreads * 8 * kSARegVecs)
-        selected = select_cand<kSAThreads, kSARegVecs>(
-            krow, p.tile_max + u * (int64_t)(p.Pmax >> 5), P, k, p.page_table + u * p.Pmax, o_sel,
-            o_log, o_n, o_kth, o_kp1, csh, ids, true,
-            prof ? &g_sa_prof[cta * 10 + 6] : nullptr);
-    if (!selected) {
-        uint16_t *skeys = reinterpret_cast<uint16_t *>(smem);
-        int *bins = reinterpret_cast<int *>(smem + sa_keys_bytes(p.Pmax));
+    // keys -> shared memory: every 16-byte load of a thread in flight before its first store
+    uint16_t *skeys = reinterpret_cast<uint16_t *>(smem);
+    int *bins = reinterpret_cast<int *>(smem + sa_keys_bytes(p.Pmax));
+    {
         const uint4 *src = reinterpret_cast<const uint4 *>(krow);
         constexpr int kMax = 8;
         const int nv = (P + 7) / 8;
@@ -153,11 +147,15 @@ __global__ void __launch_bounds__(kSAThreads) k_select_attend(const __grid_const
             for (int j = 0; j < kMax; j++)
                 if (i0 + j * kSAThreads < nv) reinterpret_cast<uint4 *>(skeys)[i0 + j * kSAThreads] = v[j];
         }
-        __syncthreads();
-        select_block<kSAThreads>(skeys, bins, P, k, p.page_table + u * p.Pmax, o_sel, o_log, o_n,
-                                 o_kth, o_kp1, sh, ids, true,
-                                 prof ? &g_sa_prof[cta * 10 + 6] : nullptr);
     }
+    __syncthreads();
+    const bool selected =
+        select_cand<kSAThreads>(skeys, p.tile_max ? p.tile_max + u * (int64_t)(p.Pmax >> 5) : nullptr,
+                                P, k, p.page_table + u * p.Pmax, o_sel, o_log, o_n, o_kth, o_kp1,
+                                csh, ids, true, prof ? &g_sa_prof[cta * 10 + 6] : nullptr);
+    if (!selected)  // take-all, or massive ties at the lower bound
+        select_block<kSAThreads>(skeys, bins, P, k, p.page_table + u * p.Pmax, o_sel, o_log, o_n,
+                                 o_kth, o_kp1, sh, ids, true);
     __syncthreads();  // ids complete; the select scratch is dead -> stage rings
     if (prof) g_sa_prof[cta * 10 + 2] = gtimer();
 

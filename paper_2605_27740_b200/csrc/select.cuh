@@ -339,231 +339,333 @@ __device__ void select_block(uint16_t *skeys, int *bins, int P, int k,
 }
 
 // ---------------------------------------------------------------------------
-// Candidate selection (the fused select+attend prologue).
+// Fast block selection over keys staged in shared memory (the fused select+attend prologue).
 //
-// Uses the per-32-page tile maxima written by the scoring kernel: the k-th largest tile
-// maximum L is a lower bound for the k-th largest key (k distinct tiles each hold a key
-// >= L), and for scores of a decode step only ~1-3 % of the keys reach it.  So:
-//   1. L = k-th largest of the ceil(P/32) tile maxima (two 8-way counting rounds relative
-//      to the overall maximum mt, packed 8-bit counters, block reductions);
-//   2. one pass over the keys (register-resident: thread t holds the 16-byte key vectors
-//      t, t+NT, ...) appends every key >= L to a shared candidate list (key << 16 | index);
-//   3. the k-th largest candidate (a 64-bin shared histogram over [L, mt]) is the
-//      threshold thr; keys > thr are selected, ties at thr by ascending logical index
-//      (rank among the tied candidates) -- the reference's rule -- emitted in ascending
-//      logical order: the same list as select_block.
-// Returns false (uniformly) when the shape or the data leave this envelope (fewer tiles
-// than k, L not within 64 values of mt, more than kCandMax candidates); the caller then
-// runs select_block.
+// Keys are processed as u16x2 words with the SIMD video instructions (VIMNMX/VSET-style
+// __vcmpgeu2 / __vmaxu2): 8 keys per 16-byte shared load, ~1.5 instructions per key per pass.
+// 1. threshold thr (the k-th largest key):
+//    - with the scoring kernel's per-32-page tile maxima (>= k tiles): L = the k-th largest
+//      tile maximum is a lower bound for thr (k distinct tiles each hold a key >= L); for
+//      decode-step scores only ~1-3 % of the keys reach it.  One pass appends the keys >= L
+//      to a candidate list in ascending logical order; thr = the k-th largest candidate
+//      (64-bin histogram over [L, max], or bisection over the candidates);
+//    - otherwise (no tile maxima, fewer tiles than k, or too many candidates): bisection over
+//      [min, max] with block-wide counts (exact for any key distribution);
+// 2. ordered compaction: keys > thr plus the first (k - #>thr) keys == thr in ascending
+//    logical index -- the reference's rule -- over the candidate list when there is one, else
+//    over all keys (one block scan per round of NT key vectors); physical ids by one parallel
+//    round of page-table loads.
+// Emission order is ascending logical (the same list as select_block).  Returns false only
+// for the take-all case (P <= k) and P > 65536 (the caller runs select_block).
 // ---------------------------------------------------------------------------
 constexpr int kCandMax = 2048;
 
 template <int NT>
 struct SelectCandShared {
-    uint32_t red[NT / 32][8];
+    uint32_t red[2][NT / 32][2];
     int bins[64];
     int below, thr, gt, eq;
     uint32_t cand[kCandMax];
 };
 
-template <int NT, int MAXJ>
-__device__ bool select_cand(const uint16_t *__restrict__ keys_g, const uint16_t *__restrict__ tmax_g,
+template <int NT>
+__device__ bool select_cand(const uint16_t *__restrict__ skeys, const uint16_t *__restrict__ tmax_g,
                             int P, int k, const int32_t *__restrict__ map,
                             int32_t *__restrict__ out, int32_t *__restrict__ out_l,
                             int32_t *__restrict__ n_sel, int32_t *__restrict__ kth,
                             int32_t *__restrict__ kplus1, SelectCandShared<NT> &sh, int *slist,
                             bool slist_physical, unsigned long long *tp = nullptr) {
+    constexpr int NWP = NT / 32;
+    constexpr int MAXT = 8;  // tile maxima per thread: ceil(P / 32) <= NT * MAXT
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (P <= k || P > 65536) return false;
     auto stamp = [&](int i) {
-        if (tp && threadIdx.x == 0) {
+        if (tp && tid == 0) {
             unsigned long long t;
             asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
             tp[i] = t;
         }
     };
-    constexpr int NWP = NT / 32;
-    constexpr int MAXT = 4;  // tile maxima per thread: ceil(P / 32) <= NT * MAXT
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int ntiles = (P + 31) >> 5;
-    if (P > NT * 8 * MAXJ || P <= k || ntiles < k || ntiles > NT * MAXT) return false;
-    // ---- issue every load up front: keys (registers) and tile maxima ----
-    const uint4 *k4 = reinterpret_cast<const uint4 *>(keys_g);
-    uint4 v[MAXJ];
+    const uint4 *s4 = reinterpret_cast<const uint4 *>(skeys);
+    const int nvec = (P + 7) >> 3;
+    const int tailn = P - (nvec - 1) * 8;  // valid keys in the last vector (1..8)
+    // per-word validity masks of vector v (only the last one can be partial)
+    auto vmask = [&](int v, uint32_t (&m)[4]) {
 #pragma unroll
-    for (int j = 0; j < MAXJ; j++) {
-        const int base = (tid + j * NT) * 8;
-        v[j] = base < P ? __ldcg(k4 + tid + j * NT) : make_uint4(0u, 0u, 0u, 0u);
-    }
+        for (int w = 0; w < 4; w++) {
+            const int nk = v < nvec - 1 ? 8 : tailn;
+            const int lo = 2 * w, hi = 2 * w + 1;
+            m[w] = (lo < nk ? 0x0000FFFFu : 0u) | (hi < nk ? 0xFFFF0000u : 0u);
+        }
+    };
+    auto words = [](const uint4 &x, uint32_t (&w)[4]) { w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w; };
+    // count of valid keys >= t (t16 = t * 0x10001) in vector v
+    auto count_ge = [&](const uint4 &x, int v, uint32_t t16) -> int {
+        uint32_t w[4], m[4];
+        words(x, w);
+        vmask(v, m);
+        int c = 0;
+#pragma unroll
+        for (int q = 0; q < 4; q++) c += __popc(__vcmpgeu2(w[q], t16) & m[q]);
+        return c >> 4;
+    };
+    auto block_sum = [&](int v) -> int {
+        v = __reduce_add_sync(0xffffffffu, v);
+        __syncthreads();
+        if (lane == 0) sh.red[0][warp][0] = (uint32_t)v;
+        __syncthreads();
+        int t = 0;
+#pragma unroll
+        for (int w = 0; w < NWP; w++) t += (int)sh.red[0][w][0];
+        return t;
+    };
+    auto block_max = [&](int v) -> int {
+        v = __reduce_max_sync(0xffffffffu, v);
+        __syncthreads();
+        if (lane == 0) sh.red[0][warp][1] = (uint32_t)v;
+        __syncthreads();
+        int t = -1;
+#pragma unroll
+        for (int w = 0; w < NWP; w++) t = max(t, (int)sh.red[0][w][1]);
+        return t;
+    };
+    const int ntiles = (P + 31) >> 5;
+    const bool use_tiles = tmax_g != nullptr && ntiles >= k && ntiles <= NT * MAXT;
     int tm[MAXT];
 #pragma unroll
     for (int i = 0; i < MAXT; i++) {
         const int t = tid + i * NT;
-        tm[i] = t < ntiles ? (int)__ldcg(tmax_g + t) : -1;
+        tm[i] = (use_tiles && t < ntiles) ? (int)__ldcg(tmax_g + t) : -1;
     }
     if (tid < 64) sh.bins[tid] = 0;
     if (tid == 0) sh.below = -1;
-    // ---- 1. L = k-th largest tile maximum ----
-    int mt = -1;
+    int mx, mn = 0, L = -1;
+    if (use_tiles) {
+        int m = -1;
 #pragma unroll
-    for (int i = 0; i < MAXT; i++) mt = max(mt, tm[i]);
-    mt = __reduce_max_sync(0xffffffffu, mt);
-    if (lane == 0) sh.red[warp][0] = (uint32_t)mt;
-    __syncthreads();
-    mt = -1;
+        for (int i = 0; i < MAXT; i++) m = max(m, tm[i]);
+        mx = block_max(m);  // the largest tile maximum is the largest key
+        auto round8 = [&](int lo, int shift, int (&tot)[8]) {
+            unsigned long long c = 0ull;
 #pragma unroll
-    for (int w = 0; w < NWP; w++) mt = max(mt, (int)sh.red[w][0]);
-    __syncthreads();
+            for (int i = 0; i < MAXT; i++) {
+                const int d = mx - tm[i] - lo, b = d >> shift;
+                if (tm[i] >= 0 && d >= 0 && b < 8) c += 1ull << (8 * b);
+            }
+            __syncthreads();
+#pragma unroll
+            for (int b = 0; b < 8; b++) {
+                const int x = __reduce_add_sync(0xffffffffu, (uint32_t)((c >> (8 * b)) & 0xFFu));
+                if (lane == 0) sh.bins[b * NWP + warp] = x;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int b = 0; b < 8; b++) {
+                int t = 0;
+#pragma unroll
+                for (int w = 0; w < NWP; w++) t += sh.bins[b * NWP + w];
+                tot[b] = t;
+            }
+        };
+        static_assert(8 * (NT / 32) <= 64, "bins scratch");
+        int ta[8], tb[8];
+        round8(0, 3, ta);
+        int ia = -1, cum = 0, before = 0;
+#pragma unroll
+        for (int b = 0; b < 8; b++) {
+            if (ia < 0 && cum + ta[b] >= k) { ia = b; before = cum; }
+            cum += ta[b];
+        }
+        if (ia >= 0) {
+            round8(8 * ia, 0, tb);
+            int c2 = before, ib = 7;
+            bool done = false;
+#pragma unroll
+            for (int b = 0; b < 8; b++) {
+                if (!done && c2 + tb[b] >= k) { ib = b; done = true; }
+                c2 += tb[b];
+            }
+            L = mx - (8 * ia + ib);
+        }
+        __syncthreads();
+        if (tid < 64) sh.bins[tid] = 0;
+    } else {
+        int m = -1, n = 0xFFFF;
+        for (int v = tid; v < nvec; v += NT) {
+            uint32_t w[4], mk[4];
+            words(s4[v], w);
+            vmask(v, mk);
+            uint32_t a = 0u, b = 0xFFFFFFFFu;
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                a = __vmaxu2(a, w[q] & mk[q]);
+                b = __vminu2(b, w[q] | ~mk[q]);
+            }
+            m = max(m, (int)max(a & 0xFFFFu, a >> 16));
+            n = min(n, (int)min(b & 0xFFFFu, b >> 16));
+        }
+        mx = block_max(m);
+        mn = 0xFFFF - block_max(0xFFFF - n);
+    }
     stamp(0);
-    auto round8 = [&](int lo, int shift, int (&tot)[8]) {
-        unsigned long long c = 0ull;
+    int thr = -1, gt_tot = 0, eq_tot = 0, C = -1;
+    if (L >= 0) {
+        // ---- candidates >= L in logical order (one block scan per round of NT vectors) ----
+        const uint32_t L16 = (uint32_t)L * 0x10001u;
+        int run = 0, below = -1, par = 0;
+        for (int v0 = 0; v0 < nvec; v0 += NT, par ^= 1) {
+            const int v = v0 + tid;
+            uint4 x = make_uint4(0u, 0u, 0u, 0u);
+            int c = 0;
+            if (v < nvec) {
+                x = s4[v];
+                uint32_t w[4], mk[4];
+                words(x, w);
+                vmask(v, mk);
+                uint32_t bl = 0u;
+                bool any_below = false;
 #pragma unroll
-        for (int i = 0; i < MAXT; i++) {
-            const int d = mt - tm[i] - lo, b = d >> shift;
-            if (tm[i] >= 0 && d >= 0 && b < 8) c += 1ull << (8 * b);
-        }
+                for (int q = 0; q < 4; q++) {
+                    const uint32_t ge = __vcmpgeu2(w[q], L16);
+                    c += __popc(ge & mk[q]);
+                    const uint32_t lt = ~ge & mk[q];
+                    any_below |= lt != 0u;
+                    bl = __vmaxu2(bl, w[q] & lt);
+                }
+                c >>= 4;
+                if (any_below) below = max(below, (int)max(bl & 0xFFFFu, bl >> 16));
+            }
+            int inc = c;
 #pragma unroll
-        for (int b = 0; b < 8; b++) {
-            const uint32_t x = __reduce_add_sync(0xffffffffu, (uint32_t)((c >> (8 * b)) & 0xFFu));
-            if (lane == 0) sh.red[warp][b] = x;
-        }
-        __syncthreads();
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+            }
+            if (lane == 31) sh.red[par][warp][0] = (uint32_t)inc;
+            __syncthreads();
+            int pos = run + inc - c;
 #pragma unroll
-        for (int b = 0; b < 8; b++) {
-            int t = 0;
+            for (int w = 0; w < NWP; w++) {
+                const int t = (int)sh.red[par][w][0];
+                if (w < warp) pos += t;
+                run += t;
+            }
+            if (c) {
+                uint32_t w[4];
+                words(x, w);
 #pragma unroll
-            for (int w = 0; w < NWP; w++) t += (int)sh.red[w][b];
-            tot[b] = t;
-        }
-        __syncthreads();
-    };
-    int ta[8], tb[8];
-    round8(0, 3, ta);
-    int ia = -1, cum = 0, before = 0;
-#pragma unroll
-    for (int b = 0; b < 8; b++) {
-        if (ia < 0 && cum + ta[b] >= k) { ia = b; before = cum; }
-        cum += ta[b];
-    }
-    if (ia < 0) return false;
-    round8(8 * ia, 0, tb);
-    int ib = 7;
-    {
-        int c2 = before;
-        bool done = false;
-#pragma unroll
-        for (int b = 0; b < 8; b++) {
-            if (!done && c2 + tb[b] >= k) { ib = b; done = true; }
-            c2 += tb[b];
-        }
-    }
-    const int L = mt - (8 * ia + ib);  // within 64 values of mt: candidate keys fit 64 bins
-    stamp(1);
-    // ---- 2. candidates: every valid key >= L, and the largest valid key below L ----
-    auto keyof = [&](const uint4 &x, int e) -> int {
-        const uint32_t w = e < 2 ? x.x : e < 4 ? x.y : e < 6 ? x.z : x.w;
-        return (e & 1) ? (int)(w >> 16) : (int)(w & 0xFFFFu);
-    };
-    // per (vector j, thread) candidate counts, scanned in logical order (j-major, then
-    // thread) so the list is written in ascending logical index; two 16-bit counts per word
-    static_assert(MAXJ % 2 == 0 && MAXJ / 2 <= 8, "MAXJ");
-    uint32_t cnt[MAXJ / 2];
-    int below = -1;
-#pragma unroll
-    for (int w = 0; w < MAXJ / 2; w++) cnt[w] = 0u;
-#pragma unroll
-    for (int j = 0; j < MAXJ; j++) {
-        const int base = (tid + j * NT) * 8;
-        if (j * NT * 8 >= P) break;
-        uint32_t c = 0;
-#pragma unroll
-        for (int e = 0; e < 8; e++) {
-            const int key = keyof(v[j], e);
-            const bool ok = base + e < P;
-            c += (ok && key >= L);
-            if (ok && key < L) below = max(below, key);
-        }
-        cnt[j >> 1] += c << (16 * (j & 1));
-    }
-    uint32_t inc[MAXJ / 2];
-#pragma unroll
-    for (int w = 0; w < MAXJ / 2; w++) inc[w] = cnt[w];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-#pragma unroll
-        for (int w = 0; w < MAXJ / 2; w++) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, inc[w], o);
-            if (lane >= o) inc[w] += y;
-        }
-    }
-    below = __reduce_max_sync(0xffffffffu, below);
-    if (lane == 0) atomicMax(&sh.below, below);
-    if (lane == 31) {
-#pragma unroll
-        for (int w = 0; w < MAXJ / 2; w++) sh.red[warp][w] = inc[w];
-    }
-    __syncthreads();
-    int run = 0;  // candidates in vectors j' < j (all threads)
-#pragma unroll
-    for (int j = 0; j < MAXJ; j++) {
-        if (j * NT * 8 >= P) break;
-        const int sh16 = 16 * (j & 1);
-        int pos = run + (int)(((inc[j >> 1] - cnt[j >> 1]) >> sh16) & 0xFFFFu);
-#pragma unroll
-        for (int w = 0; w < NWP; w++) {
-            const int t = (int)((sh.red[w][j >> 1] >> sh16) & 0xFFFFu);
-            if (w < warp) pos += t;
-            run += t;
-        }
-        if ((cnt[j >> 1] >> sh16) & 0xFFFFu) {
-            const int base = (tid + j * NT) * 8;
-#pragma unroll
-            for (int e = 0; e < 8; e++) {
-                const int key = keyof(v[j], e);
-                if (base + e < P && key >= L) {
-                    if (pos < kCandMax) sh.cand[pos] = ((uint32_t)key << 16) | (uint32_t)(base + e);
-                    pos++;
+                for (int e = 0; e < 8; e++) {
+                    const int key = (e & 1) ? (int)(w[e >> 1] >> 16) : (int)(w[e >> 1] & 0xFFFFu);
+                    if (v * 8 + e < P && key >= L) {
+                        if (pos < kCandMax) sh.cand[pos] = ((uint32_t)key << 16) | (uint32_t)(v * 8 + e);
+                        pos++;
+                    }
                 }
             }
         }
+        below = __reduce_max_sync(0xffffffffu, below);
+        if (lane == 0) atomicMax(&sh.below, below);
+        __syncthreads();
+        if (run <= kCandMax) C = run;  // else: too many keys tie at L -- bisection below
     }
-    const int C = run;
-    if (C > kCandMax) return false;  // uniform
-    __syncthreads();
-    stamp(2);
-    // ---- 3. threshold among the candidates: 64-bin histogram of mt - key ----
-    for (int i = tid; i < C; i += NT) atomicAdd(&sh.bins[mt - (int)(sh.cand[i] >> 16)], 1);
-    __syncthreads();
-    if (warp == 0) {
-        const int c0 = sh.bins[2 * lane], c1 = sh.bins[2 * lane + 1];
-        int incl = c0 + c1;
+    stamp(1);
+    if (C >= 0) {
+        // ---- thr = the k-th largest candidate ----
+        if (mx - L < 64) {
+            for (int i = tid; i < C; i += NT) atomicAdd(&sh.bins[mx - (int)(sh.cand[i] >> 16)], 1);
+            __syncthreads();
+            if (warp == 0) {
+                const int c0 = sh.bins[2 * lane], c1 = sh.bins[2 * lane + 1];
+                int incl = c0 + c1;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                const int pre = incl - c0 - c1;
+                int b = -1, g = 0, q = 0;
+                if (pre < k && pre + c0 >= k) { b = 2 * lane; g = pre; q = c0; }
+                else if (pre + c0 < k && incl >= k) { b = 2 * lane + 1; g = pre + c0; q = c1; }
+                const unsigned hit = __ballot_sync(0xffffffffu, b >= 0);
+                const int src = __ffs(hit) - 1;
+                const int bt = __shfl_sync(0xffffffffu, b, src);
+                const int nb = (c0 > 0 && 2 * lane > bt) ? 2 * lane
+                             : (c1 > 0 && 2 * lane + 1 > bt) ? 2 * lane + 1 : 999;
+                const int nbm = __reduce_min_sync(0xffffffffu, nb);
+                if (lane == src) {
+                    sh.thr = mx - b;
+                    sh.gt = g;
+                    sh.eq = q;
+                    if (nbm < 999) sh.below = mx - nbm;  // a candidate lies below thr
+                }
+            }
+            __syncthreads();
+            thr = sh.thr;
+            gt_tot = sh.gt;
+            eq_tot = sh.eq;
+        } else {
+            int lo = L, hi = mx + 1;
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                int c = 0;
+                for (int i = tid; i < C; i += NT) c += (int)(sh.cand[i] >> 16) >= mid;
+                if (block_sum(c) >= k) lo = mid; else hi = mid;
+            }
+            thr = lo;
+            int g = 0, q = 0, bl = -1;
+            for (int i = tid; i < C; i += NT) {
+                const int key = (int)(sh.cand[i] >> 16);
+                g += key > thr;
+                q += key == thr;
+                if (key < thr) bl = max(bl, key);
+            }
+            gt_tot = block_sum(g);
+            eq_tot = block_sum(q);
+            bl = __reduce_max_sync(0xffffffffu, bl);
+            if (lane == 0) atomicMax(&sh.below, bl);
+            __syncthreads();
         }
-        const int pre = incl - c0 - c1;
-        int b = -1, gt = 0, eq = 0;
-        if (pre < k && pre + c0 >= k) { b = 2 * lane; gt = pre; eq = c0; }
-        else if (pre + c0 < k && incl >= k) { b = 2 * lane + 1; gt = pre + c0; eq = c1; }
-        // largest key below thr among the candidates: the first non-empty bin past b
-        const unsigned hit = __ballot_sync(0xffffffffu, b >= 0);
-        const int src = __ffs(hit) - 1;
-        const int bt = __shfl_sync(0xffffffffu, b, src);
-        const int nb = (c0 > 0 && 2 * lane > bt) ? 2 * lane : (c1 > 0 && 2 * lane + 1 > bt) ? 2 * lane + 1 : 999;
-        const int nbm = __reduce_min_sync(0xffffffffu, nb);
-        if (lane == src) {
-            sh.thr = mt - b;
-            sh.gt = gt;
-            sh.eq = eq;
-            if (nbm < 999) sh.below = mt - nbm;  // a candidate lies below thr
+    } else {
+        // ---- bisection over all keys: thr = max t with #(keys >= t) >= k ----
+        int lo = L >= 0 ? L : mn, hi = mx + 1;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            const uint32_t m16 = (uint32_t)mid * 0x10001u;
+            int c = 0;
+            for (int v = tid; v < nvec; v += NT) c += count_ge(s4[v], v, m16);
+            if (block_sum(c) >= k) lo = mid; else hi = mid;
         }
+        thr = lo;
+        const uint32_t t16 = (uint32_t)thr * 0x10001u;
+        const uint32_t t1 = (uint32_t)(thr + 1) * 0x10001u;
+        int g = 0, ge = 0, bl = -1;
+        for (int v = tid; v < nvec; v += NT) {
+            const uint4 x = s4[v];
+            g += thr < 0xFFFF ? count_ge(x, v, t1) : 0;
+            ge += count_ge(x, v, t16);
+            uint32_t w[4], mk[4];
+            words(x, w);
+            vmask(v, mk);
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const uint32_t lt = ~__vcmpgeu2(w[q], t16) & mk[q];
+                if (lt) {
+                    const uint32_t z = w[q] & lt;
+                    if (lt & 0xFFFFu) bl = max(bl, (int)(z & 0xFFFFu));
+                    if (lt >> 16) bl = max(bl, (int)(z >> 16));
+                }
+            }
+        }
+        gt_tot = block_sum(g);
+        eq_tot = block_sum(ge) - gt_tot;
+        bl = block_max(bl);
+        if (tid == 0) sh.below = bl;
+        __syncthreads();
     }
-    __syncthreads();
-    const int thr = sh.thr, gt_tot = sh.gt, eq_tot = sh.eq;
     const int budget = k - gt_tot;  // in [1, eq_tot]
-    stamp(3);
-    // ---- ordered compaction of the (logically ordered) candidates: keys > thr, then the
-    // first `budget` ties -- contiguous per-thread segments and one block scan ----
-    {
+    stamp(2);
+    if (C >= 0) {
+        // ---- ordered compaction of the (logically ordered) candidates ----
         const int cs = (C + NT - 1) / NT;
         const int i0 = min(tid * cs, C), i1 = min(i0 + cs, C);
         int g = 0, q = 0;
@@ -579,13 +681,13 @@ __device__ bool select_cand(const uint16_t *__restrict__ keys_g, const uint16_t 
             const int yq = __shfl_up_sync(0xffffffffu, iq, o);
             if (lane >= o) { ig += yg; iq += yq; }
         }
-        __syncthreads();  // sh.red reuse
-        if (lane == 31) { sh.red[warp][0] = (uint32_t)ig; sh.red[warp][1] = (uint32_t)iq; }
+        __syncthreads();
+        if (lane == 31) { sh.red[1][warp][0] = (uint32_t)ig; sh.red[1][warp][1] = (uint32_t)iq; }
         __syncthreads();
         int gb = ig - g, qb = iq - q;
 #pragma unroll
         for (int w = 0; w < NWP; w++)
-            if (w < warp) { gb += (int)sh.red[w][0]; qb += (int)sh.red[w][1]; }
+            if (w < warp) { gb += (int)sh.red[1][w][0]; qb += (int)sh.red[1][w][1]; }
         int pos = gb + min(qb, budget);
         int seen = qb;
         for (int i = i0; i < i1; i++) {
@@ -599,7 +701,62 @@ __device__ bool select_cand(const uint16_t *__restrict__ keys_g, const uint16_t 
                 pos++;
             }
         }
+    } else {
+        // ---- ordered compaction over all keys: per round of NT vectors, a block scan of
+        // (keys > thr, keys == thr) gives each vector's output position and tie rank ----
+        const uint32_t t16 = (uint32_t)thr * 0x10001u;
+        const uint32_t t1 = (uint32_t)min(thr + 1, 0xFFFF) * 0x10001u;
+        int run_g = 0, run_q = 0, par = 0;
+        for (int v0 = 0; v0 < nvec; v0 += NT, par ^= 1) {
+            const int v = v0 + tid;
+            uint4 x = make_uint4(0u, 0u, 0u, 0u);
+            int g = 0, q = 0;
+            if (v < nvec) {
+                x = s4[v];
+                const int ge = count_ge(x, v, t16);
+                g = thr < 0xFFFF ? count_ge(x, v, t1) : 0;
+                q = ge - g;
+            }
+            const int pk = g | (q << 16);
+            int inc = pk;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+            }
+            if (lane == 31) sh.red[par][warp][0] = (uint32_t)inc;
+            __syncthreads();
+            int pre = inc - pk;
+            int tot = 0;
+#pragma unroll
+            for (int w = 0; w < NWP; w++) {
+                const int t = (int)sh.red[par][w][0];
+                if (w < warp) pre += t;
+                tot += t;
+            }
+            if (g | q) {
+                int gpos = run_g + (pre & 0xFFFF), seen = run_q + (pre >> 16);
+                int pos = gpos + min(seen, budget);
+                uint32_t w[4];
+                words(x, w);
+#pragma unroll
+                for (int e = 0; e < 8; e++) {
+                    const int key = (e & 1) ? (int)(w[e >> 1] >> 16) : (int)(w[e >> 1] & 0xFFFFu);
+                    if (v * 8 + e >= P || key < thr) continue;
+                    bool sel = key > thr;
+                    if (key == thr) { sel = seen < budget; seen++; }
+                    if (sel) {
+                        if (slist) slist[pos] = v * 8 + e;
+                        else { out[pos] = map[v * 8 + e]; if (out_l) out_l[pos] = v * 8 + e; }
+                        pos++;
+                    }
+                }
+            }
+            run_g += tot & 0xFFFF;
+            run_q += tot >> 16;
+        }
     }
+    stamp(3);
     if (slist) {
         __syncthreads();
         for (int t = tid; t < k; t += NT) {
