@@ -337,12 +337,8 @@ extern "C" int pt_score(const void *q, int q_dtype, const float *norms, const vo
     const int es = stats_dtype == PT_F32 ? 4 : 2, qes = q_dtype == PT_F32 ? 4 : 2;
     if (lamnorm_ws && G <= 8 && (D == 64 || D == 128) && !getenv("PT_SCORE_CTA") &&
         (long long)U * (Pmax / 32) < (1LL << 31)) {
-        const int rows = U * G;
-        if (q_dtype == PT_F32)
-            k_lam_norms<PT_F32><<<(rows + kLnRows - 1) / kLnRows, 256, 0, st>>>(q, norms, rows, G, D, lam, lamnorm_ws);
-        else
-            k_lam_norms<PT_BF16><<<(rows + kLnRows - 1) / kLnRows, 256, 0, st>>>(q, norms, rows, G, D, lam, lamnorm_ws);
-        PT_CUDA_TRY(cudaGetLastError());
+        const int rc0 = pt_lam_norms(q, q_dtype, norms, U, G, D, lam, lamnorm_ws, st);
+        if (rc0) return rc0;
         StreamScoreParams sp{q, lamnorm_ws, means, stds, seq_len, keys, scores, U, S, Pmax, tile_max};
         const int rc = q_dtype == PT_F32 ? launch_score_stream_q32(sp, stats_dtype, G, D, st)
                                          : launch_score_stream_q16(sp, stats_dtype, G, D, st);

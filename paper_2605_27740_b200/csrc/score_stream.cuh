@@ -19,6 +19,8 @@
 // an f32x2 add after an f32x2 mul would be contracted to FFMA2 by ptxas).  With bf16 x bf16
 // operands the products are exact in f32, so FFMA2 is bit-identical and used.
 #pragma once
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace pt {
@@ -36,7 +38,18 @@ struct StreamScoreParams {
 };
 
 constexpr int kSSWarps = 4;
-constexpr int kSSCtas = 3;  // per SM
+constexpr int kSSCtas = 3;  // per SM, at most
+// CTAs per SM of the persistent grid (PT_SS_CTAS overrides, 1..3: tuning).  Measured: two
+// (8 warps) beat three (170 vs 180 us at cfg3), and leave room for one overlapped
+// select+attend CTA per SM beside the scorer.
+static inline int ss_ctas_per_sm() {
+    static const int v = [] {
+        const char *e = getenv("PT_SS_CTAS");
+        const int x = e ? atoi(e) : 2;
+        return x < 1 ? 1 : (x > kSSCtas ? kSSCtas : x);
+    }();
+    return v;
+}
 constexpr int kSSNst = 3;   // ring stages per warp
 
 __device__ __forceinline__ float2 ss_mul2(float m, float2 q) {
@@ -109,12 +122,14 @@ __global__ void __launch_bounds__(kSSWarps * 32, kSSCtas) k_score_stream(const S
     char *ring = wbase;
     char *hdrs = wbase + NST * C::STAGE;
     float *qf = reinterpret_cast<float *>(hdrs + C::NHDR * C::HDR);
-    pdl_trigger();
     if (lane == 0) {
         for (int i = 0; i < NST; i++) mbar_init(&bars[i], 1);
         fence_mbar_init();
     }
     pdl_wait();
+    // dependents may launch only once every CTA is past its own wait: an overlapped
+    // select+attend then never runs beside a predecessor of this kernel (the append)
+    pdl_trigger();
     if (ps_smem)
         for (int i = threadIdx.x; i < U; i += blockDim.x) Ps[i] = (prm.seq_len[i] + S - 1) / S;
     __syncthreads();
