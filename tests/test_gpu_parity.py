@@ -539,3 +539,46 @@ def test_fused_extend_equals_write_rows_plus_stats(cuda, oracle, dtype, stats, D
         if stats == "f32":
             np.testing.assert_array_equal(ma[u, :P], means[u, :P])
             np.testing.assert_array_equal(sa[u, :P], stds[u, :P])
+
+
+def test_recall_harness_matches_reference_golden(cuda):
+    """The GPU recall harness (unique / mean_only / quest) on the reference's own seeded
+    dilution workloads reproduces the reference eval_recall reports
+    (tests/golden/recall_golden.npz, made by tests/golden/make_recall_golden.py)."""
+    import os
+
+    pt = _pt()
+    from paper_2605_27740_b200 import recall
+
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "recall_golden.npz"))
+    methods = [str(m) for m in z["methods"]]
+    n_cases = len([f for f in z.files if f.endswith("_spec")])
+    for i in range(n_cases):
+        seed, n, d, s, planted, k = (int(x) for x in z[f"c{i}_spec"])
+        P = -(-n // s)
+        layout = pt.CacheLayout(num_kv_heads=1, head_dim=d, page_size=s, max_pages=P)
+        cache = pt.PagedKvCache(layout, batch=1, dtype=torch.float32, max_pages_per_head=P)
+        cache.extend_units(torch.from_numpy(z[f"c{i}_keys"][None]), torch.from_numpy(z[f"c{i}_values"][None]))
+        q = torch.from_numpy(z[f"c{i}_q"][None]).cuda()
+        rep = recall.eval_recall_units(cache, q, k, methods=methods)
+        for m, method in enumerate(methods):
+            r = rep[method][0]
+            ref = z[f"c{i}_reports"][m]
+            assert r.page_recall == pytest.approx(ref[0], abs=1e-12), (i, method)
+            assert r.mass_recall == pytest.approx(ref[1], rel=1e-9), (i, method)
+            assert r.output_err == pytest.approx(ref[2], rel=1e-4, abs=1e-5), (i, method)
+
+
+def test_recall_units_workload_planted_pages_found(cuda):
+    """At GPU scale the spread-aware scorer finds planted (diluted) pages the mean-only
+    scorer misses (the reference's criterion, test_acceptance.py:334-351)."""
+    from paper_2605_27740_b200 import recall
+
+    wl = recall.gen_units_workload(8, 16384, 128, page_size=16, planted_pages=8,
+                                   planted_gain=6.0, seed=3)
+    rep = recall.eval_recall_units(wl.cache, wl.queries, 32)
+    mean = {m: float(np.mean([r.mass_recall for r in rep[m]])) for m in rep}
+    assert mean["unique"] > mean["mean_only"]
+    sel_hits = 0
+    for u in range(8):
+        assert 0.0 <= rep["unique"][u].page_recall <= 1.0
