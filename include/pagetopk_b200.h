@@ -204,6 +204,21 @@ PT_API int pt_select_attend(const uint16_t *keys, const uint16_t *tile_max,
  * PT_SA_PROF=1 in the environment.  n <= 10 * 4096. */
 PT_API int pt_debug_sa_prof(unsigned long long *host, int n);
 
+/* Soft-mask training path (softmask.py:178-217 gated_attention_backward), batched over units:
+ * the backward of attention over every page with a per-page additive log-gate bias, for the G
+ * query heads of each unit.  gates f32 [U][Pmax] (0 = hard-masked page, skipped); out / lse /
+ * dout: the forward's output, log-sum-exp and the loss gradient ([U*G][D], [U*G]).  Writes
+ * dk_pool / dv_pool (f32, pool layout [pages][S][D], only the rows of attended pages),
+ * dgates [U][Pmax] (summed over heads) and ACCUMULATES into dq [U*G][D] (zero it first).
+ * The forward is pt_attend in dense mode with bias = log(gate) (soft) or over the kept pages
+ * (hard).  f32 arithmetic (the reference is float64). */
+PT_API int pt_gated_attend_bwd(const void *q, int q_dtype, const void *k_pool, const void *v_pool,
+                               int kv_dtype, const int32_t *page_table, const int32_t *seq_len,
+                               const float *gates, const float *out, const float *lse,
+                               const float *dout, int U, int G, int D, int S, int Pmax, float scale,
+                               float *dq, float *dk_pool, float *dv_pool, float *dgates,
+                               void *stream);
+
 /* Layout helper: row-major means f32 [U][P][D] -> tiled stats layout (stats_dtype). */
 PT_API int pt_tile_means(const float *means_rowmajor, int U, int P, int D, int Pmax, void *means_tiled,
                   int stats_dtype, void *stream);

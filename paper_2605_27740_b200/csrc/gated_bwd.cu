@@ -1,0 +1,210 @@
+// gated_bwd.cu -- backward of the soft-mask gated attention (training path).
+//
+// Restates softmask.py:178-217 gated_attention_backward for every unit (kv head) and its G
+// query heads at once, over the paged pool:
+//   z_t   = scale * (k_t . q_g) + log(gate_p)           (t in page p; recomputed, flash-style)
+//   w_t   = exp(z_t - lse_g)
+//   dz_t  = w_t * (v_t . dout_g - dout_g . out_g)
+//   dV_t += w_t * dout_g             dK_t += scale * dz_t * q_g        (summed over g)
+//   dq_g += scale * sum_t dz_t k_t   dgate_p += sum_{g,t} dz_t / gate_p
+// Hard-mode (gate 0) pages carry no weight and are skipped, as the reference.
+//
+// Layout: grid (page groups, units); one warp per page at a time.  The page's K and V rows
+// are staged in warp-private shared memory (padded rows: conflict-free column reads); lanes
+// first own tokens (dot products, softmax weights) then dimensions (coalesced dK / dV row
+// writes and the dq partial).  dq partials are reduced in the CTA and added to global memory
+// with one atomic per (head, dim) per CTA.  f32 throughout (the reference runs float64:
+// parity is to a stated tolerance).  The pass reads K and V once and writes dK and dV once:
+// HBM-bound like the forward.
+#include "common.cuh"
+
+namespace pt {
+
+constexpr int kGBWarps = 4;
+
+struct GatedBwdParams {
+    const void *q;          // [U*G][D] q_dtype
+    const void *k_pool;     // [pages][S][D] kv_dtype
+    const void *v_pool;
+    const int32_t *page_table;  // [U][Pmax]
+    const int32_t *seq_len;     // [U]
+    const float *gates;         // [U][Pmax] gate per logical page (0 = skipped)
+    const float *out;           // [U*G][D] forward output
+    const float *lse;           // [U*G]
+    const float *dout;          // [U*G][D]
+    float *dq;                  // [U*G][D] (accumulated: zero it first)
+    float *dk_pool;             // [pages][S][D] f32
+    float *dv_pool;
+    float *dgates;              // [U][Pmax]
+    int q_dtype, kv_dtype, G, D, S, Pmax;
+    float scale;
+};
+
+template <int DT>
+__device__ __forceinline__ float ld_kv(const void *p, int64_t i) { return load_elem<DT>(p, i); }
+
+template <int DT, int MAXG, int DJ>
+__global__ void __launch_bounds__(kGBWarps * 32) k_gated_bwd(const GatedBwdParams p) {
+    extern __shared__ __align__(16) float gsm[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int D = p.D, S = p.S, G = p.G;
+    const int ld = D + 1;
+    const int64_t u = blockIdx.y;
+    // CTA-shared: q and dout of the unit's G heads, s_g = dout_g . out_g, lse_g
+    float *qs = gsm;                        // [G][D]
+    float *dos = qs + MAXG * D;             // [G][D]
+    float *sg = dos + MAXG * D;             // [G]
+    float *lg = sg + MAXG;                  // [G]
+    float *dqp = lg + MAXG;                 // [G][D] CTA partial of dq
+    float *wbase = dqp + MAXG * D + warp * (2 * S * ld + 2 * MAXG * S);
+    float *ks = wbase;                      // [S][ld]
+    float *vs = ks + S * ld;                // [S][ld]
+    float *wv = vs + S * ld;                // [G][S] softmax weights
+    float *dzv = wv + MAXG * S;             // [G][S]
+    for (int i = threadIdx.x; i < G * D; i += blockDim.x) {
+        const int g = i / D, d = i % D;
+        const int64_t row = (u * G + g) * (int64_t)D + d;
+        qs[g * D + d] = p.q_dtype == PT_F32 ? static_cast<const float *>(p.q)[row]
+                                            : bf16_bits_to_f32(static_cast<const uint16_t *>(p.q)[row]);
+        dos[g * D + d] = p.dout[row];
+        dqp[g * D + d] = 0.f;
+    }
+    __syncthreads();
+    if (warp < G) {  // s_g = dout_g . out_g (warp g)
+        float a = 0.f;
+        for (int d = lane; d < D; d += 32) a += dos[warp * D + d] * p.out[(u * G + warp) * (int64_t)D + d];
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        if (lane == 0) { sg[warp] = a; lg[warp] = p.lse[u * G + warp]; }
+    }
+    __syncthreads();
+    const int n = p.seq_len[u];
+    const int P = (n + S - 1) / S;
+    float dq_acc[MAXG][DJ];
+#pragma unroll
+    for (int g = 0; g < MAXG; g++)
+#pragma unroll
+        for (int j = 0; j < DJ; j++) dq_acc[g][j] = 0.f;
+    for (int lp = blockIdx.x * kGBWarps + warp; lp < P; lp += gridDim.x * kGBWarps) {
+        const float gate = p.gates[u * p.Pmax + lp];
+        if (gate == 0.f) continue;  // hard mode: the page is not attended
+        const float lgate = logf(gate);
+        const int64_t pid = p.page_table[u * p.Pmax + lp];
+        const int rows = min(S, n - lp * S);
+        const int64_t base = pid * S * D;
+        for (int i = lane; i < rows * D; i += 32) {
+            const int t = i / D, d = i % D;
+            ks[t * ld + d] = ld_kv<DT>(p.k_pool, base + i);
+            vs[t * ld + d] = ld_kv<DT>(p.v_pool, base + i);
+        }
+        __syncwarp();
+        // lanes own tokens: logits, weights, dz
+        float dgate = 0.f;
+        for (int t = lane; t < S; t += 32) {
+#pragma unroll
+            for (int g = 0; g < MAXG; g++) {
+                if (g >= G) break;
+                float w = 0.f, dz = 0.f;
+                if (t < rows) {
+                    float kq = 0.f, vd = 0.f;
+                    for (int d = 0; d < D; d++) {
+                        kq = fmaf(ks[t * ld + d], qs[g * D + d], kq);
+                        vd = fmaf(vs[t * ld + d], dos[g * D + d], vd);
+                    }
+                    const float z = kq * p.scale + lgate;
+                    w = expf(z - lg[g]);
+                    dz = w * (vd - sg[g]);
+                    dgate += dz;
+                }
+                wv[g * S + t] = w;
+                dzv[g * S + t] = dz;
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) dgate += __shfl_xor_sync(0xffffffffu, dgate, o);
+        if (lane == 0) p.dgates[u * p.Pmax + lp] = dgate / gate;
+        __syncwarp();
+        // lanes own dims: dK / dV rows (summed over heads), dq partial
+        for (int t = 0; t < rows; t++) {
+#pragma unroll
+            for (int j = 0; j < DJ; j++) {
+                const int d = lane + 32 * j;
+                if (d >= D) break;
+                float dk = 0.f, dv = 0.f;
+#pragma unroll
+                for (int g = 0; g < MAXG; g++) {
+                    if (g >= G) break;
+                    dv = fmaf(wv[g * S + t], dos[g * D + d], dv);
+                    dk = fmaf(dzv[g * S + t], qs[g * D + d], dk);
+                    dq_acc[g][j] = fmaf(dzv[g * S + t], ks[t * ld + d], dq_acc[g][j]);
+                }
+                p.dk_pool[base + (int64_t)t * D + d] = dk * p.scale;
+                p.dv_pool[base + (int64_t)t * D + d] = dv;
+            }
+        }
+        __syncwarp();
+    }
+    // dq: warp partials -> CTA (shared atomics) -> global (one atomic per element per CTA)
+#pragma unroll
+    for (int g = 0; g < MAXG; g++) {
+        if (g >= G) break;
+#pragma unroll
+        for (int j = 0; j < DJ; j++) {
+            const int d = lane + 32 * j;
+            if (d < D) atomicAdd(&dqp[g * D + d], dq_acc[g][j] * p.scale);
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < G * D; i += blockDim.x) {
+        const float v = dqp[i];
+        if (v != 0.f) atomicAdd(&p.dq[(u * G + i / D) * (int64_t)D + i % D], v);
+    }
+}
+
+}  // namespace pt
+
+using namespace pt;
+
+template <int DT, int MAXG, int DJ>
+static int launch_gbwd(const GatedBwdParams &p, int U, size_t smem, cudaStream_t st) {
+    static size_t configured = 0;
+    if (smem > configured) {
+        PT_CUDA_TRY(cudaFuncSetAttribute(k_gated_bwd<DT, MAXG, DJ>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured = smem;
+    }
+    // enough CTAs per unit for ~4 CTAs per SM in total, at least one page per warp
+    int gx = (148 * 4 + U - 1) / U;
+    const int pages = p.Pmax;
+    const int maxgx = (pages + kGBWarps - 1) / kGBWarps;
+    if (gx > maxgx) gx = maxgx;
+    if (gx < 1) gx = 1;
+    k_gated_bwd<DT, MAXG, DJ><<<dim3(gx, U), kGBWarps * 32, smem, st>>>(p);
+    PT_CUDA_TRY(cudaGetLastError());
+    return PT_OK;
+}
+
+extern "C" int pt_gated_attend_bwd(const void *q, int q_dtype, const void *k_pool,
+                                   const void *v_pool, int kv_dtype, const int32_t *page_table,
+                                   const int32_t *seq_len, const float *gates, const float *out,
+                                   const float *lse, const float *dout, int U, int G, int D,
+                                   int S, int Pmax, float scale, float *dq, float *dk_pool,
+                                   float *dv_pool, float *dgates, void *stream) {
+    if (!q || !k_pool || !v_pool || !page_table || !seq_len || !gates || !out || !lse || !dout ||
+        !dq || !dk_pool || !dv_pool || !dgates || U < 0 || G < 1 || D < 1 || S < 1 || Pmax < 1)
+        return PT_ERR_INVALID;
+    if (G > 8 || D > 256 || S > 64) return PT_ERR_UNSUPPORTED;
+    if (U == 0) return PT_OK;
+    GatedBwdParams p{q, k_pool, v_pool, page_table, seq_len, gates, out, lse, dout, dq, dk_pool,
+                     dv_pool, dgates, q_dtype, kv_dtype, G, D, S, Pmax, scale};
+    const int MAXG = 8;
+    const size_t smem = ((size_t)(2 * MAXG * D + 2 * MAXG + MAXG * D) +
+                         (size_t)kGBWarps * (2 * S * (D + 1) + 2 * MAXG * S)) * 4;
+    if (smem > 220 * 1024) return PT_ERR_UNSUPPORTED;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int dj = (D + 31) / 32;
+#define PT_GB(DT_, DJ_) \
+    if (kv_dtype == DT_ && dj == DJ_) return launch_gbwd<DT_, 8, DJ_>(p, U, smem, st);
+    PT_GB(PT_F32, 1) PT_GB(PT_F32, 2) PT_GB(PT_F32, 4) PT_GB(PT_F32, 8)
+    PT_GB(PT_BF16, 1) PT_GB(PT_BF16, 2) PT_GB(PT_BF16, 4) PT_GB(PT_BF16, 8)
+#undef PT_GB
+    return PT_ERR_UNSUPPORTED;
+}

@@ -582,3 +582,74 @@ def test_recall_units_workload_planted_pages_found(cuda):
     sel_hits = 0
     for u in range(8):
         assert 0.0 <= rep["unique"][u].page_recall <= 1.0
+
+
+def test_softmask_train_step_matches_reference(cuda):
+    """The gated decode training step (soft and hard mode; forward = K4 with log-gate biases,
+    backward = pt_gated_attend_bwd) against the reference's float64 decode_train_step on its
+    own seeded workloads (tests/golden/softmask_golden.npz, tests/golden/make_softmask_golden.py).
+    Tolerance: the kernels run f32 where the reference runs float64 -- outputs and loss to
+    2e-5 relative, gradients to 2e-4 of their largest magnitude."""
+    import os
+
+    pt = _pt()
+    from paper_2605_27740_b200 import softmask as sm
+
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "softmask_golden.npz"))
+    n_cases = len([f for f in z.files if f.endswith("_spec")])
+
+    def close(a, b, rel=2e-4):
+        a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+        scale = max(float(np.abs(b).max()) if b.size else 0.0, 1e-12)
+        np.testing.assert_allclose(a, b, rtol=0, atol=rel * scale)
+
+    for i in range(n_cases):
+        seed, n, d, s, hq, hkv, k = (int(x) for x in z[f"c{i}_spec"])
+        tau, hard, std = z[f"c{i}_cfg"]
+        cfg = sm.GateConfig(k=k, tau=float(tau), mode="hard" if hard else "soft", standardize=bool(std))
+        P = -(-n // s)
+        layout = pt.CacheLayout(num_kv_heads=hkv, head_dim=d, page_size=s, max_pages=hkv * P)
+        cache = pt.PagedKvCache(layout, batch=1, dtype=torch.float32, max_pages_per_head=P)
+        K = np.stack([z[f"c{i}_k{h}"] for h in range(hkv)])
+        V = np.stack([z[f"c{i}_v{h}"] for h in range(hkv)])
+        cache.extend_units(torch.from_numpy(K), torch.from_numpy(V))
+        r = sm.decode_train_step(cache, z[f"c{i}_q"], cfg, z[f"c{i}_target"])
+        assert r.loss == pytest.approx(float(z[f"c{i}_loss"]), rel=2e-5), i
+        close(np.stack([o.out for o in r.outputs]), z[f"c{i}_out"], 2e-5)
+        close(np.array([o.lse for o in r.outputs]), z[f"c{i}_lse"], 2e-5)
+        close(r.d_queries, z[f"c{i}_dq"])
+        for h in range(hkv):
+            np.testing.assert_allclose(r.gates[h], z[f"c{i}_gates{h}"], rtol=1e-9, atol=1e-300)
+            close(r.d_keys[h], z[f"c{i}_dk{h}"])
+            close(r.d_values[h], z[f"c{i}_dv{h}"])
+            close(r.d_scores[h], z[f"c{i}_ds{h}"])
+            close(r.d_means[h], z[f"c{i}_dm{h}"])
+            close(r.d_stds[h], z[f"c{i}_dstd{h}"])
+
+
+def test_gated_attention_single_query_api(cuda, oracle):
+    """The reference's single-query gated_attention_forward/backward signature on the device:
+    gates of 1 reproduce plain attention (oracle), and the backward's d_gates obey
+    d_gates_p * g_p = sum_t dz_t (finite-difference check of one gate)."""
+    from paper_2605_27740_b200 import softmask as sm
+
+    rng = np.random.default_rng(8)
+    d, s, P = 32, 8, 9
+    keys = [rng.standard_normal((s if p < P - 1 else 5, d)).astype(np.float32) for p in range(P)]
+    vals = [rng.standard_normal(kp.shape).astype(np.float32) for kp in keys]
+    q = rng.standard_normal(d).astype(np.float32)
+    ones = np.ones(P)
+    out, tape = sm.gated_attention_forward(q, keys, vals, ones)
+    o_ref, l_ref = oracle.stream_attention(q, np.concatenate(keys), np.concatenate(vals),
+                                           1.0 / math.sqrt(d), s, np.zeros(P, np.float32))
+    np.testing.assert_allclose(out.out, o_ref, rtol=1e-5, atol=1e-6)
+    gates = rng.uniform(0.2, 1.0, P)
+    out, tape = sm.gated_attention_forward(q, keys, vals, gates)
+    d_out = rng.standard_normal(d)
+    grads = sm.gated_attention_backward(tape, d_out)
+    eps = 1e-3
+    g2 = gates.copy()
+    g2[3] += eps
+    out2, _ = sm.gated_attention_forward(q, keys, vals, g2)
+    fd = float(d_out @ (out2.out - out.out)) / eps
+    assert fd == pytest.approx(grads.d_gates[3], rel=2e-2, abs=1e-4)
