@@ -91,32 +91,46 @@ __global__ void __launch_bounds__(kGBWarps * 32) k_gated_bwd(const GatedBwdParam
         const int64_t pid = p.page_table[u * p.Pmax + lp];
         const int rows = min(S, n - lp * S);
         const int64_t base = pid * S * D;
-        for (int i = lane; i < rows * D; i += 32) {
-            const int t = i / D, d = i % D;
-            ks[t * ld + d] = ld_kv<DT>(p.k_pool, base + i);
-            vs[t * ld + d] = ld_kv<DT>(p.v_pool, base + i);
-        }
+        constexpr int ES = DT == PT_F32 ? 4 : 2;
+        // one round of 16-byte loads per tensor (all of a lane's loads in flight first)
+        stage_rows_f32<DT, 8>(ks, ld, static_cast<const char *>(p.k_pool) + base * ES, rows * D, D, lane, 32);
+        stage_rows_f32<DT, 8>(vs, ld, static_cast<const char *>(p.v_pool) + base * ES, rows * D, D, lane, 32);
         __syncwarp();
-        // lanes own tokens: logits, weights, dz
+        // lanes own (token, dimension slice): LPT lanes per token split D, shuffle-reduced
+        const int lpt = S >= 32 ? 1 : 32 / S;      // lanes per token
+        const int part = lane % lpt, dlen = D / lpt;
         float dgate = 0.f;
-        for (int t = lane; t < S; t += 32) {
+        for (int t0 = 0; t0 < S; t0 += 32 / lpt) {
+            const int t = t0 + lane / lpt;
+            const bool live = t < rows;
 #pragma unroll
             for (int g = 0; g < MAXG; g++) {
                 if (g >= G) break;
-                float w = 0.f, dz = 0.f;
-                if (t < rows) {
-                    float kq = 0.f, vd = 0.f;
-                    for (int d = 0; d < D; d++) {
-                        kq = fmaf(ks[t * ld + d], qs[g * D + d], kq);
-                        vd = fmaf(vs[t * ld + d], dos[g * D + d], vd);
+                float kq = 0.f, vd = 0.f;
+                if (live) {
+                    const float *kr = ks + t * ld + part * dlen;
+                    const float *vr = vs + t * ld + part * dlen;
+                    const float *qg = qs + g * D + part * dlen;
+                    const float *dg = dos + g * D + part * dlen;
+                    for (int d = 0; d < dlen; d++) {
+                        kq = fmaf(kr[d], qg[d], kq);
+                        vd = fmaf(vr[d], dg[d], vd);
                     }
-                    const float z = kq * p.scale + lgate;
-                    w = expf(z - lg[g]);
+                }
+                for (int o = 1; o < lpt; o <<= 1) {
+                    kq += __shfl_xor_sync(0xffffffffu, kq, o);
+                    vd += __shfl_xor_sync(0xffffffffu, vd, o);
+                }
+                float w = 0.f, dz = 0.f;
+                if (live) {
+                    w = expf(kq * p.scale + lgate - lg[g]);
                     dz = w * (vd - sg[g]);
+                }
+                if (part == 0 && t < S) {
+                    wv[g * S + t] = w;
+                    dzv[g * S + t] = dz;
                     dgate += dz;
                 }
-                wv[g * S + t] = w;
-                dzv[g * S + t] = dz;
             }
         }
         for (int o = 16; o > 0; o >>= 1) dgate += __shfl_xor_sync(0xffffffffu, dgate, o);
@@ -191,7 +205,7 @@ extern "C" int pt_gated_attend_bwd(const void *q, int q_dtype, const void *k_poo
     if (!q || !k_pool || !v_pool || !page_table || !seq_len || !gates || !out || !lse || !dout ||
         !dq || !dk_pool || !dv_pool || !dgates || U < 0 || G < 1 || D < 1 || S < 1 || Pmax < 1)
         return PT_ERR_INVALID;
-    if (G > 8 || D > 256 || S > 64) return PT_ERR_UNSUPPORTED;
+    if (G > 8 || D > 256 || S > 64 || (S < 32 && (32 % S || D % (32 / S)))) return PT_ERR_UNSUPPORTED;
     if (U == 0) return PT_OK;
     GatedBwdParams p{q, k_pool, v_pool, page_table, seq_len, gates, out, lse, dout, dq, dk_pool,
                      dv_pool, dgates, q_dtype, kv_dtype, G, D, S, Pmax, scale};

@@ -144,21 +144,20 @@ def gated_forward(cache: PagedKvCache, queries: torch.Tensor, gates, scale: floa
     if scale is None:
         scale = 1.0 / math.sqrt(D)
     g64 = gates if isinstance(gates, torch.Tensor) and gates.dim() == 2 else _gates_tensor(cache, gates)
-    for u in range(U):
-        P = cache.num_pages(u)
-        if P == 0:
-            raise ValueError("attention over an empty context is undefined")
-        gu = g64[u, :P]
-        if mode == "soft":
-            if bool(((gu <= 0) | (gu > 1)).any()):
-                raise ValueError("soft gates must lie in (0, 1]")
-        elif mode == "hard":
-            if not bool(((gu == 0) | (gu == 1)).all()):
-                raise ValueError("hard gates must be binary")
-            if not bool((gu == 1).any()):
-                raise ValueError("hard mask keeps no pages")
-        else:
-            raise ValueError(f"unknown gate mode {mode!r}")
+    pages = torch.as_tensor(np.array([cache.num_pages(u) for u in range(U)]), device=cache.device)
+    if bool((pages == 0).any()):
+        raise ValueError("attention over an empty context is undefined")
+    live = torch.arange(cache.Pmax, device=cache.device)[None, :] < pages[:, None]
+    if mode == "soft":  # one device reduction for every unit (no per-unit host sync)
+        if bool((((g64 <= 0) | (g64 > 1)) & live).any()):
+            raise ValueError("soft gates must lie in (0, 1]")
+    elif mode == "hard":
+        if bool((((g64 != 0) & (g64 != 1)) & live).any()):
+            raise ValueError("hard gates must be binary")
+        if bool((((g64 == 1) & live).sum(dim=1) == 0).any()):
+            raise ValueError("hard mask keeps no pages")
+    else:
+        raise ValueError(f"unknown gate mode {mode!r}")
     out = torch.empty(U * G, D, dtype=torch.float32, device=cache.device)
     lse = torch.empty(U * G, dtype=torch.float32, device=cache.device)
     ws = torch.empty(_lib.load().pt_attend_workspace_bytes(U, G, D, cache.Pmax), dtype=torch.uint8,
