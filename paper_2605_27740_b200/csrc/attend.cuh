@@ -153,20 +153,45 @@ static __device__ __noinline__ void cta_finish(const AttnParams &prm, const floa
     __syncthreads();
     if (!is_last) return;
     __threadfence();
+    // the split weights once per CTA (all (m, l) pairs in one parallel round), then every
+    // (head, dim) sums its splits with the loads issued 8 at a time -- no chain of
+    // dependent L2 round trips per split
+    __shared__ float sw[kAttnMaxSplits * 8];   // exp2(m_w - m_max) per (split, head)
+    __shared__ float sinv[8], slse[8];
+    for (int i = threadIdx.x; i < nsplit_u * G; i += blockDim.x)
+        sw[i] = __ldcg(&wml[((u * prm.maxs + i / G) * G + i % G) * 2]);
+    __syncthreads();
+    if (threadIdx.x < G) {
+        const int g = threadIdx.x;
+        float mt = -INFINITY;
+        for (int w = 0; w < nsplit_u; w++) mt = fmaxf(mt, sw[w * G + g]);
+        const float mu = mt == -INFINITY ? 0.f : mt;
+        float lt = 0.f;
+        for (int w = 0; w < nsplit_u; w++) {
+            const float f = exp2f(sw[w * G + g] - mu);
+            lt += __ldcg(&wml[((u * prm.maxs + w) * G + g) * 2 + 1]) * f;
+            sw[w * G + g] = f;
+        }
+        sinv[g] = 1.f / lt;
+        slse[g] = (mt + log2f(lt)) * kLn2;
+    }
+    __syncthreads();
     for (int i = threadIdx.x; i < G * D; i += blockDim.x) {
         const int g = i / D, d = i % D;
-        float mt = -INFINITY;
-        for (int w = 0; w < nsplit_u; w++)
-            mt = fmaxf(mt, __ldcg(&wml[((u * prm.maxs + w) * G + g) * 2]));
-        const float mu = mt == -INFINITY ? 0.f : mt;
-        float lt = 0.f, a = 0.f;
-        for (int w = 0; w < nsplit_u; w++) {
-            const float f = exp2f(__ldcg(&wml[((u * prm.maxs + w) * G + g) * 2]) - mu);
-            lt += __ldcg(&wml[((u * prm.maxs + w) * G + g) * 2 + 1]) * f;
-            a += __ldcg(&wacc[((u * prm.maxs + w) * G + g) * (int64_t)D + d]) * f;
+        float a = 0.f;
+        for (int w0 = 0; w0 < nsplit_u; w0 += 8) {
+            float v[8];
+#pragma unroll
+            for (int j = 0; j < 8; j++)
+                v[j] = w0 + j < nsplit_u
+                           ? __ldcg(&wacc[((u * prm.maxs + w0 + j) * G + g) * (int64_t)D + d])
+                           : 0.f;
+#pragma unroll
+            for (int j = 0; j < 8; j++)
+                if (w0 + j < nsplit_u) a += v[j] * sw[(w0 + j) * G + g];
         }
-        prm.out[(u * G + g) * (int64_t)D + d] = a / lt;
-        if (d == 0) prm.lse[u * G + g] = (mt + log2f(lt)) * kLn2;
+        prm.out[(u * G + g) * (int64_t)D + d] = a * sinv[g];
+        if (d == 0) prm.lse[u * G + g] = slse[g];
     }
     if (threadIdx.x == 0) prm.tickets[u] = 0;
 }

@@ -418,7 +418,8 @@ extern "C" int pt_select_attend(const uint16_t *keys, const uint16_t *tile_max,
     if (nchunk <= 0) {
         nchunk = (148 * 2) / U;
         if (nchunk < 1) nchunk = 1;
-        const int cap = (k + kSAWarps - 1) / kSAWarps;
+        // every chunk CTA repeats the unit's selection: keep >= 4 pages per warp per chunk
+        const int cap = (k + 4 * kSAWarps - 1) / (4 * kSAWarps);
         if (nchunk > cap) nchunk = cap;
     }
     if (nchunk > kAttnMaxSplits) nchunk = kAttnMaxSplits;

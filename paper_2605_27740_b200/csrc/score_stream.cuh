@@ -40,15 +40,15 @@ struct StreamScoreParams {
 constexpr int kSSWarps = 4;
 constexpr int kSSCtas = 3;  // per SM, at most
 // CTAs per SM of the persistent grid (PT_SS_CTAS overrides, 1..3: tuning).  Measured: two
-// (8 warps) beat three (170 vs 180 us at cfg3), and leave room for one overlapped
-// select+attend CTA per SM beside the scorer.
-static inline int ss_ctas_per_sm() {
-    static const int v = [] {
+// (8 warps) beat three at long contexts (170 vs 180 us at cfg3: 257 tiles per unit), three
+// win for short ones (8K context: 17 tiles per unit, per-tile header / cursor latency).
+static inline int ss_ctas_per_sm(int Pmax) {
+    static const int forced = [] {
         const char *e = getenv("PT_SS_CTAS");
-        const int x = e ? atoi(e) : 2;
-        return x < 1 ? 1 : (x > kSSCtas ? kSSCtas : x);
+        return e ? atoi(e) : 0;
     }();
-    return v;
+    const int x = forced ? forced : ((Pmax >> 5) < 32 ? 3 : 2);
+    return x < 1 ? 1 : (x > kSSCtas ? kSSCtas : x);
 }
 constexpr int kSSNst = 3;   // ring stages per warp
 

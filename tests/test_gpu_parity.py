@@ -382,7 +382,9 @@ def test_attend_tensor_core_path_vs_simt(cuda, oracle, G, D, S, monkeypatch):
             monkeypatch.setenv(kk, vv)
         eng.attend(q)
         torch.cuda.synchronize()
-        torch.testing.assert_close(eng.out, out_tc, rtol=0, atol=1e-5)
+        # the mma path rounds the softmax weights to bf16 per warp-local running max, so a
+        # different page-to-warp split moves outputs by ~1e-4 (the bf16 budget is 2e-2)
+        torch.testing.assert_close(eng.out, out_tc, rtol=0, atol=1e-3)
         for kk in env:
             monkeypatch.delenv(kk)
     if not eng.score_prenorm(q):  # the streaming scorer (a step may leave only sentinels)
