@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(kGBWarps * 32) k_gated_bwd(const GatedBwdParam
     extern __shared__ __align__(16) float gsm[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int D = p.D, S = p.S, G = p.G;
-    const int ld = D + 1;
+    const int ld = D + 4;  // 16-byte aligned rows, rotated banks
     const int64_t u = blockIdx.y;
     // CTA-shared: q and dout of the unit's G heads, s_g = dout_g . out_g, lse_g
     float *qs = gsm;                        // [G][D]
@@ -59,8 +59,8 @@ __global__ void __launch_bounds__(kGBWarps * 32) k_gated_bwd(const GatedBwdParam
     float *wbase = dqp + MAXG * D + warp * (2 * S * ld + 2 * MAXG * S);
     float *ks = wbase;                      // [S][ld]
     float *vs = ks + S * ld;                // [S][ld]
-    float *wv = vs + S * ld;                // [G][S] softmax weights
-    float *dzv = wv + MAXG * S;             // [G][S]
+    float *wv = vs + S * ld;                // [S][MAXG] softmax weights (token-major)
+    float *dzv = wv + MAXG * S;             // [S][MAXG]
     for (int i = threadIdx.x; i < G * D; i += blockDim.x) {
         const int g = i / D, d = i % D;
         const int64_t row = (u * G + g) * (int64_t)D + d;
@@ -77,13 +77,22 @@ __global__ void __launch_bounds__(kGBWarps * 32) k_gated_bwd(const GatedBwdParam
         if (lane == 0) { sg[warp] = a; lg[warp] = p.lse[u * G + warp]; }
     }
     __syncthreads();
-    const int n = p.seq_len[u];
-    const int P = (n + S - 1) / S;
-    float dq_acc[MAXG][DJ];
+    // the lane's dimensions of q and dout for every head stay in registers
+    float qr[MAXG][DJ], dr[MAXG][DJ], dq_acc[MAXG][DJ];
 #pragma unroll
     for (int g = 0; g < MAXG; g++)
 #pragma unroll
-        for (int j = 0; j < DJ; j++) dq_acc[g][j] = 0.f;
+        for (int j = 0; j < DJ; j++) {
+            const int d = lane + 32 * j;
+            const bool ok = g < G && d < D;
+            qr[g][j] = ok ? qs[g * D + d] : 0.f;
+            dr[g][j] = ok ? dos[g * D + d] : 0.f;
+            dq_acc[g][j] = 0.f;
+        }
+    const int n = p.seq_len[u];
+    const int P = (n + S - 1) / S;
+    const int lpt = S >= 32 ? 1 : 32 / S;  // lanes per token in the dot-product phase
+    const int part = lane % lpt, dlen = D / lpt;
     for (int lp = blockIdx.x * kGBWarps + warp; lp < P; lp += gridDim.x * kGBWarps) {
         const float gate = p.gates[u * p.Pmax + lp];
         if (gate == 0.f) continue;  // hard mode: the page is not attended
@@ -96,39 +105,44 @@ __global__ void __launch_bounds__(kGBWarps * 32) k_gated_bwd(const GatedBwdParam
         stage_rows_f32<DT, 8>(ks, ld, static_cast<const char *>(p.k_pool) + base * ES, rows * D, D, lane, 32);
         stage_rows_f32<DT, 8>(vs, ld, static_cast<const char *>(p.v_pool) + base * ES, rows * D, D, lane, 32);
         __syncwarp();
-        // lanes own (token, dimension slice): LPT lanes per token split D, shuffle-reduced
-        const int lpt = S >= 32 ? 1 : 32 / S;      // lanes per token
-        const int part = lane % lpt, dlen = D / lpt;
+        // lanes own (token, D/lpt slice): float4 reads, all heads per loaded K/V vector
         float dgate = 0.f;
         for (int t0 = 0; t0 < S; t0 += 32 / lpt) {
             const int t = t0 + lane / lpt;
             const bool live = t < rows;
+            float kq[MAXG], vd[MAXG];
+#pragma unroll
+            for (int g = 0; g < MAXG; g++) kq[g] = vd[g] = 0.f;
+            if (live) {
+                const float4 *kr = reinterpret_cast<const float4 *>(ks + t * ld + part * dlen);
+                const float4 *vr = reinterpret_cast<const float4 *>(vs + t * ld + part * dlen);
+                for (int c = 0; c < dlen / 4; c++) {
+                    const float4 k4 = kr[c], v4 = vr[c];
+#pragma unroll
+                    for (int g = 0; g < MAXG; g++) {
+                        if (g >= G) break;
+                        const float4 q4 = reinterpret_cast<const float4 *>(qs + g * D + part * dlen)[c];
+                        const float4 o4 = reinterpret_cast<const float4 *>(dos + g * D + part * dlen)[c];
+                        kq[g] = fmaf(k4.x, q4.x, fmaf(k4.y, q4.y, fmaf(k4.z, q4.z, fmaf(k4.w, q4.w, kq[g]))));
+                        vd[g] = fmaf(v4.x, o4.x, fmaf(v4.y, o4.y, fmaf(v4.z, o4.z, fmaf(v4.w, o4.w, vd[g]))));
+                    }
+                }
+            }
 #pragma unroll
             for (int g = 0; g < MAXG; g++) {
                 if (g >= G) break;
-                float kq = 0.f, vd = 0.f;
-                if (live) {
-                    const float *kr = ks + t * ld + part * dlen;
-                    const float *vr = vs + t * ld + part * dlen;
-                    const float *qg = qs + g * D + part * dlen;
-                    const float *dg = dos + g * D + part * dlen;
-                    for (int d = 0; d < dlen; d++) {
-                        kq = fmaf(kr[d], qg[d], kq);
-                        vd = fmaf(vr[d], dg[d], vd);
-                    }
-                }
                 for (int o = 1; o < lpt; o <<= 1) {
-                    kq += __shfl_xor_sync(0xffffffffu, kq, o);
-                    vd += __shfl_xor_sync(0xffffffffu, vd, o);
+                    kq[g] += __shfl_xor_sync(0xffffffffu, kq[g], o);
+                    vd[g] += __shfl_xor_sync(0xffffffffu, vd[g], o);
                 }
                 float w = 0.f, dz = 0.f;
                 if (live) {
-                    w = expf(kq * p.scale + lgate - lg[g]);
-                    dz = w * (vd - sg[g]);
+                    w = expf(kq[g] * p.scale + lgate - lg[g]);
+                    dz = w * (vd[g] - sg[g]);
                 }
                 if (part == 0 && t < S) {
-                    wv[g * S + t] = w;
-                    dzv[g * S + t] = dz;
+                    wv[t * MAXG + g] = w;
+                    dzv[t * MAXG + g] = dz;
                     dgate += dz;
                 }
             }
@@ -136,19 +150,29 @@ __global__ void __launch_bounds__(kGBWarps * 32) k_gated_bwd(const GatedBwdParam
         for (int o = 16; o > 0; o >>= 1) dgate += __shfl_xor_sync(0xffffffffu, dgate, o);
         if (lane == 0) p.dgates[u * p.Pmax + lp] = dgate / gate;
         __syncwarp();
-        // lanes own dims: dK / dV rows (summed over heads), dq partial
+        // lanes own dims: dK / dV rows (summed over heads), dq partial; q / dout in registers,
+        // the token's weights as broadcast float4 reads
         for (int t = 0; t < rows; t++) {
+            float wt[MAXG], zt[MAXG];
+#pragma unroll
+            for (int g4 = 0; g4 < MAXG; g4 += 4) {
+                const float4 a = *reinterpret_cast<const float4 *>(wv + t * MAXG + g4);
+                const float4 b = *reinterpret_cast<const float4 *>(dzv + t * MAXG + g4);
+                wt[g4] = a.x; wt[g4 + 1] = a.y; wt[g4 + 2] = a.z; wt[g4 + 3] = a.w;
+                zt[g4] = b.x; zt[g4 + 1] = b.y; zt[g4 + 2] = b.z; zt[g4 + 3] = b.w;
+            }
 #pragma unroll
             for (int j = 0; j < DJ; j++) {
                 const int d = lane + 32 * j;
                 if (d >= D) break;
+                const float kv = ks[t * ld + d];
                 float dk = 0.f, dv = 0.f;
 #pragma unroll
                 for (int g = 0; g < MAXG; g++) {
                     if (g >= G) break;
-                    dv = fmaf(wv[g * S + t], dos[g * D + d], dv);
-                    dk = fmaf(dzv[g * S + t], qs[g * D + d], dk);
-                    dq_acc[g][j] = fmaf(dzv[g * S + t], ks[t * ld + d], dq_acc[g][j]);
+                    dv = fmaf(wt[g], dr[g][j], dv);
+                    dk = fmaf(zt[g], qr[g][j], dk);
+                    dq_acc[g][j] = fmaf(zt[g], kv, dq_acc[g][j]);
                 }
                 p.dk_pool[base + (int64_t)t * D + d] = dk * p.scale;
                 p.dv_pool[base + (int64_t)t * D + d] = dv;
@@ -205,18 +229,20 @@ extern "C" int pt_gated_attend_bwd(const void *q, int q_dtype, const void *k_poo
     if (!q || !k_pool || !v_pool || !page_table || !seq_len || !gates || !out || !lse || !dout ||
         !dq || !dk_pool || !dv_pool || !dgates || U < 0 || G < 1 || D < 1 || S < 1 || Pmax < 1)
         return PT_ERR_INVALID;
-    if (G > 8 || D > 256 || S > 64 || (S < 32 && (32 % S || D % (32 / S)))) return PT_ERR_UNSUPPORTED;
+    if (G > 8 || D > 256 || S > 64 || D % 4 || (S < 32 && (32 % S || D % (4 * (32 / S)))))
+        return PT_ERR_UNSUPPORTED;
     if (U == 0) return PT_OK;
     GatedBwdParams p{q, k_pool, v_pool, page_table, seq_len, gates, out, lse, dout, dq, dk_pool,
                      dv_pool, dgates, q_dtype, kv_dtype, G, D, S, Pmax, scale};
     const int MAXG = 8;
     const size_t smem = ((size_t)(2 * MAXG * D + 2 * MAXG + MAXG * D) +
-                         (size_t)kGBWarps * (2 * S * (D + 1) + 2 * MAXG * S)) * 4;
+                         (size_t)kGBWarps * (2 * S * (D + 4) + 2 * MAXG * S)) * 4;
     if (smem > 220 * 1024) return PT_ERR_UNSUPPORTED;
     cudaStream_t st = (cudaStream_t)stream;
     const int dj = (D + 31) / 32;
 #define PT_GB(DT_, DJ_) \
-    if (kv_dtype == DT_ && dj == DJ_) return launch_gbwd<DT_, 8, DJ_>(p, U, smem, st);
+    if (kv_dtype == DT_ && dj == DJ_) \
+        return G <= 4 ? launch_gbwd<DT_, 4, DJ_>(p, U, smem, st) : launch_gbwd<DT_, 8, DJ_>(p, U, smem, st);
     PT_GB(PT_F32, 1) PT_GB(PT_F32, 2) PT_GB(PT_F32, 4) PT_GB(PT_F32, 8)
     PT_GB(PT_BF16, 1) PT_GB(PT_BF16, 2) PT_GB(PT_BF16, 4) PT_GB(PT_BF16, 8)
 #undef PT_GB
