@@ -446,7 +446,8 @@ def test_fused_score_select_equals_two_launches(cuda, lens, k, fused):
     (2, 2, 2, 128, 64, [200 * 64 + 1], 8),                                # S=64
     (80, 8, 4, 128, 16, [100 * 16 - 3], 16),                              # warp-per-unit path
     (40, 16, 1, 64, 32, [60 * 32 + 7], 16),                               # warp path, cfg4 heads
-])
+    (1, 2, 4, 128, 16, [20000 * 16 + 3], 2500),                           # k > candidate cap:
+])                                                                        # bisection + all-keys
 @pytest.mark.parametrize("force_warp", [False, True])
 def test_select_attend_equals_two_launches(cuda, oracle, B, H, G, D, S, lens, k, force_warp,
                                            monkeypatch):
