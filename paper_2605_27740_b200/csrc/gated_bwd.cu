@@ -40,27 +40,41 @@ struct GatedBwdParams {
     float scale;
 };
 
-template <int DT>
-__device__ __forceinline__ float ld_kv(const void *p, int64_t i) { return load_elem<DT>(p, i); }
+__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
+// raw staged element -> f32
+template <int DT>
+__device__ __forceinline__ float rawval(const char *row, int d) {
+    if constexpr (DT == PT_F32) return reinterpret_cast<const float *>(row)[d];
+    else return bf16_bits_to_f32(reinterpret_cast<const uint16_t *>(row)[d]);
+}
+
+// Double-buffered: while a warp computes page i, its next page's K and V rows are already
+// in flight (cp.async, 16 B, raw storage format, padded rows); skipped (hard-masked) pages
+// and the unused rows of a partial page get zero dK / dV, so the pools need no zero fill.
 template <int DT, int MAXG, int DJ>
 __global__ void __launch_bounds__(kGBWarps * 32) k_gated_bwd(const GatedBwdParams p) {
+    constexpr int ES = DT == PT_F32 ? 4 : 2;
+    constexpr int EPV = 16 / ES;  // elements per 16-byte vector
     extern __shared__ __align__(16) float gsm[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int D = p.D, S = p.S, G = p.G;
-    const int ld = D + 4;  // 16-byte aligned rows, rotated banks
     const int64_t u = blockIdx.y;
-    // CTA-shared: q and dout of the unit's G heads, s_g = dout_g . out_g, lse_g
-    float *qs = gsm;                        // [G][D]
-    float *dos = qs + MAXG * D;             // [G][D]
-    float *sg = dos + MAXG * D;             // [G]
-    float *lg = sg + MAXG;                  // [G]
-    float *dqp = lg + MAXG;                 // [G][D] CTA partial of dq
-    float *wbase = dqp + MAXG * D + warp * (2 * S * ld + 2 * MAXG * S);
-    float *ks = wbase;                      // [S][ld]
-    float *vs = ks + S * ld;                // [S][ld]
-    float *wv = vs + S * ld;                // [S][MAXG] softmax weights (token-major)
-    float *dzv = wv + MAXG * S;             // [S][MAXG]
+    float *qs = gsm;                        // [MAXG][D]
+    float *dos = qs + MAXG * D;             // [MAXG][D]
+    float *sg = dos + MAXG * D;             // [8]
+    float *lg = sg + 8;                     // [8]
+    float *dqp = lg + 8;                    // [MAXG][D] CTA partial of dq
+    const int rowb = D * ES + 16;           // padded row (bytes)
+    const int pageb = S * rowb;
+    char *wb = reinterpret_cast<char *>(dqp + MAXG * D) + (size_t)warp * (4 * pageb + 2 * MAXG * S * 4);
+    float *wv = reinterpret_cast<float *>(wb + 4 * pageb);  // [S][MAXG]
+    float *dzv = wv + MAXG * S;                              // [S][MAXG]
     for (int i = threadIdx.x; i < G * D; i += blockDim.x) {
         const int g = i / D, d = i % D;
         const int64_t row = (u * G + g) * (int64_t)D + d;
@@ -77,7 +91,6 @@ __global__ void __launch_bounds__(kGBWarps * 32) k_gated_bwd(const GatedBwdParam
         if (lane == 0) { sg[warp] = a; lg[warp] = p.lse[u * G + warp]; }
     }
     __syncthreads();
-    // the lane's dimensions of q and dout for every head stay in registers
     float qr[MAXG][DJ], dr[MAXG][DJ], dq_acc[MAXG][DJ];
 #pragma unroll
     for (int g = 0; g < MAXG; g++)
@@ -91,21 +104,49 @@ __global__ void __launch_bounds__(kGBWarps * 32) k_gated_bwd(const GatedBwdParam
         }
     const int n = p.seq_len[u];
     const int P = (n + S - 1) / S;
-    const int lpt = S >= 32 ? 1 : 32 / S;  // lanes per token in the dot-product phase
+    // lanes per token in the dot-product phase: split a row into whole 16-byte vectors
+    int lpt = S >= 32 ? 1 : 32 / S;
+    while (lpt > 1 && (D / lpt) % EPV) lpt >>= 1;
     const int part = lane % lpt, dlen = D / lpt;
-    for (int lp = blockIdx.x * kGBWarps + warp; lp < P; lp += gridDim.x * kGBWarps) {
+    const int vpr = D * ES / 16;           // 16-byte vectors per row
+    const int stride = gridDim.x * kGBWarps;
+    auto issue = [&](int lp, int b) {      // page lp -> buffer b (nothing for a skipped page)
+        if (lp < P && p.gates[u * p.Pmax + lp] != 0.f) {
+            const int64_t pid = p.page_table[u * p.Pmax + lp];
+            const int rows = min(S, n - lp * S);
+            const char *kg = static_cast<const char *>(p.k_pool) + pid * S * D * ES;
+            const char *vg = static_cast<const char *>(p.v_pool) + pid * S * D * ES;
+            char *kb = wb + b * 2 * pageb, *vb = kb + pageb;
+            for (int i = lane; i < rows * vpr; i += 32) {
+                const int r = i / vpr, c = i - r * vpr;
+                cp_async16(kb + r * rowb + c * 16, kg + (int64_t)i * 16);
+                cp_async16(vb + r * rowb + c * 16, vg + (int64_t)i * 16);
+            }
+        }
+        cp_async_commit();  // (possibly empty) one group per page keeps the accounting uniform
+    };
+    int lp = blockIdx.x * kGBWarps + warp;
+    issue(lp, 0);
+    for (int it = 0; lp < P; it++, lp += stride) {
+        issue(lp + stride, (it + 1) & 1);
+        cp_async_wait1();  // this page's group has landed (the next one may be in flight)
+        __syncwarp();
         const float gate = p.gates[u * p.Pmax + lp];
-        if (gate == 0.f) continue;  // hard mode: the page is not attended
-        const float lgate = logf(gate);
         const int64_t pid = p.page_table[u * p.Pmax + lp];
         const int rows = min(S, n - lp * S);
         const int64_t base = pid * S * D;
-        constexpr int ES = DT == PT_F32 ? 4 : 2;
-        // one round of 16-byte loads per tensor (all of a lane's loads in flight first)
-        stage_rows_f32<DT, 8>(ks, ld, static_cast<const char *>(p.k_pool) + base * ES, rows * D, D, lane, 32);
-        stage_rows_f32<DT, 8>(vs, ld, static_cast<const char *>(p.v_pool) + base * ES, rows * D, D, lane, 32);
-        __syncwarp();
-        // lanes own (token, D/lpt slice): float4 reads, all heads per loaded K/V vector
+        if (gate == 0.f) {  // hard-masked: no weight, no gradient
+            for (int i = lane; i < S * D; i += 32) {
+                p.dk_pool[base + i] = 0.f;
+                p.dv_pool[base + i] = 0.f;
+            }
+            if (lane == 0) p.dgates[u * p.Pmax + lp] = 0.f;
+            __syncwarp();
+            continue;
+        }
+        const float lgate = logf(gate);
+        const char *kb = wb + (it & 1) * 2 * pageb, *vb = kb + pageb;
+        // lanes own (token, D/lpt slice): 16-byte raw vectors, all heads per vector
         float dgate = 0.f;
         for (int t0 = 0; t0 < S; t0 += 32 / lpt) {
             const int t = t0 + lane / lpt;
@@ -114,17 +155,36 @@ __global__ void __launch_bounds__(kGBWarps * 32) k_gated_bwd(const GatedBwdParam
 #pragma unroll
             for (int g = 0; g < MAXG; g++) kq[g] = vd[g] = 0.f;
             if (live) {
-                const float4 *kr = reinterpret_cast<const float4 *>(ks + t * ld + part * dlen);
-                const float4 *vr = reinterpret_cast<const float4 *>(vs + t * ld + part * dlen);
-                for (int c = 0; c < dlen / 4; c++) {
-                    const float4 k4 = kr[c], v4 = vr[c];
+                const char *kr = kb + t * rowb + part * dlen * ES;
+                const char *vr = vb + t * rowb + part * dlen * ES;
+                for (int c = 0; c < dlen / EPV; c++) {
+                    const uint4 kx = reinterpret_cast<const uint4 *>(kr)[c];
+                    const uint4 vx = reinterpret_cast<const uint4 *>(vr)[c];
+                    float kf[EPV], vf[EPV];
+                    if constexpr (DT == PT_F32) {
+                        kf[0] = __uint_as_float(kx.x); kf[1] = __uint_as_float(kx.y);
+                        kf[2] = __uint_as_float(kx.z); kf[3] = __uint_as_float(kx.w);
+                        vf[0] = __uint_as_float(vx.x); vf[1] = __uint_as_float(vx.y);
+                        vf[2] = __uint_as_float(vx.z); vf[3] = __uint_as_float(vx.w);
+                    } else {
+                        const uint32_t kw[4] = {kx.x, kx.y, kx.z, kx.w}, vw[4] = {vx.x, vx.y, vx.z, vx.w};
+#pragma unroll
+                        for (int q2 = 0; q2 < 4; q2++) {
+                            kf[2 * q2] = bf16_lo(kw[q2]); kf[2 * q2 + 1] = bf16_hi(kw[q2]);
+                            vf[2 * q2] = bf16_lo(vw[q2]); vf[2 * q2 + 1] = bf16_hi(vw[q2]);
+                        }
+                    }
+                    const int d0 = part * dlen + c * EPV;
 #pragma unroll
                     for (int g = 0; g < MAXG; g++) {
                         if (g >= G) break;
-                        const float4 q4 = reinterpret_cast<const float4 *>(qs + g * D + part * dlen)[c];
-                        const float4 o4 = reinterpret_cast<const float4 *>(dos + g * D + part * dlen)[c];
-                        kq[g] = fmaf(k4.x, q4.x, fmaf(k4.y, q4.y, fmaf(k4.z, q4.z, fmaf(k4.w, q4.w, kq[g]))));
-                        vd[g] = fmaf(v4.x, o4.x, fmaf(v4.y, o4.y, fmaf(v4.z, o4.z, fmaf(v4.w, o4.w, vd[g]))));
+#pragma unroll
+                        for (int e4 = 0; e4 < EPV; e4 += 4) {
+                            const float4 q4 = *reinterpret_cast<const float4 *>(qs + g * D + d0 + e4);
+                            const float4 o4 = *reinterpret_cast<const float4 *>(dos + g * D + d0 + e4);
+                            kq[g] = fmaf(kf[e4], q4.x, fmaf(kf[e4 + 1], q4.y, fmaf(kf[e4 + 2], q4.z, fmaf(kf[e4 + 3], q4.w, kq[g]))));
+                            vd[g] = fmaf(vf[e4], o4.x, fmaf(vf[e4 + 1], o4.y, fmaf(vf[e4 + 2], o4.z, fmaf(vf[e4 + 3], o4.w, vd[g]))));
+                        }
                     }
                 }
             }
@@ -150,9 +210,8 @@ __global__ void __launch_bounds__(kGBWarps * 32) k_gated_bwd(const GatedBwdParam
         for (int o = 16; o > 0; o >>= 1) dgate += __shfl_xor_sync(0xffffffffu, dgate, o);
         if (lane == 0) p.dgates[u * p.Pmax + lp] = dgate / gate;
         __syncwarp();
-        // lanes own dims: dK / dV rows (summed over heads), dq partial; q / dout in registers,
-        // the token's weights as broadcast float4 reads
-        for (int t = 0; t < rows; t++) {
+        // lanes own dims: dK / dV rows (summed over heads; zero rows past the page's end)
+        for (int t = 0; t < S; t++) {
             float wt[MAXG], zt[MAXG];
 #pragma unroll
             for (int g4 = 0; g4 < MAXG; g4 += 4) {
@@ -161,24 +220,27 @@ __global__ void __launch_bounds__(kGBWarps * 32) k_gated_bwd(const GatedBwdParam
                 wt[g4] = a.x; wt[g4 + 1] = a.y; wt[g4 + 2] = a.z; wt[g4 + 3] = a.w;
                 zt[g4] = b.x; zt[g4 + 1] = b.y; zt[g4 + 2] = b.z; zt[g4 + 3] = b.w;
             }
+            const bool live = t < rows;
 #pragma unroll
             for (int j = 0; j < DJ; j++) {
                 const int d = lane + 32 * j;
                 if (d >= D) break;
-                const float kv = ks[t * ld + d];
                 float dk = 0.f, dv = 0.f;
+                if (live) {
+                    const float kv = rawval<DT>(kb + t * rowb, d);
 #pragma unroll
-                for (int g = 0; g < MAXG; g++) {
-                    if (g >= G) break;
-                    dv = fmaf(wt[g], dr[g][j], dv);
-                    dk = fmaf(zt[g], qr[g][j], dk);
-                    dq_acc[g][j] = fmaf(zt[g], kv, dq_acc[g][j]);
+                    for (int g = 0; g < MAXG; g++) {
+                        if (g >= G) break;
+                        dv = fmaf(wt[g], dr[g][j], dv);
+                        dk = fmaf(zt[g], qr[g][j], dk);
+                        dq_acc[g][j] = fmaf(zt[g], kv, dq_acc[g][j]);
+                    }
                 }
                 p.dk_pool[base + (int64_t)t * D + d] = dk * p.scale;
                 p.dv_pool[base + (int64_t)t * D + d] = dv;
             }
         }
-        __syncwarp();
+        __syncwarp();  // the buffer is reused two pages later
     }
     // dq: warp partials -> CTA (shared atomics) -> global (one atomic per element per CTA)
 #pragma unroll
@@ -229,14 +291,15 @@ extern "C" int pt_gated_attend_bwd(const void *q, int q_dtype, const void *k_poo
     if (!q || !k_pool || !v_pool || !page_table || !seq_len || !gates || !out || !lse || !dout ||
         !dq || !dk_pool || !dv_pool || !dgates || U < 0 || G < 1 || D < 1 || S < 1 || Pmax < 1)
         return PT_ERR_INVALID;
-    if (G > 8 || D > 256 || S > 64 || D % 4 || (S < 32 && (32 % S || D % (4 * (32 / S)))))
-        return PT_ERR_UNSUPPORTED;
+    if (G > 8 || D > 256 || S > 64 || D % 8 || (S < 32 && 32 % S)) return PT_ERR_UNSUPPORTED;
     if (U == 0) return PT_OK;
     GatedBwdParams p{q, k_pool, v_pool, page_table, seq_len, gates, out, lse, dout, dq, dk_pool,
                      dv_pool, dgates, q_dtype, kv_dtype, G, D, S, Pmax, scale};
     const int MAXG = 8;
-    const size_t smem = ((size_t)(2 * MAXG * D + 2 * MAXG + MAXG * D) +
-                         (size_t)kGBWarps * (2 * S * (D + 4) + 2 * MAXG * S)) * 4;
+    const int ES = kv_dtype == PT_F32 ? 4 : 2;
+    const size_t pageb = (size_t)S * (D * ES + 16);
+    const size_t smem = (size_t)(3 * MAXG * D + 16) * 4 +
+                        (size_t)kGBWarps * (4 * pageb + 2 * MAXG * S * 4);
     if (smem > 220 * 1024) return PT_ERR_UNSUPPORTED;
     cudaStream_t st = (cudaStream_t)stream;
     const int dj = (D + 31) / 32;

@@ -198,8 +198,9 @@ def gated_backward(cache: PagedKvCache, queries: torch.Tensor, gates, out: torch
     g32 = g64.to(torch.float32).contiguous()
     d = cache.device
     dq = torch.zeros(U * G, D, dtype=torch.float32, device=d)
-    dk = torch.zeros(cache.layout.max_pages, S, D, dtype=torch.float32, device=d)
-    dv = torch.zeros_like(dk)
+    # every row of every page of every unit is written by the kernel (zeros where no gradient)
+    dk = torch.empty(cache.layout.max_pages, S, D, dtype=torch.float32, device=d)
+    dv = torch.empty_like(dk)
     dg = torch.zeros(U, cache.Pmax, dtype=torch.float32, device=d)
     _lib.call("pt_gated_attend_bwd", q.data_ptr(), dev.dtype_code(q.dtype), cache.k_pool.data_ptr(),
               cache.v_pool.data_ptr(), cache.kv_code, cache.page_table.data_ptr(),
