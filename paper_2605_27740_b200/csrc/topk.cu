@@ -1,10 +1,11 @@
 // topk.cu -- K3: per-unit top-k page selection (standalone kernel; see select.cuh).
 //
 // One CTA (128 threads) per unit stages the unit's keys once in shared memory and runs the
-// block selection of select.cuh (bisection for the threshold key, ordered compaction for
-// the lowest-logical-index tie rule, page-table translation in the epilogue).  The decode
-// engine normally runs this fused into the tail of the scoring kernel (score.cu); this
-// entry point serves pages beyond that kernel's shared-memory envelope and the C ABI.
+// block selection of select.cuh (histogram / bisection for the threshold key, ordered
+// compaction for the lowest-logical-index tie rule, page-table translation in the epilogue).
+// The decode engine normally runs the selection fused into the attention kernel
+// (attend_fused.cu, pt_select_attend); this entry point is the C-ABI K3, the fallback
+// outside the fused kernel's envelope, and the cross-check of the fused selection.
 #include <stdlib.h>
 
 #include "select.cuh"

@@ -2,15 +2,18 @@
 
 One decode step for every (sequence, kv-head) unit of a :class:`PagedKvCache`:
 
-    [append K/V row  (K1b: pt_append)]      kvcache.py:185-208
-    score + select   (K2+K3: pt_score_select) scoring.py:108-124 -> bf16 -> ordered keys ->
-                                              select.py:87-115 + page-table translation
-    attend           (K4: pt_attend)         attention.py:94-107 for the G heads of a group
+    append K/V row    (K1b: pt_append)        kvcache.py:185-208      } two graph branches
+    lambda * ||q||    (pt_lam_norms)          scoring.py:39-47        }
+    score             (K2: pt_score_prenorm)  scoring.py:108-124 -> bf16 -> ordered keys
+                                              (+ per-32-page tile maxima)
+    select + attend   (K3+K4: pt_select_attend) select.py:87-115 + page-table translation,
+                                              then attention.py:94-107 for the G heads
 
-All launches go on the current CUDA stream with device-resident buffers and no
-host synchronisation, so a step can be captured once and replayed as a CUDA graph
-(:meth:`DecodeEngine.capture`).  ``dense`` runs K4 over every page (attention.py:78-91),
-the speed-up denominator.
+All launches go on device-resident buffers with no host synchronisation (programmatic
+dependent launch between consecutive kernels), so a step can be captured once and replayed as
+a CUDA graph (:meth:`DecodeEngine.capture`).  ``select`` / ``attend`` are the same stages as
+separate launches (pt_topk / pt_attend); ``score_select`` is an alternative K2+K3 launch.
+``dense`` runs K4 over every page (attention.py:78-91), the speed-up denominator.
 """
 
 from __future__ import annotations
