@@ -150,6 +150,7 @@ __global__ void __launch_bounds__(kSSWarps * 32, kSSCtas) k_score_stream(const S
     settle(pu, pt);
     int cu = pu, ct = pt;                            // consumer
     int p_part = 0, p_seq = 0, issued = 0;
+    const uint64_t evict_first = l2_evict_first_policy();
     auto fill = [&](int consumed) {
         while (pu < U && issued < consumed + NST) {
             if (lane == 0) {
@@ -159,7 +160,8 @@ __global__ void __launch_bounds__(kSSWarps * 32, kSSCtas) k_score_stream(const S
                 uint32_t tx = C::STAGE;
                 if (p_part == 0) tx += C::QCOPY + 32 + 128;
                 mbar_arrive_expect_tx(&bars[slot], tx);
-                bulk_g2s(ring + slot * C::STAGE, gsrc + p_part * C::STAGE, C::STAGE, &bars[slot]);
+                bulk_g2s_hint(ring + slot * C::STAGE, gsrc + p_part * C::STAGE, C::STAGE, &bars[slot],
+                              evict_first);
                 if (p_part == 0) {
                     char *h = hdrs + (p_seq % C::NHDR) * C::HDR;
                     bulk_g2s(h, static_cast<const char *>(prm.q) + (int64_t)pu * G * D * C::QES,
