@@ -96,9 +96,9 @@ PT_API int pt_page_stats(const void *k_pool, int kv_dtype, const int32_t *page_t
  * (free list first, then bump; deterministic in unit order, kvcache.py:154-176); the
  * touched page's stats are recomputed exactly.  pool_state int32[4] =
  * {bump_next, free_count, max_pages, error_flag}; error_flag set to PT_ERR_CAPACITY
- * when the pool is exhausted (that unit is left unchanged).  slot_scratch: int32 [U + 4]
- * device scratch, zero-initialised once (per-unit target page + the launch's internal
- * allocation flag; self-resetting).  One launch. */
+ * when the pool is exhausted (that unit is left unchanged).  slot_scratch: int32 [2U + 4]
+ * device scratch, zero-initialised once (per-unit target page, the launch's internal flags
+ * (self-resetting), a snapshot of the lengths).  One launch. */
 PT_API int pt_append(const void *k_new, const void *v_new, void *k_pool, void *v_pool, int kv_dtype,
               int32_t *page_table, int32_t *seq_len, int U, int S, int D, int Pmax, void *means,
               int stats_dtype, float *stds, int32_t *pool_state, const int32_t *free_list,

@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(kStatsWarps * 32)
 // ---------------------------------------------------------------------------
 // Decode append, one launch (kvcache.py:185-208 for every unit).
 //
-// CTA 0 snapshots every unit's length into shared memory and publishes `flag_read`; if any
+// CTA 0 snapshots every unit's length (global scratch) and publishes `flag_read`; if any
 // unit starts a new page it runs the deterministic unit-order allocation -- the batched
 // _alloc_page (kvcache.py:154-176): free list popped from its end (list.pop()), then the
 // bump pointer; exhaustion -> error flag, unit skipped -- and publishes `flag_alloc`.
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(256)
         }
     }
     if (blockIdx.x == 0) {
-        int *sn = reinterpret_cast<int *>(asmem + per_warp * wpc);
+        int *sn = slot + U + 4;  // global scratch: no per-CTA shared memory for U lengths
         int any = 0;
         for (int i = threadIdx.x; i < U; i += blockDim.x) {
             const int ni = seq_len[i];
@@ -490,11 +490,13 @@ static int launch_append(const void *kn, const void *vn, void *kp, void *vp, int
                          int32_t *pool_state, const int32_t *free_list, int32_t *slot,
                          cudaStream_t st) {
     const size_t per_warp = append_per_warp(S, D, DT == PT_F32 ? 4 : 2);
-    const size_t snap = (size_t)U * 4;  // CTA 0's snapshot of every unit's length
-    if (snap + per_warp > 200 * 1024) return PT_ERR_UNSUPPORTED;
-    int wpc = (int)((200 * 1024 - snap) / per_warp);
-    if (wpc > 4) wpc = 4;  // spread the latency-bound per-unit warps over more SMs
-    const size_t smem = per_warp * wpc + snap;
+    if (per_warp > 200 * 1024) return PT_ERR_UNSUPPORTED;
+    int wpc = (int)((200 * 1024) / per_warp);
+    // spread the latency-bound per-unit warps over more SMs; thousands of units: keep the
+    // whole grid resident in one wave
+    const int wmax = U >= 2048 ? 8 : 4;
+    if (wpc > wmax) wpc = wmax;
+    const size_t smem = per_warp * wpc;
     const int grid = (U + wpc - 1) / wpc;
     const int dj = (D + 31) / 32;
 #define PT_APP_CASE(DJ_)                                                                      \

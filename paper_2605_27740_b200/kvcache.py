@@ -223,7 +223,7 @@ class PagedKvCache:
         # {bump_next, free_count, max_pages, error_flag}
         self.pool_state = torch.tensor([0, 0, layout.max_pages, 0], dtype=torch.int32, device=d)
         self.free_list_dev = torch.zeros(layout.max_pages, dtype=torch.int32, device=d)
-        self._slot = torch.zeros(U + 4, dtype=torch.int32, device=d)  # targets + launch flags
+        self._slot = torch.zeros(2 * U + 4, dtype=torch.int32, device=d)  # targets, flags, lengths
         # extend_units: fused pt_extend (default) or pt_write_rows + pt_page_stats (cross-check)
         self.split_extend = False
         self._seq_host = np.zeros(U, dtype=np.int64)
