@@ -444,7 +444,8 @@ extern "C" int pt_select_attend(const uint16_t *keys, const uint16_t *tile_max,
     const bool warp_path = want_warp == 1 ||
                            (want_warp != 0 && U >= 4 * 148 && k <= 64 && Pmax <= 32 * 8 * kSWMaxV);
     size_t w_per = 0;
-    int w_nst = 3, w_nw = 4;
+    // ring depth (PT_SAW_NSTAGE: tuning; a 2-deep ring measured no faster at k = 8)
+    int w_nst = sa_env_int("PT_SAW_NSTAGE", 3), w_nw = 4;
     if (warp_path && Pmax <= 32 * 8 * kSWMaxV) {
         auto per_of = [&](int nst) {
             return ((size_t)nst * stage + (((size_t)k + 1) & ~(size_t)1) * 4 + (size_t)nst * 8 + 1023) &
