@@ -122,6 +122,15 @@ class ClockSampler:
         }
 
 
+def host_cores() -> int:
+    """Every host core this process may run on (torchrun exports OMP_NUM_THREADS=1; the
+    CPU baseline sets its OpenMP team explicitly to this)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -231,12 +240,19 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dist = None
+    ndev = torch.cuda.device_count() if torch.cuda.is_available() else 1
+    # BENCH_DIST_BACKEND=gloo (+ more ranks than GPUs): a functional check of the multi-rank
+    # path on a single-GPU box; the driver's multi-GPU runs use NCCL, one rank per GPU
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    device = torch.device("cuda", local if torch.cuda.is_available() else 0)
+        torch.cuda.set_device(local % ndev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    device = torch.device("cuda", (local % ndev) if torch.cuda.is_available() else 0)
     G = args.q_heads // args.kv_heads
     H, D, S = args.kv_heads, args.head_dim, args.page
     kp = -(-args.budget // S)
@@ -256,7 +272,7 @@ def main():
             return
         from oracle import oracle as O
 
-        ncores = O.max_threads()
+        ncores = host_cores()
         # the oracle sample needs the same cache contents: build a 2-sequence cache on the GPU
         # when one is present, else generate on the host (identical distribution).
         if torch.cuda.is_available():
@@ -331,7 +347,7 @@ def main():
         torch.cuda.synchronize()
 
     # ---- timed region: K graph replays -------------------------------------------
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(local % ndev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     with sampler:
@@ -497,7 +513,7 @@ def main():
 
     # ---- optional output all-gather (NCCL over NVLink), reported beside the line ------
     allgather_us = None
-    if dist is not None:
+    if dist is not None and backend == "nccl":
         outs = [torch.empty_like(eng.out) for _ in range(world)]
         for _ in range(3):
             dist.all_gather(outs, eng.out)
@@ -531,7 +547,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu:
         from oracle import oracle as O
 
-        nth = O.max_threads()
+        nth = host_cores()
         r = cpu_baseline(cache, qs[0], args, args.cpu_seconds, nth)
         cb = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
 
