@@ -189,7 +189,10 @@ PT_API int pt_attend(const void *q, int q_dtype, const void *k_pool, const void 
  * (attention.py:137-146).  bf16 KV, G <= 8, D in {64,128,256}, S in {16,32,64}; returns
  * PT_ERR_UNSUPPORTED outside that envelope (the caller runs pt_topk + pt_attend).
  * tile_max: pt_score's per-tile maxima or NULL (they let the selection skip the keys below
- * the k-th largest tile maximum).  Emission order equals pt_topk's (ascending logical). */
+ * the k-th largest tile maximum).  Emission order equals pt_topk's (ascending logical).
+ * Launched with programmatic dependent launch: its prologue reads seq_len, page_table and q
+ * before waiting on the preceding kernel, which therefore must not write those (the
+ * package's scorers do not). */
 PT_API int pt_select_attend(const uint16_t *keys, const uint16_t *tile_max,
                             const int32_t *seq_len, const int32_t *page_table,
                             int U, int S, int Pmax, int k, int32_t *sel, int32_t *sel_logical,

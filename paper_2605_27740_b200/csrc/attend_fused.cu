@@ -79,8 +79,9 @@ __global__ void __launch_bounds__(kSAThreads) k_select_attend(const __grid_const
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + p.region + (((size_t)k * 4 + 7) & ~(size_t)7)) +
                      warp * nstage;
 
+    // PDL: the prologue below (lengths, tail page, query fragments) reads nothing the scoring
+    // kernel writes, so it runs while the scorer drains; keys / tile maxima wait for it
     pdl_trigger();
-    pdl_wait();
     const int n = p.seq_len[u];
     const int P = (n + S - 1) / S;
     const bool lead = (c == 0);
@@ -119,6 +120,7 @@ __global__ void __launch_bounds__(kSAThreads) k_select_attend(const __grid_const
             qb[ks][1] = b1;
         }
     }
+    pdl_wait();
     if (prof) g_sa_prof[cta * 10 + 1] = gtimer();
 
     // ---- selection (select.py:87-115): physical ids land in `ids` in emission order ----
