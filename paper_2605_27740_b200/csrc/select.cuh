@@ -510,30 +510,41 @@ __device__ bool select_cand(const uint16_t *__restrict__ skeys, const uint16_t *
     stamp(0);
     int thr = -1, gt_tot = 0, eq_tot = 0, C = -1;
     if (L >= 0) {
-        // ---- candidates >= L in logical order (one block scan per round of NT vectors) ----
+        // ---- candidates >= L in logical order: each round a thread owns VPT consecutive
+        // key vectors (so thread order is logical order) and one block scan ranks them ----
+        constexpr int VPT = 4;
         const uint32_t L16 = (uint32_t)L * 0x10001u;
         int run = 0, below = -1, par = 0;
-        for (int v0 = 0; v0 < nvec; v0 += NT, par ^= 1) {
-            const int v = v0 + tid;
-            uint4 x = make_uint4(0u, 0u, 0u, 0u);
+        for (int v0 = 0; v0 < nvec; v0 += NT * VPT, par ^= 1) {
+            const int vt = v0 + tid * VPT;
+            uint4 x[VPT];
+            int cv[VPT];
             int c = 0;
-            if (v < nvec) {
-                x = s4[v];
-                uint32_t w[4], mk[4];
-                words(x, w);
-                vmask(v, mk);
-                uint32_t bl = 0u;
-                bool any_below = false;
 #pragma unroll
-                for (int q = 0; q < 4; q++) {
-                    const uint32_t ge = __vcmpgeu2(w[q], L16);
-                    c += __popc(ge & mk[q]);
-                    const uint32_t lt = ~ge & mk[q];
-                    any_below |= lt != 0u;
-                    bl = __vmaxu2(bl, w[q] & lt);
+            for (int j = 0; j < VPT; j++) {
+                const int v = vt + j;
+                x[j] = make_uint4(0u, 0u, 0u, 0u);
+                cv[j] = 0;
+                if (v < nvec) {
+                    x[j] = s4[v];
+                    uint32_t w[4], mk[4];
+                    words(x[j], w);
+                    vmask(v, mk);
+                    uint32_t bl = 0u;
+                    bool any_below = false;
+                    int cc = 0;
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        const uint32_t ge = __vcmpgeu2(w[q], L16);
+                        cc += __popc(ge & mk[q]);
+                        const uint32_t lt = ~ge & mk[q];
+                        any_below |= lt != 0u;
+                        bl = __vmaxu2(bl, w[q] & lt);
+                    }
+                    cv[j] = cc >> 4;
+                    c += cv[j];
+                    if (any_below) below = max(below, (int)max(bl & 0xFFFFu, bl >> 16));
                 }
-                c >>= 4;
-                if (any_below) below = max(below, (int)max(bl & 0xFFFFu, bl >> 16));
             }
             int inc = c;
 #pragma unroll
@@ -551,14 +562,19 @@ __device__ bool select_cand(const uint16_t *__restrict__ skeys, const uint16_t *
                 run += t;
             }
             if (c) {
-                uint32_t w[4];
-                words(x, w);
 #pragma unroll
-                for (int e = 0; e < 8; e++) {
-                    const int key = (e & 1) ? (int)(w[e >> 1] >> 16) : (int)(w[e >> 1] & 0xFFFFu);
-                    if (v * 8 + e < P && key >= L) {
-                        if (pos < kCandMax) sh.cand[pos] = ((uint32_t)key << 16) | (uint32_t)(v * 8 + e);
-                        pos++;
+                for (int j = 0; j < VPT; j++) {
+                    if (!cv[j]) continue;
+                    const int v = vt + j;
+                    uint32_t w[4];
+                    words(x[j], w);
+#pragma unroll
+                    for (int e = 0; e < 8; e++) {
+                        const int key = (e & 1) ? (int)(w[e >> 1] >> 16) : (int)(w[e >> 1] & 0xFFFFu);
+                        if (v * 8 + e < P && key >= L) {
+                            if (pos < kCandMax) sh.cand[pos] = ((uint32_t)key << 16) | (uint32_t)(v * 8 + e);
+                            pos++;
+                        }
                     }
                 }
             }
@@ -702,20 +718,27 @@ __device__ bool select_cand(const uint16_t *__restrict__ skeys, const uint16_t *
             }
         }
     } else {
-        // ---- ordered compaction over all keys: per round of NT vectors, a block scan of
+        // ---- ordered compaction over all keys: per round of 4 NT vectors, a block scan of
         // (keys > thr, keys == thr) gives each vector's output position and tie rank ----
         const uint32_t t16 = (uint32_t)thr * 0x10001u;
         const uint32_t t1 = (uint32_t)min(thr + 1, 0xFFFF) * 0x10001u;
         int run_g = 0, run_q = 0, par = 0;
-        for (int v0 = 0; v0 < nvec; v0 += NT, par ^= 1) {
-            const int v = v0 + tid;
-            uint4 x = make_uint4(0u, 0u, 0u, 0u);
+        constexpr int VPT = 4;  // consecutive vectors per thread per round (one scan each)
+        for (int v0 = 0; v0 < nvec; v0 += NT * VPT, par ^= 1) {
+            const int vt = v0 + tid * VPT;
+            uint4 x[VPT];
             int g = 0, q = 0;
-            if (v < nvec) {
-                x = s4[v];
-                const int ge = count_ge(x, v, t16);
-                g = thr < 0xFFFF ? count_ge(x, v, t1) : 0;
-                q = ge - g;
+#pragma unroll
+            for (int j = 0; j < VPT; j++) {
+                const int v = vt + j;
+                x[j] = make_uint4(0u, 0u, 0u, 0u);
+                if (v < nvec) {
+                    x[j] = s4[v];
+                    const int ge = count_ge(x[j], v, t16);
+                    const int gj = thr < 0xFFFF ? count_ge(x[j], v, t1) : 0;
+                    g += gj;
+                    q += ge - gj;
+                }
             }
             const int pk = g | (q << 16);
             int inc = pk;
@@ -737,18 +760,23 @@ __device__ bool select_cand(const uint16_t *__restrict__ skeys, const uint16_t *
             if (g | q) {
                 int gpos = run_g + (pre & 0xFFFF), seen = run_q + (pre >> 16);
                 int pos = gpos + min(seen, budget);
-                uint32_t w[4];
-                words(x, w);
 #pragma unroll
-                for (int e = 0; e < 8; e++) {
-                    const int key = (e & 1) ? (int)(w[e >> 1] >> 16) : (int)(w[e >> 1] & 0xFFFFu);
-                    if (v * 8 + e >= P || key < thr) continue;
-                    bool sel = key > thr;
-                    if (key == thr) { sel = seen < budget; seen++; }
-                    if (sel) {
-                        if (slist) slist[pos] = v * 8 + e;
-                        else { out[pos] = map[v * 8 + e]; if (out_l) out_l[pos] = v * 8 + e; }
-                        pos++;
+                for (int j = 0; j < VPT; j++) {
+                    const int v = vt + j;
+                    if (v >= nvec) break;
+                    uint32_t w[4];
+                    words(x[j], w);
+#pragma unroll
+                    for (int e = 0; e < 8; e++) {
+                        const int key = (e & 1) ? (int)(w[e >> 1] >> 16) : (int)(w[e >> 1] & 0xFFFFu);
+                        if (v * 8 + e >= P || key < thr) continue;
+                        bool sel = key > thr;
+                        if (key == thr) { sel = seen < budget; seen++; }
+                        if (sel) {
+                            if (slist) slist[pos] = v * 8 + e;
+                            else { out[pos] = map[v * 8 + e]; if (out_l) out_l[pos] = v * 8 + e; }
+                            pos++;
+                        }
                     }
                 }
             }
