@@ -656,3 +656,25 @@ def test_gated_attention_single_query_api(cuda, oracle):
     out2, _ = sm.gated_attention_forward(q, keys, vals, g2)
     fd = float(d_out @ (out2.out - out.out)) / eps
     assert fd == pytest.approx(grads.d_gates[3], rel=2e-2, abs=1e-4)
+
+
+def test_bench_runs_end_to_end(cuda):
+    """bench.py (the driver's entry point) on a reduced shape: one JSON line with the contract
+    keys, positive throughput, roofline and e2e blocks."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--batch", "2", "--ctx", "8192",
+                        "--steps", "5", "--warmup", "3", "--no-dense", "--cpu-seconds", "0.5"],
+                       capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+                "higher_is_better", "scaling", "dtype", "config", "roofline", "e2e", "clocks",
+                "gpu_launches", "cpu_baseline"):
+        assert key in line, key
+    assert line["value"] > 0 and line["e2e"]["value"] > 0 and line["roofline"]["achieved"] > 0
+    assert line["cpu_baseline"]["cores"] >= 1
