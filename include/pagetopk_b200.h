@@ -207,6 +207,11 @@ PT_API int pt_select_attend(const uint16_t *keys, const uint16_t *tile_max,
  * PT_SA_PROF=1 in the environment.  n <= 10 * 4096. */
 PT_API int pt_debug_sa_prof(unsigned long long *host, int n);
 
+/* Tuning aid: per-unit phase timestamps of the last pt_append launch made with PT_APP_PROF=1
+ * (8 per unit: entry, after the PDL wait, row loaded, tail page id known, page staged, stats
+ * stored, length snapshot seen, exit).  n <= 8 * 8192. */
+PT_API int pt_debug_append_prof(unsigned long long *host, int n);
+
 /* Soft-mask training path (softmask.py:178-217 gated_attention_backward), batched over units:
  * the backward of attention over every page with a per-page additive log-gate bias, for the G
  * query heads of each unit.  gates f32 [U][Pmax] (0 = hard-masked page, skipped); out / lse /

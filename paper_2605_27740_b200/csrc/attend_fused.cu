@@ -11,7 +11,8 @@
 // prologue instead of a kernel, and the sel / n_sel / kth / kplus1 outputs are still written
 // for the caller (bit-identical to pt_topk: same select_block).
 //
-// Grid (nchunk, U), 4 warps.  Every chunk CTA of a unit runs the (deterministic) selection;
+// Grid (nchunk, U), 8 warps (4 with PT_SA_SEL_THREADS=128): all select, the first 4 stream.
+// Every chunk CTA of a unit runs the (deterministic) selection;
 // chunk 0 publishes it.  Chunk c attends the c-th contiguous slice of the emitted list; the
 // warps of the CTA interleave pages (warp w: slice[w], slice[w+4], ...), each through a
 // private nstage-deep ring of TMA tensor copies (one K + one V page per stage), QK / PV on
@@ -52,14 +53,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
-constexpr int kSAThreads = kSAWarps * 32;
 
 __host__ __device__ __forceinline__ size_t sa_keys_bytes(int Pmax) {
     return (size_t)((Pmax + 8) / 8) * 16;
 }
 
-template <int D, int MT>
-__global__ void __launch_bounds__(kSAThreads) k_select_attend(const __grid_constant__ CUtensorMap tmk,
+// NT threads run the selection (NT / 32 warps); the first kSAWarps warps stream the pages
+template <int D, int MT, int NT>
+__global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__ CUtensorMap tmk,
                                                               const __grid_constant__ CUtensorMap tmv,
                                                               const SelAttnParams p) {
     constexpr int S = 16 * MT;
@@ -68,8 +69,8 @@ __global__ void __launch_bounds__(kSAThreads) k_select_attend(const __grid_const
     constexpr uint32_t PAGE_BYTES = S * D * 2;
     constexpr uint32_t STAGE_BYTES = 2 * PAGE_BYTES;
     extern __shared__ __align__(1024) char smem[];
-    __shared__ SelectShared<kSAThreads> sh;
-    __shared__ SelectCandShared<kSAThreads> csh;
+    __shared__ SelectShared<NT> sh;
+    __shared__ SelectCandShared<NT> csh;
     __shared__ int sdummy[3];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t u = blockIdx.y;
@@ -77,7 +78,7 @@ __global__ void __launch_bounds__(kSAThreads) k_select_attend(const __grid_const
     const int G = p.G, k = p.k, nstage = p.nstage;
     int *ids = reinterpret_cast<int *>(smem + p.region);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + p.region + (((size_t)k * 4 + 7) & ~(size_t)7)) +
-                     warp * nstage;
+                     (warp < NW ? warp : 0) * nstage;
 
     // PDL: the prologue below (lengths, tail page, query fragments) reads nothing the scoring
     // kernel writes, so it runs while the scorer drains; keys / tile maxima wait for it
@@ -136,27 +137,40 @@ __global__ void __launch_bounds__(kSAThreads) k_select_attend(const __grid_const
     // keys -> shared memory: every 16-byte load of a thread in flight before its first store
     uint16_t *skeys = reinterpret_cast<uint16_t *>(smem);
     int *bins = reinterpret_cast<int *>(smem + sa_keys_bytes(p.Pmax));
+    // the tile maxima (one u16 per 32 pages) ride in the same load round as the keys
+    uint16_t *stm = reinterpret_cast<uint16_t *>(smem + sa_keys_bytes(p.Pmax) + kSelectBins * 4);
+    const int ntiles = (P + 31) >> 5;
+    const bool tm_stage = p.tile_max != nullptr && ntiles <= NT * 8;
     {
+        constexpr int kTm = 8;
+        const uint16_t *tsrc = p.tile_max + u * (int64_t)(p.Pmax >> 5);
+        uint16_t tv[kTm];
+#pragma unroll
+        for (int j = 0; j < kTm; j++)
+            if (tm_stage && threadIdx.x + j * NT < ntiles) tv[j] = __ldcg(tsrc + threadIdx.x + j * NT);
         const uint4 *src = reinterpret_cast<const uint4 *>(krow);
         constexpr int kMax = 8;
         const int nv = (P + 7) / 8;
-        for (int i0 = threadIdx.x; i0 < nv; i0 += kMax * kSAThreads) {
+        for (int i0 = threadIdx.x; i0 < nv; i0 += kMax * NT) {
             uint4 v[kMax];
 #pragma unroll
             for (int j = 0; j < kMax; j++)
-                if (i0 + j * kSAThreads < nv) v[j] = __ldcg(src + i0 + j * kSAThreads);
+                if (i0 + j * NT < nv) v[j] = __ldcg(src + i0 + j * NT);
 #pragma unroll
             for (int j = 0; j < kMax; j++)
-                if (i0 + j * kSAThreads < nv) reinterpret_cast<uint4 *>(skeys)[i0 + j * kSAThreads] = v[j];
+                if (i0 + j * NT < nv) reinterpret_cast<uint4 *>(skeys)[i0 + j * NT] = v[j];
         }
+#pragma unroll
+        for (int j = 0; j < kTm; j++)
+            if (tm_stage && threadIdx.x + j * NT < ntiles) stm[threadIdx.x + j * NT] = tv[j];
     }
     __syncthreads();
     const bool selected =
-        select_cand<kSAThreads>(skeys, p.tile_max ? p.tile_max + u * (int64_t)(p.Pmax >> 5) : nullptr,
+        select_cand<NT>(skeys, tm_stage ? stm : nullptr,
                                 P, k, p.page_table + u * p.Pmax, o_sel, o_log, o_n, o_kth, o_kp1,
-                                csh, ids, true, prof ? &g_sa_prof[cta * 10 + 6] : nullptr);
+                                csh, ids, true, prof ? &g_sa_prof[cta * 10 + 6] : nullptr, true);
     if (!selected)  // take-all, or massive ties at the lower bound
-        select_block<kSAThreads>(skeys, bins, P, k, p.page_table + u * p.Pmax, o_sel, o_log, o_n,
+        select_block<NT>(skeys, bins, P, k, p.page_table + u * p.Pmax, o_sel, o_log, o_n,
                                  o_kth, o_kp1, sh, ids, true);
     __syncthreads();  // ids complete; the select scratch is dead -> stage rings
     if (prof) g_sa_prof[cta * 10 + 2] = gtimer();
@@ -169,7 +183,7 @@ __global__ void __launch_bounds__(kSAThreads) k_select_attend(const __grid_const
     const int nchunk_u = (ns + per - 1) / per;
     char *my_stages = smem + (size_t)warp * nstage * STAGE_BYTES;
     const int rem = last - first - warp;
-    const int my_count = rem > 0 ? (rem + NW - 1) / NW : 0;
+    const int my_count = (warp < NW && rem > 0) ? (rem + NW - 1) / NW : 0;
     auto issue = [&](int i) {
         const int pid = ids[first + warp + i * NW];
         const int st = i % nstage;
@@ -181,7 +195,7 @@ __global__ void __launch_bounds__(kSAThreads) k_select_attend(const __grid_const
             tma_load_2d(ks + PAGE_BYTES + b * S * 128, &tmv, b * 64, pid * S, &bars[st]);
         }
     };
-    if (lane == 0) {
+    if (lane == 0 && warp < NW) {
         for (int i = 0; i < nstage; i++) mbar_init(&bars[i], 1);
         fence_mbar_init();
         for (int i = 0; i < min(nstage, my_count); i++) issue(i);
@@ -211,6 +225,7 @@ __global__ void __launch_bounds__(kSAThreads) k_select_attend(const __grid_const
     float *macc = reinterpret_cast<float *>(smem);             // [NW][8][D]
     float *mml = macc + (size_t)NW * kMmaGP * D;                // [NW][8][2]
     const int g0 = 2 * (lane & 3);
+    if (warp < NW) {
 #pragma unroll
     for (int dm = 0; dm < KS; dm++) {
         const int d = dm * 16 + (lane >> 2);
@@ -224,6 +239,7 @@ __global__ void __launch_bounds__(kSAThreads) k_select_attend(const __grid_const
         mml[(warp * kMmaGP + g0) * 2 + 1] = l_run[0];
         mml[(warp * kMmaGP + g0 + 1) * 2 + 0] = m_run[1];
         mml[(warp * kMmaGP + g0 + 1) * 2 + 1] = l_run[1];
+    }
     }
     __syncthreads();
     AttnParams ap{};
@@ -366,18 +382,25 @@ static int launch_saw(const CUtensorMap &tk, const CUtensorMap &tv, const SelAtt
     return PT_OK;
 }
 
-template <int D, int MT>
-static int launch_sa(const CUtensorMap &tk, const CUtensorMap &tv, const SelAttnParams &p,
-                     size_t smem, cudaStream_t st) {
+template <int D, int MT, int NT>
+static int launch_sa_nt(const CUtensorMap &tk, const CUtensorMap &tv, const SelAttnParams &p,
+                        size_t smem, cudaStream_t st) {
     static size_t configured = 0;
     if (smem > configured) {
-        PT_CUDA_TRY(cudaFuncSetAttribute(k_select_attend<D, MT>,
+        PT_CUDA_TRY(cudaFuncSetAttribute(k_select_attend<D, MT, NT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured = smem;
     }
     dim3 grid(p.nchunk, p.U);
-    PT_CUDA_TRY(pt_launch(k_select_attend<D, MT>, grid, dim3(kSAThreads), smem, st, tk, tv, p));
+    PT_CUDA_TRY(pt_launch(k_select_attend<D, MT, NT>, grid, dim3(NT), smem, st, tk, tv, p));
     return PT_OK;
+}
+
+template <int D, int MT>
+static int launch_sa(const CUtensorMap &tk, const CUtensorMap &tv, const SelAttnParams &p,
+                     size_t smem, cudaStream_t st, int sel_threads) {
+    return sel_threads == 256 ? launch_sa_nt<D, MT, 256>(tk, tv, p, smem, st)
+                              : launch_sa_nt<D, MT, 128>(tk, tv, p, smem, st);
 }
 
 }  // namespace pt
@@ -425,7 +448,7 @@ extern "C" int pt_select_attend(const uint16_t *keys, const uint16_t *tile_max,
         if (nchunk > cap) nchunk = cap;
     }
     if (nchunk > kAttnMaxSplits) nchunk = kAttnMaxSplits;
-    const size_t sel_scratch = sa_keys_bytes(Pmax) + (size_t)kSelectBins * 4;
+    const size_t sel_scratch = sa_keys_bytes(Pmax) + (size_t)kSelectBins * 4 + (size_t)(Pmax / 32) * 2;
     const size_t merge = (size_t)kSAWarps * kMmaGP * (D + 2) * 4;
     auto smem_of = [&](int nst, size_t *region_out) {
         const size_t rings = (size_t)kSAWarps * nst * stage;
@@ -469,6 +492,8 @@ extern "C" int pt_select_attend(const uint16_t *keys, const uint16_t *tile_max,
     p.nstage = nstage; p.region = (int)region; p.scale = scale;
     p.prof = sa_env_int("PT_SA_PROF", 0);
     cudaStream_t st = (cudaStream_t)stream;
+    // selection threads: 8 warps halve the selection's block-wide passes; 4 of them stream
+    const int sel_threads = sa_env_int("PT_SA_SEL_THREADS", 256) == 128 ? 128 : 256;
     if (w_per) {
         SelAttnParams pw = p;
         pw.nstage = w_nst;
@@ -481,7 +506,7 @@ extern "C" int pt_select_attend(const uint16_t *keys, const uint16_t *tile_max,
 #undef PT_SAW
     }
 #define PT_SA(D_, MT_) \
-    if (D == D_ && S == 16 * MT_) return launch_sa<D_, MT_>(tk, tv, p, smem, st);
+    if (D == D_ && S == 16 * MT_) return launch_sa<D_, MT_>(tk, tv, p, smem, st, sel_threads);
     PT_SA(64, 1) PT_SA(64, 2) PT_SA(64, 4)
     PT_SA(128, 1) PT_SA(128, 2) PT_SA(128, 4)
     PT_SA(256, 1) PT_SA(256, 2) PT_SA(256, 4)

@@ -219,6 +219,36 @@ struct DoubleArray {
     const double *a;
     __device__ __forceinline__ double operator()(int i) const { return a[i]; }
 };
+// np.sum of n float64 values in shared memory, by a whole warp (result valid in lane 0):
+// numpy's leaf keeps 8 running sums r[j] over x[j], x[j+8], ...; here lane j (and lane 8 + j
+// for the second half when n > 128 splits once) runs r[j], and the fixed combine tree
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) is done by shuffles -- the same operations in the
+// same order as np_sum.  Other n (not a multiple of 8, or > 256) take the one-thread np_sum.
+__device__ __forceinline__ double np_sum_warp(const double *x, int n, int lane) {
+    if (n % 8 != 0 || n > 256 || n < 8) {
+        double v = 0.0;
+        if (lane == 0) v = np_sum(DoubleArray{x}, n);
+        return v;
+    }
+    int off = 0, len = n;
+    if (n > 128) {
+        int n2 = n / 2;
+        n2 -= n2 % 8;
+        if (lane < 8) len = n2; else { off = n2; len = n - n2; }
+    }
+    const int j = lane & 7;
+    double r = 0.0;
+    if (lane < 16) {
+        r = x[off + j];
+        for (int i = 8; i < len; i += 8) r = __dadd_rn(r, x[off + i + j]);
+    }
+    const double a = __dadd_rn(r, __shfl_down_sync(0xffffffffu, r, 1));  // lanes 0,2,4,6: r0+r1, ...
+    const double b = __dadd_rn(a, __shfl_down_sync(0xffffffffu, a, 2));  // lanes 0,4
+    const double c = __dadd_rn(b, __shfl_down_sync(0xffffffffu, b, 4));  // lane 0 (and 8)
+    const double hi = __shfl_down_sync(0xffffffffu, c, 8);
+    return __dadd_rn(0.0, n > 128 ? __dadd_rn(c, hi) : c);
+}
+
 // squares of f32 values widened to f64: np.sum(f64(q)**2) (scoring.py:45)
 struct SquaresOfF32 {
     const float *a;

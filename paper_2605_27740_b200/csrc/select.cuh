@@ -374,7 +374,8 @@ __device__ bool select_cand(const uint16_t *__restrict__ skeys, const uint16_t *
                             int32_t *__restrict__ out, int32_t *__restrict__ out_l,
                             int32_t *__restrict__ n_sel, int32_t *__restrict__ kth,
                             int32_t *__restrict__ kplus1, SelectCandShared<NT> &sh, int *slist,
-                            bool slist_physical, unsigned long long *tp = nullptr) {
+                            bool slist_physical, unsigned long long *tp = nullptr,
+                            bool tmax_shared = false) {
     constexpr int NWP = NT / 32;
     constexpr int MAXT = 8;  // tile maxima per thread: ceil(P / 32) <= NT * MAXT
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -435,7 +436,7 @@ __device__ bool select_cand(const uint16_t *__restrict__ skeys, const uint16_t *
 #pragma unroll
     for (int i = 0; i < MAXT; i++) {
         const int t = tid + i * NT;
-        tm[i] = (use_tiles && t < ntiles) ? (int)__ldcg(tmax_g + t) : -1;
+        tm[i] = (use_tiles && t < ntiles) ? (int)(tmax_shared ? tmax_g[t] : __ldcg(tmax_g + t)) : -1;
     }
     if (tid < 64) sh.bins[tid] = 0;
     if (tid == 0) sh.below = -1;

@@ -9,6 +9,7 @@
 // Layout: one warp per page; lane owns dims d = lane + 32*j (a warp load is one
 // contiguous row slice, coalesced); float64 per-dim accumulators live in registers;
 // the D per-dim variances go through shared memory for numpy's pairwise sum.
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -165,6 +166,18 @@ __device__ void alloc_scan(int32_t *__restrict__ page_table, const int *__restri
     }
 }
 
+// Optional per-unit phase timestamps (%globaltimer, ns) for tuning: PT_APP_PROF=1 on the host,
+// read back with pt_debug_append_prof().  8 stamps per unit.
+constexpr int kAppProfUnits = 8192;
+__device__ unsigned long long g_app_prof[kAppProfUnits * 8];
+__device__ __forceinline__ void app_stamp(bool on, int64_t u, int i) {
+    if (on) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        g_app_prof[u * 8 + i] = t;
+    }
+}
+
 template <int DT, int SDT, int DJ>
 __global__ void __launch_bounds__(256)
     k_append(const void *__restrict__ k_new, const void *__restrict__ v_new,
@@ -172,7 +185,7 @@ __global__ void __launch_bounds__(256)
              int32_t *__restrict__ page_table, int32_t *__restrict__ seq_len, int U, int S, int D,
              int Pmax, void *__restrict__ means, float *__restrict__ stds,
              int32_t *__restrict__ pool_state, const int32_t *__restrict__ free_list,
-             int32_t *__restrict__ slot) {
+             int32_t *__restrict__ slot, int prof) {
     extern __shared__ __align__(16) char asmem[];
     __shared__ int warp_tot[8];
     __shared__ int carry;
@@ -181,9 +194,12 @@ __global__ void __launch_bounds__(256)
     int *flag_alloc = slot + U, *done = slot + U + 1, *flag_read = slot + U + 2;
     constexpr int ES = DT == PT_F32 ? 4 : 2;
     const size_t per_warp = append_per_warp(S, D, ES);
+    const int64_t u = (int64_t)blockIdx.x * wpc + warp;
+    const bool pr = prof && lane == 0 && u < U && u < kAppProfUnits;
+    app_stamp(pr, u, 0);
     pdl_trigger();
     pdl_wait();
-    const int64_t u = (int64_t)blockIdx.x * wpc + warp;
+    app_stamp(pr, u, 1);
     using Bits = typename std::conditional<DT == PT_F32, uint32_t, uint16_t>::type;
     // this unit's length (read before anyone advances it) and the new K/V row
     const int n = u < U ? seq_len[u] : 0;
@@ -220,6 +236,7 @@ __global__ void __launch_bounds__(256)
         return DT == PT_F32 ? (double)__uint_as_float((uint32_t)rows_s[i])
                             : (double)bf16_bits_to_f32((uint32_t)rows_s[i]);
     };
+    app_stamp(pr, u, 2);
     if (u < U) {
         int pid;
         if (n % S == 0) {  // starts a page: CTA 0's allocation
@@ -229,6 +246,7 @@ __global__ void __launch_bounds__(256)
         } else {
             pid = page_table[u * Pmax + n / S];
         }
+        app_stamp(pr, u, 3);
         if (pid >= 0) {
             const int row = n % S;
             const int64_t base = (int64_t)pid * S * D;
@@ -245,34 +263,45 @@ __global__ void __launch_bounds__(256)
                 }
             }
             __syncwarp();
+            app_stamp(pr, u, 4);
             const int cnt = row + 1;
-            double mean[DJ];
+            // rows outer, the lane's DJ columns inner: DJ independent f64 chains in flight (each
+            // column still sums its rows in row order, as numpy's axis-0 reduction)
+            const bool dok = (D % 32 == 0) || lane + 32 * (DJ - 1) < D;
+            double mean[DJ], vacc[DJ];
 #pragma unroll
-            for (int j = 0; j < DJ; j++) {
-                const int d = lane + 32 * j;
-                double sacc = 0.0;
-                if (d < D)
-                    for (int r = 0; r < cnt; r++) sacc = __dadd_rn(sacc, rowval(r * D + d));
-                mean[j] = __ddiv_rn(sacc, (double)cnt);
-            }
+            for (int j = 0; j < DJ; j++) mean[j] = 0.0;
+#pragma unroll 4
+            for (int r = 0; r < cnt; r++)
+#pragma unroll
+                for (int j = 0; j < DJ; j++)
+                    if (dok || lane + 32 * j < D) mean[j] = __dadd_rn(mean[j], rowval(r * D + lane + 32 * j));
+#pragma unroll
+            for (int j = 0; j < DJ; j++) { mean[j] = __ddiv_rn(mean[j], (double)cnt); vacc[j] = 0.0; }
+#pragma unroll 4
+            for (int r = 0; r < cnt; r++)
+#pragma unroll
+                for (int j = 0; j < DJ; j++)
+                    if (dok || lane + 32 * j < D) {
+                        const double t = __dsub_rn(rowval(r * D + lane + 32 * j), mean[j]);
+                        vacc[j] = __dadd_rn(vacc[j], __dmul_rn(t, t));
+                    }
             constexpr int V = StatsTile<SDT>::V;
 #pragma unroll
             for (int j = 0; j < DJ; j++) {
                 const int d = lane + 32 * j;
                 if (d < D) {
-                    double sacc = 0.0;
-                    for (int r = 0; r < cnt; r++) {
-                        const double t = __dsub_rn(rowval(r * D + d), mean[j]);
-                        sacc = __dadd_rn(sacc, __dmul_rn(t, t));
-                    }
-                    var_s[d] = __ddiv_rn(sacc, (double)cnt);
+                    var_s[d] = __ddiv_rn(vacc[j], (double)cnt);
                     store_elem<SDT>(means, mean_offset(u, n / S, d, D, Pmax, V), __double2float_rn(mean[j]));
                 }
             }
             __syncwarp();
+            const double vsum = np_sum_warp(var_s, D, lane);
             if (lane == 0) {
-                stds[u * Pmax + n / S] = __double2float_rn(__dsqrt_rn(np_sum(DoubleArray{var_s}, D)));
+                stds[u * Pmax + n / S] = __double2float_rn(__dsqrt_rn(vsum));
+                app_stamp(pr, u, 5);
                 spin_flag(flag_read, false);  // CTA 0 has snapshotted every length (no data to acquire)
+                app_stamp(pr, u, 6);
                 seq_len[u] = n + 1;
             }
         }
@@ -286,6 +315,7 @@ __global__ void __launch_bounds__(256)
             atomicExch(done, 0);
         }
     }
+    if (prof && lane == 0 && u < U && u < kAppProfUnits) app_stamp(true, u, 7);
 }
 
 // ---------------------------------------------------------------------------
@@ -499,6 +529,8 @@ static int launch_append(const void *kn, const void *vn, void *kp, void *vp, int
     const size_t smem = per_warp * wpc;
     const int grid = (U + wpc - 1) / wpc;
     const int dj = (D + 31) / 32;
+    const char *pe = getenv("PT_APP_PROF");
+    const int app_prof = (pe && *pe == '1') ? 1 : 0;
 #define PT_APP_CASE(DJ_)                                                                      \
     case DJ_: {                                                                               \
         static size_t configured = 0;                                                         \
@@ -510,7 +542,7 @@ static int launch_append(const void *kn, const void *vn, void *kp, void *vp, int
         }                                                                                     \
         PT_CUDA_TRY(pt_launch(k_append<DT, SDT, DJ_>, dim3(grid), dim3(wpc * 32), smem, st,   \
                               kn, vn, kp, vp, ptab, sl, U, S, D, Pmax, means, stds,           \
-                              pool_state, free_list, slot));                                  \
+                              pool_state, free_list, slot, app_prof));                        \
         break;                                                                                \
     }
     switch (dj) {
@@ -548,6 +580,13 @@ extern "C" int pt_append(const void *k_new, const void *v_new, void *k_pool, voi
     if (kv_dtype == PT_F32 && stats_dtype == PT_BF16)
         return launch_append<PT_F32, PT_BF16>(k_new, v_new, k_pool, v_pool, page_table, seq_len, U, S, D, Pmax, means, stds, pool_state, free_list, slot, st);
     return PT_ERR_INVALID;
+}
+
+// tuning aid: copy the phase timestamps of the last PT_APP_PROF=1 append (n <= 8 * 8192)
+extern "C" int pt_debug_append_prof(unsigned long long *host, int n) {
+    if (!host || n < 0 || n > kAppProfUnits * 8) return PT_ERR_INVALID;
+    PT_CUDA_TRY(cudaMemcpyFromSymbol(host, g_app_prof, (size_t)n * 8));
+    return PT_OK;
 }
 
 extern "C" int pt_write_rows(const void *k_rows, const void *v_rows, int n_max,
