@@ -50,7 +50,9 @@ static inline int ss_ctas_per_sm(int Pmax) {
     const int x = forced ? forced : ((Pmax >> 5) < 32 ? 3 : 2);
     return x < 1 ? 1 : (x > kSSCtas ? kSSCtas : x);
 }
-constexpr int kSSNst = 3;   // ring stages per warp
+// ring stages per warp: 4 with two CTAs per SM (more bytes in flight: 168 vs 172 us at
+// cfg3), 3 with three (the smem of a fourth stage would not fit three CTAs)
+constexpr int kSSNstMax = 4;
 
 __device__ __forceinline__ float2 ss_mul2(float m, float2 q) {
     unsigned long long r;
@@ -72,8 +74,9 @@ __device__ __forceinline__ float2 ss_fma2(float m, float2 q, float2 acc) {
     return *reinterpret_cast<float2 *>(&r);
 }
 
-template <int QDT, int SDT, int G, int D>
+template <int QDT, int SDT, int G, int D, int NST_>
 struct SSCfg {
+    static constexpr int NST = NST_;
     static constexpr int ES = SDT == PT_F32 ? 4 : 2;
     static constexpr int QES = QDT == PT_F32 ? 4 : 2;
     static constexpr int V = 16 / ES;            // means per 16-byte chunk
@@ -85,9 +88,9 @@ struct SSCfg {
     static constexpr int HDR_LN = (G * D * QES + 15) & ~15;
     static constexpr int HDR_SD = HDR_LN + 32;
     static constexpr int HDR = (HDR_SD + 128 + 127) & ~127;
-    static constexpr int NHDR = kSSNst / SPT + 2;
+    static constexpr int NHDR = NST / SPT + 2;
     static constexpr int QF = (GP2 * 2 * D * 4 + 127) & ~127;
-    static constexpr int PER_WARP = kSSNst * STAGE + NHDR * HDR + QF;
+    static constexpr int PER_WARP = NST * STAGE + NHDR * HDR + QF;
     static constexpr uint32_t QCOPY = (uint32_t)((G * D * QES + 15) & ~15);
     static_assert(NCH % CPS == 0, "chunks per stage must divide the row");
 };
@@ -99,14 +102,13 @@ constexpr int kSSPsMax = 2048;
 __host__ __device__ __forceinline__ size_t ss_hdr_bytes(int U) {
     if (U > kSSPsMax) U = kSSPsMax;
     const size_t ps = ((size_t)U * 4 + 15) & ~(size_t)15;
-    return (ps + (size_t)kSSWarps * kSSNst * 8 + 127) & ~(size_t)127;
+    return (ps + (size_t)kSSWarps * kSSNstMax * 8 + 127) & ~(size_t)127;
 }
 
-template <int QDT, int SDT, int G, int D>
+template <int QDT, int SDT, int G, int D, int NST>
 __global__ void __launch_bounds__(kSSWarps * 32, kSSCtas) k_score_stream(const StreamScoreParams prm) {
-    using C = SSCfg<QDT, SDT, G, D>;
+    using C = SSCfg<QDT, SDT, G, D, NST>;
     constexpr bool kExactProduct = (QDT == PT_BF16 && SDT == PT_BF16);
-    constexpr int NST = kSSNst;
     extern __shared__ __align__(128) char smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int S = prm.S, Pmax = prm.Pmax, U = prm.U;
@@ -117,7 +119,7 @@ __global__ void __launch_bounds__(kSSWarps * 32, kSSCtas) k_score_stream(const S
     const bool ps_smem = U <= kSSPsMax;
     uint64_t *bars =
         reinterpret_cast<uint64_t *>(smem + (((size_t)(ps_smem ? U : kSSPsMax) * 4 + 15) & ~(size_t)15)) +
-        warp * NST;
+        warp * kSSNstMax;
     char *wbase = smem + ss_hdr_bytes(U) + (size_t)warp * C::PER_WARP;
     char *ring = wbase;
     char *hdrs = wbase + NST * C::STAGE;
