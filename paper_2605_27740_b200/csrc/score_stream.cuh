@@ -50,9 +50,11 @@ static inline int ss_ctas_per_sm(int Pmax) {
     const int x = forced ? forced : ((Pmax >> 5) < 32 ? 3 : 2);
     return x < 1 ? 1 : (x > kSSCtas ? kSSCtas : x);
 }
-// ring stages per warp: 4 with two CTAs per SM (more bytes in flight: 168 vs 172 us at
-// cfg3), 3 with three (the smem of a fourth stage would not fit three CTAs)
-constexpr int kSSNstMax = 4;
+// ring shape per warp (stages x chunk): two CTAs per SM stream 2 x 8 KB stages (cfg3: 160
+// us = 6.77 TB/s, vs 168 us for 4 x 4 KB and 172 us for 3 x 4 KB -- fewer, larger bulk
+// copies for the same bytes in flight); three CTAs per SM (short contexts) keep 3 x 4 KB,
+// the most that fits three
+constexpr int kSSNstMax = 3;
 
 __device__ __forceinline__ float2 ss_mul2(float m, float2 q) {
     unsigned long long r;
@@ -74,14 +76,14 @@ __device__ __forceinline__ float2 ss_fma2(float m, float2 q, float2 acc) {
     return *reinterpret_cast<float2 *>(&r);
 }
 
-template <int QDT, int SDT, int G, int D, int NST_>
+template <int QDT, int SDT, int G, int D, int NST_, int CPSW>
 struct SSCfg {
     static constexpr int NST = NST_;
     static constexpr int ES = SDT == PT_F32 ? 4 : 2;
     static constexpr int QES = QDT == PT_F32 ? 4 : 2;
     static constexpr int V = 16 / ES;            // means per 16-byte chunk
     static constexpr int NCH = D / V;            // chunks per page row
-    static constexpr int CPS = NCH < 8 ? NCH : 8;
+    static constexpr int CPS = NCH < CPSW ? NCH : CPSW;  // 16-byte chunks per stage
     static constexpr int SPT = NCH / CPS;        // stages per tile
     static constexpr int GP2 = (G + 1) / 2;      // head pairs
     static constexpr int STAGE = CPS * 512;
@@ -105,9 +107,9 @@ __host__ __device__ __forceinline__ size_t ss_hdr_bytes(int U) {
     return (ps + (size_t)kSSWarps * kSSNstMax * 8 + 127) & ~(size_t)127;
 }
 
-template <int QDT, int SDT, int G, int D, int NST>
+template <int QDT, int SDT, int G, int D, int NST, int CPSW>
 __global__ void __launch_bounds__(kSSWarps * 32, kSSCtas) k_score_stream(const StreamScoreParams prm) {
-    using C = SSCfg<QDT, SDT, G, D, NST>;
+    using C = SSCfg<QDT, SDT, G, D, NST, CPSW>;
     constexpr bool kExactProduct = (QDT == PT_BF16 && SDT == PT_BF16);
     extern __shared__ __align__(128) char smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

@@ -3,19 +3,19 @@
 
 namespace pt {
 
-template <int SDT, int G, int D, int NST>
+template <int SDT, int G, int D, int NST, int CPSW>
 static int ss_launch_n(const StreamScoreParams &sp, int ctas, cudaStream_t st) {
-    using C = SSCfg<PT_BF16, SDT, G, D, NST>;
+    using C = SSCfg<PT_BF16, SDT, G, D, NST, CPSW>;
     const size_t smem = ss_hdr_bytes(sp.U) + (size_t)kSSWarps * C::PER_WARP;
     while (ctas > 1 && smem * ctas > 226 * 1024) ctas--;
     if (smem * ctas > 226 * 1024) return PT_ERR_UNSUPPORTED;
     static size_t configured = 0;
     if (smem > configured) {
-        PT_CUDA_TRY(cudaFuncSetAttribute(k_score_stream<PT_BF16, SDT, G, D, NST>,
+        PT_CUDA_TRY(cudaFuncSetAttribute(k_score_stream<PT_BF16, SDT, G, D, NST, CPSW>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured = smem;
     }
-    PT_CUDA_TRY(pt_launch(k_score_stream<PT_BF16, SDT, G, D, NST>, dim3(148 * ctas), dim3(kSSWarps * 32),
+    PT_CUDA_TRY(pt_launch(k_score_stream<PT_BF16, SDT, G, D, NST, CPSW>, dim3(148 * ctas), dim3(kSSWarps * 32),
                           smem, st, sp));
     return PT_OK;
 }
@@ -23,7 +23,7 @@ static int ss_launch_n(const StreamScoreParams &sp, int ctas, cudaStream_t st) {
 template <int SDT, int G, int D>
 static int ss_launch(const StreamScoreParams &sp, cudaStream_t st) {
     const int ctas = ss_ctas_per_sm(sp.Pmax);
-    return ctas >= 3 ? ss_launch_n<SDT, G, D, 3>(sp, ctas, st) : ss_launch_n<SDT, G, D, kSSNstMax>(sp, ctas, st);
+    return ctas >= 3 ? ss_launch_n<SDT, G, D, 3, 8>(sp, ctas, st) : ss_launch_n<SDT, G, D, 2, 16>(sp, ctas, st);
 }
 
 template <int SDT, int D>
