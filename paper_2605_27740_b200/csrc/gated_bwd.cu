@@ -10,7 +10,7 @@
 // Hard-mode (gate 0) pages carry no weight and are skipped, as the reference.
 //
 // Layout: grid (page groups, units); one warp per page at a time.  The page's K and V rows
-// are staged in warp-private shared memory (padded rows: conflict-free column reads); lanes
+// are staged in warp-private shared memory (XOR-swizzled 16-byte chunks); lanes
 // first own tokens (dot products, softmax weights) then dimensions (coalesced dK / dV row
 // writes and the dq partial).  dq partials are reduced in the CTA and added to global memory
 // with one atomic per (head, dim) per CTA.  f32 throughout (the reference runs float64:
@@ -47,11 +47,21 @@ __device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
-// raw staged element -> f32
+// Staged rows are unpadded; the 16-byte chunk c of row r sits at chunk c ^ (r & m), m + 1 =
+// the largest power of two <= 8 dividing the chunks per row (an XOR swizzle: rows of a page
+// map the same logical chunk to different banks, as the former 16-byte row padding did,
+// without its shared memory -- three CTAs per SM instead of two)
+__device__ __forceinline__ int gb_swz_mask(int vpr) {
+    const int low = vpr & -vpr;
+    return (low < 8 ? low : 8) - 1;
+}
+// raw staged element d of row r -> f32
 template <int DT>
-__device__ __forceinline__ float rawval(const char *row, int d) {
-    if constexpr (DT == PT_F32) return reinterpret_cast<const float *>(row)[d];
-    else return bf16_bits_to_f32(reinterpret_cast<const uint16_t *>(row)[d]);
+__device__ __forceinline__ float rawval(const char *row, int r, int d, int m) {
+    constexpr int ES = DT == PT_F32 ? 4 : 2, EPV = 16 / ES;
+    const char *a = row + (((d / EPV) ^ (r & m)) << 4) + (d % EPV) * ES;
+    if constexpr (DT == PT_F32) return *reinterpret_cast<const float *>(a);
+    else return bf16_bits_to_f32(*reinterpret_cast<const uint16_t *>(a));
 }
 
 // Double-buffered: while a warp computes page i, its next page's K and V rows are already
@@ -70,7 +80,7 @@ __global__ void __launch_bounds__(kGBWarps * 32) k_gated_bwd(const GatedBwdParam
     float *sg = dos + MAXG * D;             // [8]
     float *lg = sg + 8;                     // [8]
     float *dqp = lg + 8;                    // [MAXG][D] CTA partial of dq
-    const int rowb = D * ES + 16;           // padded row (bytes)
+    const int rowb = D * ES;                // unpadded row (bytes), chunks swizzled
     const int pageb = S * rowb;
     char *wb = reinterpret_cast<char *>(dqp + MAXG * D) + (size_t)warp * (4 * pageb + 2 * MAXG * S * 4);
     float *wv = reinterpret_cast<float *>(wb + 4 * pageb);  // [S][MAXG]
@@ -109,6 +119,7 @@ __global__ void __launch_bounds__(kGBWarps * 32) k_gated_bwd(const GatedBwdParam
     while (lpt > 1 && (D / lpt) % EPV) lpt >>= 1;
     const int part = lane % lpt, dlen = D / lpt;
     const int vpr = D * ES / 16;           // 16-byte vectors per row
+    const int swm = gb_swz_mask(vpr);
     const int stride = gridDim.x * kGBWarps;
     auto issue = [&](int lp, int b) {      // page lp -> buffer b (nothing for a skipped page)
         if (lp < P && p.gates[u * p.Pmax + lp] != 0.f) {
@@ -119,8 +130,9 @@ __global__ void __launch_bounds__(kGBWarps * 32) k_gated_bwd(const GatedBwdParam
             char *kb = wb + b * 2 * pageb, *vb = kb + pageb;
             for (int i = lane; i < rows * vpr; i += 32) {
                 const int r = i / vpr, c = i - r * vpr;
-                cp_async16(kb + r * rowb + c * 16, kg + (int64_t)i * 16);
-                cp_async16(vb + r * rowb + c * 16, vg + (int64_t)i * 16);
+                const int cs = (c ^ (r & swm)) << 4;
+                cp_async16(kb + r * rowb + cs, kg + (int64_t)i * 16);
+                cp_async16(vb + r * rowb + cs, vg + (int64_t)i * 16);
             }
         }
         cp_async_commit();  // (possibly empty) one group per page keeps the accounting uniform
@@ -155,11 +167,13 @@ __global__ void __launch_bounds__(kGBWarps * 32) k_gated_bwd(const GatedBwdParam
 #pragma unroll
             for (int g = 0; g < MAXG; g++) kq[g] = vd[g] = 0.f;
             if (live) {
-                const char *kr = kb + t * rowb + part * dlen * ES;
-                const char *vr = vb + t * rowb + part * dlen * ES;
+                const char *kr = kb + t * rowb;
+                const char *vr = vb + t * rowb;
+                const int c0 = part * dlen / EPV;
                 for (int c = 0; c < dlen / EPV; c++) {
-                    const uint4 kx = reinterpret_cast<const uint4 *>(kr)[c];
-                    const uint4 vx = reinterpret_cast<const uint4 *>(vr)[c];
+                    const int cs = ((c0 + c) ^ (t & swm)) << 4;
+                    const uint4 kx = *reinterpret_cast<const uint4 *>(kr + cs);
+                    const uint4 vx = *reinterpret_cast<const uint4 *>(vr + cs);
                     float kf[EPV], vf[EPV];
                     if constexpr (DT == PT_F32) {
                         kf[0] = __uint_as_float(kx.x); kf[1] = __uint_as_float(kx.y);
@@ -227,7 +241,7 @@ __global__ void __launch_bounds__(kGBWarps * 32) k_gated_bwd(const GatedBwdParam
                 if (d >= D) break;
                 float dk = 0.f, dv = 0.f;
                 if (live) {
-                    const float kv = rawval<DT>(kb + t * rowb, d);
+                    const float kv = rawval<DT>(kb + t * rowb, t, d, swm);
 #pragma unroll
                     for (int g = 0; g < MAXG; g++) {
                         if (g >= G) break;
@@ -264,15 +278,27 @@ __global__ void __launch_bounds__(kGBWarps * 32) k_gated_bwd(const GatedBwdParam
 using namespace pt;
 
 template <int DT, int MAXG, int DJ>
-static int launch_gbwd(const GatedBwdParams &p, int U, size_t smem, cudaStream_t st) {
+static int launch_gbwd(const GatedBwdParams &p, int U, cudaStream_t st) {
+    constexpr int ES = DT == PT_F32 ? 4 : 2;
+    const size_t pageb = (size_t)p.S * p.D * ES;
+    const size_t smem = (size_t)(3 * MAXG * p.D + 16) * 4 +
+                        (size_t)kGBWarps * (4 * pageb + 2 * MAXG * p.S * 4);
+    if (smem > 220 * 1024) return PT_ERR_UNSUPPORTED;
     static size_t configured = 0;
     if (smem > configured) {
         PT_CUDA_TRY(cudaFuncSetAttribute(k_gated_bwd<DT, MAXG, DJ>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured = smem;
     }
-    // enough CTAs per unit for ~4 CTAs per SM in total, at least one page per warp
-    int gx = (148 * 4 + U - 1) / U;
+    // one wave: every resident CTA slot (warps stride over the unit's pages), at least one
+    // page per warp
+    int dev = 0, nsm = 0, per_sm = 0;
+    PT_CUDA_TRY(cudaGetDevice(&dev));
+    PT_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    PT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gated_bwd<DT, MAXG, DJ>,
+                                                              kGBWarps * 32, smem));
+    if (per_sm < 1) per_sm = 1;
+    int gx = nsm * per_sm / U;
     const int pages = p.Pmax;
     const int maxgx = (pages + kGBWarps - 1) / kGBWarps;
     if (gx > maxgx) gx = maxgx;
@@ -295,17 +321,11 @@ extern "C" int pt_gated_attend_bwd(const void *q, int q_dtype, const void *k_poo
     if (U == 0) return PT_OK;
     GatedBwdParams p{q, k_pool, v_pool, page_table, seq_len, gates, out, lse, dout, dq, dk_pool,
                      dv_pool, dgates, q_dtype, kv_dtype, G, D, S, Pmax, scale};
-    const int MAXG = 8;
-    const int ES = kv_dtype == PT_F32 ? 4 : 2;
-    const size_t pageb = (size_t)S * (D * ES + 16);
-    const size_t smem = (size_t)(3 * MAXG * D + 16) * 4 +
-                        (size_t)kGBWarps * (4 * pageb + 2 * MAXG * S * 4);
-    if (smem > 220 * 1024) return PT_ERR_UNSUPPORTED;
     cudaStream_t st = (cudaStream_t)stream;
     const int dj = (D + 31) / 32;
 #define PT_GB(DT_, DJ_) \
     if (kv_dtype == DT_ && dj == DJ_) \
-        return G <= 4 ? launch_gbwd<DT_, 4, DJ_>(p, U, smem, st) : launch_gbwd<DT_, 8, DJ_>(p, U, smem, st);
+        return G <= 4 ? launch_gbwd<DT_, 4, DJ_>(p, U, st) : launch_gbwd<DT_, 8, DJ_>(p, U, st);
     PT_GB(PT_F32, 1) PT_GB(PT_F32, 2) PT_GB(PT_F32, 4) PT_GB(PT_F32, 8)
     PT_GB(PT_BF16, 1) PT_GB(PT_BF16, 2) PT_GB(PT_BF16, 4) PT_GB(PT_BF16, 8)
 #undef PT_GB

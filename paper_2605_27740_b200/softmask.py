@@ -144,17 +144,21 @@ def gated_forward(cache: PagedKvCache, queries: torch.Tensor, gates, scale: floa
     if scale is None:
         scale = 1.0 / math.sqrt(D)
     g64 = gates if isinstance(gates, torch.Tensor) and gates.dim() == 2 else _gates_tensor(cache, gates)
-    pages = torch.as_tensor(np.array([cache.num_pages(u) for u in range(U)]), device=cache.device)
-    if bool((pages == 0).any()):
+    npages = np.array([cache.num_pages(u) for u in range(U)])  # host mirror: no device work
+    if int(npages.min()) == 0:
         raise ValueError("attention over an empty context is undefined")
+    pages = torch.as_tensor(npages, device=cache.device)
     live = torch.arange(cache.Pmax, device=cache.device)[None, :] < pages[:, None]
-    if mode == "soft":  # one device reduction for every unit (no per-unit host sync)
+    # every check of a mode in one device reduction and one host read (no per-unit sync)
+    if mode == "soft":
         if bool((((g64 <= 0) | (g64 > 1)) & live).any()):
             raise ValueError("soft gates must lie in (0, 1]")
     elif mode == "hard":
-        if bool((((g64 != 0) & (g64 != 1)) & live).any()):
+        flags = torch.stack([(((g64 != 0) & (g64 != 1)) & live).any(),
+                             (((g64 == 1) & live).sum(dim=1) == 0).any()]).cpu()
+        if bool(flags[0]):
             raise ValueError("hard gates must be binary")
-        if bool((((g64 == 1) & live).sum(dim=1) == 0).any()):
+        if bool(flags[1]):
             raise ValueError("hard mask keeps no pages")
     else:
         raise ValueError(f"unknown gate mode {mode!r}")

@@ -43,16 +43,40 @@ def main():
     stream = torch.cuda.current_stream()
 
     def timeit(fn, reps=10):
-        fn()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(reps):
-            r = fn()
-        e1.record(stream)
+        # median of individually timed calls: a back-to-back loop that keeps the previous
+        # result alive makes the caching allocator cudaMalloc fresh 0.5 GB gradient pools
+        # now and then (one 16 ms outlier dominated the former 10-call mean)
+        r = fn()
         torch.cuda.synchronize()
-        return e0.elapsed_time(e1) * 1000 / reps, r
+        ts = []
+        for _ in range(reps):
+            del r
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            r = fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1000)
+        return sorted(ts)[len(ts) // 2], r
 
     t_fwd, (out, lse) = timeit(lambda: sm.gated_forward(cache, q, gates))
+    # the forward's kernel alone (pt_attend dense mode + per-page bias), buffers preallocated
+    from paper_2605_27740_b200 import _lib
+    from paper_2605_27740_b200 import _device as dv
+    bias = torch.log(gates).to(torch.float32).contiguous()
+    o2, l2 = torch.empty_like(out), torch.empty_like(lse)
+    ws = torch.empty(_lib.load().pt_attend_workspace_bytes(U, G, D, cache.Pmax), dtype=torch.uint8, device=d)
+    tk = torch.zeros(U, dtype=torch.int32, device=d)
+
+    def fwd_kernel():
+        _lib.call("pt_attend", q.data_ptr(), dv.dtype_code(q.dtype), cache.k_pool.data_ptr(),
+                  cache.v_pool.data_ptr(), cache.kv_code, cache.layout.max_pages,
+                  cache.page_table.data_ptr(), cache.Pmax, None, cache.page_table.data_ptr(),
+                  cache.seq_lens.data_ptr(), U, G, D, S, cache.Pmax, bias.data_ptr(),
+                  1.0 / math.sqrt(D), o2.data_ptr(), l2.data_ptr(), ws.data_ptr(), ws.numel(),
+                  tk.data_ptr(), 0, dv.stream_handle())
+        return o2
+    t_fwd_k, _ = timeit(fwd_kernel)
     dout = torch.randn(U * G, D, generator=g, device=d)
     t_bwd, _ = timeit(lambda: sm.gated_backward(cache, q, gates, out, lse, dout))
     bwd_bytes_all = None
@@ -61,9 +85,11 @@ def main():
     bwd_bytes = ntok * D * 2 * 2 + ntok * D * 4 * 2
     print(json.dumps({"units": U, "group": G, "ctx": a.ctx, "tokens": ntok,
                       "fwd_us": t_fwd, "fwd_GBs": fwd_bytes / (t_fwd * 1e-6) / 1e9,
+                      "fwd_kernel_us": t_fwd_k, "fwd_kernel_GBs": fwd_bytes / (t_fwd_k * 1e-6) / 1e9,
                       "bwd_us": t_bwd, "bwd_GBs": bwd_bytes / (t_bwd * 1e-6) / 1e9,
-                      "note": "fwd = pt_attend dense + log-gate bias (incl. the host-side gate "
-                              "checks); bwd = pt_gated_attend_bwd (K, V read; f32 dK, dV written)"},
+                      "note": "median of 10 individually timed calls (CUDA events); fwd = pt_attend dense + "
+                              "log-gate bias (incl. the host-side gate checks); bwd = gated_backward "
+                              "(pt_gated_attend_bwd + output allocation: K, V read; f32 dK, dV written)"},
                      indent=1))
 
 
