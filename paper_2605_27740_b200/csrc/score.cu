@@ -339,7 +339,8 @@ extern "C" int pt_score(const void *q, int q_dtype, const float *norms, const vo
         (long long)U * (Pmax / 32) < (1LL << 31)) {
         const int rc0 = pt_lam_norms(q, q_dtype, norms, U, G, D, lam, lamnorm_ws, st);
         if (rc0) return rc0;
-        StreamScoreParams sp{q, lamnorm_ws, means, stds, seq_len, keys, scores, U, S, Pmax, tile_max};
+        StreamScoreParams sp{q, lamnorm_ws, means, stds, seq_len, keys, scores, U, S, Pmax, tile_max,
+                             ss_contig(stats_dtype)};
         const int rc = q_dtype == PT_F32 ? launch_score_stream_q32(sp, stats_dtype, G, D, st)
                                          : launch_score_stream_q16(sp, stats_dtype, G, D, st);
         if (rc != PT_ERR_UNSUPPORTED) return rc;
@@ -381,7 +382,8 @@ extern "C" int pt_score_prenorm(const void *q, int q_dtype, const float *lamnorm
         return PT_ERR_UNSUPPORTED;
     if (U == 0) return PT_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    StreamScoreParams sp{q, lamnorm, means, stds, seq_len, keys, scores, U, S, Pmax, tile_max};
+    StreamScoreParams sp{q, lamnorm, means, stds, seq_len, keys, scores, U, S, Pmax, tile_max,
+                         ss_contig(stats_dtype)};
     return q_dtype == PT_F32 ? launch_score_stream_q32(sp, stats_dtype, G, D, st)
                              : launch_score_stream_q16(sp, stats_dtype, G, D, st);
 }

@@ -35,7 +35,18 @@ struct StreamScoreParams {
     float *scores;
     int U, S, Pmax;
     uint16_t *tile_max;  // [U][Pmax/32] max key of each 32-page tile, or null
+    int contig;          // contiguous per-warp tile ranges (set by the launcher, see below)
 };
+
+// Tile order: contiguous per-warp ranges (one query-header fetch + widening per run of a
+// unit's tiles) win for bf16 page means (cfg3: 104 vs 117 us -- half the bytes per element,
+// so the per-tile overhead matters); the grid-stride order (all warps sweep one moving window
+// of the means) wins for f32 (155 vs 160 us).  PT_SS_CONTIG=0/1 overrides (tuning).
+static inline int ss_contig(int sdt) {
+    const char *e = getenv("PT_SS_CONTIG");
+    const int forced = e && *e ? atoi(e) : -1;
+    return forced >= 0 ? forced : (sdt == PT_BF16 ? 1 : 0);
+}
 
 constexpr int kSSWarps = 4;
 constexpr int kSSCtas = 3;  // per SM, at most
@@ -87,12 +98,16 @@ struct SSCfg {
     static constexpr int SPT = NCH / CPS;        // stages per tile
     static constexpr int GP2 = (G + 1) / 2;      // head pairs
     static constexpr int STAGE = CPS * 512;
-    static constexpr int HDR_LN = (G * D * QES + 15) & ~15;
-    static constexpr int HDR_SD = HDR_LN + 32;
-    static constexpr int HDR = (HDR_SD + 128 + 127) & ~127;
+    // unit header (the unit's G query rows + lam*||q_g|| padded to 8): fetched once per run of
+    // consecutive tiles of one unit.  The producer is at most NST stages ahead of the consumer,
+    // i.e. at most (SPT - 1 + NST) / SPT tiles (and runs) ahead: one slot more than that
+    static constexpr int UH_LN = (G * D * QES + 15) & ~15;
+    static constexpr int UHDR = (UH_LN + 32 + 127) & ~127;
+    static constexpr int NHU = (SPT - 1 + NST) / SPT + 1;
+    // per-tile header (the 32 page stds), NHDR slots
     static constexpr int NHDR = NST / SPT + 2;
     static constexpr int QF = (GP2 * 2 * D * 4 + 127) & ~127;
-    static constexpr int PER_WARP = NST * STAGE + NHDR * HDR + QF;
+    static constexpr int PER_WARP = NST * STAGE + NHU * UHDR + NHDR * 128 + QF;
     static constexpr uint32_t QCOPY = (uint32_t)((G * D * QES + 15) & ~15);
     static_assert(NCH % CPS == 0, "chunks per stage must divide the row");
 };
@@ -103,7 +118,7 @@ constexpr int kSSPsMax = 2048;
 
 __host__ __device__ __forceinline__ size_t ss_hdr_bytes(int U) {
     if (U > kSSPsMax) U = kSSPsMax;
-    const size_t ps = ((size_t)U * 4 + 15) & ~(size_t)15;
+    const size_t ps = ((size_t)(U + 1) * 4 + 15) & ~(size_t)15;
     return (ps + (size_t)kSSWarps * kSSNstMax * 8 + 127) & ~(size_t)127;
 }
 
@@ -117,15 +132,24 @@ __global__ void __launch_bounds__(kSSWarps * 32, kSSCtas) k_score_stream(const S
     const int TPU = Pmax >> 5;
     const int W = gridDim.x * kSSWarps;
     const int gw = blockIdx.x * kSSWarps + warp;
-    int *Ps = reinterpret_cast<int *>(smem);
-    const bool ps_smem = U <= kSSPsMax;
+    // contiguous order (U <= kSSPsMax): Tp[u] = first tile of unit u in the concatenation of
+    // every unit's ceil(P_u / 32) tiles, and warp gw streams the tiles [gw T / W, (gw+1) T / W)
+    // (runs of one unit: its query header is fetched and widened once per run).  Grid-stride
+    // order: tiles gw, gw + W, ... of the unit-major tile space (a header per tile).
+    // one shared array: Tp (contiguous order) or the page counts Ps (grid-stride order, the
+    // cursor's skip test reads them per tile)
+    int *Tp = reinterpret_cast<int *>(smem);
+    int *Ps = Tp;
+    const bool contig = prm.contig && U <= kSSPsMax;
+    const bool ps_smem = !contig && U <= kSSPsMax;
     uint64_t *bars =
-        reinterpret_cast<uint64_t *>(smem + (((size_t)(ps_smem ? U : kSSPsMax) * 4 + 15) & ~(size_t)15)) +
+        reinterpret_cast<uint64_t *>(smem + (((size_t)((U < kSSPsMax ? U : kSSPsMax) + 1) * 4 + 15) & ~(size_t)15)) +
         warp * kSSNstMax;
     char *wbase = smem + ss_hdr_bytes(U) + (size_t)warp * C::PER_WARP;
     char *ring = wbase;
-    char *hdrs = wbase + NST * C::STAGE;
-    float *qf = reinterpret_cast<float *>(hdrs + C::NHDR * C::HDR);
+    char *uhdrs = wbase + NST * C::STAGE;
+    char *thdrs = uhdrs + C::NHU * C::UHDR;
+    float *qf = reinterpret_cast<float *>(thdrs + C::NHDR * 128);
     if (lane == 0) {
         for (int i = 0; i < NST; i++) mbar_init(&bars[i], 1);
         fence_mbar_init();
@@ -134,60 +158,125 @@ __global__ void __launch_bounds__(kSSWarps * 32, kSSCtas) k_score_stream(const S
     // dependents may launch only once every CTA is past its own wait: an overlapped
     // select+attend then never runs beside a predecessor of this kernel (the append)
     pdl_trigger();
-    if (ps_smem)
+    if (contig) {  // tile prefix over units (block scan; U <= kSSPsMax)
+        __shared__ int wsum[kSSWarps];
+        int carry = 0;
+        for (int b0 = 0; b0 < U; b0 += kSSWarps * 32) {
+            const int uu = b0 + threadIdx.x;
+            const int nt = uu < U ? ((prm.seq_len[uu] + S - 1) / S + 31) >> 5 : 0;
+            int inc = nt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+            }
+            if (lane == 31) wsum[warp] = inc;
+            __syncthreads();
+            int pw = 0, tot = 0;
+#pragma unroll
+            for (int w = 0; w < kSSWarps; w++) {
+                if (w < warp) pw += wsum[w];
+                tot += wsum[w];
+            }
+            if (uu < U) Tp[uu] = carry + pw + inc - nt;
+            carry += tot;
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) Tp[U] = carry;
+    } else if (ps_smem) {
         for (int i = threadIdx.x; i < U; i += blockDim.x) Ps[i] = (prm.seq_len[i] + S - 1) / S;
+    }
     __syncthreads();
     auto pages_of = [&](int uu) -> int {
         return ps_smem ? Ps[uu] : (__ldg(prm.seq_len + uu) + S - 1) / S;
     };
-
-    // tile cursors (u, t): advance by W tiles, skipping tiles past a unit's last page
-    // (a division, not a loop over units: W / TPU is in the hundreds for short contexts)
-    auto settle = [&](int &u, int &t) {
-        while (u < U) {
-            if (t >= TPU) { u += t / TPU; t %= TPU; }
-            if (u >= U || t * 32 < pages_of(u)) return;
-            t += W;
+    // ---- tile cursor: (u, t) plus the position in this warp's range ----
+    struct Cur { int u, t, g; };
+    int64_t g_end = 0;
+    auto first_cursor = [&]() -> Cur {
+        Cur c{U, 0, 0};
+        if (contig) {
+            const int64_t T = Tp[U];
+            const int64_t g0 = (int64_t)gw * T / W;
+            g_end = (int64_t)(gw + 1) * T / W;
+            if (g0 >= g_end) return c;
+            int lo = 0, hi = U;  // last unit with Tp[u] <= g0 (it has tiles)
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (Tp[mid] <= g0) lo = mid; else hi = mid;
+            }
+            c.u = lo;
+            c.t = (int)(g0 - Tp[lo]);
+            c.g = (int)g0;
+        } else {
+            c.u = gw / TPU;
+            c.t = gw - c.u * TPU;
+            while (c.u < U) {  // settle: skip tiles past a unit's last page
+                if (c.t >= TPU) { c.u += c.t / TPU; c.t %= TPU; }
+                if (c.u >= U || c.t * 32 < pages_of(c.u)) break;
+                c.t += W;
+            }
+        }
+        return c;
+    };
+    auto advance = [&](Cur &c) {
+        if (contig) {
+            c.g++;
+            if (c.g >= g_end) { c.u = U; return; }
+            c.t++;
+            while (c.t >= Tp[c.u + 1] - Tp[c.u]) { c.u++; c.t = 0; }  // c.g < T: a unit follows
+        } else {
+            c.t += W;
+            while (c.u < U) {
+                if (c.t >= TPU) { c.u += c.t / TPU; c.t %= TPU; }
+                if (c.u >= U || c.t * 32 < pages_of(c.u)) break;
+                c.t += W;
+            }
         }
     };
-    int pu = gw / TPU, pt = gw - (gw / TPU) * TPU;  // producer
-    settle(pu, pt);
-    int cu = pu, ct = pt;                            // consumer
-    int p_part = 0, p_seq = 0, issued = 0;
+    Cur pc = first_cursor();  // producer
+    Cur cc = pc;              // consumer
+    int p_part = 0, p_seq = 0, p_run = -1, p_unit = -1, issued = 0;
     const uint64_t evict_first = l2_evict_first_policy();
     auto fill = [&](int consumed) {
-        while (pu < U && issued < consumed + NST) {
+        while (pc.u < U && issued < consumed + NST) {
+            const int slot = issued % NST;
+            const bool new_run = p_part == 0 && pc.u != p_unit;
+            if (new_run) { p_run++; p_unit = pc.u; }
             if (lane == 0) {
-                const int slot = issued % NST;
                 const char *gsrc = static_cast<const char *>(prm.means) +
-                                   ((int64_t)pu * Pmax + (int64_t)pt * 32) * D * C::ES;
+                                   ((int64_t)pc.u * Pmax + (int64_t)pc.t * 32) * D * C::ES;
                 uint32_t tx = C::STAGE;
-                if (p_part == 0) tx += C::QCOPY + 32 + 128;
+                if (p_part == 0) tx += 128 + (new_run ? C::QCOPY + 32 : 0);
                 mbar_arrive_expect_tx(&bars[slot], tx);
                 bulk_g2s_hint(ring + slot * C::STAGE, gsrc + p_part * C::STAGE, C::STAGE, &bars[slot],
                               evict_first);
                 if (p_part == 0) {
-                    char *h = hdrs + (p_seq % C::NHDR) * C::HDR;
-                    bulk_g2s(h, static_cast<const char *>(prm.q) + (int64_t)pu * G * D * C::QES,
-                             C::QCOPY, &bars[slot]);
-                    bulk_g2s(h + C::HDR_LN, prm.lamnorm + (int64_t)pu * 8, 32, &bars[slot]);
-                    bulk_g2s(h + C::HDR_SD, prm.stds + (int64_t)pu * Pmax + pt * 32, 128, &bars[slot]);
+                    bulk_g2s(thdrs + (p_seq % C::NHDR) * 128, prm.stds + (int64_t)pc.u * Pmax + pc.t * 32,
+                             128, &bars[slot]);
+                    if (new_run) {
+                        char *h = uhdrs + (p_run % C::NHU) * C::UHDR;
+                        bulk_g2s(h, static_cast<const char *>(prm.q) + (int64_t)pc.u * G * D * C::QES,
+                                 C::QCOPY, &bars[slot]);
+                        bulk_g2s(h + C::UH_LN, prm.lamnorm + (int64_t)pc.u * 8, 32, &bars[slot]);
+                    }
                 }
             }
             issued++;
             if (++p_part == C::SPT) {
                 p_part = 0;
                 p_seq++;
-                pt += W;
-                settle(pu, pt);
+                advance(pc);
             }
         }
     };
     fill(0);
-    int consumed = 0, seq = 0;
+    int consumed = 0, seq = 0, c_run = -1, c_unit = -1;
     float2 *qf2 = reinterpret_cast<float2 *>(qf);
-    while (cu < U) {
-        const char *h = hdrs + (seq % C::NHDR) * C::HDR;
+    while (cc.u < U) {
+        const bool new_run = cc.u != c_unit;
+        if (new_run) { c_run++; c_unit = cc.u; }
+        const char *uh = uhdrs + (c_run % C::NHU) * C::UHDR;
         float2 acc[C::GP2];
 #pragma unroll
         for (int g = 0; g < C::GP2; g++) acc[g] = make_float2(0.f, 0.f);
@@ -195,18 +284,18 @@ __global__ void __launch_bounds__(kSSWarps * 32, kSSCtas) k_score_stream(const S
         for (int part = 0; part < C::SPT; part++) {
             const int slot = consumed % NST;
             mbar_wait(&bars[slot], (uint32_t)((consumed / NST) & 1));
-            if (part == 0) {  // widen this tile's query rows, head-pair interleaved
+            if (part == 0 && new_run) {  // widen the run's query rows, head-pair interleaved
 #pragma unroll
                 for (int pr = 0; pr < C::GP2; pr++) {
 #pragma unroll
                     for (int d = lane; d < D; d += 32) {
                         float a, b = 0.f;
                         if constexpr (QDT == PT_F32) {
-                            const float *qh = reinterpret_cast<const float *>(h);
+                            const float *qh = reinterpret_cast<const float *>(uh);
                             a = qh[(2 * pr) * D + d];
                             if (2 * pr + 1 < G) b = qh[(2 * pr + 1) * D + d];
                         } else {
-                            const uint16_t *qh = reinterpret_cast<const uint16_t *>(h);
+                            const uint16_t *qh = reinterpret_cast<const uint16_t *>(uh);
                             a = bf16_bits_to_f32(qh[(2 * pr) * D + d]);
                             if (2 * pr + 1 < G) b = bf16_bits_to_f32(qh[(2 * pr + 1) * D + d]);
                         }
@@ -252,8 +341,8 @@ __global__ void __launch_bounds__(kSSWarps * 32, kSSCtas) k_score_stream(const S
             consumed++;
             if (part < C::SPT - 1) fill(consumed);
         }
-        const float *ln = reinterpret_cast<const float *>(h + C::HDR_LN);
-        const float sd = reinterpret_cast<const float *>(h + C::HDR_SD)[lane];
+        const float *ln = reinterpret_cast<const float *>(uh + C::UH_LN);
+        const float sd = reinterpret_cast<const float *>(thdrs + (seq % C::NHDR) * 128)[lane];
         float best = -INFINITY;
 #pragma unroll
         for (int g = 0; g < G; g++) {
@@ -261,22 +350,21 @@ __global__ void __launch_bounds__(kSSWarps * 32, kSSCtas) k_score_stream(const S
             const float a = __fadd_rn(ag, __fmul_rn(ln[g], sd));
             if (a > best) best = a;
         }
-        const int p = ct * 32 + lane;
+        const int p = cc.t * 32 + lane;
         const uint32_t key = encode_ordered(f32_to_bf16_rne(best));
-        const int Pc = pages_of(cu);
+        const int Pc = pages_of(cc.u);
         if (p < Pc) {
-            prm.keys[(int64_t)cu * Pmax + p] = (uint16_t)key;
-            if (prm.scores) prm.scores[(int64_t)cu * Pmax + p] = best;
+            prm.keys[(int64_t)cc.u * Pmax + p] = (uint16_t)key;
+            if (prm.scores) prm.scores[(int64_t)cc.u * Pmax + p] = best;
         }
         if (prm.tile_max) {  // the tile's largest key (pads contribute key 0, the minimum)
             const uint32_t m = __reduce_max_sync(0xffffffffu, p < Pc ? key : 0u);
-            if (lane == 0) prm.tile_max[(int64_t)cu * TPU + ct] = (uint16_t)m;
+            if (lane == 0) prm.tile_max[(int64_t)cc.u * TPU + cc.t] = (uint16_t)m;
         }
         __syncwarp();  // header + qf reads done before their slots are refilled
         fill(consumed);
         seq++;
-        ct += W;
-        settle(cu, ct);
+        advance(cc);
     }
 }
 

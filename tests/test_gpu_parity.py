@@ -87,10 +87,18 @@ def test_compute_page_stats_golden(cuda):
 # ---------------------------------------------------------------------------
 # K2: scoring (f32 scores and ordered bf16 keys, bit-exact)
 # ---------------------------------------------------------------------------
+# tile order of the streaming scorer: the launcher's choice per stats dtype, or forced
+# contiguous per-warp ranges / grid-stride (PT_SS_CONTIG)
+ORDERS = {"auto": None, "contig": "1", "stride": "0"}
+
+
 @pytest.mark.parametrize("G", [1, 2, 3, 4, 8])
 @pytest.mark.parametrize("qdt", ["f32", "bf16"])
-def test_scores_bit_exact(cuda, oracle, G, qdt):
+@pytest.mark.parametrize("order", list(ORDERS))
+def test_scores_bit_exact(cuda, oracle, G, qdt, order, monkeypatch):
     pt = _pt()
+    if ORDERS[order] is not None:
+        monkeypatch.setenv("PT_SS_CONTIG", ORDERS[order])
     rng = np.random.default_rng(7 + G)
     B, H, D, S = 2, 2, 128, 16
     lens = rng.integers(S, 300 * S, size=B * H)
@@ -113,8 +121,11 @@ def test_scores_bit_exact(cuda, oracle, G, qdt):
         np.testing.assert_array_equal(keys, oracle.encode_ordered(oracle.f32_to_bf16(want)))
 
 
-def test_scores_bf16_stats_bit_exact(cuda, oracle):
+@pytest.mark.parametrize("order", list(ORDERS))
+def test_scores_bf16_stats_bit_exact(cuda, oracle, order, monkeypatch):
     pt = _pt()
+    if ORDERS[order] is not None:
+        monkeypatch.setenv("PT_SS_CONTIG", ORDERS[order])
     rng = np.random.default_rng(11)
     cache = make_cache(rng, 1, 2, 128, 16, [5000, 3001], dtype="bf16", stats="bf16")
     eng = pt.DecodeEngine(cache, 4, 8, keep_scores=True)
