@@ -427,11 +427,13 @@ def main():
         os.environ["PT_ATTEND_SPLIT"] = "1"
         tune["attend_split_auto"] = timeit(lambda: eng.attend(qs[0]))
         os.environ.pop("PT_ATTEND_SPLIT")
-        for nst in ("2", "3", "4"):
-            for cps in ("4", "8", "16"):
-                os.environ["PT_SCORE_NST"], os.environ["PT_SCORE_CPS"] = nst, cps
-                tune[f"score_stream_nst{nst}_cps{cps}"] = timeit(lambda: eng.score(qs[0]))
-        os.environ.pop("PT_SCORE_NST"); os.environ.pop("PT_SCORE_CPS")
+        # streaming scorer: CTAs per SM (ring shape follows: 2 x 8 KB stages at <= 2 CTAs,
+        # 3 x 4 KB at 3) x tile order (contiguous per-warp ranges or grid-stride)
+        for ctas in ("1", "2", "3"):
+            for contig in ("0", "1"):
+                os.environ["PT_SS_CTAS"], os.environ["PT_SS_CONTIG"] = ctas, contig
+                tune[f"score_stream_ctas{ctas}_contig{contig}"] = timeit(lambda: eng.score(qs[0]))
+        os.environ.pop("PT_SS_CTAS"); os.environ.pop("PT_SS_CONTIG")
         os.environ["PT_SCORE_CTA"] = "1"
         tune["score_cta"] = timeit(lambda: eng.score(qs[0]))
         os.environ.pop("PT_SCORE_CTA")

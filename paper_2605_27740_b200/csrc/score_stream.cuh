@@ -51,13 +51,11 @@ static inline int ss_contig(int sdt) {
 constexpr int kSSWarps = 4;
 constexpr int kSSCtas = 3;  // per SM, at most
 // CTAs per SM of the persistent grid (PT_SS_CTAS overrides, 1..3: tuning).  Measured: two
-// (8 warps) beat three at long contexts (170 vs 180 us at cfg3: 257 tiles per unit), three
-// win for short ones (8K context: 17 tiles per unit, per-tile header / cursor latency).
+// (8 warps) beat three at long contexts (cfg3: 161 vs 169 us f32, 105 vs 107 us bf16 means),
+// three win for short ones (8K context: 17 tiles per unit, per-tile header / cursor latency).
 static inline int ss_ctas_per_sm(int Pmax) {
-    static const int forced = [] {
-        const char *e = getenv("PT_SS_CTAS");
-        return e ? atoi(e) : 0;
-    }();
+    const char *e = getenv("PT_SS_CTAS");
+    const int forced = e && *e ? atoi(e) : 0;
     const int x = forced ? forced : ((Pmax >> 5) < 32 ? 3 : 2);
     return x < 1 ? 1 : (x > kSSCtas ? kSSCtas : x);
 }
