@@ -181,11 +181,9 @@ def build_cache(args, device, seed):
     return cache
 
 
-def cpu_baseline(cache, q_bf16, args, budget_s, nthreads):
-    """Reference decode_step (oracle port, bit-identical to the compiled backend) on host
-    cores over a bounded sample of whole sequences of the same workload."""
-    from oracle import oracle as O
-
+def _sample_arrays(cache, q_bf16, args):
+    """Host copies (f32) of the first 2 sequences of the workload: q, compacted K/V pool,
+    page table, lengths, page stats."""
     H, D, S = args.kv_heads, args.head_dim, args.page
     G = args.q_heads // args.kv_heads
     kp = -(-args.budget // S)
@@ -209,6 +207,19 @@ def cpu_baseline(cache, q_bf16, args, budget_s, nthreads):
     means = means[: len(units)].to(torch.float32).cpu().numpy()
     stds = cache.stds[: len(units)].cpu().numpy()
     q = q_bf16.reshape(cache.num_units, G, D)[: len(units)].to(torch.float32).cpu().numpy()
+    return dict(seqs=seqs, units=units, q=q, kpool=kpool, vpool=vpool, tab=tab2, seq=seq,
+                means=means, stds=stds, kp=kp, S=S, D=D, H=H, pids=pids)
+
+
+def cpu_baseline(cache, q_bf16, args, budget_s, nthreads):
+    """Reference decode_step (oracle port, bit-identical to the compiled backend) on host
+    cores over a bounded sample of whole sequences of the same workload."""
+    from oracle import oracle as O
+
+    a = _sample_arrays(cache, q_bf16, args)
+    seqs, units, q, kpool, vpool = a["seqs"], a["units"], a["q"], a["kpool"], a["vpool"]
+    tab2, seq, means, stds, kp, S, D, H, pids = (a[k] for k in ("tab", "seq", "means", "stds",
+                                                              "kp", "S", "D", "H", "pids"))
     reps, t0 = 0, time.perf_counter()
     res = None
     while True:
@@ -229,6 +240,50 @@ def cpu_baseline(cache, q_bf16, args, budget_s, nthreads):
         "_res": res,
         "_units": len(units),
         "_pids": pids,
+    }
+
+
+def ref_kernels_baseline(cache, q_bf16, args, budget_s, nproc, reps_max=None):
+    """The reference's OWN compiled kernels (oracle/_ref, built from the reference sources)
+    driven as its decode_step, units fanned out over a process pool; cross-checked against
+    the port (selection sets equal, outputs within 1e-5).  None when oracle/_ref is absent."""
+    from oracle import oracle as O
+    from oracle import ref_arm
+
+    if ref_arm.so_path() is None:
+        return None
+    a = _sample_arrays(cache, q_bf16, args)
+    arm = ref_arm.RefArm(a["q"], a["kpool"], a["vpool"], a["tab"], a["seq"], a["means"],
+                         a["stds"], a["kp"], 0.5, a["S"], nproc)
+    try:
+        res = arm.run()  # warm the workers
+        reps, t0 = 0, time.perf_counter()
+        while True:
+            res = arm.run()
+            reps += 1
+            if time.perf_counter() - t0 > budget_s or (reps_max and reps >= reps_max):
+                break
+        dt = (time.perf_counter() - t0) / reps
+    finally:
+        arm.close()
+    port = O.decode_units(a["q"], a["kpool"], a["vpool"], a["tab"], a["seq"], a["means"],
+                          a["stds"], a["kp"], 0.5, 1.0 / math.sqrt(a["D"]), a["S"])
+    for u, (phys, out, lse) in enumerate(res):
+        got = set(port["sel"][u][: port["n_sel"][u]].tolist())
+        if set(phys.tolist()) != got:
+            raise RuntimeError(f"reference kernels and oracle port disagree on unit {u}'s pages")
+        np.testing.assert_allclose(out, port["out"][u], rtol=1e-5, atol=1e-5)
+    return {
+        "value": a["seqs"] / dt,
+        "unit": UNIT,
+        "cores": arm.nproc,
+        "kind": "reference",
+        "sample": f"{a['seqs']} sequences x {a['H']} kv-heads (128K ctx, k={a['kp']} pages, bf16 "
+                  f"values upcast to f32) per rep, {reps} reps in {time.perf_counter() - t0:.1f}s; "
+                  "the reference's own compiled kernels (oracle/_ref/_kernels_cy from "
+                  "pkg/src/pagetopk/_kernels_cy.pyx) driven as attention.decode_step, one unit "
+                  f"per task over {arm.nproc} forked processes (kernels hold the GIL); "
+                  "selections/outputs checked against the port",
     }
 
 
@@ -284,10 +339,18 @@ def main():
             q = torch.randn(cache.num_units * G, D, generator=qg, device=device).to(torch.bfloat16)
             budget = args.cpu_seconds
             vals = []
-            for _ in range(args.warmup and 1):
-                cpu_baseline(cache, q, a2, 0.5, ncores)
-            for _ in range(max(1, min(args.steps, 3))):
-                vals.append(cpu_baseline(cache, q, a2, budget / 3, ncores))
+            # the reference's own compiled kernels when oracle/_ref was built from the
+            # reference sources (kind "reference"), else the oracle port (kind "port")
+            r = ref_kernels_baseline(cache, q, a2, budget / 4, ncores)
+            if r is not None:
+                vals.append(r)
+                for _ in range(max(1, min(args.steps, 3)) - 1):
+                    vals.append(ref_kernels_baseline(cache, q, a2, budget / 4, ncores))
+            else:
+                for _ in range(args.warmup and 1):
+                    cpu_baseline(cache, q, a2, 0.5, ncores)
+                for _ in range(max(1, min(args.steps, 3))):
+                    vals.append(cpu_baseline(cache, q, a2, budget / 3, ncores))
             v = statistics.median([x["value"] for x in vals])
             cb = {k: vals[0][k] for k in ("unit", "cores", "kind", "sample")}
             cb["value"] = v
