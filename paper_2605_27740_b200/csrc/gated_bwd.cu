@@ -85,29 +85,39 @@ __global__ void __launch_bounds__(kGBWarps * 32) k_gated_bwd(const GatedBwdParam
     char *wb = reinterpret_cast<char *>(dqp + MAXG * D) + (size_t)warp * (4 * pageb + 2 * MAXG * S * 4);
     float *wv = reinterpret_cast<float *>(wb + 4 * pageb);  // [S][MAXG]
     float *dzv = wv + MAXG * S;                              // [S][MAXG]
-    for (int i = threadIdx.x; i < G * D; i += blockDim.x) {
+    // heads G..MAXG-1 are padding: zero q / dout and lse = +inf, so their softmax weights
+    // and gradients are exactly zero and every per-head loop runs MAXG times, branch-free
+    for (int i = threadIdx.x; i < MAXG * D; i += blockDim.x) {
         const int g = i / D, d = i % D;
-        const int64_t row = (u * G + g) * (int64_t)D + d;
-        qs[g * D + d] = p.q_dtype == PT_F32 ? static_cast<const float *>(p.q)[row]
-                                            : bf16_bits_to_f32(static_cast<const uint16_t *>(p.q)[row]);
-        dos[g * D + d] = p.dout[row];
+        float qv = 0.f, dv = 0.f;
+        if (g < G) {
+            const int64_t row = (u * G + g) * (int64_t)D + d;
+            qv = p.q_dtype == PT_F32 ? static_cast<const float *>(p.q)[row]
+                                     : bf16_bits_to_f32(static_cast<const uint16_t *>(p.q)[row]);
+            dv = p.dout[row];
+        }
+        qs[g * D + d] = qv;
+        dos[g * D + d] = dv;
         dqp[g * D + d] = 0.f;
     }
     __syncthreads();
-    if (warp < G) {  // s_g = dout_g . out_g (warp g)
+    for (int g = warp; g < MAXG; g += kGBWarps) {  // s_g = dout_g . out_g (warp per head)
         float a = 0.f;
-        for (int d = lane; d < D; d += 32) a += dos[warp * D + d] * p.out[(u * G + warp) * (int64_t)D + d];
+        if (g < G)
+            for (int d = lane; d < D; d += 32) a += dos[g * D + d] * p.out[(u * G + g) * (int64_t)D + d];
         for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-        if (lane == 0) { sg[warp] = a; lg[warp] = p.lse[u * G + warp]; }
+        if (lane == 0) { sg[g] = a; lg[g] = g < G ? p.lse[u * G + g] : INFINITY; }
     }
     __syncthreads();
+    // lanes own DJ consecutive dimensions (d = lane * DJ + j): vector shared loads of the
+    // staged K row and vector dK / dV stores in the dims phase
     float qr[MAXG][DJ], dr[MAXG][DJ], dq_acc[MAXG][DJ];
 #pragma unroll
     for (int g = 0; g < MAXG; g++)
 #pragma unroll
         for (int j = 0; j < DJ; j++) {
-            const int d = lane + 32 * j;
-            const bool ok = g < G && d < D;
+            const int d = lane * DJ + j;
+            const bool ok = d < D;
             qr[g][j] = ok ? qs[g * D + d] : 0.f;
             dr[g][j] = ok ? dos[g * D + d] : 0.f;
             dq_acc[g][j] = 0.f;
@@ -191,7 +201,6 @@ __global__ void __launch_bounds__(kGBWarps * 32) k_gated_bwd(const GatedBwdParam
                     const int d0 = part * dlen + c * EPV;
 #pragma unroll
                     for (int g = 0; g < MAXG; g++) {
-                        if (g >= G) break;
 #pragma unroll
                         for (int e4 = 0; e4 < EPV; e4 += 4) {
                             const float4 q4 = *reinterpret_cast<const float4 *>(qs + g * D + d0 + e4);
@@ -204,7 +213,6 @@ __global__ void __launch_bounds__(kGBWarps * 32) k_gated_bwd(const GatedBwdParam
             }
 #pragma unroll
             for (int g = 0; g < MAXG; g++) {
-                if (g >= G) break;
                 for (int o = 1; o < lpt; o <<= 1) {
                     kq[g] += __shfl_xor_sync(0xffffffffu, kq[g], o);
                     vd[g] += __shfl_xor_sync(0xffffffffu, vd[g], o);
@@ -235,23 +243,57 @@ __global__ void __launch_bounds__(kGBWarps * 32) k_gated_bwd(const GatedBwdParam
                 zt[g4] = b.x; zt[g4 + 1] = b.y; zt[g4 + 2] = b.z; zt[g4 + 3] = b.w;
             }
             const bool live = t < rows;
+            float kv[DJ];
+            if (DJ % 4 == 0 && D == 32 * DJ) {  // 4 consecutive dims share one 16-byte chunk
 #pragma unroll
-            for (int j = 0; j < DJ; j++) {
-                const int d = lane + 32 * j;
-                if (d >= D) break;
-                float dk = 0.f, dv = 0.f;
-                if (live) {
-                    const float kv = rawval<DT>(kb + t * rowb, t, d, swm);
-#pragma unroll
-                    for (int g = 0; g < MAXG; g++) {
-                        if (g >= G) break;
-                        dv = fmaf(wt[g], dr[g][j], dv);
-                        dk = fmaf(zt[g], qr[g][j], dk);
-                        dq_acc[g][j] = fmaf(zt[g], kv, dq_acc[g][j]);
+                for (int j4 = 0; j4 < DJ; j4 += 4) {
+                    const int d = lane * DJ + j4;
+                    const char *a = kb + t * rowb + (((d / EPV) ^ (t & swm)) << 4) + (d % EPV) * ES;
+                    if constexpr (DT == PT_F32) {
+                        const float4 x = *reinterpret_cast<const float4 *>(a);
+                        kv[j4] = x.x; kv[j4 + 1] = x.y; kv[j4 + 2] = x.z; kv[j4 + 3] = x.w;
+                    } else {
+                        const uint2 x = *reinterpret_cast<const uint2 *>(a);
+                        kv[j4] = bf16_lo(x.x); kv[j4 + 1] = bf16_hi(x.x);
+                        kv[j4 + 2] = bf16_lo(x.y); kv[j4 + 3] = bf16_hi(x.y);
                     }
                 }
-                p.dk_pool[base + (int64_t)t * D + d] = dk * p.scale;
-                p.dv_pool[base + (int64_t)t * D + d] = dv;
+            } else {
+#pragma unroll
+                for (int j = 0; j < DJ; j++) {
+                    const int d = lane * DJ + j;
+                    kv[j] = d < D ? rawval<DT>(kb + t * rowb, t, d, swm) : 0.f;
+                }
+            }
+            float dk[DJ], dv[DJ];
+#pragma unroll
+            for (int j = 0; j < DJ; j++) {
+                dk[j] = dv[j] = 0.f;
+                if (live) {
+#pragma unroll
+                    for (int g = 0; g < MAXG; g++) {
+                        dv[j] = fmaf(wt[g], dr[g][j], dv[j]);
+                        dk[j] = fmaf(zt[g], qr[g][j], dk[j]);
+                        dq_acc[g][j] = fmaf(zt[g], kv[j], dq_acc[g][j]);
+                    }
+                }
+                dk[j] *= p.scale;
+            }
+            float *dkr = p.dk_pool + base + (int64_t)t * D;
+            float *dvr = p.dv_pool + base + (int64_t)t * D;
+            if (DJ % 4 == 0 && D == 32 * DJ) {
+#pragma unroll
+                for (int j4 = 0; j4 < DJ; j4 += 4) {
+                    const int d = lane * DJ + j4;
+                    __stcs(reinterpret_cast<float4 *>(dkr + d), make_float4(dk[j4], dk[j4 + 1], dk[j4 + 2], dk[j4 + 3]));
+                    __stcs(reinterpret_cast<float4 *>(dvr + d), make_float4(dv[j4], dv[j4 + 1], dv[j4 + 2], dv[j4 + 3]));
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < DJ; j++) {
+                    const int d = lane * DJ + j;
+                    if (d < D) { dkr[d] = dk[j]; dvr[d] = dv[j]; }
+                }
             }
         }
         __syncwarp();  // the buffer is reused two pages later
@@ -262,7 +304,7 @@ __global__ void __launch_bounds__(kGBWarps * 32) k_gated_bwd(const GatedBwdParam
         if (g >= G) break;
 #pragma unroll
         for (int j = 0; j < DJ; j++) {
-            const int d = lane + 32 * j;
+            const int d = lane * DJ + j;
             if (d < D) atomicAdd(&dqp[g * D + d], dq_acc[g][j] * p.scale);
         }
     }
