@@ -138,11 +138,21 @@ __global__ void __launch_bounds__(kGBWarps * 32) k_gated_bwd(const GatedBwdParam
             const char *kg = static_cast<const char *>(p.k_pool) + pid * S * D * ES;
             const char *vg = static_cast<const char *>(p.v_pool) + pid * S * D * ES;
             char *kb = wb + b * 2 * pageb, *vb = kb + pageb;
-            for (int i = lane; i < rows * vpr; i += 32) {
-                const int r = i / vpr, c = i - r * vpr;
-                const int cs = (c ^ (r & swm)) << 4;
-                cp_async16(kb + r * rowb + cs, kg + (int64_t)i * 16);
-                cp_async16(vb + r * rowb + cs, vg + (int64_t)i * 16);
+            if (vpr <= 32 && 32 % vpr == 0) {  // fixed chunk per lane, 32 / vpr rows per round
+                const int c = lane % vpr, rpi = 32 / vpr;
+                for (int r = lane / vpr; r < rows; r += rpi) {
+                    const int cs = (c ^ (r & swm)) << 4;
+                    const int64_t off = (int64_t)(r * vpr + c) * 16;
+                    cp_async16(kb + r * rowb + cs, kg + off);
+                    cp_async16(vb + r * rowb + cs, vg + off);
+                }
+            } else {
+                for (int i = lane; i < rows * vpr; i += 32) {
+                    const int r = i / vpr, c = i - r * vpr;
+                    const int cs = (c ^ (r & swm)) << 4;
+                    cp_async16(kb + r * rowb + cs, kg + (int64_t)i * 16);
+                    cp_async16(vb + r * rowb + cs, vg + (int64_t)i * 16);
+                }
             }
         }
         cp_async_commit();  // (possibly empty) one group per page keeps the accounting uniform
@@ -232,8 +242,9 @@ __global__ void __launch_bounds__(kGBWarps * 32) k_gated_bwd(const GatedBwdParam
         for (int o = 16; o > 0; o >>= 1) dgate += __shfl_xor_sync(0xffffffffu, dgate, o);
         if (lane == 0) p.dgates[u * p.Pmax + lp] = dgate / gate;
         __syncwarp();
-        // lanes own dims: dK / dV rows (summed over heads; zero rows past the page's end)
-        for (int t = 0; t < S; t++) {
+        // lanes own dims: dK / dV rows (summed over heads); rows past the page's end are
+        // written as zeros below (their staged K rows are stale, so they stay out of dq)
+        for (int t = 0; t < rows; t++) {
             float wt[MAXG], zt[MAXG];
 #pragma unroll
             for (int g4 = 0; g4 < MAXG; g4 += 4) {
@@ -242,7 +253,6 @@ __global__ void __launch_bounds__(kGBWarps * 32) k_gated_bwd(const GatedBwdParam
                 wt[g4] = a.x; wt[g4 + 1] = a.y; wt[g4 + 2] = a.z; wt[g4 + 3] = a.w;
                 zt[g4] = b.x; zt[g4 + 1] = b.y; zt[g4 + 2] = b.z; zt[g4 + 3] = b.w;
             }
-            const bool live = t < rows;
             float kv[DJ];
             if (DJ % 4 == 0 && D == 32 * DJ) {  // 4 consecutive dims share one 16-byte chunk
 #pragma unroll
@@ -269,13 +279,11 @@ __global__ void __launch_bounds__(kGBWarps * 32) k_gated_bwd(const GatedBwdParam
 #pragma unroll
             for (int j = 0; j < DJ; j++) {
                 dk[j] = dv[j] = 0.f;
-                if (live) {
 #pragma unroll
-                    for (int g = 0; g < MAXG; g++) {
-                        dv[j] = fmaf(wt[g], dr[g][j], dv[j]);
-                        dk[j] = fmaf(zt[g], qr[g][j], dk[j]);
-                        dq_acc[g][j] = fmaf(zt[g], kv[j], dq_acc[g][j]);
-                    }
+                for (int g = 0; g < MAXG; g++) {
+                    dv[j] = fmaf(wt[g], dr[g][j], dv[j]);
+                    dk[j] = fmaf(zt[g], qr[g][j], dk[j]);
+                    dq_acc[g][j] = fmaf(zt[g], kv[j], dq_acc[g][j]);
                 }
                 dk[j] *= p.scale;
             }
@@ -295,6 +303,10 @@ __global__ void __launch_bounds__(kGBWarps * 32) k_gated_bwd(const GatedBwdParam
                     if (d < D) { dkr[d] = dk[j]; dvr[d] = dv[j]; }
                 }
             }
+        }
+        for (int i = rows * D + lane; i < S * D; i += 32) {
+            p.dk_pool[base + i] = 0.f;
+            p.dv_pool[base + i] = 0.f;
         }
         __syncwarp();  // the buffer is reused two pages later
     }
