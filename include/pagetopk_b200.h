@@ -227,6 +227,13 @@ PT_API int pt_gated_attend_bwd(const void *q, int q_dtype, const void *k_pool, c
                                float *dq, float *dk_pool, float *dv_pool, float *dgates,
                                void *stream);
 
+/* Soft-mask forward prologue (softmask.py:108-176, soft mode): checks every gate of a live
+ * page (page < ceil(seq_len[u] / S)) lies in (0, 1] and writes bias[u][p] = f32(log(gate)) for
+ * all U x Pmax slots (gates float64 [U][Pmax]).  *flag (device int32) is set to 1 when a live
+ * gate is out of range ("soft gates must lie in (0, 1]"); the caller reads it. */
+PT_API int pt_gate_bias(const double *gates, const int32_t *seq_len, int U, int S, int Pmax,
+                        float *bias, int32_t *flag, void *stream);
+
 /* Layout helper: row-major means f32 [U][P][D] -> tiled stats layout (stats_dtype). */
 PT_API int pt_tile_means(const float *means_rowmajor, int U, int P, int D, int Pmax, void *means_tiled,
                   int stats_dtype, void *stream);

@@ -62,6 +62,7 @@ _PROTOS = {
     "pt_debug_append_prof": (_i, [_vp, _i]),
     "pt_gated_attend_bwd": (_i, [_vp, _i, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i,
                                  _i, _f, _vp, _vp, _vp, _vp, _vp]),
+    "pt_gate_bias": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp, _vp]),
     "pt_tile_means": (_i, [_vp, _i, _i, _i, _i, _vp, _i, _vp]),
 }
 

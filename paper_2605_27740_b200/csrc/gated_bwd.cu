@@ -385,3 +385,37 @@ extern "C" int pt_gated_attend_bwd(const void *q, int q_dtype, const void *k_poo
 #undef PT_GB
     return PT_ERR_UNSUPPORTED;
 }
+
+// ---------------------------------------------------------------------------
+// Soft-mode forward prologue (softmask.py:108-176): every gate of a live page must lie in
+// (0, 1] -- bad = (g <= 0) | (g > 1), NaN passes as in the reference's numpy check -- and the
+// attention bias is f32(log(g)) for every (unit, page) slot (the float64 log rounded once,
+// as torch.log(g64).to(float32)).  One pass, one flag word for the caller to read.
+// ---------------------------------------------------------------------------
+__global__ void k_gate_bias(const double *__restrict__ gates, const int32_t *__restrict__ seq_len,
+                            int U, int S, int Pmax, float *__restrict__ bias, int32_t *__restrict__ flag) {
+    const int64_t total = (int64_t)U * Pmax;
+    int bad = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int u = (int)(i / Pmax), pg = (int)(i - (int64_t)u * Pmax);
+        const double g = gates[i];
+        const int P = (seq_len[u] + S - 1) / S;
+        bad |= (pg < P) && ((g <= 0.0) || (g > 1.0));
+        bias[i] = __double2float_rn(log(g));
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+extern "C" int pt_gate_bias(const double *gates, const int32_t *seq_len, int U, int S, int Pmax,
+                            float *bias, int32_t *flag, void *stream) {
+    if (!gates || !seq_len || !bias || !flag || U < 0 || S < 1 || Pmax < 0) return PT_ERR_INVALID;
+    if ((int64_t)U * Pmax == 0) return PT_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    PT_CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int32_t), st));
+    int64_t blocks = ((int64_t)U * Pmax + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    k_gate_bias<<<(int)blocks, 256, 0, st>>>(gates, seq_len, U, S, Pmax, bias, flag);
+    PT_CUDA_TRY(cudaGetLastError());
+    return PT_OK;
+}

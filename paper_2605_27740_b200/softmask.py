@@ -147,13 +147,18 @@ def gated_forward(cache: PagedKvCache, queries: torch.Tensor, gates, scale: floa
     npages = np.array([cache.num_pages(u) for u in range(U)])  # host mirror: no device work
     if int(npages.min()) == 0:
         raise ValueError("attention over an empty context is undefined")
-    pages = torch.as_tensor(npages, device=cache.device)
-    live = torch.arange(cache.Pmax, device=cache.device)[None, :] < pages[:, None]
-    # every check of a mode in one device reduction and one host read (no per-unit sync)
     if mode == "soft":
-        if bool((((g64 <= 0) | (g64 > 1)) & live).any()):
+        # range check of the live gates and the f32 log-gate bias in one kernel, one flag read
+        g64 = g64.to(cache.device, torch.float64).contiguous()
+        bias = torch.empty(U, cache.Pmax, dtype=torch.float32, device=cache.device)
+        flag = torch.empty(1, dtype=torch.int32, device=cache.device)
+        _lib.call("pt_gate_bias", g64.data_ptr(), cache.seq_lens.data_ptr(), U, S, cache.Pmax,
+                  bias.data_ptr(), flag.data_ptr(), dev.stream_handle())
+        if int(flag.item()):
             raise ValueError("soft gates must lie in (0, 1]")
     elif mode == "hard":
+        pages = torch.as_tensor(npages, device=cache.device)
+        live = torch.arange(cache.Pmax, device=cache.device)[None, :] < pages[:, None]
         flags = torch.stack([(((g64 != 0) & (g64 != 1)) & live).any(),
                              (((g64 == 1) & live).sum(dim=1) == 0).any()]).cpu()
         if bool(flags[0]):
@@ -169,7 +174,6 @@ def gated_forward(cache: PagedKvCache, queries: torch.Tensor, gates, scale: floa
     tickets = torch.zeros(U, dtype=torch.int32, device=cache.device)
     qc = dev.dtype_code(q.dtype)
     if mode == "soft":
-        bias = torch.log(g64).to(torch.float32).contiguous()  # log(GATE_FLOOR) ~ -691: finite
         _lib.call("pt_attend", q.data_ptr(), qc, cache.k_pool.data_ptr(), cache.v_pool.data_ptr(),
                   cache.kv_code, cache.layout.max_pages, cache.page_table.data_ptr(), cache.Pmax,
                   None, cache.page_table.data_ptr(), cache.seq_lens.data_ptr(), U, G, D, S,

@@ -641,6 +641,33 @@ def test_softmask_train_step_matches_reference(cuda):
             close(r.d_stds[h], z[f"c{i}_dstd{h}"])
 
 
+def test_gate_bias_kernel(cuda):
+    """pt_gate_bias: f32(log(gate)) bit-equal to torch.log(g64).to(float32) on every slot; the
+    range check sees live pages only (a bad gate past a unit's last page is ignored)."""
+    pt = _pt()
+    from paper_2605_27740_b200 import _device as dev, _lib
+    from paper_2605_27740_b200 import softmask as sm
+
+    rng = np.random.default_rng(21)
+    B, H, D, S = 2, 2, 64, 16
+    cache = make_cache(rng, B, H, D, S, [100, 33, 16, 7], dtype="bf16")
+    U, Pmax = cache.num_units, cache.Pmax
+    g = torch.from_numpy(rng.uniform(1e-300, 1.0, (U, Pmax))).cuda()
+    g[0, 0], g[1, 1] = 1.0, 1e-300
+    bias = torch.empty(U, Pmax, dtype=torch.float32, device="cuda")
+    flag = torch.empty(1, dtype=torch.int32, device="cuda")
+    _lib.call("pt_gate_bias", g.data_ptr(), cache.seq_lens.data_ptr(), U, S, Pmax, bias.data_ptr(),
+              flag.data_ptr(), dev.stream_handle())
+    assert int(flag.item()) == 0
+    assert torch.equal(bias, torch.log(g).to(torch.float32))
+    q = torch.randn(U * 2, D, device="cuda")
+    g[3, 1] = 2.0  # unit 3 holds 7 rows = 1 page: page 1 is not live
+    sm.gated_forward(cache, q, g)
+    g[3, 0] = 0.0
+    with pytest.raises(ValueError, match=r"soft gates must lie in \(0, 1\]"):
+        sm.gated_forward(cache, q, g)
+
+
 def test_gated_attention_single_query_api(cuda, oracle):
     """The reference's single-query gated_attention_forward/backward signature on the device:
     gates of 1 reproduce plain attention (oracle), and the backward's d_gates obey

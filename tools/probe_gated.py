@@ -77,6 +77,15 @@ def main():
                   tk.data_ptr(), 0, dv.stream_handle())
         return o2
     t_fwd_k, _ = timeit(fwd_kernel)
+    # back-to-back launches (no host gap between them): the kernel's own rate
+    fwd_kernel()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(20):
+        fwd_kernel()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t_fwd_k_b2b = e0.elapsed_time(e1) * 1000 / 20
     dout = torch.randn(U * G, D, generator=g, device=d)
     t_bwd, _ = timeit(lambda: sm.gated_backward(cache, q, gates, out, lse, dout))
     bwd_bytes_all = None
@@ -86,8 +95,10 @@ def main():
     print(json.dumps({"units": U, "group": G, "ctx": a.ctx, "tokens": ntok,
                       "fwd_us": t_fwd, "fwd_GBs": fwd_bytes / (t_fwd * 1e-6) / 1e9,
                       "fwd_kernel_us": t_fwd_k, "fwd_kernel_GBs": fwd_bytes / (t_fwd_k * 1e-6) / 1e9,
+                      "fwd_kernel_b2b_us": t_fwd_k_b2b,
+                      "fwd_kernel_b2b_GBs": fwd_bytes / (t_fwd_k_b2b * 1e-6) / 1e9,
                       "bwd_us": t_bwd, "bwd_GBs": bwd_bytes / (t_bwd * 1e-6) / 1e9,
-                      "note": "median of 10 individually timed calls (CUDA events); fwd = pt_attend dense + "
+                      "note": "median of 10 individually timed calls (CUDA events; fwd_kernel_b2b: 20 back-to-back launches); fwd = pt_attend dense + "
                               "log-gate bias (incl. the host-side gate checks); bwd = gated_backward "
                               "(pt_gated_attend_bwd + output allocation: K, V read; f32 dK, dV written)"},
                      indent=1))
