@@ -86,6 +86,25 @@ def main():
     e1.record(stream)
     torch.cuda.synchronize()
     t_fwd_k_b2b = e0.elapsed_time(e1) * 1000 / 20
+    # the same dense pass through the streaming kernel (every page listed, n_sel = pages)
+    nsel = ((cache.seq_lens + S - 1) // S).to(torch.int32)
+    o3, l3 = torch.empty_like(out), torch.empty_like(lse)
+
+    def fwd_stream():
+        _lib.call("pt_attend", q.data_ptr(), dv.dtype_code(q.dtype), cache.k_pool.data_ptr(),
+                  cache.v_pool.data_ptr(), cache.kv_code, cache.layout.max_pages,
+                  cache.page_table.data_ptr(), cache.Pmax, nsel.data_ptr(), cache.page_table.data_ptr(),
+                  cache.seq_lens.data_ptr(), U, G, D, S, cache.Pmax, bias.data_ptr(),
+                  1.0 / math.sqrt(D), o3.data_ptr(), l3.data_ptr(), ws.data_ptr(), ws.numel(),
+                  tk.data_ptr(), 0, dv.stream_handle())
+    fwd_stream()
+    e0.record(stream)
+    for _ in range(20):
+        fwd_stream()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t_fwd_s_b2b = e0.elapsed_time(e1) * 1000 / 20
+    stream_diff = float((o3 - o2).abs().max()), float((l3 - l2).abs().max())
     dout = torch.randn(U * G, D, generator=g, device=d)
     t_bwd, _ = timeit(lambda: sm.gated_backward(cache, q, gates, out, lse, dout))
     bwd_bytes_all = None
@@ -97,6 +116,7 @@ def main():
                       "fwd_kernel_us": t_fwd_k, "fwd_kernel_GBs": fwd_bytes / (t_fwd_k * 1e-6) / 1e9,
                       "fwd_kernel_b2b_us": t_fwd_k_b2b,
                       "fwd_kernel_b2b_GBs": fwd_bytes / (t_fwd_k_b2b * 1e-6) / 1e9,
+                      "fwd_stream_b2b_us": t_fwd_s_b2b, "fwd_stream_vs_split_maxdiff": stream_diff,
                       "bwd_us": t_bwd, "bwd_GBs": bwd_bytes / (t_bwd * 1e-6) / 1e9,
                       "note": "median of 10 individually timed calls (CUDA events; fwd_kernel_b2b: 20 back-to-back launches); fwd = pt_attend dense + "
                               "log-gate bias (incl. the host-side gate checks); bwd = gated_backward "
