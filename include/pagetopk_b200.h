@@ -140,6 +140,11 @@ PT_API int pt_score(const void *q, int q_dtype, const float *norms, const void *
  * returns PT_ERR_UNSUPPORTED outside that kernel's envelope (G <= 8, D in {64, 128}). */
 PT_API int pt_lam_norms(const void *q, int q_dtype, const float *norms, int U, int G, int D,
                         float lam, float *lamnorm, void *stream);
+/* pt_lam_norms_chained: the same norms for a straight PDL chain (append -> norms -> score):
+ * it runs beside the kernel launched before it on the stream (it reads only q) and completes
+ * only after that kernel, so the scoring kernel launched next sees both kernels' writes. */
+PT_API int pt_lam_norms_chained(const void *q, int q_dtype, const float *norms, int U, int G,
+                                int D, float lam, float *lamnorm, void *stream);
 PT_API int pt_score_prenorm(const void *q, int q_dtype, const float *lamnorm, const void *means,
                             int stats_dtype, const float *stds, const int32_t *seq_len, int U,
                             int G, int D, int S, int Pmax, uint16_t *keys, float *scores,

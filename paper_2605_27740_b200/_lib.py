@@ -48,6 +48,7 @@ _PROTOS = {
     "pt_score": (_i, [_vp, _i, _vp, _vp, _i, _vp, _vp, _i, _i, _i, _i, _i, _f, _vp, _vp, _vp, _vp,
                       _vp]),
     "pt_lam_norms": (_i, [_vp, _i, _vp, _i, _i, _i, _f, _vp, _vp]),
+    "pt_lam_norms_chained": (_i, [_vp, _i, _vp, _i, _i, _i, _f, _vp, _vp]),
     "pt_score_prenorm": (_i, [_vp, _i, _vp, _vp, _i, _vp, _vp, _i, _i, _i, _i, _i, _vp, _vp, _vp,
                               _vp]),
     "pt_topk": (_i, [_vp, _vp, _vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp]),

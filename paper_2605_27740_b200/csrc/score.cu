@@ -212,13 +212,17 @@ __global__ void __launch_bounds__(128) k_score(const ScoreParams prm) {
 // then thread r runs numpy's pairwise float64 sum over row r from shared memory -- the
 // accessor-driven sum over global memory would be a chain of dependent load rounds.
 constexpr int kLnRows = 32;
-template <int QDT>
+// LATE (pt_lam_norms_chained): the kernel reads only q, so it runs beside the kernel launched
+// before it and takes its PDL wait at the very end -- it completes only after that kernel, so
+// a PDL successor that waits on it also sees the earlier kernel's writes (a straight chain
+// append -> norms -> score instead of a fork/join of two streams).
+template <int QDT, bool LATE = false>
 __global__ void __launch_bounds__(256) k_lam_norms(const void *__restrict__ q,
                                                    const float *__restrict__ norms_in, int rows,
                                                    int G, int D, float lam, float *__restrict__ out) {
     __shared__ float qs[kLnRows * (kScoreMaxD + 1)];
     pdl_trigger();
-    pdl_wait();
+    if (!LATE) pdl_wait();
     const int r0 = blockIdx.x * kLnRows;
     const int nr = min(kLnRows, rows - r0);
     const int ld = D + 1;  // odd stride: thread r's sequential reads hit distinct banks
@@ -228,22 +232,24 @@ __global__ void __launch_bounds__(256) k_lam_norms(const void *__restrict__ q,
     }
     __syncthreads();
     const int r = threadIdx.x;
-    if (r >= nr) return;
-    float nrm;
-    if (norms_in) {
-        nrm = norms_in[r0 + r];
-    } else {
-        struct Sq {
-            const float *row;
-            __device__ double operator()(int i) const {
-                const double v = (double)row[i];
-                return __dmul_rn(v, v);
-            }
-        } sq{qs + r * ld};
-        nrm = __double2float_rn(__dsqrt_rn(np_sum(sq, D)));
+    if (r < nr) {
+        float nrm;
+        if (norms_in) {
+            nrm = norms_in[r0 + r];
+        } else {
+            struct Sq {
+                const float *row;
+                __device__ double operator()(int i) const {
+                    const double v = (double)row[i];
+                    return __dmul_rn(v, v);
+                }
+            } sq{qs + r * ld};
+            nrm = __double2float_rn(__dsqrt_rn(np_sum(sq, D)));
+        }
+        const int u = (r0 + r) / G, g = (r0 + r) - u * G;
+        out[(int64_t)u * 8 + g] = __fmul_rn(lam, nrm);
     }
-    const int u = (r0 + r) / G, g = (r0 + r) - u * G;
-    out[(int64_t)u * 8 + g] = __fmul_rn(lam, nrm);
+    if (LATE) pdl_wait();
 }
 
 // row-major f32 means [U][P][D] -> tiled stats layout (stats dtype)
@@ -354,7 +360,8 @@ extern "C" int pt_score(const void *q, int q_dtype, const float *norms, const vo
 
 // lam * ||q_g|| of every query row into the padded [U][8] layout of the streaming kernel
 // (scoring.py:39-47 norms, numpy's float64 pairwise order; or lam * the given norms).
-extern "C" int pt_lam_norms(const void *q, int q_dtype, const float *norms, int U, int G, int D,
+template <bool LATE>
+static int lam_norms_launch(const void *q, int q_dtype, const float *norms, int U, int G, int D,
                             float lam, float *lamnorm, void *stream) {
     if (!q || !lamnorm || U < 0 || G < 1 || G > 8 || D < 1 || D > kScoreMaxD) return PT_ERR_INVALID;
     if (U == 0) return PT_OK;
@@ -362,10 +369,20 @@ extern "C" int pt_lam_norms(const void *q, int q_dtype, const float *norms, int 
     const int rows = U * G;
     const dim3 grid((rows + kLnRows - 1) / kLnRows);
     if (q_dtype == PT_F32)
-        PT_CUDA_TRY(pt_launch(k_lam_norms<PT_F32>, grid, dim3(256), 0, st, q, norms, rows, G, D, lam, lamnorm));
+        PT_CUDA_TRY(pt_launch(k_lam_norms<PT_F32, LATE>, grid, dim3(256), 0, st, q, norms, rows, G, D, lam, lamnorm));
     else
-        PT_CUDA_TRY(pt_launch(k_lam_norms<PT_BF16>, grid, dim3(256), 0, st, q, norms, rows, G, D, lam, lamnorm));
+        PT_CUDA_TRY(pt_launch(k_lam_norms<PT_BF16, LATE>, grid, dim3(256), 0, st, q, norms, rows, G, D, lam, lamnorm));
     return PT_OK;
+}
+
+extern "C" int pt_lam_norms(const void *q, int q_dtype, const float *norms, int U, int G, int D,
+                            float lam, float *lamnorm, void *stream) {
+    return lam_norms_launch<false>(q, q_dtype, norms, U, G, D, lam, lamnorm, stream);
+}
+
+extern "C" int pt_lam_norms_chained(const void *q, int q_dtype, const float *norms, int U, int G,
+                                    int D, float lam, float *lamnorm, void *stream) {
+    return lam_norms_launch<true>(q, q_dtype, norms, U, G, D, lam, lamnorm, stream);
 }
 
 // K2 with lam * ||q|| precomputed by pt_lam_norms (so the norms launch can run beside the

@@ -19,6 +19,7 @@ separate launches (pt_topk / pt_attend); ``score_select`` is an alternative K2+K
 from __future__ import annotations
 
 import math
+import os
 
 import torch
 
@@ -78,6 +79,8 @@ class DecodeEngine:
         self.dense_tickets = torch.zeros(U, dtype=torch.int32, device=d)
         self.graph: torch.cuda.CUDAGraph | None = None
         self._side = torch.cuda.Stream(device=d)
+        # append -> norms -> score as one PDL chain (PT_NO_PDL=1: the fork/join instead)
+        self.chain_norms = os.environ.get("PT_NO_PDL", "") != "1" and os.environ.get("PT_NORMS_FORK", "") != "1"
 
     # ------------------------------------------------------------------
     def _q(self, q: torch.Tensor) -> tuple[torch.Tensor, int]:
@@ -98,12 +101,15 @@ class DecodeEngine:
                   dev.ptr(self.scores), self.lamnorm.data_ptr(), self.tile_max.data_ptr(),
                   dev.stream_handle(stream))
 
-    def lam_norms(self, q: torch.Tensor, norms: torch.Tensor | None = None, stream=None) -> None:
+    def lam_norms(self, q: torch.Tensor, norms: torch.Tensor | None = None, stream=None,
+                  chained: bool = False) -> None:
         """fl(lam * ||q_g||) for every query row (scoring.py:39-47) into the [U][8] scratch read
-        by :meth:`score_prenorm`."""
+        by :meth:`score_prenorm`.  ``chained``: pt_lam_norms_chained (runs beside the kernel
+        launched before it, completes after it)."""
         q2, qc = self._q(q)
-        _lib.call("pt_lam_norms", q2.data_ptr(), qc, dev.ptr(norms), self.U, self.G, self.D,
-                  self.lam, self.lamnorm.data_ptr(), dev.stream_handle(stream))
+        _lib.call("pt_lam_norms_chained" if chained else "pt_lam_norms", q2.data_ptr(), qc,
+                  dev.ptr(norms), self.U, self.G, self.D, self.lam, self.lamnorm.data_ptr(),
+                  dev.stream_handle(stream))
 
     def score_prenorm(self, q: torch.Tensor, stream=None) -> bool:
         """K2 reading the norms of :meth:`lam_norms`; False when the shape needs :meth:`score`."""
@@ -202,14 +208,20 @@ class DecodeEngine:
             self.score_select(q, stream=stream)
             self.attend(q, stream=stream)
             return self.out, self.lse
-        # the query norms do not depend on the append: run them beside it on a side stream
-        # (a fork/join that CUDA-graph capture records as two parallel branches)
+        # the query norms do not depend on the append: with PDL they run beside it as the next
+        # link of one chain (append -> norms -> score -> select+attend); without PDL, on a
+        # side stream (a fork/join that CUDA-graph capture records as two parallel branches)
         main = stream if stream is not None else torch.cuda.current_stream()
-        self._side.wait_stream(main)
-        self.lam_norms(q, stream=self._side)
-        if k_new is not None:
-            self.cache.append_batch(k_new, v_new, stream=main)
-        main.wait_stream(self._side)
+        if self.chain_norms:
+            if k_new is not None:
+                self.cache.append_batch(k_new, v_new, stream=main)
+            self.lam_norms(q, stream=main, chained=True)
+        else:
+            self._side.wait_stream(main)
+            self.lam_norms(q, stream=self._side)
+            if k_new is not None:
+                self.cache.append_batch(k_new, v_new, stream=main)
+            main.wait_stream(self._side)
         if not self.score_prenorm(q, stream=main):
             self.score(q, stream=main)
         self.select_attend(q, stream=main)
