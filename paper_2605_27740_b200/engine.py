@@ -2,8 +2,8 @@
 
 One decode step for every (sequence, kv-head) unit of a :class:`PagedKvCache`:
 
-    append K/V row    (K1b: pt_append)        kvcache.py:185-208      } two graph branches
-    lambda * ||q||    (pt_lam_norms)          scoring.py:39-47        }
+    append K/V row    (K1b: pt_append)        kvcache.py:185-208
+    lambda * ||q||    (pt_lam_norms_chained)  scoring.py:39-47        (runs beside the append)
     score             (K2: pt_score_prenorm)  scoring.py:108-124 -> bf16 -> ordered keys
                                               (+ per-32-page tile maxima)
     select + attend   (K3+K4: pt_select_attend) select.py:87-115 + page-table translation,
