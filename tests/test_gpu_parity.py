@@ -320,6 +320,37 @@ def test_append_batch_and_graph_replay(cuda, oracle):
     torch.testing.assert_close(eng.out, out_eager, rtol=0, atol=0)
 
 
+
+def test_chained_norms_equal_fork_join(cuda):
+    """The step as one PDL chain (append -> chained norms -> score -> select+attend) and the
+    fork/join variant (norms on a side stream) give bit-identical pools, stats and outputs."""
+    pt = _pt()
+    B, H, G, D, S = 2, 2, 4, 128, 16
+    lens = [33, 47, 16, 1]
+    caches = [make_cache(np.random.default_rng(5), B, H, D, S, lens, dtype="bf16", spare=4)
+              for _ in range(2)]
+    U = B * H
+    rng = np.random.default_rng(6)
+    q = torch.from_numpy(rng.standard_normal((U * G, D)).astype(np.float32)).cuda().to(torch.bfloat16)
+    kn = torch.from_numpy(rng.standard_normal((U, D)).astype(np.float32)).cuda().to(torch.bfloat16)
+    vn = torch.from_numpy(rng.standard_normal((U, D)).astype(np.float32)).cuda().to(torch.bfloat16)
+    engs = [pt.DecodeEngine(c, G, 4) for c in caches]
+    engs[0].chain_norms, engs[1].chain_norms = True, False
+    for e in engs:
+        e.capture(q, kn, vn)
+    for _ in range(18):  # crosses page boundaries
+        outs = []
+        for e in engs:
+            e.replay()
+            torch.cuda.synchronize()
+            outs.append(e.out.clone())
+        torch.testing.assert_close(outs[0], outs[1], rtol=0, atol=0)
+    for c in caches:
+        c.check_errors()
+    assert [caches[0].seq_len(u) for u in range(U)] == [51, 65, 34, 19]
+    for a, b in zip(gpu_stats(caches[0]), gpu_stats(caches[1])):
+        np.testing.assert_array_equal(a, b)
+
 def test_append_capacity_error(cuda):
     pt = _pt()
     layout = pt.CacheLayout(num_kv_heads=1, head_dim=16, page_size=8, max_pages=2)
