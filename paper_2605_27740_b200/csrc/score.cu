@@ -232,6 +232,7 @@ __global__ void __launch_bounds__(256) k_lam_norms(const void *__restrict__ q,
     }
     __syncthreads();
     const int r = threadIdx.x;
+    float val = 0.f;
     if (r < nr) {
         float nrm;
         if (norms_in) {
@@ -246,10 +247,15 @@ __global__ void __launch_bounds__(256) k_lam_norms(const void *__restrict__ q,
             } sq{qs + r * ld};
             nrm = __double2float_rn(__dsqrt_rn(np_sum(sq, D)));
         }
-        const int u = (r0 + r) / G, g = (r0 + r) - u * G;
-        out[(int64_t)u * 8 + g] = __fmul_rn(lam, nrm);
+        val = __fmul_rn(lam, nrm);
     }
+    // LATE: the norms are computed beside the predecessor, but stored only after its wait --
+    // the previous step's scorer may still be reading lamnorm until then (WAR across steps)
     if (LATE) pdl_wait();
+    if (r < nr) {
+        const int u = (r0 + r) / G, g = (r0 + r) - u * G;
+        out[(int64_t)u * 8 + g] = val;
+    }
 }
 
 // row-major f32 means [U][P][D] -> tiled stats layout (stats dtype)
