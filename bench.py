@@ -441,7 +441,7 @@ def main():
         ev[1].record(stream)
         eng.lam_norms(q)
         ev[2].record(stream)
-        eng.score_prenorm(q)
+        eng.score_step(q)
         ev[3].record(stream)
         eng.select_attend(q)
         ev[4].record(stream)

@@ -84,12 +84,20 @@ PT_API int pt_stream_attention_host(const float *q, const float *keys, const flo
  *   Pmax % 32 == 0.
  */
 
+/* The mirror block (bounded scoring): one device allocation of
+ * pt_mirror_bytes(U, Pmax, D) bytes holding, for every page, its f32 mean rounded to bf16
+ * (page-interleaved tiles [U][Pmax/32][D/8][32][8]), the f32 mean again row-major ([U][Pmax][D],
+ * one contiguous row per page) and an upper bound of ||bf16 mean - f32 mean|| plus the
+ * accumulation slack of pt_score_bounded (f32 [U][Pmax]).  Written by K1 / K1b / the fused
+ * extend when they are given one (f32 stats, D % 8 == 0); NULL: no mirror. */
+PT_API size_t pt_mirror_bytes(int U, int Pmax, int D);
+
 /* K1. kvcache.py:59-71 + :178-183: page statistics of logical pages
  * [page_begin[u], ceil(seq_len[u]/S)) of every unit (page_begin NULL -> all pages).
  * float64 accumulation in numpy's order; means rounded to stats_dtype, std to f32. */
 PT_API int pt_page_stats(const void *k_pool, int kv_dtype, const int32_t *page_table,
                   const int32_t *seq_len, const int32_t *page_begin, int U, int S, int D,
-                  int Pmax, void *means, int stats_dtype, float *stds, void *stream);
+                  int Pmax, void *means, int stats_dtype, float *stds, void *mirror, void *stream);
 
 /* K1b. kvcache.py:185-208 append, batched: one new K/V row per unit ([U][D] kv_dtype)
  * lands in the unit's tail page; a full/absent tail page takes a fresh physical page
@@ -102,7 +110,7 @@ PT_API int pt_page_stats(const void *k_pool, int kv_dtype, const int32_t *page_t
 PT_API int pt_append(const void *k_new, const void *v_new, void *k_pool, void *v_pool, int kv_dtype,
               int32_t *page_table, int32_t *seq_len, int U, int S, int D, int Pmax, void *means,
               int stats_dtype, float *stds, int32_t *pool_state, const int32_t *free_list,
-              int32_t *slot_scratch, void *stream);
+              int32_t *slot_scratch, void *mirror, void *stream);
 
 /* Copy n_rows[u] rows per unit from a dense [U][n_max][D] staging buffer into the pool
  * starting at token position row_begin[u] (kvcache.py:210-233 extend; pages must
@@ -119,7 +127,7 @@ PT_API int pt_write_rows(const void *k_rows, const void *v_rows, int n_max, cons
 PT_API int pt_extend(const void *k_rows, const void *v_rows, int n_max, const int32_t *row_begin,
                      const int32_t *n_rows, void *k_pool, void *v_pool, int kv_dtype,
                      const int32_t *page_table, int U, int S, int D, int Pmax, void *means,
-                     int stats_dtype, float *stds, void *stream);
+                     int stats_dtype, float *stds, void *mirror, void *stream);
 
 /* K2. scoring.py:108-124 + _kernels_cy.pyx:19-43 + bf16.py:18-33 + select.py:51-57:
  * q [U*G][D] (q_dtype); norms f32 [U*G] or NULL (computed as scoring.py:39-47);
@@ -137,17 +145,29 @@ PT_API int pt_score(const void *q, int q_dtype, const float *norms, const void *
  * pt_lam_norms writes fl(lam * ||q_g||) (norms NULL: computed in numpy's float64 order,
  * scoring.py:39-47) into lamnorm f32 [U][8]; pt_score_prenorm is pt_score's streaming
  * kernel reading it (same keys / scores / tile_max, bit for bit).  pt_score_prenorm
- * returns PT_ERR_UNSUPPORTED outside that kernel's envelope (G <= 8, D in {64, 128}). */
+ * returns PT_ERR_UNSUPPORTED outside that kernel's envelope (G <= 8, D in {64, 128}).
+ * qnorm: f32 [U][8] or NULL -- upper bounds of ||q_g|| (for pt_score_bounded). */
 PT_API int pt_lam_norms(const void *q, int q_dtype, const float *norms, int U, int G, int D,
-                        float lam, float *lamnorm, void *stream);
+                        float lam, float *lamnorm, float *qnorm, void *stream);
 /* pt_lam_norms_chained: the same norms for a straight PDL chain (append -> norms -> score):
  * it runs beside the kernel launched before it on the stream (it reads only q) and completes
  * only after that kernel, so the scoring kernel launched next sees both kernels' writes. */
 PT_API int pt_lam_norms_chained(const void *q, int q_dtype, const float *norms, int U, int G,
-                                int D, float lam, float *lamnorm, void *stream);
+                                int D, float lam, float *lamnorm, float *qnorm, void *stream);
 PT_API int pt_score_prenorm(const void *q, int q_dtype, const float *lamnorm, const void *means,
                             int stats_dtype, const float *stds, const int32_t *seq_len, int U,
                             int G, int D, int S, int Pmax, uint16_t *keys, float *scores,
+                            uint16_t *tile_max, void *stream);
+
+/* K2b. Bounded scoring over the bf16 mirror of the f32 page means (half the bytes of K2):
+ * for every page, keys_lo / keys_hi u16 [U][Pmax] = the ordered keys of a lower and an upper
+ * bound of the reference score (the exact key lies in [keys_lo, keys_hi]), and tile_max u16
+ * [U][Pmax/32] = the largest keys_lo of each 32-page tile.  pt_select_attend given keys_hi
+ * turns these into the exact selection of the f32 reference.  bf16 queries, G <= 8,
+ * D in {64, 128}, U <= 2048; PT_ERR_UNSUPPORTED otherwise (use pt_score_prenorm). */
+PT_API int pt_score_bounded(const void *q, int q_dtype, const float *lamnorm, const float *qnorm,
+                            const void *mirror, const float *stds, const int32_t *seq_len, int U,
+                            int G, int D, int S, int Pmax, uint16_t *keys_lo, uint16_t *keys_hi,
                             uint16_t *tile_max, void *stream);
 
 /* K2+K3 fused: pt_score followed by pt_topk in ONE launch -- the last CTA to finish a unit's
@@ -197,9 +217,14 @@ PT_API int pt_attend(const void *q, int q_dtype, const void *k_pool, const void 
  * the k-th largest tile maximum).  Emission order equals pt_topk's (ascending logical).
  * Launched with programmatic dependent launch: its prologue reads seq_len, page_table and q
  * before waiting on the preceding kernel, which therefore must not write those (the
- * package's scorers do not). */
+ * package's scorers do not).
+ * Bounded mode (keys_hi non-NULL): keys / keys_hi / tile_max are pt_score_bounded's; the
+ * exact key of every page whose interval reaches the cut is recomputed from the mirror's
+ * row-major f32 means, stds and lamnorm (pt_lam_norms' [U][8]) -- the outputs equal the
+ * exact mode's over the f32 reference keys.  NULL: keys are exact (the other three unused). */
 PT_API int pt_select_attend(const uint16_t *keys, const uint16_t *tile_max,
-                            const int32_t *seq_len, const int32_t *page_table,
+                            const uint16_t *keys_hi, const void *mirror, const float *stds,
+                            const float *lamnorm, const int32_t *seq_len, const int32_t *page_table,
                             int U, int S, int Pmax, int k, int32_t *sel, int32_t *sel_logical,
                             int32_t *n_sel, int32_t *kth, int32_t *kplus1, const void *q,
                             int q_dtype, const void *k_pool, const void *v_pool, int kv_dtype,

@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB_NAME = "libpagetopk_b200.so"
 LIB_PATH = os.path.join(HERE, LIB_NAME)
-SOURCES = ("stats.cu", "score.cu", "score_stream_q32.cu", "score_stream_q16.cu", "topk.cu", "attend.cu", "attend_mma.cu", "attend_fused.cu", "gated_bwd.cu", "attend_simt_f32.cu",
+SOURCES = ("stats.cu", "score.cu", "score_bounded.cu", "score_stream_q32.cu", "score_stream_q16.cu", "topk.cu", "attend.cu", "attend_mma.cu", "attend_fused.cu", "gated_bwd.cu", "attend_simt_f32.cu",
            "attend_simt_bf16.cu", "capi.cu")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler",
@@ -46,8 +46,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
 
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
+    headers.append(os.path.join(HERE, "..", "include", "pagetopk_b200.h"))
+    newest_header = max(os.path.getmtime(h) for h in headers if os.path.exists(h))
+
     def compile_one(src: str) -> str:
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        if (not force and os.path.exists(obj) and os.path.getmtime(obj) > newest_header
+                and os.path.getmtime(obj) > os.path.getmtime(os.path.join(CSRC, src))):
+            return obj  # up to date (incremental rebuild)
         cmd = [nv, *ARCH, *NVCC_FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

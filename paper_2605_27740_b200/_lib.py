@@ -39,16 +39,19 @@ _PROTOS = {
     "pt_fused_scores_host": (_i, [_vp, _vp, _vp, _vp, _i, _i64, _i, _f, _vp]),
     "pt_radix_select_desc_host": (_i, [_vp, _i64, _i64, _vp, _vp, _vp]),
     "pt_stream_attention_host": (_i, [_vp, _vp, _vp, _i64, _i, _f, _i64, _vp, _vp, _vp]),
-    "pt_page_stats": (_i, [_vp, _i, _vp, _vp, _vp, _i, _i, _i, _i, _vp, _i, _vp, _vp]),
+    "pt_mirror_bytes": (_sz, [_i, _i, _i]),
+    "pt_page_stats": (_i, [_vp, _i, _vp, _vp, _vp, _i, _i, _i, _i, _vp, _i, _vp, _vp, _vp]),
     "pt_append": (_i, [_vp, _vp, _vp, _vp, _i, _vp, _vp, _i, _i, _i, _i, _vp, _i, _vp, _vp,
-                       _vp, _vp, _vp]),
+                       _vp, _vp, _vp, _vp]),
     "pt_write_rows": (_i, [_vp, _vp, _i, _vp, _vp, _vp, _vp, _i, _vp, _i, _i, _i, _i, _vp]),
     "pt_extend": (_i, [_vp, _vp, _i, _vp, _vp, _vp, _vp, _i, _vp, _i, _i, _i, _i, _vp, _i, _vp,
-                       _vp]),
+                       _vp, _vp]),
     "pt_score": (_i, [_vp, _i, _vp, _vp, _i, _vp, _vp, _i, _i, _i, _i, _i, _f, _vp, _vp, _vp, _vp,
                       _vp]),
-    "pt_lam_norms": (_i, [_vp, _i, _vp, _i, _i, _i, _f, _vp, _vp]),
-    "pt_lam_norms_chained": (_i, [_vp, _i, _vp, _i, _i, _i, _f, _vp, _vp]),
+    "pt_lam_norms": (_i, [_vp, _i, _vp, _i, _i, _i, _f, _vp, _vp, _vp]),
+    "pt_lam_norms_chained": (_i, [_vp, _i, _vp, _i, _i, _i, _f, _vp, _vp, _vp]),
+    "pt_score_bounded": (_i, [_vp, _i, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _vp, _vp, _vp,
+                              _vp]),
     "pt_score_prenorm": (_i, [_vp, _i, _vp, _vp, _i, _vp, _vp, _i, _i, _i, _i, _i, _vp, _vp, _vp,
                               _vp]),
     "pt_topk": (_i, [_vp, _vp, _vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp]),
@@ -57,7 +60,8 @@ _PROTOS = {
     "pt_attend_workspace_bytes": (_sz, [_i, _i, _i, _i]),
     "pt_attend": (_i, [_vp, _i, _vp, _vp, _i, _i, _vp, _i, _vp, _vp, _vp, _i, _i, _i, _i, _i, _vp,
                        _f, _vp, _vp, _vp, _sz, _vp, _i, _vp]),
-    "pt_select_attend": (_i, [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp,
+    "pt_select_attend": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp,
+                              _vp, _vp, _i, _vp,
                               _vp, _i, _i, _i, _i, _f, _vp, _vp, _vp, _sz, _vp, _vp]),
     "pt_debug_sa_prof": (_i, [_vp, _i]),
     "pt_debug_append_prof": (_i, [_vp, _i]),

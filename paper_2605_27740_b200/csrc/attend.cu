@@ -89,7 +89,7 @@ extern "C" int pt_attend(const void *q, int q_dtype, const void *k_pool, const v
         int nstage = env_int("PT_ATTEND_NSTAGE", 0);
         if (nstage <= 0) nstage = 3;
         const int ctas_per_sm = env_int("PT_ATTEND_CTAS", 2);
-        const int grid = 148 * ctas_per_sm;
+        const int grid = pt_num_sms() * ctas_per_sm;
         const int W = grid * NW;
         const long long pages_ub = (long long)U * sel_stride;  // bound; exact count on device
         int L = (int)((pages_ub + W - 1) / W);
@@ -136,7 +136,7 @@ extern "C" int pt_attend(const void *q, int q_dtype, const void *k_pool, const v
     const int ctas_per_sm = smem_of(NW, nstage, kMaxPps) <= 110 * 1024 ? 2 : 1;
     if (nsplit <= 0) {
         // enough CTAs for ~4 waves of the resident slots
-        const int target = 148 * ctas_per_sm * 4;
+        const int target = pt_num_sms() * ctas_per_sm * 4;
         nsplit = (target + U - 1) / U;
     }
     const int max_useful = (sel_stride + NW - 1) / NW;

@@ -39,27 +39,88 @@ struct SelAttnParams {
     int region;  // bytes of the shared region (multiple of 1024)
     int prof;    // record phase timestamps into g_sa_prof
     float scale;
+    // bounded mode (keys = lower keys of pt_score_bounded's intervals): the upper keys, and
+    // what the exact key of a page needs -- f32 means (tile layout), stds, fl(lam * ||q_g||)
+    const uint16_t *keys_hi;
+    const float *rows32, *stds, *lamnorm;  // rows32: the mirror's row-major f32 means
+    int rcap;  // pages resolved per round (their f32 means staged in shared memory)
 };
 
 constexpr int kSAWarps = 4;
 
 // Optional phase timestamps (%globaltimer, ns) per CTA for tuning: enabled by
-// PT_SA_PROF=1 on the host, read back with pt_debug_sa_prof().  10 stamps per CTA
-// (6 kernel phases + 4 inside the selection).
+// PT_SA_PROF=1 on the host, read back with pt_debug_sa_prof().  16 stamps per CTA
+// (6 kernel phases + 4 inside the selection + 5 inside the bounded-mode resolve + its rounds).
 constexpr int kSAProfCtas = 4096;
-__device__ unsigned long long g_sa_prof[kSAProfCtas * 10];
+constexpr int kSAProfN = 20;
+__device__ unsigned long long g_sa_prof[kSAProfCtas * kSAProfN];
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
 
+__device__ __forceinline__ void sa_cp_async16(void *smem_dst, const void *gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc)
+                 : "memory");
+}
+__device__ __forceinline__ void sa_cp_async4(void *smem_dst, const void *gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(smem_dst)), "l"(gsrc)
+                 : "memory");
+}
+__device__ __forceinline__ void sa_cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
+// the exact reference score of one page from its staged f32 mean row (the resolve step of
+// bounded mode): K2's exact order -- sequential d, fl(q * m) then fl(acc + .) -- for GG >= G
+// heads (GG = 4 or 8: the compile-time head loop), + fl(lamnorm_g * std), strict-> max
+template <int D, int GG>
+__device__ __forceinline__ float sa_exact_score(const float *row, const float *sq, const float *sln,
+                                                float sd, int G) {
+    const float4 *row4 = reinterpret_cast<const float4 *>(row);
+    float acc[GG];
+#pragma unroll
+    for (int g = 0; g < GG; g++) acc[g] = 0.f;
+#pragma unroll 2
+    for (int c = 0; c < D / 4; c++) {
+        const float4 m4 = row4[c];
+        const float mv[4] = {m4.x, m4.y, m4.z, m4.w};
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+            const float4 *q4 = reinterpret_cast<const float4 *>(sq + (4 * c + e) * 8);
+            const float4 qa = q4[0];
+            float qv[8] = {qa.x, qa.y, qa.z, qa.w, 0.f, 0.f, 0.f, 0.f};
+            if constexpr (GG > 4) {
+                const float4 qc = q4[1];
+                qv[4] = qc.x; qv[5] = qc.y; qv[6] = qc.z; qv[7] = qc.w;
+            }
+#pragma unroll
+            for (int g = 0; g < GG; g++) acc[g] = __fadd_rn(acc[g], __fmul_rn(qv[g], mv[e]));
+        }
+    }
+    float best = -INFINITY;
+#pragma unroll
+    for (int g = 0; g < GG; g++) {
+        if (g < G) {
+            const float a = __fadd_rn(acc[g], __fmul_rn(sln[g], sd));
+            if (a > best) best = a;
+        }
+    }
+    return best;
+}
+
 __host__ __device__ __forceinline__ size_t sa_keys_bytes(int Pmax) {
     return (size_t)((Pmax + 8) / 8) * 16;
 }
+// bounded-mode scratch after the exact-mode selection scratch: upper keys, the query rows
+// widened to f32 [D][8], the resolve list + its counter, the staged f32 means [rcap][D + 4]
+__host__ __device__ __forceinline__ size_t sa_bnd_bytes(int Pmax, int D, int rcap) {
+    return sa_keys_bytes(Pmax) + (size_t)D * 32 + 32 + (size_t)rcap * 8 + 16 + (size_t)rcap * (D + 4) * 4 + 16;
+}
 
 // NT threads run the selection (NT / 32 warps); the first kSAWarps warps stream the pages
-template <int D, int MT, int NT>
+template <int D, int MT, int NT, bool BND>
 __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__ CUtensorMap tmk,
                                                               const __grid_constant__ CUtensorMap tmv,
                                                               const SelAttnParams p) {
@@ -88,7 +149,7 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
     const bool lead = (c == 0);
     const int cta = blockIdx.y * gridDim.x + blockIdx.x;
     const bool prof = p.prof && threadIdx.x == 0 && cta < kSAProfCtas;
-    if (prof) g_sa_prof[cta * 10 + 0] = gtimer();
+    if (prof) g_sa_prof[cta * kSAProfN + 0] = gtimer();
     if (P == 0) {
         if (lead && threadIdx.x == 0) { p.n_sel[u] = 0; p.kth[u] = 0; p.kplus1[u] = -1; }
         return;
@@ -98,7 +159,7 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
     const int tail_pid = p.page_table[u * p.Pmax + P - 1];
     const int tail_rows = n - (P - 1) * S;
     uint32_t qb[KS][2];
-    {
+    if constexpr (!BND) {  // bounded mode: from the f32 rows in shared memory after selecting
         const int gq = lane >> 2;
 #pragma unroll
         for (int ks = 0; ks < KS; ks++) {
@@ -122,7 +183,7 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
         }
     }
     pdl_wait();
-    if (prof) g_sa_prof[cta * 10 + 1] = gtimer();
+    if (prof) g_sa_prof[cta * kSAProfN + 1] = gtimer();
 
     // ---- selection (select.py:87-115): physical ids land in `ids` in emission order ----
     // candidate selection (select_cand: tile-maximum lower bound or bisection, then the
@@ -164,16 +225,170 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
         for (int j = 0; j < kTm; j++)
             if (tm_stage && threadIdx.x + j * NT < ntiles) stm[threadIdx.x + j * NT] = tv[j];
     }
+    // bounded mode: the upper keys and the widened query rows beside them
+    const size_t sel_end = sa_keys_bytes(p.Pmax) + kSelectBins * 4 + (size_t)(p.Pmax / 32) * 2;
+    uint16_t *skhi = reinterpret_cast<uint16_t *>(smem + ((sel_end + 15) & ~(size_t)15));
+    float *sq = reinterpret_cast<float *>(reinterpret_cast<char *>(skhi) + sa_keys_bytes(p.Pmax));
+    float *sln = sq + D * 8;  // fl(lam * ||q_g||), 8
+    int *rlist = reinterpret_cast<int *>(sln + 8);
+    float *rstd = reinterpret_cast<float *>(rlist + p.rcap);
+    int *rcnt = reinterpret_cast<int *>(rstd + p.rcap);
+    float *rstage = reinterpret_cast<float *>(rcnt + 4);
+    if constexpr (BND) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(p.keys_hi + u * (int64_t)p.Pmax);
+        constexpr int kMax = 8;
+        const int nv = (P + 7) / 8;
+        for (int i0 = threadIdx.x; i0 < nv; i0 += kMax * NT) {
+            uint4 v[kMax];
+#pragma unroll
+            for (int j = 0; j < kMax; j++)
+                if (i0 + j * NT < nv) v[j] = __ldcg(src + i0 + j * NT);
+#pragma unroll
+            for (int j = 0; j < kMax; j++)
+                if (i0 + j * NT < nv) reinterpret_cast<uint4 *>(skhi)[i0 + j * NT] = v[j];
+        }
+        for (int i = threadIdx.x; i < D * 8; i += NT) {
+            const int d = i >> 3, g = i & 7;
+            float x = 0.f;
+            if (g < G) {
+                const int64_t e = (u * G + g) * (int64_t)D + d;
+                x = p.q_dtype == PT_BF16 ? bf16_bits_to_f32(static_cast<const uint16_t *>(p.q)[e])
+                                         : static_cast<const float *>(p.q)[e];
+            }
+            sq[i] = x;
+        }
+        if (threadIdx.x < 8) sln[threadIdx.x] = p.lamnorm[u * 8 + threadIdx.x];
+    }
     __syncthreads();
-    const bool selected =
-        select_cand<NT>(skeys, tm_stage ? stm : nullptr,
-                                P, k, p.page_table + u * p.Pmax, o_sel, o_log, o_n, o_kth, o_kp1,
-                                csh, ids, true, prof ? &g_sa_prof[cta * 10 + 6] : nullptr, true);
+    // Exact keys (the reference's f32 score, K2's exact order: sequential d, fl(q * m) then
+    // fl(acc + .), + fl(fl(lam ||q||) * std), strict-> max over heads) of every page whose
+    // interval [klo, khi] is not one key and reaches L; the largest key written, block-wide.
+    auto resolve = [&](int L) -> int {
+        int mxr = -1;
+        const int nvec = (P + 7) >> 3;
+        const uint32_t Lc = (uint32_t)(L < 0 ? 0 : L);
+        const float *m32 = p.rows32 + u * (int64_t)p.Pmax * D;
+        constexpr int RS = D + 4;  // staged row stride (floats): conflict-free float4 reads
+        uint64_t *rbar = reinterpret_cast<uint64_t *>(rstage + (size_t)p.rcap * RS);
+        if (threadIdx.x == 0) {
+            mbar_init(rbar, 1);
+            fence_mbar_init();
+        }
+        int rounds = 0;
+        if (prof) g_sa_prof[cta * kSAProfN + 10] = gtimer();
+        for (;;) {
+            if (threadIdx.x == 0) *rcnt = 0;
+            __syncthreads();
+            if (prof && rounds == 0) g_sa_prof[cta * kSAProfN + 16] = gtimer();
+            // warp-aggregated compaction (one shared atomic per warp and round of vectors)
+            const int lane_ = threadIdx.x & 31;
+            const uint32_t lt = (1u << lane_) - 1u;
+            for (int v0 = 0; v0 < nvec; v0 += NT) {
+                const int v = v0 + threadIdx.x;
+                uint32_t f = 0u;  // bit e: key 8 v + e needs resolving
+                if (v < nvec) {
+                    const uint4 a = reinterpret_cast<const uint4 *>(skeys)[v];
+                    const uint4 b = reinterpret_cast<const uint4 *>(skhi)[v];
+                    const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, bw[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+                    for (int e = 0; e < 8; e++) {
+                        const uint32_t lo = (aw[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
+                        const uint32_t hi = (bw[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
+                        if (v * 8 + e < P && hi >= Lc && lo != hi) f |= 1u << e;
+                    }
+                }
+                const int c = __popc(f);
+                int inc = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane_ >= o) inc += y;
+                }
+                const int tot = __shfl_sync(0xffffffffu, inc, 31);
+                int base = 0;
+                if (lane_ == 31 && tot) base = atomicAdd(rcnt, tot);
+                base = __shfl_sync(0xffffffffu, base, 31) + inc - c;
+                (void)lt;
+                while (f) {
+                    const int e = __ffs(f) - 1;
+                    f &= f - 1;
+                    if (base < p.rcap) rlist[base] = v * 8 + e;
+                    base++;
+                }
+            }
+            if (prof && rounds == 0) g_sa_prof[cta * kSAProfN + 17] = gtimer();
+            __syncthreads();
+            if (prof && rounds == 0) g_sa_prof[cta * kSAProfN + 18] = gtimer();
+            if (prof) g_sa_prof[cta * kSAProfN + 11] = gtimer();
+            const int n = *rcnt;
+            const int nr = n < p.rcap ? n : p.rcap;
+            // one round: every listed page's f32 mean row by one bulk copy (all on one
+            // mbarrier), its std by a 4-byte async copy
+            if (threadIdx.x == 0 && nr) mbar_arrive_expect_tx(rbar, (uint32_t)(nr * D * 4));
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads
+            __syncthreads();
+            for (int i = threadIdx.x; i < nr; i += NT) {
+                bulk_g2s(rstage + i * RS, m32 + (int64_t)rlist[i] * D, D * 4, rbar);
+                sa_cp_async4(rstd + i, p.stds + u * (int64_t)p.Pmax + rlist[i]);
+            }
+            sa_cp_async_wait_all();
+            if (nr) mbar_wait(rbar, (uint32_t)(rounds & 1));
+            __syncthreads();
+            if (prof) g_sa_prof[cta * kSAProfN + 12] = gtimer();
+            if (prof && rounds == 0) g_sa_prof[cta * kSAProfN + 19] = gtimer();
+            for (int i = threadIdx.x; i < nr; i += NT) {
+                const int pg = rlist[i];
+                const float best = G <= 4 ? sa_exact_score<D, 4>(rstage + i * RS, sq, sln, rstd[i], G)
+                                          : sa_exact_score<D, 8>(rstage + i * RS, sq, sln, rstd[i], G);
+                const uint16_t key = encode_ordered(f32_to_bf16_rne(best));
+                skeys[pg] = key;
+                skhi[pg] = key;
+                mxr = max(mxr, (int)key);
+            }
+            __syncthreads();
+            if (prof && rounds == 0) g_sa_prof[cta * kSAProfN + 15] = gtimer();
+            rounds++;
+            if (prof) g_sa_prof[cta * kSAProfN + 13] = gtimer();
+            if (n <= p.rcap) break;
+        }
+
+        mxr = __reduce_max_sync(0xffffffffu, mxr);
+        if ((threadIdx.x & 31) == 0) csh.red[1][threadIdx.x >> 5][1] = (uint32_t)mxr;
+        __syncthreads();
+        int t = -1;
+#pragma unroll
+        for (int w = 0; w < NT / 32; w++) t = max(t, (int)csh.red[1][w][1]);
+        __syncthreads();
+        return t;
+    };
+    bool selected;
+    if (prof) g_sa_prof[cta * kSAProfN + 14] = gtimer();
+    if constexpr (BND) {
+        selected = select_cand<NT>(skeys, tm_stage ? stm : nullptr, P, k, p.page_table + u * p.Pmax, o_sel,
+                                   o_log, o_n, o_kth, o_kp1, csh, ids, true,
+                                   prof ? &g_sa_prof[cta * kSAProfN + 6] : nullptr, true, k + 1, resolve);
+        // take-all (P <= k) and P > 65536 return before resolving: resolve every page
+        if (!selected && (P <= k || P > 65536)) resolve(-1);
+    } else {
+        selected = select_cand<NT>(skeys, tm_stage ? stm : nullptr, P, k, p.page_table + u * p.Pmax, o_sel,
+                                   o_log, o_n, o_kth, o_kp1, csh, ids, true,
+                                   prof ? &g_sa_prof[cta * kSAProfN + 6] : nullptr, true);
+    }
     if (!selected)  // take-all, or massive ties at the lower bound
         select_block<NT>(skeys, bins, P, k, p.page_table + u * p.Pmax, o_sel, o_log, o_n,
                                  o_kth, o_kp1, sh, ids, true);
+    if constexpr (BND) {  // query fragments from the widened rows (bf16 values: exact)
+        const int gq = lane >> 2;
+#pragma unroll
+        for (int ks = 0; ks < KS; ks++) {
+            const int d0 = ks * 16 + 2 * (lane & 3);
+            const int g = gq < 8 ? gq : 0;
+            qb[ks][0] = gq < G ? pack_bf16(sq[d0 * 8 + g], sq[(d0 + 1) * 8 + g]) : 0u;
+            qb[ks][1] = gq < G ? pack_bf16(sq[(d0 + 8) * 8 + g], sq[(d0 + 9) * 8 + g]) : 0u;
+        }
+    }
     __syncthreads();  // ids complete; the select scratch is dead -> stage rings
-    if (prof) g_sa_prof[cta * 10 + 2] = gtimer();
+    if (prof) g_sa_prof[cta * kSAProfN + 2] = gtimer();
 
     // ---- this chunk's slice of the selection ----
     const int per = (ns + p.nchunk - 1) / p.nchunk;
@@ -212,7 +427,7 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
         const int pid = ids[first + warp + i * NW];
         const int rows = (pid == tail_pid) ? tail_rows : S;
         mbar_wait(&bars[st], (uint32_t)((i / nstage) & 1));
-        if (prof && i == 0) g_sa_prof[cta * 10 + 3] = gtimer();
+        if (prof && i == 0) g_sa_prof[cta * kSAProfN + 3] = gtimer();
         const uint32_t kbase = smem_u32(my_stages + (size_t)st * STAGE_BYTES);
         mma_page<D, MT>(kbase, kbase + PAGE_BYTES, rows, 0.f, qscale, qb, acc, m_run, l_run, lane);
         __syncwarp();
@@ -220,7 +435,7 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
     }
 
     // ---- per-warp partials to shared memory, then the CTA / chunk merge (attend.cuh) ----
-    if (prof) g_sa_prof[cta * 10 + 4] = gtimer();
+    if (prof) g_sa_prof[cta * kSAProfN + 4] = gtimer();
     __syncthreads();
     float *macc = reinterpret_cast<float *>(smem);             // [NW][8][D]
     float *mml = macc + (size_t)NW * kMmaGP * D;                // [NW][8][2]
@@ -246,7 +461,7 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
     ap.out = p.out; ap.lse = p.lse; ap.ws = p.ws; ap.tickets = p.tickets;
     ap.G = G; ap.D = D; ap.maxs = kAttnMaxSplits;
     cta_finish(ap, macc, mml, NW, kMmaGP, u, c, nchunk_u);
-    if (prof) g_sa_prof[cta * 10 + 5] = gtimer();
+    if (prof) g_sa_prof[cta * kSAProfN + 5] = gtimer();
 }
 
 // ---------------------------------------------------------------------------
@@ -382,25 +597,26 @@ static int launch_saw(const CUtensorMap &tk, const CUtensorMap &tv, const SelAtt
     return PT_OK;
 }
 
-template <int D, int MT, int NT>
+template <int D, int MT, int NT, bool BND>
 static int launch_sa_nt(const CUtensorMap &tk, const CUtensorMap &tv, const SelAttnParams &p,
                         size_t smem, cudaStream_t st) {
     static size_t configured = 0;
     if (smem > configured) {
-        PT_CUDA_TRY(cudaFuncSetAttribute(k_select_attend<D, MT, NT>,
+        PT_CUDA_TRY(cudaFuncSetAttribute(k_select_attend<D, MT, NT, BND>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured = smem;
     }
     dim3 grid(p.nchunk, p.U);
-    PT_CUDA_TRY(pt_launch(k_select_attend<D, MT, NT>, grid, dim3(NT), smem, st, tk, tv, p));
+    PT_CUDA_TRY(pt_launch(k_select_attend<D, MT, NT, BND>, grid, dim3(NT), smem, st, tk, tv, p));
     return PT_OK;
 }
 
 template <int D, int MT>
 static int launch_sa(const CUtensorMap &tk, const CUtensorMap &tv, const SelAttnParams &p,
                      size_t smem, cudaStream_t st, int sel_threads) {
-    return sel_threads == 256 ? launch_sa_nt<D, MT, 256>(tk, tv, p, smem, st)
-                              : launch_sa_nt<D, MT, 128>(tk, tv, p, smem, st);
+    if (p.keys_hi) return launch_sa_nt<D, MT, 256, true>(tk, tv, p, smem, st);
+    return sel_threads == 256 ? launch_sa_nt<D, MT, 256, false>(tk, tv, p, smem, st)
+                              : launch_sa_nt<D, MT, 128, false>(tk, tv, p, smem, st);
 }
 
 }  // namespace pt
@@ -418,7 +634,8 @@ static int sa_env_int(const char *name, int dflt) {
 // followed by pt_attend (sel_stride = k); PT_ERR_UNSUPPORTED when the shape is outside the
 // fused kernel's envelope (the caller then runs the two-launch path).
 extern "C" int pt_select_attend(const uint16_t *keys, const uint16_t *tile_max,
-                                const int32_t *seq_len,
+                                const uint16_t *keys_hi, const void *mirror, const float *stds,
+                                const float *lamnorm, const int32_t *seq_len,
                                 const int32_t *page_table, int U, int S, int Pmax, int k,
                                 int32_t *sel, int32_t *sel_logical, int32_t *n_sel, int32_t *kth,
                                 int32_t *kplus1, const void *q, int q_dtype, const void *k_pool,
@@ -434,6 +651,8 @@ extern "C" int pt_select_attend(const uint16_t *keys, const uint16_t *tile_max,
         !(S == 16 || S == 32 || S == 64) || num_phys_pages <= 0 || !workspace || !tickets ||
         workspace_bytes < pt_attend_workspace_bytes(U, G, D, k) || sa_env_int("PT_NO_FUSED_SA", 0))
         return PT_ERR_UNSUPPORTED;
+    const bool bnd = keys_hi != nullptr;
+    if (bnd && (!mirror || !stds || !lamnorm || !tile_max)) return PT_ERR_INVALID;
     const int stage = 2 * S * D * 2;
     int nstage = sa_env_int("PT_SA_NSTAGE", 3);
     if (nstage < 1) nstage = 1;
@@ -441,14 +660,26 @@ extern "C" int pt_select_attend(const uint16_t *keys, const uint16_t *tile_max,
     // keep at least one page per warp in a chunk
     int nchunk = sa_env_int("PT_SA_CHUNKS", 0);
     if (nchunk <= 0) {
-        nchunk = (148 * 2) / U;
+        nchunk = (pt_num_sms() * 2) / U;
         if (nchunk < 1) nchunk = 1;
         // every chunk CTA repeats the unit's selection: keep >= 4 pages per warp per chunk
         const int cap = (k + 4 * kSAWarps - 1) / (4 * kSAWarps);
         if (nchunk > cap) nchunk = cap;
     }
     if (nchunk > kAttnMaxSplits) nchunk = kAttnMaxSplits;
-    const size_t sel_scratch = sa_keys_bytes(Pmax) + (size_t)kSelectBins * 4 + (size_t)(Pmax / 32) * 2;
+    const size_t sel_base = sa_keys_bytes(Pmax) + (size_t)kSelectBins * 4 + (size_t)(Pmax / 32) * 2;
+    size_t sel_scratch = sel_base;
+    int rcap = 0;
+    if (bnd) {
+        // pages resolved per round: as many as fit beside the keys in the ring region of a
+        // 2-deep-or-more ring at two CTAs per SM (>= 32), at most 256
+        const size_t base = ((sel_base + 15) & ~(size_t)15) + sa_bnd_bytes(Pmax, D, 0);
+        const size_t budget = (size_t)kSAWarps * 3 * stage;
+        rcap = budget > base ? (int)((budget - base) / ((size_t)(D + 4) * 4 + 8)) : 0;
+        rcap = sa_env_int("PT_SA_RCAP", rcap);
+        rcap = (rcap < 32 ? 32 : rcap > 256 ? 256 : rcap) & ~3;
+        sel_scratch = ((sel_base + 15) & ~(size_t)15) + sa_bnd_bytes(Pmax, D, rcap);
+    }
     const size_t merge = (size_t)kSAWarps * kMmaGP * (D + 2) * 4;
     auto smem_of = [&](int nst, size_t *region_out) {
         const size_t rings = (size_t)kSAWarps * nst * stage;
@@ -467,7 +698,7 @@ extern "C" int pt_select_attend(const uint16_t *keys, const uint16_t *tile_max,
     // many short units with a small budget: one warp per unit (no CTA-wide selection/merge)
     const int want_warp = sa_env_int("PT_SA_WARP", -1);
     const bool warp_path = want_warp == 1 ||
-                           (want_warp != 0 && U >= 4 * 148 && k <= 64 && Pmax <= 32 * 8 * kSWMaxV);
+                           (want_warp != 0 && U >= 4 * pt_num_sms() && k <= 64 && Pmax <= 32 * 8 * kSWMaxV);
     size_t w_per = 0;
     // ring depth (PT_SAW_NSTAGE: tuning; a 2-deep ring measured no faster at k = 8)
     int w_nst = sa_env_int("PT_SAW_NSTAGE", 3), w_nw = 4;
@@ -491,10 +722,11 @@ extern "C" int pt_select_attend(const uint16_t *keys, const uint16_t *tile_max,
     p.q_dtype = q_dtype; p.U = U; p.G = G; p.Pmax = Pmax; p.k = k; p.nchunk = nchunk;
     p.nstage = nstage; p.region = (int)region; p.scale = scale;
     p.prof = sa_env_int("PT_SA_PROF", 0);
+    p.keys_hi = keys_hi; p.rows32 = mirror_view(mirror, U, Pmax, D).rows; p.stds = stds; p.lamnorm = lamnorm; p.rcap = rcap;
     cudaStream_t st = (cudaStream_t)stream;
     // selection threads: 8 warps halve the selection's block-wide passes; 4 of them stream
     const int sel_threads = sa_env_int("PT_SA_SEL_THREADS", 256) == 128 ? 128 : 256;
-    if (w_per) {
+    if (w_per && !bnd) {
         SelAttnParams pw = p;
         pw.nstage = w_nst;
         pw.region = (int)w_per;
@@ -516,7 +748,7 @@ extern "C" int pt_select_attend(const uint16_t *keys, const uint16_t *tile_max,
 
 // tuning aid: copy the phase timestamps of the last PT_SA_PROF=1 launch (n <= 10 * 4096)
 extern "C" int pt_debug_sa_prof(unsigned long long *host, int n) {
-    if (!host || n < 0 || n > kSAProfCtas * 10) return PT_ERR_INVALID;
+    if (!host || n < 0 || n > kSAProfCtas * kSAProfN) return PT_ERR_INVALID;
     PT_CUDA_TRY(cudaMemcpyFromSymbol(host, g_sa_prof, (size_t)n * 8));
     return PT_OK;
 }

@@ -41,7 +41,23 @@ bool pt_pdl_enabled() {
     return on;
 }
 
-extern "C" int pt_version(void) { return 100; }
+int pt_num_sms() {
+    static int cache[64] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) return 148;
+    if (dev < 64 && cache[dev]) return cache[dev];
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    if (dev < 64) cache[dev] = n;
+    return n;
+}
+
+extern "C" int pt_version(void) { return 200; }
+
+extern "C" size_t pt_mirror_bytes(int U, int Pmax, int D) {
+    if (U < 0 || Pmax < 0 || D < 1) return 0;
+    return pt::mirror_bytes(U, Pmax, D);
+}
 
 extern "C" const char *pt_status_string(int status) {
     switch (status) {

@@ -249,6 +249,76 @@ __device__ __forceinline__ double np_sum_warp(const double *x, int n, int lane) 
     return __dadd_rn(0.0, n > 128 ? __dadd_rn(c, hi) : c);
 }
 
+// ---------------------------------------------------------------------------
+// bf16 mirror of the f32 page means (bounded scoring).
+// Every stats writer that is given a mirror also stores m~ = bf16_rne(m) (tile layout,
+// V = 8) and err_p = ||m~ - m|| + kMirrorAccSlack(D) * (||m|| + ||m~||), rounded up.  Then for
+// any query q: |dot_ref(q, m) - dot_mirror(q, m~)| <= ||q|| * err_p, where dot_ref is the
+// reference's sequential f32 dot (error <= gamma_D ||q|| ||m||) and dot_mirror is the
+// scorer's bf16 x bf16 tensor-core dot (exact products, f32 accumulation; its accumulation
+// error is bounded with 64x the RN gamma_D -- tests/test_gpu_bounded.py measures it).
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ double mirror_acc_slack(int D) { return (double)(D + 2) * 0x1p-18; }
+
+// The mirror block (one caller allocation of pt_mirror_bytes(U, Pmax, D) bytes):
+//   tiles: bf16 means in the page-interleaved layout (V = 8)  [U][Pmax/32][D/8][32][8]
+//   rows : the same f32 means row-major (one 4D-byte row per page: the selection's resolve
+//          step fetches a page's exact mean with ONE bulk copy)  [U][Pmax][D]
+//   err  : the per-page error bound                                [U][Pmax]
+struct MirrorView {
+    uint16_t *tiles;
+    float *rows;
+    float *err;
+};
+__host__ __device__ __forceinline__ size_t mirror_align(size_t x) { return (x + 255) & ~(size_t)255; }
+__host__ __device__ __forceinline__ size_t mirror_bytes(int U, int Pmax, int D) {
+    const size_t n = (size_t)U * Pmax;
+    return mirror_align(n * D * 2) + mirror_align(n * D * 4) + n * 4;
+}
+__host__ __device__ __forceinline__ MirrorView mirror_view(const void *base, int U, int Pmax, int D) {
+    MirrorView v{nullptr, nullptr, nullptr};
+    if (!base) return v;
+    char *b = static_cast<char *>(const_cast<void *>(base));
+    const size_t n = (size_t)U * Pmax;
+    v.tiles = reinterpret_cast<uint16_t *>(b);
+    v.rows = reinterpret_cast<float *>(b + mirror_align(n * D * 2));
+    v.err = reinterpret_cast<float *>(b + mirror_align(n * D * 2) + mirror_align(n * D * 4));
+    return v;
+}
+
+template <int DJ>
+__device__ __forceinline__ void store_mirror(const double (&mean)[DJ], int D, int64_t u, int64_t p,
+                                             int64_t Pmax, const MirrorView &mv, int lane) {
+    double dd = 0.0, mm = 0.0, tt = 0.0;
+#pragma unroll
+    for (int j = 0; j < DJ; j++) {
+        const int d = lane + 32 * j;
+        if (d < D) {
+            const float m = __double2float_rn(mean[j]);
+            const uint16_t b = f32_to_bf16_rne(m);
+            const double mt = (double)bf16_bits_to_f32(b), m64 = (double)m;
+            mv.tiles[mean_offset(u, p, d, D, Pmax, 8)] = b;
+            mv.rows[(u * Pmax + p) * D + d] = m;
+            const double e = mt - m64;  // exact: m~ and m are f32 within a factor 2
+            dd = fma(e, e, dd);
+            mm = fma(m64, m64, mm);
+            tt = fma(mt, mt, tt);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        dd += __shfl_xor_sync(0xffffffffu, dd, o);
+        mm += __shfl_xor_sync(0xffffffffu, mm, o);
+        tt += __shfl_xor_sync(0xffffffffu, tt, o);
+    }
+    if (lane == 0) {
+        // f64 rounding of the sums / roots: relative 1e-14, covered by the (1 + 2^-30) factor;
+        // the absolute term covers subnormal products
+        const double e = (sqrt(dd) + mirror_acc_slack(D) * (sqrt(mm) + sqrt(tt))) * (1.0 + 0x1p-30) + 0x1p-120;
+        mv.err[u * Pmax + p] = __double2float_ru(e);
+    }
+}
+
 // squares of f32 values widened to f64: np.sum(f64(q)**2) (scoring.py:45)
 struct SquaresOfF32 {
     const float *a;
@@ -276,6 +346,7 @@ __device__ __forceinline__ void pdl_trigger() {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 bool pt_pdl_enabled();  // capi.cu: false when PT_NO_PDL=1
+int pt_num_sms();       // capi.cu: SM count of the current device (cached per device)
 
 template <typename... KArgs, typename... Args>
 static inline cudaError_t pt_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,

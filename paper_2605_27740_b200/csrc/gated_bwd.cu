@@ -414,7 +414,7 @@ extern "C" int pt_gate_bias(const double *gates, const int32_t *seq_len, int U, 
     cudaStream_t st = (cudaStream_t)stream;
     PT_CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int32_t), st));
     int64_t blocks = ((int64_t)U * Pmax + 255) / 256;
-    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks > pt_num_sms() * 8) blocks = pt_num_sms() * 8;
     k_gate_bias<<<(int)blocks, 256, 0, st>>>(gates, seq_len, U, S, Pmax, bias, flag);
     PT_CUDA_TRY(cudaGetLastError());
     return PT_OK;

@@ -219,25 +219,25 @@ constexpr int kLnRows = 32;
 template <int QDT, bool LATE = false>
 __global__ void __launch_bounds__(256) k_lam_norms(const void *__restrict__ q,
                                                    const float *__restrict__ norms_in, int rows,
-                                                   int G, int D, float lam, float *__restrict__ out) {
+                                                   int G, int D, float lam, float *__restrict__ out,
+                                                   float *__restrict__ qnorm) {
     __shared__ float qs[kLnRows * (kScoreMaxD + 1)];
     pdl_trigger();
     if (!LATE) pdl_wait();
     const int r0 = blockIdx.x * kLnRows;
     const int nr = min(kLnRows, rows - r0);
     const int ld = D + 1;  // odd stride: thread r's sequential reads hit distinct banks
-    if (!norms_in) {
+    if (!norms_in || qnorm) {
         const char *src = static_cast<const char *>(q) + (int64_t)r0 * D * (QDT == PT_F32 ? 4 : 2);
         stage_rows_f32<QDT, 8>(qs, ld, src, nr * D, D, threadIdx.x, blockDim.x);
     }
     __syncthreads();
     const int r = threadIdx.x;
-    float val = 0.f;
+    float val = 0.f, qn = 0.f;
     if (r < nr) {
-        float nrm;
-        if (norms_in) {
-            nrm = norms_in[r0 + r];
-        } else {
+        float nrm = 0.f;
+        double ss = 0.0;
+        if (!norms_in || qnorm) {
             struct Sq {
                 const float *row;
                 __device__ double operator()(int i) const {
@@ -245,9 +245,13 @@ __global__ void __launch_bounds__(256) k_lam_norms(const void *__restrict__ q,
                     return __dmul_rn(v, v);
                 }
             } sq{qs + r * ld};
-            nrm = __double2float_rn(__dsqrt_rn(np_sum(sq, D)));
+            ss = np_sum(sq, D);
         }
+        nrm = norms_in ? norms_in[r0 + r] : __double2float_rn(__dsqrt_rn(ss));
         val = __fmul_rn(lam, nrm);
+        // bounded scoring: an upper bound of the true ||q_g|| (f64 sum of exact squares,
+        // relative error < 1e-13, then rounded up)
+        qn = __double2float_ru(__dsqrt_ru(ss) * (1.0 + 0x1p-30));
     }
     // LATE: the norms are computed beside the predecessor, but stored only after its wait --
     // the previous step's scorer may still be reading lamnorm until then (WAR across steps)
@@ -255,6 +259,7 @@ __global__ void __launch_bounds__(256) k_lam_norms(const void *__restrict__ q,
     if (r < nr) {
         const int u = (r0 + r) / G, g = (r0 + r) - u * G;
         out[(int64_t)u * 8 + g] = val;
+        if (qnorm) qnorm[(int64_t)u * 8 + g] = qn;
     }
 }
 
@@ -349,7 +354,7 @@ extern "C" int pt_score(const void *q, int q_dtype, const float *norms, const vo
     const int es = stats_dtype == PT_F32 ? 4 : 2, qes = q_dtype == PT_F32 ? 4 : 2;
     if (lamnorm_ws && G <= 8 && (D == 64 || D == 128) && !getenv("PT_SCORE_CTA") &&
         (long long)U * (Pmax / 32) < (1LL << 31)) {
-        const int rc0 = pt_lam_norms(q, q_dtype, norms, U, G, D, lam, lamnorm_ws, st);
+        const int rc0 = pt_lam_norms(q, q_dtype, norms, U, G, D, lam, lamnorm_ws, nullptr, st);
         if (rc0) return rc0;
         StreamScoreParams sp{q, lamnorm_ws, means, stds, seq_len, keys, scores, U, S, Pmax, tile_max,
                              ss_contig(stats_dtype)};
@@ -368,27 +373,27 @@ extern "C" int pt_score(const void *q, int q_dtype, const float *norms, const vo
 // (scoring.py:39-47 norms, numpy's float64 pairwise order; or lam * the given norms).
 template <bool LATE>
 static int lam_norms_launch(const void *q, int q_dtype, const float *norms, int U, int G, int D,
-                            float lam, float *lamnorm, void *stream) {
+                            float lam, float *lamnorm, float *qnorm, void *stream) {
     if (!q || !lamnorm || U < 0 || G < 1 || G > 8 || D < 1 || D > kScoreMaxD) return PT_ERR_INVALID;
     if (U == 0) return PT_OK;
     cudaStream_t st = (cudaStream_t)stream;
     const int rows = U * G;
     const dim3 grid((rows + kLnRows - 1) / kLnRows);
     if (q_dtype == PT_F32)
-        PT_CUDA_TRY(pt_launch(k_lam_norms<PT_F32, LATE>, grid, dim3(256), 0, st, q, norms, rows, G, D, lam, lamnorm));
+        PT_CUDA_TRY(pt_launch(k_lam_norms<PT_F32, LATE>, grid, dim3(256), 0, st, q, norms, rows, G, D, lam, lamnorm, qnorm));
     else
-        PT_CUDA_TRY(pt_launch(k_lam_norms<PT_BF16, LATE>, grid, dim3(256), 0, st, q, norms, rows, G, D, lam, lamnorm));
+        PT_CUDA_TRY(pt_launch(k_lam_norms<PT_BF16, LATE>, grid, dim3(256), 0, st, q, norms, rows, G, D, lam, lamnorm, qnorm));
     return PT_OK;
 }
 
 extern "C" int pt_lam_norms(const void *q, int q_dtype, const float *norms, int U, int G, int D,
-                            float lam, float *lamnorm, void *stream) {
-    return lam_norms_launch<false>(q, q_dtype, norms, U, G, D, lam, lamnorm, stream);
+                            float lam, float *lamnorm, float *qnorm, void *stream) {
+    return lam_norms_launch<false>(q, q_dtype, norms, U, G, D, lam, lamnorm, qnorm, stream);
 }
 
 extern "C" int pt_lam_norms_chained(const void *q, int q_dtype, const float *norms, int U, int G,
-                                    int D, float lam, float *lamnorm, void *stream) {
-    return lam_norms_launch<true>(q, q_dtype, norms, U, G, D, lam, lamnorm, stream);
+                                    int D, float lam, float *lamnorm, float *qnorm, void *stream) {
+    return lam_norms_launch<true>(q, q_dtype, norms, U, G, D, lam, lamnorm, qnorm, stream);
 }
 
 // K2 with lam * ||q|| precomputed by pt_lam_norms (so the norms launch can run beside the
@@ -440,7 +445,7 @@ extern "C" int pt_tile_means(const float *src, int U, int P, int D, int Pmax, vo
     cudaStream_t st = (cudaStream_t)stream;
     int64_t total = (int64_t)U * P * D;
     int blocks = (int)((total + 255) / 256);
-    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks > pt_num_sms() * 16) blocks = pt_num_sms() * 16;
     if (stats_dtype == PT_F32) k_tile_means<PT_F32><<<blocks, 256, 0, st>>>(src, U, P, D, Pmax, dst);
     else if (stats_dtype == PT_BF16) k_tile_means<PT_BF16><<<blocks, 256, 0, st>>>(src, U, P, D, Pmax, dst);
     else return PT_ERR_INVALID;

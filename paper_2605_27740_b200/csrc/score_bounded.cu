@@ -1,0 +1,313 @@
+// score_bounded.cu -- K2b: bounded page scoring over the bf16 mirror of the page means.
+//
+// The reference score of page p (scoring.py:108-124, _kernels_cy.pyx:19-43) is
+//   s_p = max_g fl(dot_g + fl(fl(lam*||q_g||) * std_p)),   dot_g = sequential f32 sum of q_g . m_p
+// over the f32 page means m_p, and the selection works on key_p = ordered(bf16_rne(s_p)).
+// Streaming the f32 means costs P*D*4 bytes per unit -- twice SURVEY 8(d)'s model, which
+// reads the means at the KV element size.  This kernel streams the bf16 mirror m~_p instead
+// (half the bytes) and computes, on the tensor cores (mma.sync m16n8k16, bf16 x bf16 -> f32:
+// products exact), dot~_g = q_g . m~_p.  With err_p = ||m~_p - m_p|| + slack (written by the
+// stats kernels, common.cuh store_mirror) and qn_g >= ||q_g|| (pt_lam_norms), the reference
+// dot lies in [dot~ - E, dot~ + E], E = qn_g * err_p, so with directed rounding
+//   lo_p = max_g fl(RD(dot~_g - E) + off_g) <= s_p <= max_g fl(RU(dot~_g + E) + off_g) = hi_p
+// (fl(x + off) is monotone in x).  bf16 rounding and the ordered encoding are monotone too,
+// so klo_p = key(lo_p) <= key_p <= key(hi_p) = khi_p: both are written, and the selection
+// (attend_fused.cu, bounded mode) recomputes the exact key -- from the f32 means, in the
+// reference's order -- only for the pages whose interval is not a single key and reaches the
+// cut.  The selected page set, kth and kplus1 are therefore those of the f32 reference.
+//
+// Structure: persistent grid (CTAs x 4 warps per SM); warp gw streams the contiguous range
+// [gw T / W, (gw+1) T / W) of the concatenated 32-page tiles of all units through a private
+// ring of NST stages, one stage = one tile (32 pages x D bf16 = one contiguous block of the
+// page-interleaved mirror, fetched by one cp.async.bulk) plus its 32 stds and 32 errs; the
+// unit's query rows + lam*||q|| + ||q|| ride on the first stage of a run.  Per tile: two
+// 16-page MMA row blocks x D/16 k-steps, A fragments by ldmatrix straight from the stage
+// (one 16-byte row = 8 dims of one page), B = the G <= 8 query heads (N = 8).
+#include "attend.cuh"
+
+namespace pt {
+
+struct BoundedScoreParams {
+    const uint16_t *q;       // bf16 [U*G][D]
+    const float *lamnorm;    // [U][8] fl(lam * ||q_g||)
+    const float *qnorm;      // [U][8] upper bounds of ||q_g||
+    const uint16_t *mirror;  // bf16 mirror of the means, tiles [U][Pmax/32][D/8][32][8]
+    const float *stds;       // [U][Pmax]
+    const float *merr;       // [U][Pmax]
+    const int32_t *seq_len;
+    uint16_t *keys_lo, *keys_hi;  // [U][Pmax]
+    uint16_t *tile_max;           // [U][Pmax/32]: max klo of each tile
+    int U, S, Pmax;
+};
+
+constexpr int kSBWarps = 4;
+constexpr int kSBMaxUnits = 2048;  // tile prefix over units in shared memory
+
+template <int G, int D, int NST>
+struct SBCfg {
+    static constexpr int TILE = 32 * D * 2;
+    static constexpr int QB = G * D * 2;
+    static constexpr int UHDR = (QB + 64 + 127) & ~127;  // q rows | lamnorm[8] | qnorm[8]
+    static constexpr int NHU = NST + 1;
+    static constexpr int THDR = 256;  // 32 stds | 32 errs
+    static constexpr int NHDR = NST;
+    static constexpr int PER_WARP = NST * TILE + NHU * UHDR + NHDR * THDR;
+};
+
+__host__ __device__ __forceinline__ size_t sb_hdr_bytes(int U) {
+    const size_t ps = ((size_t)(U + 1) * 4 + 15) & ~(size_t)15;
+    return (ps + (size_t)kSBWarps * 8 * 8 + 127) & ~(size_t)127;
+}
+
+template <int G, int D, int NST>
+__global__ void __launch_bounds__(kSBWarps * 32) k_score_bounded(const BoundedScoreParams prm) {
+    using C = SBCfg<G, D, NST>;
+    constexpr int KS = D / 16;
+    extern __shared__ __align__(1024) char smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int S = prm.S, Pmax = prm.Pmax, U = prm.U;
+    const int TPU = Pmax >> 5;
+    const int W = gridDim.x * kSBWarps;
+    const int gw = blockIdx.x * kSBWarps + warp;
+    int *Tp = reinterpret_cast<int *>(smem);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + (((size_t)(U + 1) * 4 + 15) & ~(size_t)15)) + warp * 8;
+    char *ring = smem + sb_hdr_bytes(U) + (size_t)warp * C::PER_WARP;
+    char *uhdrs = ring + NST * C::TILE;
+    char *thdrs = uhdrs + C::NHU * C::UHDR;
+    if (lane == 0) {
+        for (int i = 0; i < NST; i++) mbar_init(&bars[i], 1);
+        fence_mbar_init();
+    }
+    pdl_wait();
+    pdl_trigger();
+    {  // tile prefix over units (block scan)
+        __shared__ int wsum[kSBWarps];
+        int carry = 0;
+        for (int b0 = 0; b0 < U; b0 += kSBWarps * 32) {
+            const int uu = b0 + threadIdx.x;
+            const int nt = uu < U ? ((prm.seq_len[uu] + S - 1) / S + 31) >> 5 : 0;
+            int inc = nt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+            }
+            if (lane == 31) wsum[warp] = inc;
+            __syncthreads();
+            int pw = 0, tot = 0;
+#pragma unroll
+            for (int w = 0; w < kSBWarps; w++) {
+                if (w < warp) pw += wsum[w];
+                tot += wsum[w];
+            }
+            if (uu < U) Tp[uu] = carry + pw + inc - nt;
+            carry += tot;
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) Tp[U] = carry;
+    }
+    __syncthreads();
+    struct Cur { int u, t, g; };
+    const int64_t T = Tp[U];
+    const int64_t g0 = (int64_t)gw * T / W, g_end = (int64_t)(gw + 1) * T / W;
+    Cur pc{U, 0, 0};
+    if (g0 < g_end) {
+        int lo = 0, hi = U;  // last unit with Tp[u] <= g0
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (Tp[mid] <= g0) lo = mid; else hi = mid;
+        }
+        pc = Cur{lo, (int)(g0 - Tp[lo]), (int)g0};
+    }
+    auto advance = [&](Cur &c) {
+        c.g++;
+        if (c.g >= g_end) { c.u = U; return; }
+        c.t++;
+        while (c.t >= Tp[c.u + 1] - Tp[c.u]) { c.u++; c.t = 0; }
+    };
+    Cur cc = pc;
+    int issued = 0, p_run = -1, p_unit = -1;
+    const uint64_t evict_first = l2_evict_first_policy();
+    auto fill = [&](int consumed) {
+        while (pc.u < U && issued < consumed + NST) {
+            const int slot = issued % NST;
+            const bool new_run = pc.u != p_unit;
+            if (new_run) { p_run++; p_unit = pc.u; }
+            if (lane == 0) {
+                const int64_t pg = (int64_t)pc.u * Pmax + (int64_t)pc.t * 32;
+                mbar_arrive_expect_tx(&bars[slot], C::TILE + C::THDR + (new_run ? C::QB + 64 : 0));
+                bulk_g2s_hint(ring + slot * C::TILE, prm.mirror + pg * D, C::TILE, &bars[slot], evict_first);
+                char *th = thdrs + (issued % C::NHDR) * C::THDR;
+                bulk_g2s(th, prm.stds + pg, 128, &bars[slot]);
+                bulk_g2s(th + 128, prm.merr + pg, 128, &bars[slot]);
+                if (new_run) {
+                    char *h = uhdrs + (p_run % C::NHU) * C::UHDR;
+                    bulk_g2s(h, prm.q + (int64_t)pc.u * G * D, C::QB, &bars[slot]);
+                    bulk_g2s(h + C::QB, prm.lamnorm + (int64_t)pc.u * 8, 32, &bars[slot]);
+                    bulk_g2s(h + C::QB + 32, prm.qnorm + (int64_t)pc.u * 8, 32, &bars[slot]);
+                }
+            }
+            issued++;
+            advance(pc);
+        }
+    };
+    fill(0);
+    const int h0 = 2 * (lane & 3), h1 = h0 + 1;
+    const int gq = lane >> 2;
+    uint32_t qb[KS][2];
+    float ln0 = 0.f, ln1 = 0.f, qn0 = 0.f, qn1 = 0.f;
+    int consumed = 0, c_run = -1, c_unit = -1;
+    // ldmatrix row address of this lane within a tile: matrix mi = lane / 8 holds pages
+    // (mi & 1) * 8 + lane % 8 of the 16-page block, dims 8 * (2 ks + (mi >> 1)) ..
+    const int lrow = ((lane >> 3) & 1) * 8 + (lane & 7);
+    const int lchk = lane >> 4;
+    while (cc.u < U) {
+        const int slot = consumed % NST;
+        mbar_wait(&bars[slot], (uint32_t)((consumed / NST) & 1));
+        if (cc.u != c_unit) {  // a new run: the unit's query fragments and norms
+            c_run++;
+            c_unit = cc.u;
+            const char *uh = uhdrs + (c_run % C::NHU) * C::UHDR;
+            const uint16_t *qh = reinterpret_cast<const uint16_t *>(uh);
+#pragma unroll
+            for (int ks = 0; ks < KS; ks++) {
+                const int d0 = ks * 16 + h0;
+                qb[ks][0] = gq < G ? *reinterpret_cast<const uint32_t *>(qh + gq * D + d0) : 0u;
+                qb[ks][1] = gq < G ? *reinterpret_cast<const uint32_t *>(qh + gq * D + d0 + 8) : 0u;
+            }
+            const float *lnp = reinterpret_cast<const float *>(uh + C::QB);
+            ln0 = lnp[h0]; ln1 = lnp[h1]; qn0 = lnp[8 + h0]; qn1 = lnp[8 + h1];
+        }
+        float acc[2][4];
+#pragma unroll
+        for (int mb = 0; mb < 2; mb++) acc[mb][0] = acc[mb][1] = acc[mb][2] = acc[mb][3] = 0.f;
+        const uint32_t sbase = smem_u32(ring + slot * C::TILE) + (uint32_t)(lchk * 512 + lrow * 16);
+#pragma unroll
+        for (int ks = 0; ks < KS; ks++) {
+#pragma unroll
+            for (int mb = 0; mb < 2; mb++) {
+                uint32_t a[4];
+                ldsm_x4(sbase + (uint32_t)(ks * 1024 + mb * 256), a);
+                mma_bf16(acc[mb], a, qb[ks][0], qb[ks][1]);
+            }
+        }
+        // epilogue: per (page, head) the interval of the reference score, max over heads
+        const float *th = reinterpret_cast<const float *>(thdrs + (consumed % C::NHDR) * C::THDR);
+        float lo[4], hi[4];  // pages gq, gq + 8, gq + 16, gq + 24 of the tile
+#pragma unroll
+        for (int mb = 0; mb < 2; mb++) {
+#pragma unroll
+            for (int half = 0; half < 2; half++) {
+                const int pp = mb * 16 + half * 8 + gq;
+                const float sd = th[pp], er = th[32 + pp];
+                float l = -INFINITY, h = -INFINITY;
+                if (h0 < G) {
+                    const float c = acc[mb][2 * half], off = __fmul_rn(ln0, sd);
+                    const float E = __fadd_ru(__fmul_ru(qn0, er), 1.17549435e-38f);
+                    l = __fadd_rn(__fsub_rd(c, E), off);
+                    h = __fadd_rn(__fadd_ru(c, E), off);
+                }
+                if (h1 < G) {
+                    const float c = acc[mb][2 * half + 1], off = __fmul_rn(ln1, sd);
+                    const float E = __fadd_ru(__fmul_ru(qn1, er), 1.17549435e-38f);
+                    l = fmaxf(l, __fadd_rn(__fsub_rd(c, E), off));
+                    h = fmaxf(h, __fadd_rn(__fadd_ru(c, E), off));
+                }
+                l = fmaxf(l, __shfl_xor_sync(0xffffffffu, l, 1));
+                h = fmaxf(h, __shfl_xor_sync(0xffffffffu, h, 1));
+                l = fmaxf(l, __shfl_xor_sync(0xffffffffu, l, 2));
+                h = fmaxf(h, __shfl_xor_sync(0xffffffffu, h, 2));
+                lo[mb * 2 + half] = l;
+                hi[mb * 2 + half] = h;
+            }
+        }
+        __syncwarp();  // stage + headers read: the slot may be refilled
+        consumed++;
+        fill(consumed);
+        // lane (gq, j) writes page gq + 8 j: one 64-byte store per array per tile
+        const int j = lane & 3;
+        const float l = j == 0 ? lo[0] : j == 1 ? lo[1] : j == 2 ? lo[2] : lo[3];
+        const float h = j == 0 ? hi[0] : j == 1 ? hi[1] : j == 2 ? hi[2] : hi[3];
+        const int p = cc.t * 32 + gq + 8 * j;
+        const int Pc = (__ldg(prm.seq_len + cc.u) + S - 1) / S;
+        const uint32_t klo = encode_ordered(f32_to_bf16_rne(l));
+        const uint32_t khi = encode_ordered(f32_to_bf16_rne(h));
+        if (p < Pc) {
+            prm.keys_lo[(int64_t)cc.u * Pmax + p] = (uint16_t)klo;
+            prm.keys_hi[(int64_t)cc.u * Pmax + p] = (uint16_t)khi;
+        }
+        const uint32_t m = __reduce_max_sync(0xffffffffu, p < Pc ? klo : 0u);
+        if (lane == 0) prm.tile_max[(int64_t)cc.u * TPU + cc.t] = (uint16_t)m;
+        advance(cc);
+    }
+}
+
+template <int G, int D, int NST>
+static int sb_launch(const BoundedScoreParams &sp, int ctas, cudaStream_t st) {
+    using C = SBCfg<G, D, NST>;
+    const size_t smem = sb_hdr_bytes(sp.U) + (size_t)kSBWarps * C::PER_WARP;
+    while (ctas > 1 && (smem + 1024) * ctas > 227 * 1024) ctas--;
+    if (smem > 227 * 1024) return PT_ERR_UNSUPPORTED;
+    static size_t configured = 0;
+    if (smem > configured) {
+        PT_CUDA_TRY(cudaFuncSetAttribute(k_score_bounded<G, D, NST>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured = smem;
+    }
+    PT_CUDA_TRY(pt_launch(k_score_bounded<G, D, NST>, dim3(pt_num_sms() * ctas), dim3(kSBWarps * 32),
+                          smem, st, sp));
+    return PT_OK;
+}
+
+static int sb_env(const char *name, int dflt) {
+    const char *e = getenv(name);
+    return (e && *e) ? atoi(e) : dflt;
+}
+
+template <int G, int D>
+static int sb_nst(const BoundedScoreParams &sp, cudaStream_t st) {
+    // ring depth x CTAs per SM (PT_SB_NST / PT_SB_CTAS: tuning)
+    const int nst = sb_env("PT_SB_NST", 2), ctas = sb_env("PT_SB_CTAS", 2);
+    switch (nst) {
+        case 3: return sb_launch<G, D, 3>(sp, ctas, st);
+        case 4: return sb_launch<G, D, 4>(sp, ctas, st);
+        default: return sb_launch<G, D, 2>(sp, ctas, st);
+    }
+}
+
+template <int D>
+static int sb_g(const BoundedScoreParams &sp, int G, cudaStream_t st) {
+    switch (G) {
+        case 1: return sb_nst<1, D>(sp, st);
+        case 2: return sb_nst<2, D>(sp, st);
+        case 3: return sb_nst<3, D>(sp, st);
+        case 4: return sb_nst<4, D>(sp, st);
+        case 5: return sb_nst<5, D>(sp, st);
+        case 6: return sb_nst<6, D>(sp, st);
+        case 7: return sb_nst<7, D>(sp, st);
+        case 8: return sb_nst<8, D>(sp, st);
+        default: return PT_ERR_UNSUPPORTED;
+    }
+}
+
+}  // namespace pt
+
+using namespace pt;
+
+extern "C" int pt_score_bounded(const void *q, int q_dtype, const float *lamnorm, const float *qnorm,
+                                const void *mirror, const float *stds, const int32_t *seq_len, int U,
+                                int G, int D, int S, int Pmax, uint16_t *keys_lo, uint16_t *keys_hi,
+                                uint16_t *tile_max, void *stream) {
+    if (!q || !lamnorm || !qnorm || !mirror || !stds || !seq_len || !keys_lo || !keys_hi ||
+        !tile_max || U < 0 || S < 1 || Pmax % 32 || G < 1)
+        return PT_ERR_INVALID;
+    if (q_dtype != PT_BF16 || G > 8 || !(D == 64 || D == 128) || U > kSBMaxUnits ||
+        (long long)U * (Pmax / 32) >= (1LL << 31))
+        return PT_ERR_UNSUPPORTED;
+    if (U == 0) return PT_OK;
+    const MirrorView mv = mirror_view(mirror, U, Pmax, D);
+    BoundedScoreParams sp{static_cast<const uint16_t *>(q), lamnorm, qnorm, mv.tiles, stds, mv.err,
+                          seq_len, keys_lo, keys_hi, tile_max, U, S, Pmax};
+    cudaStream_t st = (cudaStream_t)stream;
+    return D == 128 ? sb_g<128>(sp, G, st) : sb_g<64>(sp, G, st);
+}

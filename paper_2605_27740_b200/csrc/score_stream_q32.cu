@@ -15,7 +15,7 @@ static int ss_launch_n(const StreamScoreParams &sp, int ctas, cudaStream_t st) {
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured = smem;
     }
-    PT_CUDA_TRY(pt_launch(k_score_stream<PT_F32, SDT, G, D, NST, CPSW>, dim3(148 * ctas), dim3(kSSWarps * 32),
+    PT_CUDA_TRY(pt_launch(k_score_stream<PT_F32, SDT, G, D, NST, CPSW>, dim3(pt_num_sms() * ctas), dim3(kSSWarps * 32),
                           smem, st, sp));
     return PT_OK;
 }

@@ -368,18 +368,29 @@ struct SelectCandShared {
     uint32_t cand[kCandMax];
 };
 
-template <int NT>
+// Bounded mode (attend_fused.cu with pt_score_bounded's key intervals): skeys holds the
+// interval's lower keys, `resolve(L)` (block-wide) replaces the key of every page whose
+// interval reaches L by its exact key and returns the largest key it wrote (or -1), and L is
+// the kL-th (= k + 1-th) largest tile maximum -- so the k + 1 largest exact keys all lie in
+// the candidate list and everything below it is strictly smaller.
+struct NoResolve {
+    __device__ int operator()(int) const { return -1; }
+};
+
+template <int NT, class Resolve = NoResolve>
 __device__ bool select_cand(const uint16_t *__restrict__ skeys, const uint16_t *__restrict__ tmax_g,
                             int P, int k, const int32_t *__restrict__ map,
                             int32_t *__restrict__ out, int32_t *__restrict__ out_l,
                             int32_t *__restrict__ n_sel, int32_t *__restrict__ kth,
                             int32_t *__restrict__ kplus1, SelectCandShared<NT> &sh, int *slist,
                             bool slist_physical, unsigned long long *tp = nullptr,
-                            bool tmax_shared = false) {
+                            bool tmax_shared = false, int kL = 0,
+                            const Resolve &resolve = Resolve()) {
     constexpr int NWP = NT / 32;
     constexpr int MAXT = 8;  // tile maxima per thread: ceil(P / 32) <= NT * MAXT
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (P <= k || P > 65536) return false;
+    const int kl = kL > 0 ? kL : k;
     auto stamp = [&](int i) {
         if (tp && tid == 0) {
             unsigned long long t;
@@ -431,7 +442,7 @@ __device__ bool select_cand(const uint16_t *__restrict__ skeys, const uint16_t *
         return t;
     };
     const int ntiles = (P + 31) >> 5;
-    const bool use_tiles = tmax_g != nullptr && ntiles >= k && ntiles <= NT * MAXT;
+    const bool use_tiles = tmax_g != nullptr && ntiles >= kl && ntiles <= NT * MAXT;
     int tm[MAXT];
 #pragma unroll
     for (int i = 0; i < MAXT; i++) {
@@ -474,7 +485,7 @@ __device__ bool select_cand(const uint16_t *__restrict__ skeys, const uint16_t *
         int ia = -1, cum = 0, before = 0;
 #pragma unroll
         for (int b = 0; b < 8; b++) {
-            if (ia < 0 && cum + ta[b] >= k) { ia = b; before = cum; }
+            if (ia < 0 && cum + ta[b] >= kl) { ia = b; before = cum; }
             cum += ta[b];
         }
         if (ia >= 0) {
@@ -483,14 +494,16 @@ __device__ bool select_cand(const uint16_t *__restrict__ skeys, const uint16_t *
             bool done = false;
 #pragma unroll
             for (int b = 0; b < 8; b++) {
-                if (!done && c2 + tb[b] >= k) { ib = b; done = true; }
+                if (!done && c2 + tb[b] >= kl) { ib = b; done = true; }
                 c2 += tb[b];
             }
             L = mx - (8 * ia + ib);
         }
         __syncthreads();
         if (tid < 64) sh.bins[tid] = 0;
+        mx = max(mx, resolve(L));  // L < 0: every uncertain key
     } else {
+        resolve(-1);
         int m = -1, n = 0xFFFF;
         for (int v = tid; v < nvec; v += NT) {
             uint32_t w[4], mk[4];

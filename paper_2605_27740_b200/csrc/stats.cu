@@ -22,7 +22,8 @@ constexpr int kMaxD = 512;
 template <int DT, int SDT, int DJ>
 __device__ __forceinline__ void page_stats_warp(const void *k_pool, int64_t pid, int rows, int S,
                                                 int D, int64_t u, int64_t p, int64_t Pmax,
-                                                void *means, float *stds, double *var_smem) {
+                                                void *means, float *stds, double *var_smem,
+                                                const MirrorView mv) {
     const int lane = threadIdx.x & 31;
     const int64_t base = pid * (int64_t)S * D;
     double mean[DJ];
@@ -50,6 +51,7 @@ __device__ __forceinline__ void page_stats_warp(const void *k_pool, int64_t pid,
             store_elem<SDT>(means, mean_offset(u, p, d, D, Pmax, V), __double2float_rn(mean[j]));
         }
     }
+    if (mv.tiles) store_mirror<DJ>(mean, D, u, p, Pmax, mv, lane);
     __syncwarp();
     if (lane == 0) stds[u * Pmax + p] = __double2float_rn(__dsqrt_rn(np_sum(DoubleArray{var_smem}, D)));
     __syncwarp();
@@ -60,7 +62,8 @@ template <int DT, int SDT, int DJ>
 __global__ void __launch_bounds__(kStatsWarps * 32)
     k_page_stats(const void *__restrict__ k_pool, const int32_t *__restrict__ page_table,
                  const int32_t *__restrict__ seq_len, const int32_t *__restrict__ page_begin,
-                 int S, int D, int Pmax, void *__restrict__ means, float *__restrict__ stds) {
+                 int S, int D, int Pmax, void *__restrict__ means, float *__restrict__ stds,
+                 const MirrorView mv) {
     __shared__ double var_smem[kStatsWarps][kMaxD];
     const int warp = threadIdx.x >> 5;
     const int64_t u = blockIdx.y;
@@ -71,7 +74,7 @@ __global__ void __launch_bounds__(kStatsWarps * 32)
     if (p >= P || p < p0) return;
     const int rows = (p == P - 1) ? n - (int)p * S : S;
     const int64_t pid = page_table[u * Pmax + p];
-    page_stats_warp<DT, SDT, DJ>(k_pool, pid, rows, S, D, u, p, Pmax, means, stds, var_smem[warp]);
+    page_stats_warp<DT, SDT, DJ>(k_pool, pid, rows, S, D, u, p, Pmax, means, stds, var_smem[warp], mv);
 }
 
 // ---------------------------------------------------------------------------
@@ -185,7 +188,7 @@ __global__ void __launch_bounds__(256)
              int32_t *__restrict__ page_table, int32_t *__restrict__ seq_len, int U, int S, int D,
              int Pmax, void *__restrict__ means, float *__restrict__ stds,
              int32_t *__restrict__ pool_state, const int32_t *__restrict__ free_list,
-             int32_t *__restrict__ slot, int prof) {
+             int32_t *__restrict__ slot, int prof, const MirrorView mv) {
     extern __shared__ __align__(16) char asmem[];
     __shared__ int warp_tot[8];
     __shared__ int carry;
@@ -295,6 +298,7 @@ __global__ void __launch_bounds__(256)
                     store_elem<SDT>(means, mean_offset(u, n / S, d, D, Pmax, V), __double2float_rn(mean[j]));
                 }
             }
+            if (mv.tiles) store_mirror<DJ>(mean, D, u, n / S, Pmax, mv, lane);
             __syncwarp();
             const double vsum = np_sum_warp(var_s, D, lane);
             if (lane == 0) {
@@ -369,7 +373,7 @@ __global__ void __launch_bounds__(256)
              const int32_t *__restrict__ row_begin, const int32_t *__restrict__ n_rows,
              void *__restrict__ k_pool, void *__restrict__ v_pool,
              const int32_t *__restrict__ page_table, int S, int D, int Pmax,
-             void *__restrict__ means, float *__restrict__ stds) {
+             void *__restrict__ means, float *__restrict__ stds, const MirrorView mv) {
     extern __shared__ __align__(16) char esmem[];
     constexpr int ES = DT == PT_F32 ? 4 : 2;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpc = blockDim.x >> 5;
@@ -433,6 +437,7 @@ __global__ void __launch_bounds__(256)
             store_elem<SDT>(means, mean_offset(u, p, d, D, Pmax, V), __double2float_rn(mean[j]));
         }
     }
+    if (mv.tiles) store_mirror<DJ>(mean, D, u, p, Pmax, mv, lane);
     __syncwarp();
     if (lane == 0) stds[u * Pmax + p] = __double2float_rn(__dsqrt_rn(np_sum(DoubleArray{var_s}, D)));
 }
@@ -467,13 +472,13 @@ using namespace pt;
 template <int DT, int SDT>
 static int launch_stats(const void *k_pool, const int32_t *pt_, const int32_t *sl,
                         const int32_t *pb, int U, int S, int D, int Pmax, void *means,
-                        float *stds, cudaStream_t st) {
+                        float *stds, const MirrorView mv, cudaStream_t st) {
     dim3 grid((Pmax + kStatsWarps - 1) / kStatsWarps, U);
     const int dj = (D + 31) / 32;
 #define PT_STATS_CASE(DJ_)                                                                    \
     case DJ_:                                                                                 \
         k_page_stats<DT, SDT, DJ_><<<grid, kStatsWarps * 32, 0, st>>>(k_pool, pt_, sl, pb, S, D, \
-                                                                       Pmax, means, stds);    \
+                                                                       Pmax, means, stds, mv);    \
         break;
     switch (dj) {
         PT_STATS_CASE(1)
@@ -497,20 +502,21 @@ static int stats_dj_ok(int D) {
 extern "C" int pt_page_stats(const void *k_pool, int kv_dtype, const int32_t *page_table,
                              const int32_t *seq_len, const int32_t *page_begin, int U, int S,
                              int D, int Pmax, void *means, int stats_dtype, float *stds,
-                             void *stream) {
-    if (!k_pool || !page_table || !seq_len || !means || !stds || U < 0 || S < 1 || Pmax % 32)
+                             void *mirror, void *stream) {
+    if (!k_pool || !page_table || !seq_len || !means || !stds || U < 0 || S < 1 || Pmax % 32 ||
+        (mirror && (stats_dtype != PT_F32 || D % 8)))
         return PT_ERR_INVALID;
     if (!stats_dj_ok(D)) return PT_ERR_UNSUPPORTED;
     if (U == 0) return PT_OK;
     cudaStream_t st = (cudaStream_t)stream;
     if (kv_dtype == PT_F32 && stats_dtype == PT_F32)
-        return launch_stats<PT_F32, PT_F32>(k_pool, page_table, seq_len, page_begin, U, S, D, Pmax, means, stds, st);
+        return launch_stats<PT_F32, PT_F32>(k_pool, page_table, seq_len, page_begin, U, S, D, Pmax, means, stds, mirror_view(mirror, U, Pmax, D), st);
     if (kv_dtype == PT_BF16 && stats_dtype == PT_F32)
-        return launch_stats<PT_BF16, PT_F32>(k_pool, page_table, seq_len, page_begin, U, S, D, Pmax, means, stds, st);
+        return launch_stats<PT_BF16, PT_F32>(k_pool, page_table, seq_len, page_begin, U, S, D, Pmax, means, stds, mirror_view(mirror, U, Pmax, D), st);
     if (kv_dtype == PT_BF16 && stats_dtype == PT_BF16)
-        return launch_stats<PT_BF16, PT_BF16>(k_pool, page_table, seq_len, page_begin, U, S, D, Pmax, means, stds, st);
+        return launch_stats<PT_BF16, PT_BF16>(k_pool, page_table, seq_len, page_begin, U, S, D, Pmax, means, stds, mirror_view(mirror, U, Pmax, D), st);
     if (kv_dtype == PT_F32 && stats_dtype == PT_BF16)
-        return launch_stats<PT_F32, PT_BF16>(k_pool, page_table, seq_len, page_begin, U, S, D, Pmax, means, stds, st);
+        return launch_stats<PT_F32, PT_BF16>(k_pool, page_table, seq_len, page_begin, U, S, D, Pmax, means, stds, mirror_view(mirror, U, Pmax, D), st);
     return PT_ERR_INVALID;
 }
 
@@ -518,7 +524,7 @@ template <int DT, int SDT>
 static int launch_append(const void *kn, const void *vn, void *kp, void *vp, int32_t *ptab,
                          int32_t *sl, int U, int S, int D, int Pmax, void *means, float *stds,
                          int32_t *pool_state, const int32_t *free_list, int32_t *slot,
-                         cudaStream_t st) {
+                         const MirrorView mv, cudaStream_t st) {
     const size_t per_warp = append_per_warp(S, D, DT == PT_F32 ? 4 : 2);
     if (per_warp > 200 * 1024) return PT_ERR_UNSUPPORTED;
     int wpc = (int)((200 * 1024) / per_warp);
@@ -542,7 +548,7 @@ static int launch_append(const void *kn, const void *vn, void *kp, void *vp, int
         }                                                                                     \
         PT_CUDA_TRY(pt_launch(k_append<DT, SDT, DJ_>, dim3(grid), dim3(wpc * 32), smem, st,   \
                               kn, vn, kp, vp, ptab, sl, U, S, D, Pmax, means, stds,           \
-                              pool_state, free_list, slot, app_prof));                        \
+                              pool_state, free_list, slot, app_prof, mv));                    \
         break;                                                                                \
     }
     switch (dj) {
@@ -563,22 +569,23 @@ extern "C" int pt_append(const void *k_new, const void *v_new, void *k_pool, voi
                          int kv_dtype, int32_t *page_table, int32_t *seq_len, int U, int S, int D,
                          int Pmax, void *means, int stats_dtype, float *stds,
                          int32_t *pool_state, const int32_t *free_list, int32_t *slot_scratch,
-                         void *stream) {
+                         void *mirror, void *stream) {
     if (!k_new || !v_new || !k_pool || !v_pool || !page_table || !seq_len || !means || !stds ||
-        !pool_state || !slot_scratch || U < 0 || S < 1 || Pmax % 32)
+        !pool_state || !slot_scratch || U < 0 || S < 1 || Pmax % 32 ||
+        (mirror && (stats_dtype != PT_F32 || D % 8)))
         return PT_ERR_INVALID;
     if (!stats_dj_ok(D)) return PT_ERR_UNSUPPORTED;
     if (U == 0) return PT_OK;
     cudaStream_t st = (cudaStream_t)stream;
     int32_t *slot = slot_scratch;
     if (kv_dtype == PT_F32 && stats_dtype == PT_F32)
-        return launch_append<PT_F32, PT_F32>(k_new, v_new, k_pool, v_pool, page_table, seq_len, U, S, D, Pmax, means, stds, pool_state, free_list, slot, st);
+        return launch_append<PT_F32, PT_F32>(k_new, v_new, k_pool, v_pool, page_table, seq_len, U, S, D, Pmax, means, stds, pool_state, free_list, slot, mirror_view(mirror, U, Pmax, D), st);
     if (kv_dtype == PT_BF16 && stats_dtype == PT_F32)
-        return launch_append<PT_BF16, PT_F32>(k_new, v_new, k_pool, v_pool, page_table, seq_len, U, S, D, Pmax, means, stds, pool_state, free_list, slot, st);
+        return launch_append<PT_BF16, PT_F32>(k_new, v_new, k_pool, v_pool, page_table, seq_len, U, S, D, Pmax, means, stds, pool_state, free_list, slot, mirror_view(mirror, U, Pmax, D), st);
     if (kv_dtype == PT_BF16 && stats_dtype == PT_BF16)
-        return launch_append<PT_BF16, PT_BF16>(k_new, v_new, k_pool, v_pool, page_table, seq_len, U, S, D, Pmax, means, stds, pool_state, free_list, slot, st);
+        return launch_append<PT_BF16, PT_BF16>(k_new, v_new, k_pool, v_pool, page_table, seq_len, U, S, D, Pmax, means, stds, pool_state, free_list, slot, mirror_view(mirror, U, Pmax, D), st);
     if (kv_dtype == PT_F32 && stats_dtype == PT_BF16)
-        return launch_append<PT_F32, PT_BF16>(k_new, v_new, k_pool, v_pool, page_table, seq_len, U, S, D, Pmax, means, stds, pool_state, free_list, slot, st);
+        return launch_append<PT_F32, PT_BF16>(k_new, v_new, k_pool, v_pool, page_table, seq_len, U, S, D, Pmax, means, stds, pool_state, free_list, slot, mirror_view(mirror, U, Pmax, D), st);
     return PT_ERR_INVALID;
 }
 
@@ -619,7 +626,8 @@ extern "C" int pt_write_rows(const void *k_rows, const void *v_rows, int n_max,
 template <int DT, int SDT>
 static int launch_extend(const void *kr, const void *vr, int n_max, const int32_t *rb,
                          const int32_t *nrw, void *kp, void *vp, const int32_t *ptab, int U, int S,
-                         int D, int Pmax, void *means, float *stds, cudaStream_t st) {
+                         int D, int Pmax, void *means, float *stds, const MirrorView mv,
+                         cudaStream_t st) {
     const size_t per_warp = (size_t)S * D * 4 + (size_t)D * 8;
     int wpc = (int)((96 * 1024) / per_warp);  // >= 2 CTAs per SM
     if (wpc > 8) wpc = 8;
@@ -638,7 +646,8 @@ static int launch_extend(const void *kr, const void *vr, int n_max, const int32_
             configured = smem;                                                                \
         }                                                                                     \
         k_extend<DT, SDT, DJ_><<<grid, wpc * 32, smem, st>>>(kr, vr, n_max, rb, nrw, kp, vp,  \
-                                                             ptab, S, D, Pmax, means, stds); \
+                                                             ptab, S, D, Pmax, means, stds,   \
+                                                             mv);                             \
         break;                                                                                \
     }
     switch (dj) {
@@ -659,9 +668,10 @@ extern "C" int pt_extend(const void *k_rows, const void *v_rows, int n_max,
                          const int32_t *row_begin, const int32_t *n_rows, void *k_pool,
                          void *v_pool, int kv_dtype, const int32_t *page_table, int U, int S,
                          int D, int Pmax, void *means, int stats_dtype, float *stds,
-                         void *stream) {
+                         void *mirror, void *stream) {
     if (!k_rows || !v_rows || !row_begin || !n_rows || !k_pool || !v_pool || !page_table ||
-        !means || !stds || U < 0 || n_max < 0 || S < 1 || Pmax % 32)
+        !means || !stds || U < 0 || n_max < 0 || S < 1 || Pmax % 32 ||
+        (mirror && (stats_dtype != PT_F32 || D % 8)))
         return PT_ERR_INVALID;
     if (!stats_dj_ok(D)) return PT_ERR_UNSUPPORTED;
     if (U == 0 || n_max == 0) return PT_OK;
@@ -669,7 +679,7 @@ extern "C" int pt_extend(const void *k_rows, const void *v_rows, int n_max,
 #define PT_EXT(DT_, SDT_)                                                                     \
     if (kv_dtype == DT_ && stats_dtype == SDT_)                                               \
         return launch_extend<DT_, SDT_>(k_rows, v_rows, n_max, row_begin, n_rows, k_pool,     \
-                                        v_pool, page_table, U, S, D, Pmax, means, stds, st);
+                                        v_pool, page_table, U, S, D, Pmax, means, stds, mirror_view(mirror, U, Pmax, D), st);
     PT_EXT(PT_F32, PT_F32) PT_EXT(PT_BF16, PT_F32) PT_EXT(PT_BF16, PT_BF16) PT_EXT(PT_F32, PT_BF16)
 #undef PT_EXT
     return PT_ERR_INVALID;

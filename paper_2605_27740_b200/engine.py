@@ -4,8 +4,10 @@ One decode step for every (sequence, kv-head) unit of a :class:`PagedKvCache`:
 
     append K/V row    (K1b: pt_append)        kvcache.py:185-208
     lambda * ||q||    (pt_lam_norms_chained)  scoring.py:39-47        (runs beside the append)
-    score             (K2: pt_score_prenorm)  scoring.py:108-124 -> bf16 -> ordered keys
-                                              (+ per-32-page tile maxima)
+    score             (K2b: pt_score_bounded) scoring.py:108-124 -> bf16 -> ordered keys, as
+                                              [lower, upper] key intervals from the bf16 mirror
+                                              of the f32 means (+ per-32-page tile maxima);
+                      (K2: pt_score_prenorm)  exact keys from the f32 means (no mirror, f32 q)
     select + attend   (K3+K4: pt_select_attend) select.py:87-115 + page-table translation,
                                               then attention.py:94-107 for the G heads
 
@@ -71,6 +73,13 @@ class DecodeEngine:
         self.tickets = torch.zeros(U, dtype=torch.int32, device=d)
         self.score_counters = torch.zeros(U, dtype=torch.int32, device=d)
         self.lamnorm = torch.zeros(U * 8, dtype=torch.float32, device=d)
+        # bounded scoring (cache.mirror): upper keys of the score intervals and ||q|| bounds;
+        # the selection resolves the straddling pages exactly
+        self.bounded = (cache.mirror is not None and not keep_scores
+                        and os.environ.get("PT_NO_BOUNDED", "") != "1")
+        self.keys_hi = torch.zeros(U, Pmax, dtype=torch.int16, device=d) if self.bounded else None
+        self.qnorm = torch.zeros(U * 8, dtype=torch.float32, device=d) if self.bounded else None
+        self._step_bounded = False  # the keys of the last scoring are intervals
         # K2 streaming kernel + K3 (two launches) is the default; the one-launch fused
         # score+select CTA kernel (pt_score_select) is kept as an alternative
         self.fused_select = False
@@ -93,6 +102,7 @@ class DecodeEngine:
         return q2, dev.dtype_code(q2.dtype)
 
     def score(self, q: torch.Tensor, norms: torch.Tensor | None = None, stream=None) -> None:
+        self._step_bounded = False
         q2, qc = self._q(q)
         c = self.cache
         _lib.call("pt_score", q2.data_ptr(), qc, dev.ptr(norms), c.means.data_ptr(), c.stats_code,
@@ -109,10 +119,38 @@ class DecodeEngine:
         q2, qc = self._q(q)
         _lib.call("pt_lam_norms_chained" if chained else "pt_lam_norms", q2.data_ptr(), qc,
                   dev.ptr(norms), self.U, self.G, self.D, self.lam, self.lamnorm.data_ptr(),
-                  dev.stream_handle(stream))
+                  dev.ptr(self.qnorm), dev.stream_handle(stream))
+
+    def score_bounded(self, q: torch.Tensor, stream=None) -> bool:
+        """K2b over the bf16 mirror (reads the norms of :meth:`lam_norms`): key intervals into
+        keys / keys_hi; False when the shape needs the exact scorer."""
+        if not self.bounded:
+            return False
+        q2, qc = self._q(q)
+        c = self.cache
+        rc = _lib.load().pt_score_bounded(
+            q2.data_ptr(), qc, self.lamnorm.data_ptr(), self.qnorm.data_ptr(), c.mirror.data_ptr(),
+            c.stds.data_ptr(), c.seq_lens.data_ptr(), self.U, self.G,
+            self.D, c.layout.page_size, c.Pmax, self.keys.data_ptr(), self.keys_hi.data_ptr(),
+            self.tile_max.data_ptr(), dev.stream_handle(stream))
+        if rc == _lib.PT_ERR_UNSUPPORTED:
+            return False
+        _lib.check(rc, "pt_score_bounded")
+        self._step_bounded = True
+        return True
+
+    def score_step(self, q: torch.Tensor, stream=None) -> None:
+        """The scoring launch of :meth:`step` (after :meth:`lam_norms`): bounded where the
+        shape allows, else the exact streaming scorer, else the CTA scorer."""
+        self._step_bounded = False
+        if self.score_bounded(q, stream=stream):
+            return
+        if not self.score_prenorm(q, stream=stream):
+            self.score(q, stream=stream)
 
     def score_prenorm(self, q: torch.Tensor, stream=None) -> bool:
         """K2 reading the norms of :meth:`lam_norms`; False when the shape needs :meth:`score`."""
+        self._step_bounded = False
         q2, qc = self._q(q)
         c = self.cache
         rc = _lib.load().pt_score_prenorm(
@@ -180,11 +218,15 @@ class DecodeEngine:
         """K3 + K4 in one launch (pt_select_attend): per unit, select the top-k pages from the
         keys of :meth:`score`, then attend over them -- identical outputs to :meth:`select`
         followed by :meth:`attend`, which run instead outside the fused kernel's envelope."""
-        if self.fused_attend:
+        bnd = self._step_bounded
+        if self.fused_attend or bnd:
             q2, qc = self._q(q)
             c = self.cache
             rc = _lib.load().pt_select_attend(
-                self.keys.data_ptr(), self.tile_max.data_ptr(), c.seq_lens.data_ptr(), c.page_table.data_ptr(), self.U,
+                self.keys.data_ptr(), self.tile_max.data_ptr(),
+                self.keys_hi.data_ptr() if bnd else None, c.mirror.data_ptr() if bnd else None,
+                c.stds.data_ptr() if bnd else None, self.lamnorm.data_ptr() if bnd else None,
+                c.seq_lens.data_ptr(), c.page_table.data_ptr(), self.U,
                 c.layout.page_size, c.Pmax, self.k, self.sel.data_ptr(),
                 dev.ptr(self.sel_logical), self.n_sel.data_ptr(), self.kth.data_ptr(),
                 self.kplus1.data_ptr(), q2.data_ptr(), qc, c.k_pool.data_ptr(),
@@ -195,6 +237,12 @@ class DecodeEngine:
                 return
             if rc != _lib.PT_ERR_UNSUPPORTED:
                 _lib.check(rc, "pt_select_attend")
+            if bnd:
+                # interval keys need the fused kernel's resolution: rescore exactly instead
+                self.bounded = self._step_bounded = False
+                if not self.score_prenorm(q, stream=stream):
+                    self.score(q, stream=stream)
+                return self.select_attend(q, stream=stream)
             self.fused_attend = False
         self.select(stream=stream)
         self.attend(q, stream=stream)
@@ -222,8 +270,7 @@ class DecodeEngine:
             if k_new is not None:
                 self.cache.append_batch(k_new, v_new, stream=main)
             main.wait_stream(self._side)
-        if not self.score_prenorm(q, stream=main):
-            self.score(q, stream=main)
+        self.score_step(q, stream=main)
         self.select_attend(q, stream=main)
         return self.out, self.lse
 

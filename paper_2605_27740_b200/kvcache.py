@@ -87,7 +87,7 @@ def compute_page_stats(keys) -> PageStats:
     means = torch.zeros(32 * D, dtype=torch.float32, device=device)
     stds = torch.zeros(1, 32, dtype=torch.float32, device=device)
     _lib.call("pt_page_stats", pool.data_ptr(), _lib.PT_F32, table.data_ptr(), seq.data_ptr(),
-              None, 1, c, D, 32, means.data_ptr(), _lib.PT_F32, stds.data_ptr(),
+              None, 1, c, D, 32, means.data_ptr(), _lib.PT_F32, stds.data_ptr(), None, None,
               dev.stream_handle())
     mean = dev.untile_means(means, 1, 32, D, torch.float32)[0, 0].cpu().numpy()
     return PageStats(count=c, mean=mean, std=float(stds[0, 0].item()))
@@ -192,6 +192,7 @@ class PagedKvCache:
         stats_dtype: torch.dtype = torch.float32,
         max_pages_per_head: int | None = None,
         device=None,
+        mirror: bool | None = None,
     ) -> None:
         if batch < 1:
             raise ValueError("batch must be positive")
@@ -220,6 +221,17 @@ class PagedKvCache:
         self.seq_lens = torch.zeros(U, dtype=torch.int32, device=d)
         self.means = torch.zeros(U * self.Pmax * D, dtype=stats_dtype, device=d)
         self.stds = torch.zeros(U, self.Pmax, dtype=torch.float32, device=d)
+        # bf16 mirror of the f32 means + its per-page error bound (bounded scoring,
+        # DESIGN.md): on by default for bf16 KV with exact f32 stats (the decode engine then
+        # streams half the scoring bytes and still selects exactly as the f32 reference)
+        if mirror is None:
+            mirror = stats_dtype == torch.float32 and dtype == torch.bfloat16 and D % 8 == 0
+        if mirror and (stats_dtype != torch.float32 or D % 8):
+            raise ValueError("the bf16 mirror needs f32 page stats and head_dim % 8 == 0")
+        self.mirror = None
+        if mirror:
+            nb = _lib.load().pt_mirror_bytes(U, self.Pmax, D)
+            self.mirror = torch.zeros(nb, dtype=torch.uint8, device=d)
         # {bump_next, free_count, max_pages, error_flag}
         self.pool_state = torch.tensor([0, 0, layout.max_pages, 0], dtype=torch.int32, device=d)
         self.free_list_dev = torch.zeros(layout.max_pages, dtype=torch.int32, device=d)
@@ -228,6 +240,23 @@ class PagedKvCache:
         self.split_extend = False
         self._seq_host = np.zeros(U, dtype=np.int64)
         self.table = _DevicePageTable(self)
+
+    def _mirror_args(self):
+        return (None if self.mirror is None else self.mirror.data_ptr(),)
+
+    def mirror_views(self):
+        """(bf16 tiles [U*Pmax*D], f32 rows [U][Pmax][D], err [U][Pmax]) views of the mirror
+        block (readback / tests), or None."""
+        if self.mirror is None:
+            return None
+        U, P, D = self.num_units, self.Pmax, self.layout.head_dim
+        al = lambda x: (x + 255) // 256 * 256  # noqa: E731
+        n = U * P
+        t0, t1 = al(n * D * 2), al(n * D * 4)
+        tiles = self.mirror[: n * D * 2].view(torch.bfloat16)
+        rows = self.mirror[t0 : t0 + n * D * 4].view(torch.float32).view(U, P, D)
+        err = self.mirror[t0 + t1 : t0 + t1 + n * 4].view(torch.float32).view(U, P)
+        return tiles, rows, err
 
     # ------------------------------------------------------------------
     # Shape queries
@@ -305,7 +334,8 @@ class PagedKvCache:
             _lib.call("pt_extend", kk.data_ptr(), vv.data_ptr(), n_max, row_begin.data_ptr(),
                       nrows_t.data_ptr(), self.k_pool.data_ptr(), self.v_pool.data_ptr(),
                       self.kv_code, self.page_table.data_ptr(), U, S, D, self.Pmax,
-                      self.means.data_ptr(), self.stats_code, self.stds.data_ptr(), sh)
+                      self.means.data_ptr(), self.stats_code, self.stds.data_ptr(),
+                      *self._mirror_args(), sh)
             self.seq_lens.copy_(torch.from_numpy(n1.astype(np.int32)))
             return
         _lib.call("pt_write_rows", kk.data_ptr(), vv.data_ptr(), n_max, row_begin.data_ptr(),
@@ -316,7 +346,8 @@ class PagedKvCache:
         page_begin = torch.from_numpy(first).to(d)
         _lib.call("pt_page_stats", self.k_pool.data_ptr(), self.kv_code,
                   self.page_table.data_ptr(), self.seq_lens.data_ptr(), page_begin.data_ptr(), U,
-                  S, D, self.Pmax, self.means.data_ptr(), self.stats_code, self.stds.data_ptr(), sh)
+                  S, D, self.Pmax, self.means.data_ptr(), self.stats_code, self.stds.data_ptr(),
+                  *self._mirror_args(), sh)
 
     def extend(self, head: int, keys, values) -> None:
         """Bulk append to one head; same result as appending row by row (kvcache.py:210-233)."""
@@ -364,7 +395,7 @@ class PagedKvCache:
                   self.seq_lens.data_ptr(), U, self.layout.page_size, D, self.Pmax,
                   self.means.data_ptr(), self.stats_code, self.stds.data_ptr(),
                   self.pool_state.data_ptr(), self.free_list_dev.data_ptr(),
-                  self._slot.data_ptr(), dev.stream_handle(stream))
+                  self._slot.data_ptr(), *self._mirror_args(), dev.stream_handle(stream))
         self._seq_host += 1
 
     def check_errors(self) -> None:

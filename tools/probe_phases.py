@@ -11,6 +11,14 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
+def eng_nchunk(U):
+    """chunks per unit of the fused kernel's grid (attend_fused.cu: 2 CTAs per SM)"""
+    import torch
+
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    return max(1, (sms * 2) // U)
+
+
 def main():
     import torch
 
@@ -22,6 +30,7 @@ def main():
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--ctx", type=int, default=131072)
     ap.add_argument("--budget", type=int, default=2048)
+    ap.add_argument("--exact", action="store_true", help="exact f32-means keys (no mirror)")
     a = ap.parse_args()
     ns = argparse.Namespace(batch=a.batch, ctx=a.ctx, q_heads=32, kv_heads=8, head_dim=128,
                             page=16, budget=a.budget, stats_dtype="f32", warmup=3, steps=10)
@@ -33,7 +42,29 @@ def main():
     g.manual_seed(7)
     q = torch.randn(U * G, D, generator=g, device=dev).to(torch.bfloat16)
     eng = pt.DecodeEngine(cache, G, a.budget // S)
-    eng.score(q)
+    if a.exact:
+        eng.bounded = False
+    eng.lam_norms(q)
+    eng.score_step(q)
+    stats = {"bounded": bool(eng._step_bounded)}
+    if eng._step_bounded:
+        # how many pages the selection must resolve: interval not one key and reaching L
+        # (the (k+1)-th largest tile maximum of the lower keys)
+        k = a.budget // S
+        klo = eng.keys.cpu().numpy().view(np.uint16).astype(np.int64)
+        khi = eng.keys_hi.cpu().numpy().view(np.uint16).astype(np.int64)
+        tm = eng.tile_max.cpu().numpy().view(np.uint16).astype(np.int64)
+        P = cache.num_pages(0)
+        nt = -(-P // 32)
+        L = -np.sort(-tm[:, :nt], axis=1)[:, k]
+        unsure = klo[:, :P] != khi[:, :P]
+        reach = khi[:, :P] >= L[:, None]
+        stats["unsure_frac"] = float(unsure.mean())
+        stats["cand_per_unit"] = float(reach.sum(1).mean())
+        stats["resolve_per_unit_mean"] = float((unsure & reach).sum(1).mean())
+        stats["resolve_per_unit_max"] = int((unsure & reach).sum(1).max())
+        stats["exact_ge_L_per_unit"] = float((klo[:, :P] >= L[:, None]).sum(1).mean())
+        stats["width_keys_mean"] = float((khi[:, :P] - klo[:, :P]).mean())
     for _ in range(3):
         eng.select_attend(q)
     torch.cuda.synchronize()
@@ -41,15 +72,22 @@ def main():
     eng.select_attend(q)
     torch.cuda.synchronize()
     os.environ.pop("PT_SA_PROF")
-    n = U * 10
+    nch = int(eng_nchunk(U))
+    n = U * nch * 20
     buf = np.zeros(n, dtype=np.uint64)
     _lib.check(_lib.load().pt_debug_sa_prof(buf.ctypes.data, n))
-    t = buf.reshape(U, 10).astype(np.float64)
+    raw = buf.reshape(U * nch, 20)
+    t = raw[:, :15].astype(np.float64)
+    t[:, 15 - 1] = raw[:, 14]
+    # stamps 10..13: resolve start / scan done / rows staged / resolved; 14: khi+q staged;
+    # 15: rounds * 1e6 + pages listed in the last round
+    info = raw[:, 15]
     t0 = t[:, 0].min()
     rel = (t - t0) / 1000.0
     names = ["entry", "keys_staged", "selected", "first_page", "stream_done", "exit",
-             "sel_loads_max", "sel_L", "sel_cands", "sel_thr"]
-    out = {}
+             "sel_loads_max", "sel_L", "sel_cands", "sel_thr", "res_start", "res_scan", "res_staged",
+             "res_done", "bnd_staged"]
+    out = {"resolve": stats}
     for i, nm in enumerate(names):
         col = rel[:, i]
         out[nm] = {p: round(float(np.percentile(col, p)), 2) for p in (0, 10, 50, 90, 100)}
@@ -65,6 +103,21 @@ def main():
         "sel_thr": float(np.median(rel[:, 9] - rel[:, 8])),
         "sel_pick_translate": float(np.median(rel[:, 2] - rel[:, 9])),
     }
+    if stats.get("bounded"):
+        out["durations_us_median"].update({
+            "bnd_khi_q_staged": float(np.median(rel[:, 14] - rel[:, 1])),
+            "res_scan": float(np.median(rel[:, 11] - rel[:, 10])),
+            "res_stage": float(np.median(rel[:, 12] - rel[:, 11])),
+            "res_compute": float(np.median(rel[:, 13] - rel[:, 12])),
+            "res_total": float(np.median(rel[:, 13] - rel[:, 10])),
+            "L_before_resolve": float(np.median(rel[:, 10] - rel[:, 14])),
+            "r1_first_barrier": float(np.median((raw[:, 16].astype(np.float64) - t0) / 1000.0 - rel[:, 10])),
+            "r1_scan_loop_t0": float(np.median((raw[:, 17].astype(np.float64) - raw[:, 16].astype(np.float64)) / 1000.0)),
+            "r1_trailing_barrier": float(np.median((raw[:, 18].astype(np.float64) - raw[:, 17].astype(np.float64)) / 1000.0)),
+            "r1_stage": float(np.median((raw[:, 19].astype(np.float64) - raw[:, 18].astype(np.float64)) / 1000.0)),
+            "r1_compute": float(np.median((raw[:, 15].astype(np.float64) - raw[:, 19].astype(np.float64)) / 1000.0)),
+        })
+
     print(json.dumps(out, indent=1))
 
 
