@@ -116,7 +116,8 @@ __host__ __device__ __forceinline__ size_t sa_keys_bytes(int Pmax) {
 // bounded-mode scratch after the exact-mode selection scratch: upper keys, the query rows
 // widened to f32 [D][8], the resolve list + its counter, the staged f32 means [rcap][D + 4]
 __host__ __device__ __forceinline__ size_t sa_bnd_bytes(int Pmax, int D, int rcap) {
-    return sa_keys_bytes(Pmax) + (size_t)D * 32 + 32 + (size_t)rcap * 8 + 16 + (size_t)rcap * (D + 4) * 4 + 16;
+    return sa_keys_bytes(Pmax) + (size_t)D * 32 + 32 + (size_t)rcap * 8 + 16 + (size_t)rcap * (D + 4) * 4 + 16 +
+           (size_t)kCandMax * 2;
 }
 
 // NT threads run the selection (NT / 32 warps); the first kSAWarps warps stream the pages
@@ -182,6 +183,31 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
             qb[ks][1] = b1;
         }
     }
+    // bounded mode scratch (after the exact-mode selection scratch): the upper keys, the
+    // query rows widened to f32 [D][8], lam ||q||, the resolve list / stds / counter / rows
+    const size_t sel_end = sa_keys_bytes(p.Pmax) + kSelectBins * 4 + (size_t)(p.Pmax / 32) * 2;
+    uint16_t *skhi = reinterpret_cast<uint16_t *>(smem + ((sel_end + 15) & ~(size_t)15));
+    float *sq = reinterpret_cast<float *>(reinterpret_cast<char *>(skhi) + sa_keys_bytes(p.Pmax));
+    float *sln = sq + D * 8;  // fl(lam * ||q_g||), 8
+    int *rlist = reinterpret_cast<int *>(sln + 8);
+    float *rstd = reinterpret_cast<float *>(rlist + p.rcap);
+    int *rcnt = reinterpret_cast<int *>(rstd + p.rcap);
+    float *rstage = reinterpret_cast<float *>(rcnt + 4);
+    // after rstage [rcap][RS] and the resolve mbarrier (16 bytes): the candidates' upper keys
+    uint16_t *candhi = reinterpret_cast<uint16_t *>(reinterpret_cast<char *>(rstage) +
+                                                    (size_t)p.rcap * (D + 4) * 4 + 16);
+    if constexpr (BND) {  // q is not written by the scorer: widened before the PDL wait
+        for (int i = threadIdx.x; i < D * 8; i += NT) {
+            const int d = i >> 3, g = i & 7;
+            float x = 0.f;
+            if (g < G) {
+                const int64_t e = (u * G + g) * (int64_t)D + d;
+                x = p.q_dtype == PT_BF16 ? bf16_bits_to_f32(static_cast<const uint16_t *>(p.q)[e])
+                                         : static_cast<const float *>(p.q)[e];
+            }
+            sq[i] = x;
+        }
+    }
     pdl_wait();
     if (prof) g_sa_prof[cta * kSAProfN + 1] = gtimer();
 
@@ -210,79 +236,114 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
         for (int j = 0; j < kTm; j++)
             if (tm_stage && threadIdx.x + j * NT < ntiles) tv[j] = __ldcg(tsrc + threadIdx.x + j * NT);
         const uint4 *src = reinterpret_cast<const uint4 *>(krow);
-        constexpr int kMax = 8;
+        const uint4 *hsrc = reinterpret_cast<const uint4 *>(BND ? p.keys_hi + u * (int64_t)p.Pmax : krow);
+        constexpr int kMax = BND ? 4 : 8;  // bounded: the upper keys in the same load round
         const int nv = (P + 7) / 8;
         for (int i0 = threadIdx.x; i0 < nv; i0 += kMax * NT) {
-            uint4 v[kMax];
+            uint4 v[kMax], w[kMax];
 #pragma unroll
             for (int j = 0; j < kMax; j++)
-                if (i0 + j * NT < nv) v[j] = __ldcg(src + i0 + j * NT);
+                if (i0 + j * NT < nv) {
+                    v[j] = __ldcg(src + i0 + j * NT);
+                    if constexpr (BND) w[j] = __ldcg(hsrc + i0 + j * NT);
+                }
 #pragma unroll
             for (int j = 0; j < kMax; j++)
-                if (i0 + j * NT < nv) reinterpret_cast<uint4 *>(skeys)[i0 + j * NT] = v[j];
+                if (i0 + j * NT < nv) {
+                    reinterpret_cast<uint4 *>(skeys)[i0 + j * NT] = v[j];
+                    if constexpr (BND) reinterpret_cast<uint4 *>(skhi)[i0 + j * NT] = w[j];
+                }
         }
 #pragma unroll
         for (int j = 0; j < kTm; j++)
             if (tm_stage && threadIdx.x + j * NT < ntiles) stm[threadIdx.x + j * NT] = tv[j];
     }
-    // bounded mode: the upper keys and the widened query rows beside them
-    const size_t sel_end = sa_keys_bytes(p.Pmax) + kSelectBins * 4 + (size_t)(p.Pmax / 32) * 2;
-    uint16_t *skhi = reinterpret_cast<uint16_t *>(smem + ((sel_end + 15) & ~(size_t)15));
-    float *sq = reinterpret_cast<float *>(reinterpret_cast<char *>(skhi) + sa_keys_bytes(p.Pmax));
-    float *sln = sq + D * 8;  // fl(lam * ||q_g||), 8
-    int *rlist = reinterpret_cast<int *>(sln + 8);
-    float *rstd = reinterpret_cast<float *>(rlist + p.rcap);
-    int *rcnt = reinterpret_cast<int *>(rstd + p.rcap);
-    float *rstage = reinterpret_cast<float *>(rcnt + 4);
     if constexpr (BND) {
-        const uint4 *src = reinterpret_cast<const uint4 *>(p.keys_hi + u * (int64_t)p.Pmax);
-        constexpr int kMax = 8;
-        const int nv = (P + 7) / 8;
-        for (int i0 = threadIdx.x; i0 < nv; i0 += kMax * NT) {
-            uint4 v[kMax];
-#pragma unroll
-            for (int j = 0; j < kMax; j++)
-                if (i0 + j * NT < nv) v[j] = __ldcg(src + i0 + j * NT);
-#pragma unroll
-            for (int j = 0; j < kMax; j++)
-                if (i0 + j * NT < nv) reinterpret_cast<uint4 *>(skhi)[i0 + j * NT] = v[j];
-        }
-        for (int i = threadIdx.x; i < D * 8; i += NT) {
-            const int d = i >> 3, g = i & 7;
-            float x = 0.f;
-            if (g < G) {
-                const int64_t e = (u * G + g) * (int64_t)D + d;
-                x = p.q_dtype == PT_BF16 ? bf16_bits_to_f32(static_cast<const uint16_t *>(p.q)[e])
-                                         : static_cast<const float *>(p.q)[e];
-            }
-            sq[i] = x;
-        }
         if (threadIdx.x < 8) sln[threadIdx.x] = p.lamnorm[u * 8 + threadIdx.x];
     }
     __syncthreads();
     // Exact keys (the reference's f32 score, K2's exact order: sequential d, fl(q * m) then
-    // fl(acc + .), + fl(fl(lam ||q||) * std), strict-> max over heads) of every page whose
-    // interval [klo, khi] is not one key and reaches L; the largest key written, block-wide.
-    auto resolve = [&](int L) -> int {
-        int mxr = -1;
-        const int nvec = (P + 7) >> 3;
-        const uint32_t Lc = (uint32_t)(L < 0 ? 0 : L);
-        const float *m32 = p.rows32 + u * (int64_t)p.Pmax * D;
-        constexpr int RS = D + 4;  // staged row stride (floats): conflict-free float4 reads
-        uint64_t *rbar = reinterpret_cast<uint64_t *>(rstage + (size_t)p.rcap * RS);
+    // fl(acc + .), + fl(fl(lam ||q||) * std), strict-> max over heads) of listed pages: rows of
+    // the mirror's row-major f32 means by one bulk copy each (one mbarrier phase per round).
+    constexpr int RS = D + 4;  // staged row stride (floats): conflict-free float4 reads
+    uint64_t *rbar = reinterpret_cast<uint64_t *>(rstage + (size_t)p.rcap * RS);
+    int rphase = 0;
+    if constexpr (BND) {
         if (threadIdx.x == 0) {
             mbar_init(rbar, 1);
             fence_mbar_init();
         }
-        int rounds = 0;
+    }
+    const float *m32 = p.rows32 + u * (int64_t)p.Pmax * D;
+    // one round over rlist[0 .. nr) (nr <= rcap): page_of(entry) -> logical page,
+    // store(entry, key) writes the exact key; returns the largest key (this thread's)
+    auto resolve_batch = [&](int nr, auto page_of, auto store) -> int {
+        int mxr = -1;
+        if (threadIdx.x == 0 && nr) mbar_arrive_expect_tx(rbar, (uint32_t)(nr * D * 4));
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads
+        __syncthreads();
+        for (int i = threadIdx.x; i < nr; i += NT) {
+            const int pg = page_of(rlist[i]);
+            bulk_g2s(rstage + i * RS, m32 + (int64_t)pg * D, D * 4, rbar);
+            sa_cp_async4(rstd + i, p.stds + u * (int64_t)p.Pmax + pg);
+        }
+        sa_cp_async_wait_all();
+        if (nr) mbar_wait(rbar, (uint32_t)(rphase & 1));
+        rphase += nr ? 1 : 0;
+        __syncthreads();
+        if (prof) g_sa_prof[cta * kSAProfN + 12] = gtimer();
+        for (int i = threadIdx.x; i < nr; i += NT) {
+            const float best = G <= 4 ? sa_exact_score<D, 4>(rstage + i * RS, sq, sln, rstd[i], G)
+                                      : sa_exact_score<D, 8>(rstage + i * RS, sq, sln, rstd[i], G);
+            const uint16_t key = encode_ordered(f32_to_bf16_rne(best));
+            store(rlist[i], key);
+            mxr = max(mxr, (int)key);
+        }
+        __syncthreads();
+        if (prof) g_sa_prof[cta * kSAProfN + 13] = gtimer();
+        return mxr;
+    };
+    // warp-aggregated append of the flagged entries (bit e of f: entry base_e + e) to rlist
+    auto list_append = [&](uint32_t f, int first) {
+        const int lane_ = threadIdx.x & 31;
+        const int c = __popc(f);
+        int inc = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane_ >= o) inc += y;
+        }
+        const int tot = __shfl_sync(0xffffffffu, inc, 31);
+        int base = 0;
+        if (lane_ == 31 && tot) base = atomicAdd(rcnt, tot);
+        base = __shfl_sync(0xffffffffu, base, 31) + inc - c;
+        while (f) {
+            const int e = __ffs(f) - 1;
+            f &= f - 1;
+            if (base < p.rcap) rlist[base] = first + e;
+            base++;
+        }
+    };
+    auto block_max_int = [&](int v) -> int {
+        v = __reduce_max_sync(0xffffffffu, v);
+        if ((threadIdx.x & 31) == 0) csh.red[1][threadIdx.x >> 5][1] = (uint32_t)v;
+        __syncthreads();
+        int t = -1;
+#pragma unroll
+        for (int w = 0; w < NT / 32; w++) t = max(t, (int)csh.red[1][w][1]);
+        __syncthreads();
+        return t;
+    };
+    // (a) the key array: every page whose interval is not one key and reaches L (L < 0: all);
+    // returns the largest key written, block-wide
+    auto resolve = [&](int L) -> int {
+        int mxr = -1;
+        const int nvec = (P + 7) >> 3;
+        const uint32_t Lc = (uint32_t)(L < 0 ? 0 : L);
         if (prof) g_sa_prof[cta * kSAProfN + 10] = gtimer();
         for (;;) {
             if (threadIdx.x == 0) *rcnt = 0;
             __syncthreads();
-            if (prof && rounds == 0) g_sa_prof[cta * kSAProfN + 16] = gtimer();
-            // warp-aggregated compaction (one shared atomic per warp and round of vectors)
-            const int lane_ = threadIdx.x & 31;
-            const uint32_t lt = (1u << lane_) - 1u;
             for (int v0 = 0; v0 < nvec; v0 += NT) {
                 const int v = v0 + threadIdx.x;
                 uint32_t f = 0u;  // bit e: key 8 v + e needs resolving
@@ -297,76 +358,51 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
                         if (v * 8 + e < P && hi >= Lc && lo != hi) f |= 1u << e;
                     }
                 }
-                const int c = __popc(f);
-                int inc = c;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int y = __shfl_up_sync(0xffffffffu, inc, o);
-                    if (lane_ >= o) inc += y;
-                }
-                const int tot = __shfl_sync(0xffffffffu, inc, 31);
-                int base = 0;
-                if (lane_ == 31 && tot) base = atomicAdd(rcnt, tot);
-                base = __shfl_sync(0xffffffffu, base, 31) + inc - c;
-                (void)lt;
-                while (f) {
-                    const int e = __ffs(f) - 1;
-                    f &= f - 1;
-                    if (base < p.rcap) rlist[base] = v * 8 + e;
-                    base++;
-                }
+                list_append(f, v * 8);
             }
-            if (prof && rounds == 0) g_sa_prof[cta * kSAProfN + 17] = gtimer();
             __syncthreads();
-            if (prof && rounds == 0) g_sa_prof[cta * kSAProfN + 18] = gtimer();
             if (prof) g_sa_prof[cta * kSAProfN + 11] = gtimer();
             const int n = *rcnt;
-            const int nr = n < p.rcap ? n : p.rcap;
-            // one round: every listed page's f32 mean row by one bulk copy (all on one
-            // mbarrier), its std by a 4-byte async copy
-            if (threadIdx.x == 0 && nr) mbar_arrive_expect_tx(rbar, (uint32_t)(nr * D * 4));
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads
-            __syncthreads();
-            for (int i = threadIdx.x; i < nr; i += NT) {
-                bulk_g2s(rstage + i * RS, m32 + (int64_t)rlist[i] * D, D * 4, rbar);
-                sa_cp_async4(rstd + i, p.stds + u * (int64_t)p.Pmax + rlist[i]);
-            }
-            sa_cp_async_wait_all();
-            if (nr) mbar_wait(rbar, (uint32_t)(rounds & 1));
-            __syncthreads();
-            if (prof) g_sa_prof[cta * kSAProfN + 12] = gtimer();
-            if (prof && rounds == 0) g_sa_prof[cta * kSAProfN + 19] = gtimer();
-            for (int i = threadIdx.x; i < nr; i += NT) {
-                const int pg = rlist[i];
-                const float best = G <= 4 ? sa_exact_score<D, 4>(rstage + i * RS, sq, sln, rstd[i], G)
-                                          : sa_exact_score<D, 8>(rstage + i * RS, sq, sln, rstd[i], G);
-                const uint16_t key = encode_ordered(f32_to_bf16_rne(best));
-                skeys[pg] = key;
-                skhi[pg] = key;
-                mxr = max(mxr, (int)key);
-            }
-            __syncthreads();
-            if (prof && rounds == 0) g_sa_prof[cta * kSAProfN + 15] = gtimer();
-            rounds++;
-            if (prof) g_sa_prof[cta * kSAProfN + 13] = gtimer();
+            mxr = max(mxr, resolve_batch(n < p.rcap ? n : p.rcap, [](int e) { return e; },
+                                         [&](int e, uint16_t key) { skeys[e] = key; skhi[e] = key; }));
             if (n <= p.rcap) break;
         }
-
-        mxr = __reduce_max_sync(0xffffffffu, mxr);
-        if ((threadIdx.x & 31) == 0) csh.red[1][threadIdx.x >> 5][1] = (uint32_t)mxr;
-        __syncthreads();
-        int t = -1;
-#pragma unroll
-        for (int w = 0; w < NT / 32; w++) t = max(t, (int)csh.red[1][w][1]);
-        __syncthreads();
-        return t;
+        return block_max_int(mxr);
+    };
+    // (b) the candidate list of select_cand: candidates with an uncertain key whose interval
+    // meets the threshold bracket [A, B]; exact keys go into the list entries
+    auto resolve_cands = [&](int C, int A, int B) {
+        if (prof) g_sa_prof[cta * kSAProfN + 10] = gtimer();
+        for (;;) {
+            if (threadIdx.x == 0) *rcnt = 0;
+            __syncthreads();
+            for (int i0 = 0; i0 < C; i0 += NT) {
+                const int i = i0 + threadIdx.x;
+                uint32_t f = 0u;
+                if (i < C) {
+                    const int lo = (int)(csh.cand[i] >> 16), hi = candhi[i];
+                    if (lo != hi && hi >= A && lo <= B) f = 1u;
+                }
+                list_append(f, i);
+            }
+            __syncthreads();
+            if (prof) g_sa_prof[cta * kSAProfN + 11] = gtimer();
+            const int n = *rcnt;
+            resolve_batch(n < p.rcap ? n : p.rcap, [&](int i) { return (int)(csh.cand[i] & 0xFFFFu); },
+                          [&](int i, uint16_t key) {
+                              csh.cand[i] = ((uint32_t)key << 16) | (csh.cand[i] & 0xFFFFu);
+                              candhi[i] = key;
+                          });
+            if (n <= p.rcap) break;
+        }
     };
     bool selected;
     if (prof) g_sa_prof[cta * kSAProfN + 14] = gtimer();
     if constexpr (BND) {
         selected = select_cand<NT>(skeys, tm_stage ? stm : nullptr, P, k, p.page_table + u * p.Pmax, o_sel,
                                    o_log, o_n, o_kth, o_kp1, csh, ids, true,
-                                   prof ? &g_sa_prof[cta * kSAProfN + 6] : nullptr, true, k + 1, resolve);
+                                   prof ? &g_sa_prof[cta * kSAProfN + 6] : nullptr, true, k + 1, resolve,
+                                   skhi, candhi, resolve_cands);
         // take-all (P <= k) and P > 65536 return before resolving: resolve every page
         if (!selected && (P <= k || P > 65536)) resolve(-1);
     } else {
@@ -378,6 +414,8 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
         select_block<NT>(skeys, bins, P, k, p.page_table + u * p.Pmax, o_sel, o_log, o_n,
                                  o_kth, o_kp1, sh, ids, true);
     if constexpr (BND) {  // query fragments from the widened rows (bf16 values: exact)
+        // the resolve mbarrier's memory becomes part of the stage rings
+        if (threadIdx.x == 0) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(rbar)) : "memory");
         const int gq = lane >> 2;
 #pragma unroll
         for (int ks = 0; ks < KS; ks++) {

@@ -376,8 +376,11 @@ struct SelectCandShared {
 struct NoResolve {
     __device__ int operator()(int) const { return -1; }
 };
+struct NoResolveCands {
+    __device__ void operator()(int, int, int) const {}
+};
 
-template <int NT, class Resolve = NoResolve>
+template <int NT, class Resolve = NoResolve, class ResolveCands = NoResolveCands>
 __device__ bool select_cand(const uint16_t *__restrict__ skeys, const uint16_t *__restrict__ tmax_g,
                             int P, int k, const int32_t *__restrict__ map,
                             int32_t *__restrict__ out, int32_t *__restrict__ out_l,
@@ -385,7 +388,9 @@ __device__ bool select_cand(const uint16_t *__restrict__ skeys, const uint16_t *
                             int32_t *__restrict__ kplus1, SelectCandShared<NT> &sh, int *slist,
                             bool slist_physical, unsigned long long *tp = nullptr,
                             bool tmax_shared = false, int kL = 0,
-                            const Resolve &resolve = Resolve()) {
+                            const Resolve &resolve = Resolve(), const uint16_t *shi = nullptr,
+                            uint16_t *candhi = nullptr,
+                            const ResolveCands &resolve_cands = ResolveCands()) {
     constexpr int NWP = NT / 32;
     constexpr int MAXT = 8;  // tile maxima per thread: ceil(P / 32) <= NT * MAXT
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -501,7 +506,9 @@ __device__ bool select_cand(const uint16_t *__restrict__ skeys, const uint16_t *
         }
         __syncthreads();
         if (tid < 64) sh.bins[tid] = 0;
-        mx = max(mx, resolve(L));  // L < 0: every uncertain key
+        // bounded mode: the candidates are resolved after the candidate pass (only those
+        // meeting the threshold bracket); without tile-maximum bound every uncertain key now
+        if (!shi || L < 0) mx = max(mx, resolve(L));
     } else {
         resolve(-1);
         int m = -1, n = 0xFFFF;
@@ -531,25 +538,28 @@ __device__ bool select_cand(const uint16_t *__restrict__ skeys, const uint16_t *
         int run = 0, below = -1, par = 0;
         for (int v0 = 0; v0 < nvec; v0 += NT * VPT, par ^= 1) {
             const int vt = v0 + tid * VPT;
-            uint4 x[VPT];
+            uint4 x[VPT], y[VPT];
             int cv[VPT];
             int c = 0;
 #pragma unroll
             for (int j = 0; j < VPT; j++) {
                 const int v = vt + j;
                 x[j] = make_uint4(0u, 0u, 0u, 0u);
+                y[j] = x[j];
                 cv[j] = 0;
                 if (v < nvec) {
                     x[j] = s4[v];
-                    uint32_t w[4], mk[4];
+                    y[j] = shi ? reinterpret_cast<const uint4 *>(shi)[v] : x[j];
+                    uint32_t w[4], wh[4], mk[4];
                     words(x[j], w);
+                    words(y[j], wh);
                     vmask(v, mk);
                     uint32_t bl = 0u;
                     bool any_below = false;
                     int cc = 0;
 #pragma unroll
                     for (int q = 0; q < 4; q++) {
-                        const uint32_t ge = __vcmpgeu2(w[q], L16);
+                        const uint32_t ge = __vcmpgeu2(wh[q], L16);  // bounded: the upper key
                         cc += __popc(ge & mk[q]);
                         const uint32_t lt = ~ge & mk[q];
                         any_below |= lt != 0u;
@@ -580,13 +590,18 @@ __device__ bool select_cand(const uint16_t *__restrict__ skeys, const uint16_t *
                 for (int j = 0; j < VPT; j++) {
                     if (!cv[j]) continue;
                     const int v = vt + j;
-                    uint32_t w[4];
+                    uint32_t w[4], wh[4];
                     words(x[j], w);
+                    words(y[j], wh);
 #pragma unroll
                     for (int e = 0; e < 8; e++) {
                         const int key = (e & 1) ? (int)(w[e >> 1] >> 16) : (int)(w[e >> 1] & 0xFFFFu);
-                        if (v * 8 + e < P && key >= L) {
-                            if (pos < kCandMax) sh.cand[pos] = ((uint32_t)key << 16) | (uint32_t)(v * 8 + e);
+                        const int kh = (e & 1) ? (int)(wh[e >> 1] >> 16) : (int)(wh[e >> 1] & 0xFFFFu);
+                        if (v * 8 + e < P && kh >= L) {
+                            if (pos < kCandMax) {
+                                sh.cand[pos] = ((uint32_t)key << 16) | (uint32_t)(v * 8 + e);
+                                if (candhi) candhi[pos] = (uint16_t)kh;
+                            }
                             pos++;
                         }
                     }
@@ -598,11 +613,73 @@ __device__ bool select_cand(const uint16_t *__restrict__ skeys, const uint16_t *
         __syncthreads();
         if (run <= kCandMax) C = run;  // else: too many keys tie at L -- bisection below
     }
+    if (shi && L >= 0) {
+        stamp(10);
+        if (C >= 0) {
+            // bounded mode, threshold bracket over the candidates: A = the (k+1)-th largest
+            // lower key <= the exact (k+1)-th key, B = the k-th largest upper key >= the exact
+            // threshold.  Only uncertain candidates whose interval meets [A, B] need their exact
+            // key: the others are certainly above the threshold (lower key > B) or certainly
+            // below the (k+1)-th key (upper key < A), so their counts, ties and kplus1 are
+            // decided either way.
+            int mh = -1;
+            for (int i = tid; i < C; i += NT) mh = max(mh, (int)candhi[i]);
+            const int mxh = block_max(mh);
+            stamp(11);
+            int A = L, B = mxh;
+            if (mxh - L < 64) {
+                auto kth_bin = [&](bool hi, int rank) -> int {
+                    if (tid < 64) sh.bins[tid] = 0;
+                    __syncthreads();
+                    for (int i = tid; i < C; i += NT) {
+                        const int key = hi ? (int)candhi[i] : (int)(sh.cand[i] >> 16);
+                        if (key >= L) atomicAdd(&sh.bins[mxh - key], 1);
+                    }
+                    __syncthreads();
+                    int b = 63;
+                    if (warp == 0) {
+                        const int c0 = sh.bins[2 * lane], c1 = sh.bins[2 * lane + 1];
+                        int incl = c0 + c1;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const int y2 = __shfl_up_sync(0xffffffffu, incl, o);
+                            if (lane >= o) incl += y2;
+                        }
+                        const int pre = incl - c0 - c1;
+                        int bb = 999;
+                        if (pre < rank && pre + c0 >= rank) bb = 2 * lane;
+                        else if (pre + c0 < rank && incl >= rank) bb = 2 * lane + 1;
+                        bb = __reduce_min_sync(0xffffffffu, bb);
+                        if (lane == 0) sh.thr = bb < 999 ? bb : 63;
+                    }
+                    __syncthreads();
+                    b = sh.thr;
+                    __syncthreads();
+                    return mxh - b;
+                };
+                B = kth_bin(true, k);
+                stamp(12);
+                A = kth_bin(false, k + 1);
+                stamp(13);
+                if (tid < 64) sh.bins[tid] = 0;
+            }
+            resolve_cands(C, A, B);
+            int m2 = -1;
+            for (int i = tid; i < C; i += NT) m2 = max(m2, (int)(sh.cand[i] >> 16));
+            mx = max(mx, block_max(m2));
+        } else {
+            mx = max(mx, resolve(L));  // candidate overflow: resolve the key array
+        }
+    }
     stamp(1);
     if (C >= 0) {
         // ---- thr = the k-th largest candidate ----
         if (mx - L < 64) {
-            for (int i = tid; i < C; i += NT) atomicAdd(&sh.bins[mx - (int)(sh.cand[i] >> 16)], 1);
+            // (bounded mode: candidates whose key ended below L are below the threshold)
+            for (int i = tid; i < C; i += NT) {
+                const int key = (int)(sh.cand[i] >> 16);
+                if (key >= L) atomicAdd(&sh.bins[mx - key], 1);
+            }
             __syncthreads();
             if (warp == 0) {
                 const int c0 = sh.bins[2 * lane], c1 = sh.bins[2 * lane + 1];

@@ -65,6 +65,14 @@ def main():
         stats["resolve_per_unit_max"] = int((unsure & reach).sum(1).max())
         stats["exact_ge_L_per_unit"] = float((klo[:, :P] >= L[:, None]).sum(1).mean())
         stats["width_keys_mean"] = float((khi[:, :P] - klo[:, :P]).mean())
+        # bracket: A = (k+1)-th largest lower key <= exact (k+1)-th key, B = k-th largest upper
+        # key >= the threshold; only intervals meeting [A, B] matter
+        A = -np.sort(-klo[:, :P], axis=1)[:, k]
+        Bq = -np.sort(-khi[:, :P], axis=1)[:, k - 1]
+        br = unsure & (khi[:, :P] >= A[:, None]) & (klo[:, :P] <= Bq[:, None])
+        stats["bracket_per_unit_mean"] = float(br.sum(1).mean())
+        stats["bracket_per_unit_max"] = int(br.sum(1).max())
+        stats["bracket_width_keys_mean"] = float((Bq - A).mean())
     for _ in range(3):
         eng.select_attend(q)
     torch.cuda.synchronize()
@@ -78,11 +86,11 @@ def main():
     _lib.check(_lib.load().pt_debug_sa_prof(buf.ctypes.data, n))
     raw = buf.reshape(U * nch, 20)
     t = raw[:, :15].astype(np.float64)
-    t[:, 15 - 1] = raw[:, 14]
     # stamps 10..13: resolve start / scan done / rows staged / resolved; 14: khi+q staged;
     # 15: rounds * 1e6 + pages listed in the last round
     info = raw[:, 15]
     t0 = t[:, 0].min()
+    T = lambda i: (raw[:, i].astype(np.float64) - t0) / 1000.0  # noqa: E731
     rel = (t - t0) / 1000.0
     names = ["entry", "keys_staged", "selected", "first_page", "stream_done", "exit",
              "sel_loads_max", "sel_L", "sel_cands", "sel_thr", "res_start", "res_scan", "res_staged",
@@ -111,11 +119,11 @@ def main():
             "res_compute": float(np.median(rel[:, 13] - rel[:, 12])),
             "res_total": float(np.median(rel[:, 13] - rel[:, 10])),
             "L_before_resolve": float(np.median(rel[:, 10] - rel[:, 14])),
-            "r1_first_barrier": float(np.median((raw[:, 16].astype(np.float64) - t0) / 1000.0 - rel[:, 10])),
-            "r1_scan_loop_t0": float(np.median((raw[:, 17].astype(np.float64) - raw[:, 16].astype(np.float64)) / 1000.0)),
-            "r1_trailing_barrier": float(np.median((raw[:, 18].astype(np.float64) - raw[:, 17].astype(np.float64)) / 1000.0)),
-            "r1_stage": float(np.median((raw[:, 19].astype(np.float64) - raw[:, 18].astype(np.float64)) / 1000.0)),
-            "r1_compute": float(np.median((raw[:, 15].astype(np.float64) - raw[:, 19].astype(np.float64)) / 1000.0)),
+            "b_cand_pass": float(np.median(T(16) - rel[:, 6])),
+            "b_mxh": float(np.median(T(17) - T(16))),
+            "b_histB": float(np.median(T(18) - T(17))),
+            "b_histA": float(np.median(T(19) - T(18))),
+            "b_to_resolve": float(np.median(rel[:, 10] - T(19))),
         })
 
     print(json.dumps(out, indent=1))
