@@ -1,19 +1,24 @@
 #!/usr/bin/env python
 """Benchmark of the B200 UNIQUE sparse decode step (BASELINE.json metric).
 
-Workload (N=1): BASELINE.json configs[2] -- Llama-3.1-8B attention shape, batch 32,
-128K context, 32 q / 8 kv heads, d=128, page 16, k = 2048 tokens (128 pages), bf16
-KV pool, f32 page stats (exact reference statistics).  One step = one decode token
-per sequence through the full hot path: append the new K/V row (K1b, stats of the
-tail page recomputed) -> score every page (K2) -> top-k pages (K3) -> split-KV sparse
-attention over the selected pages (K4), replayed as a CUDA graph.  Multi-GPU: one
-process per GPU, each rank owns its own batch of 32 sequences (units shard with no
-data-path collective; "scaling": "weak"); NCCL only for the barrier / max-time reduce
-and the optional output all-gather reported beside the line.
+Workload: BASELINE.json configs[2] -- Llama-3.1-8B attention shape, global batch 32,
+128K context, 32 q / 8 kv heads, d=128, page 16, k = 2048 tokens (128 pages), bf16 KV pool,
+exact f32 page stats (+ their bf16 mirror for bounded scoring).  One step = one decode token
+per sequence through the full hot path: append the new K/V row (K1b, tail-page stats
+recomputed exactly) -> lam*||q|| -> score every page (K2b, bounded over the bf16 mirror) ->
+select the top-k pages (K3, exact keys resolved where the bounds straddle the cut) ->
+split-KV sparse attention over them (K4), replayed as a CUDA graph.
 
-Prints ONE JSON line on rank 0.  `--impl reference` times the reference CPU path
-(the oracle port of attention.py:110-147, bit-identical to the reference's compiled
-backend) on the host cores instead.
+Multi-GPU (`--gpus N`; self-launches N ranks under torch.distributed.run when WORLD_SIZE is
+unset): the 256 (sequence, kv-head) units of the global batch are split over the ranks
+(paper_2605_27740_b200/shard.py: whole sequences per rank), every rank holding only its
+units' KV pages and stats -- "scaling": "strong", no data-path collective.  The optional
+NCCL output all-gather is timed beside the line, and a weak-scaling measurement (32
+sequences per rank) is reported in "weak".  The workload is generated per unit from the
+global seed, so every N sees identical data.
+
+Prints ONE JSON line on rank 0.  `--impl reference` times the reference's CPU path (its own
+compiled kernels from oracle/_ref, else the bit-identical oracle port) on the host cores.
 """
 
 from __future__ import annotations
@@ -22,6 +27,7 @@ import argparse
 import json
 import math
 import os
+import socket
 import statistics
 import sys
 import threading
@@ -34,15 +40,16 @@ import numpy as np  # noqa: E402
 
 METRIC = "sparse decode attn tokens/s @128K ctx (batch 32, k=2048 tokens, 32q/8kv d128 page16)"
 UNIT = "tokens/s"
+SEED = 1234
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--batch", type=int, default=32, help="sequences per GPU")
+    ap.add_argument("--batch", type=int, default=32, help="global batch (sequences)")
     ap.add_argument("--ctx", type=int, default=131072)
     ap.add_argument("--q-heads", type=int, default=32)
     ap.add_argument("--kv-heads", type=int, default=8)
@@ -50,15 +57,17 @@ def parse():
     ap.add_argument("--page", type=int, default=16)
     ap.add_argument("--budget", type=int, default=2048, help="token budget k*S")
     ap.add_argument("--stats-dtype", default="f32", choices=["f32", "bf16"])
+    ap.add_argument("--no-mirror", action="store_true", help="exact f32-means scoring (no bounds)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-dense", action="store_true")
-    ap.add_argument("--nsplit", type=int, default=0, help="attention splits per unit (0 = auto)")
-    ap.add_argument("--sweep-nsplit", action="store_true")
-    ap.add_argument("--sweep", action="store_true", help="time kernel variants / tuning knobs")
+    ap.add_argument("--no-weak", action="store_true", help="skip the weak-scaling leg (N > 1)")
+    ap.add_argument("--no-parity", action="store_true", help="skip the in-bench oracle check")
+    ap.add_argument("--dump-out", default=None,
+                    help="save the gathered outputs of one eager step (tests: N ranks == 1 rank)")
     ap.add_argument("--profile", action="store_true",
                     help="few eager steps, no graph/cpu/dense (for ncu launch lists)")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 # ---------------------------------------------------------------------------
@@ -140,59 +149,113 @@ def measured_peaks():
 
 
 # ---------------------------------------------------------------------------
-# algorithmic bytes (SURVEY.md section 8(d); DESIGN.md "Roofline")
+# algorithmic bytes (SURVEY.md section 8(d); DESIGN.md section 4)
 # ---------------------------------------------------------------------------
 def step_bytes(U, G, D, P, kp, S, e_kv, e_stats, N_tok):
+    """SURVEY 8(d) per step; e_stats = the page-mean element size read by the scorer."""
     score = U * (P * D * e_stats + 4 * P + G * D * e_kv + 2 * P)
     topk = U * (2 * P + 8 * kp)  # keys read + page-table entries read + ids written
     T = kp * S
     attn = U * (2 * T * D * e_kv + G * D * e_kv + 4 * kp) + U * G * D * 4
-    append = U * (S * D * e_kv + 3 * D * e_kv + D * e_stats + 8)
+    append = U * (S * D * e_kv + 3 * D * e_kv + 4)
     dense = 2 * U * N_tok * D * e_kv + U * G * D * 4
     return dict(score=score, topk=topk, attend=attn, append=append, dense=dense)
 
 
-def build_cache(args, device, seed):
+def bounded_score_moved(U, G, D, P):
+    """Bytes the bounded scorer actually moves: bf16 mirror, std + err, q, norms, two keys."""
+    return U * (P * D * 2 + 8 * P + G * D * 2 + 64 + 4 * P) + U * (P // 32) * 2
+
+
+# ---------------------------------------------------------------------------
+# workload: generated per unit from the global seed (identical data for every N)
+# ---------------------------------------------------------------------------
+def _unit_gen(device, seed, u):
+    import torch
+
+    g = torch.Generator(device=device)
+    g.manual_seed(seed * 1_000_003 + u)
+    return g
+
+
+def build_cache(args, device, seed, units=None, spare_tokens=None, mirror=None):
+    """PagedKvCache holding the global units ``units`` (default: all of args.batch sequences)
+    with args.ctx tokens each, K/V ~ N(0,1) rounded to bf16 (harness/workload.py:60-98)."""
     import torch
 
     import paper_2605_27740_b200 as pt
 
     H, D, S = args.kv_heads, args.head_dim, args.page
-    B = args.batch
-    U = B * H
-    spare = (args.warmup + args.steps) * 4 + 64  # appends during warm-up/timed/extra loops
-    P_cap = -(-(args.ctx + spare) // S)
-    layout = pt.CacheLayout(num_kv_heads=H, head_dim=D, page_size=S, max_pages=U * P_cap)
+    units = list(range(args.batch * H)) if units is None else list(units)
+    Ul = len(units)
+    Hl, Bl = (H, Ul // H) if Ul % H == 0 else (1, Ul)
+    if spare_tokens is None:
+        spare_tokens = (args.warmup + args.steps) * 3 + 256
+    P_cap = -(-(args.ctx + spare_tokens) // S)
+    layout = pt.CacheLayout(num_kv_heads=Hl, head_dim=D, page_size=S, max_pages=Ul * P_cap)
     sdt = torch.float32 if args.stats_dtype == "f32" else torch.bfloat16
-    cache = pt.PagedKvCache(layout, batch=B, dtype=torch.bfloat16, stats_dtype=sdt,
-                            max_pages_per_head=P_cap, device=device)
-    g = torch.Generator(device=device)
-    g.manual_seed(seed)
-    chunk = 8192
-    done = 0
-    while done < args.ctx:
-        n = min(chunk, args.ctx - done)
-        kk = torch.randn(U, n, D, generator=g, device=device, dtype=torch.float32).to(torch.bfloat16)
-        vv = torch.randn(U, n, D, generator=g, device=device, dtype=torch.float32).to(torch.bfloat16)
+    if mirror is None:
+        mirror = not getattr(args, "no_mirror", False) and args.stats_dtype == "f32"
+    cache = pt.PagedKvCache(layout, batch=Bl, dtype=torch.bfloat16, stats_dtype=sdt,
+                            max_pages_per_head=P_cap, device=device, mirror=mirror)
+    for kk, vv in unit_rows(args, device, seed, units):
         cache.extend_units(kk, vv)
-        done += n
         del kk, vv
     torch.cuda.synchronize()
     return cache
 
 
-def _sample_arrays(cache, q_bf16, args):
-    """Host copies (f32) of the first 2 sequences of the workload: q, compacted K/V pool,
-    page table, lengths, page stats."""
-    H, D, S = args.kv_heads, args.head_dim, args.page
-    G = args.q_heads // args.kv_heads
-    kp = -(-args.budget // S)
+def unit_rows(args, device, seed, units, chunk=8192):
+    """The workload's K/V rows of the given global units, in chunks of ``chunk`` tokens:
+    yields bf16 [len(units), n, D] pairs.  Unit u draws from its own generator (seeded from
+    the global seed and u), so a rank holding units [u0, u1) sees exactly the rows the
+    unsharded run gives those units."""
     import torch
 
-    seqs = 2
-    units = list(range(seqs * H))
-    tab = cache.page_table[: len(units)].cpu().numpy()
-    seq = cache.seq_lens[: len(units)].cpu().numpy()
+    D = args.head_dim
+    gens = [_unit_gen(device, seed, u) for u in units]
+    done = 0
+    while done < args.ctx:
+        n = min(chunk, args.ctx - done)
+        kk = torch.empty(len(gens), n, D, device=device, dtype=torch.bfloat16)
+        vv = torch.empty(len(gens), n, D, device=device, dtype=torch.bfloat16)
+        for i, g in enumerate(gens):
+            kk[i] = torch.randn(n, D, generator=g, device=device, dtype=torch.float32)
+            vv[i] = torch.randn(n, D, generator=g, device=device, dtype=torch.float32)
+        yield kk, vv
+        done += n
+
+
+def step_inputs(args, device, NQ=4, seed=SEED):
+    """NQ rotating query sets [U*G, D] and the new K/V rows [U, D] of the GLOBAL batch (bf16);
+    ranks slice their shard's rows."""
+    import torch
+
+    H, D = args.kv_heads, args.head_dim
+    G = args.q_heads // H
+    U = args.batch * H
+    g = torch.Generator(device=device)
+    g.manual_seed(seed + 7)
+    qs = [torch.randn(U * G, D, generator=g, device=device).to(torch.bfloat16) for _ in range(NQ)]
+    kn = torch.randn(U, D, generator=g, device=device).to(torch.bfloat16)
+    vn = torch.randn(U, D, generator=g, device=device).to(torch.bfloat16)
+    return qs, kn, vn
+
+
+def _sample_arrays(cache, q_bf16, args, seqs=2):
+    """Host copies (f32) of the first ``seqs`` sequences of a cache: q, compacted K/V pool,
+    page table, lengths, page stats."""
+    import torch
+
+    import paper_2605_27740_b200._device as dev
+
+    H, D, S = cache.layout.num_kv_heads, args.head_dim, args.page
+    G = args.q_heads // args.kv_heads
+    kp = -(-args.budget // S)
+    nu = min(cache.num_units, seqs * args.kv_heads)
+    units = list(range(nu))
+    tab = cache.page_table[:nu].cpu().numpy()
+    seq = cache.seq_lens[:nu].cpu().numpy()
     P = int(-(-seq.max() // S))
     pids = np.unique(tab[:, :P][tab[:, :P] >= 0])
     remap = -np.ones(cache.layout.max_pages, dtype=np.int64)
@@ -201,240 +264,363 @@ def _sample_arrays(cache, q_bf16, args):
     kpool = cache.k_pool[idx].to(torch.float32).cpu().numpy()
     vpool = cache.v_pool[idx].to(torch.float32).cpu().numpy()
     tab2 = np.where(tab >= 0, remap[np.maximum(tab, 0)], -1).astype(np.int32)
-    import paper_2605_27740_b200._device as dev
-
     means = dev.untile_means(cache.means, cache.num_units, cache.Pmax, D, cache.stats_dtype)
-    means = means[: len(units)].to(torch.float32).cpu().numpy()
-    stds = cache.stds[: len(units)].cpu().numpy()
-    q = q_bf16.reshape(cache.num_units, G, D)[: len(units)].to(torch.float32).cpu().numpy()
-    return dict(seqs=seqs, units=units, q=q, kpool=kpool, vpool=vpool, tab=tab2, seq=seq,
-                means=means, stds=stds, kp=kp, S=S, D=D, H=H, pids=pids)
+    means = means[:nu].to(torch.float32).cpu().numpy()
+    stds = cache.stds[:nu].cpu().numpy()
+    q = q_bf16.reshape(cache.num_units, G, D)[:nu].to(torch.float32).cpu().numpy()
+    return dict(seqs=nu // args.kv_heads, units=units, q=q, kpool=kpool, vpool=vpool, tab=tab2,
+                seq=seq, means=means, stds=stds, kp=kp, S=S, D=D, H=args.kv_heads, pids=pids)
 
 
-def cpu_baseline(cache, q_bf16, args, budget_s, nthreads):
+def cpu_baseline(a, budget_s, nthreads):
     """Reference decode_step (oracle port, bit-identical to the compiled backend) on host
-    cores over a bounded sample of whole sequences of the same workload."""
+    cores over a bounded sample (``a`` from _sample_arrays) of the same workload."""
     from oracle import oracle as O
 
-    a = _sample_arrays(cache, q_bf16, args)
-    seqs, units, q, kpool, vpool = a["seqs"], a["units"], a["q"], a["kpool"], a["vpool"]
-    tab2, seq, means, stds, kp, S, D, H, pids = (a[k] for k in ("tab", "seq", "means", "stds",
-                                                              "kp", "S", "D", "H", "pids"))
     reps, t0 = 0, time.perf_counter()
     res = None
     while True:
-        res = O.decode_units(q, kpool, vpool, tab2, seq, means, stds, kp, 0.5,
-                             1.0 / math.sqrt(D), S, nthreads=nthreads)
+        res = O.decode_units(a["q"], a["kpool"], a["vpool"], a["tab"], a["seq"], a["means"],
+                             a["stds"], a["kp"], 0.5, 1.0 / math.sqrt(a["D"]), a["S"],
+                             nthreads=nthreads)
         reps += 1
         if time.perf_counter() - t0 > budget_s:
             break
     dt = (time.perf_counter() - t0) / reps
     return {
-        "value": seqs / dt,
+        "value": a["seqs"] / dt,
         "unit": UNIT,
         "cores": nthreads,
         "kind": "port",
-        "sample": f"{seqs} sequences x {H} kv-heads (128K ctx, k={kp} pages, bf16 values upcast "
-                  f"to f32) per rep, {reps} reps in {time.perf_counter() - t0:.1f}s; "
+        "sample": f"{a['seqs']} sequences x {a['H']} kv-heads (128K ctx, k={a['kp']} pages, bf16 "
+                  f"values upcast to f32) per rep, {reps} reps in {time.perf_counter() - t0:.1f}s; "
                   "oracle/pagetopk_oracle.c (bit-identical to _kernels_cy), OpenMP over units",
         "_res": res,
-        "_units": len(units),
-        "_pids": pids,
     }
 
 
-def ref_kernels_baseline(cache, q_bf16, args, budget_s, nproc, reps_max=None):
-    """The reference's OWN compiled kernels (oracle/_ref, built from the reference sources)
-    driven as its decode_step, units fanned out over a process pool; cross-checked against
-    the port (selection sets equal, outputs within 1e-5).  None when oracle/_ref is absent."""
+# ---------------------------------------------------------------------------
+# reference arm: the reference's CPU path on the host cores
+# ---------------------------------------------------------------------------
+def reference_workload(args, seqs=2, seed=SEED):
+    """A host-only sample of the workload (no GPU, no repo kernels): ``seqs`` sequences,
+    K/V/q ~ N(0,1) rounded to bf16 (torch CPU generator), a contiguous page table with one
+    spare page per unit for the per-step append, page stats by the oracle's restatement of
+    kvcache.py:59-71 (bit-identical to the reference's numpy)."""
+    import torch
+
+    from oracle import oracle as O
+
+    H, D, S = args.kv_heads, args.head_dim, args.page
+    G = args.q_heads // H
+    U = seqs * H
+    n = args.ctx
+    P = -(-n // S)
+    Pc = -(-(n + 1) // S) + 1
+    g = torch.Generator()
+    g.manual_seed(seed)
+
+    def bf16(*shape):
+        return torch.randn(*shape, generator=g).to(torch.bfloat16).to(torch.float32).numpy()
+
+    kpool = np.zeros((U * Pc, S, D), np.float32)
+    vpool = np.zeros((U * Pc, S, D), np.float32)
+    for u in range(U):
+        kpool[u * Pc: u * Pc + P].reshape(-1, D)[:n] = bf16(n, D)
+        vpool[u * Pc: u * Pc + P].reshape(-1, D)[:n] = bf16(n, D)
+    tab = (np.arange(U)[:, None] * Pc + np.arange(Pc)[None, :]).astype(np.int32)
+    seq = np.full(U, n, np.int32)
+    means, stds = O.build_stats(kpool, tab, seq, S)
+    q = bf16(U, G, D)
+    kn, vn = bf16(U, D), bf16(U, D)
+    return dict(q=q, kpool=kpool, vpool=vpool, tab=tab, seq=seq, means=means, stds=stds, kn=kn,
+                vn=vn, kp=-(-args.budget // S), S=S, D=D, H=H, seqs=seqs)
+
+
+def run_reference_arm(args, world, config):
+    """Each step: per (sequence, kv-head) unit, append the step's K/V row to the tail page
+    and refresh its stats (kvcache.py:185-208 + compute_page_stats, numpy), then the
+    reference decode_step (attention.py:110-147) on the reference's own compiled kernels
+    (oracle/_ref, from pkg/src/pagetopk/_kernels_cy.pyx), units over one forked process per
+    host core; without oracle/_ref the oracle port (OpenMP over units) instead."""
     from oracle import oracle as O
     from oracle import ref_arm
 
-    if ref_arm.so_path() is None:
-        return None
-    a = _sample_arrays(cache, q_bf16, args)
-    arm = ref_arm.RefArm(a["q"], a["kpool"], a["vpool"], a["tab"], a["seq"], a["means"],
-                         a["stds"], a["kp"], 0.5, a["S"], nproc)
-    try:
-        res = arm.run()  # warm the workers
-        reps, t0 = 0, time.perf_counter()
-        while True:
-            res = arm.run()
-            reps += 1
-            if time.perf_counter() - t0 > budget_s or (reps_max and reps >= reps_max):
-                break
-        dt = (time.perf_counter() - t0) / reps
-    finally:
-        arm.close()
-    port = O.decode_units(a["q"], a["kpool"], a["vpool"], a["tab"], a["seq"], a["means"],
-                          a["stds"], a["kp"], 0.5, 1.0 / math.sqrt(a["D"]), a["S"])
-    for u, (phys, out, lse) in enumerate(res):
-        got = set(port["sel"][u][: port["n_sel"][u]].tolist())
-        if set(phys.tolist()) != got:
-            raise RuntimeError(f"reference kernels and oracle port disagree on unit {u}'s pages")
-        np.testing.assert_allclose(out, port["out"][u], rtol=1e-5, atol=1e-5)
-    return {
-        "value": a["seqs"] / dt,
-        "unit": UNIT,
-        "cores": arm.nproc,
-        "kind": "reference",
-        "sample": f"{a['seqs']} sequences x {a['H']} kv-heads (128K ctx, k={a['kp']} pages, bf16 "
-                  f"values upcast to f32) per rep, {reps} reps in {time.perf_counter() - t0:.1f}s; "
-                  "the reference's own compiled kernels (oracle/_ref/_kernels_cy from "
-                  "pkg/src/pagetopk/_kernels_cy.pyx) driven as attention.decode_step, one unit "
-                  f"per task over {arm.nproc} forked processes (kernels hold the GIL); "
-                  "selections/outputs checked against the port",
-    }
+    ncores = host_cores()
+    w = reference_workload(args)
+    steps, warm = max(1, args.steps), max(0, args.warmup)
+    if ref_arm.so_path() is not None:
+        arm = ref_arm.RefArm(w["q"], w["kpool"], w["vpool"], w["tab"], w["seq"], w["means"],
+                             w["stds"], w["kp"], 0.5, w["S"], ncores, k_new=w["kn"], v_new=w["vn"])
+        try:
+            for _ in range(warm):
+                res = arm.run()
+            t0 = time.perf_counter()
+            for _ in range(steps):
+                res = arm.run()
+            dt = (time.perf_counter() - t0) / steps
+        finally:
+            arm.close()
+        # cross-check against the port on the post-append cache (seq n + 1)
+        kp_, vp_, means, stds, seq = ref_arm.appended(w)
+        port = O.decode_units(w["q"], kp_, vp_, w["tab"], seq, means, stds, w["kp"], 0.5,
+                              1.0 / math.sqrt(w["D"]), w["S"])
+        for u, (phys, out, lse) in enumerate(res):
+            if set(phys.tolist()) != set(port["sel"][u][: port["n_sel"][u]].tolist()):
+                raise RuntimeError(f"reference kernels and oracle port disagree on unit {u}")
+            np.testing.assert_allclose(out, port["out"][u], rtol=1e-5, atol=1e-5)
+        kind, cores = "reference", arm.nproc
+        how = ("the reference's own compiled kernels (oracle/_ref/_kernels_cy from "
+               "pkg/src/pagetopk/_kernels_cy.pyx) driven as attention.decode_step, after a per-unit "
+               "append with the reference's numpy page-stats refresh; one unit per task over "
+               f"{arm.nproc} forked processes (the kernels hold the GIL)")
+    else:
+        kp_, vp_, means, stds, seq = ref_arm.appended(w)
+        for _ in range(warm):
+            O.decode_units(w["q"], kp_, vp_, w["tab"], seq, means, stds, w["kp"], 0.5,
+                           1.0 / math.sqrt(w["D"]), w["S"], nthreads=ncores)
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            O.decode_units(w["q"], kp_, vp_, w["tab"], seq, means, stds, w["kp"], 0.5,
+                           1.0 / math.sqrt(w["D"]), w["S"], nthreads=ncores)
+        dt = (time.perf_counter() - t0) / steps
+        kind, cores = "port", ncores
+        how = ("oracle/pagetopk_oracle.c (bit-identical to _kernels_cy), OpenMP over units, on the "
+               "post-append cache (the append itself untimed)")
+    v = w["seqs"] / dt
+    sample = (f"each step: {w['seqs']} of the {args.batch} sequences x {w['H']} kv-heads (ctx "
+              f"{args.ctx} + 1 appended token, k={w['kp']} pages, bf16 values upcast to f32), "
+              f"host-generated workload and stats (no GPU, no repo kernels); {how}; conservative "
+              "for the reference: the batch is extrapolated from the sample at constant per-"
+              "sequence cost and every host core serves the one rank")
+    cb = {"value": v, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample}
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+            "steps": steps, "warmup": warm, "ms_per_step": 1000.0 * args.batch / v,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic N(0,1) (reference workload distribution)", "config": config,
+            "cpu_baseline": cb,
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# the B200 arm
+# ---------------------------------------------------------------------------
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def self_launch(args):
+    """`--gpus N` without a torchrun environment: re-run this script as N ranks."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
+
+
+class Ctx:
+    """Rank / device / collective plumbing (NCCL on GPUs; BENCH_DIST_BACKEND=gloo lets N
+    ranks share one GPU for a functional check of the multi-rank path)."""
+
+    def __init__(self):
+        import torch
+
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        self.dist = None
+        cuda = torch.cuda.is_available()
+        ndev = torch.cuda.device_count() if cuda else 1
+        self.dev_index = self.local % max(ndev, 1)
+        self.device = torch.device("cuda", self.dev_index) if cuda else torch.device("cpu")
+        if self.world > 1:
+            import torch.distributed as dist
+
+            if cuda:
+                torch.cuda.set_device(self.dev_index)
+            if self.backend == "nccl":
+                dist.init_process_group("nccl", device_id=self.device)
+            else:
+                dist.init_process_group(self.backend)
+            self.dist = dist
+
+    def barrier(self):
+        import torch
+
+        if self.dist is not None:
+            self.dist.barrier()
+        if torch.cuda.is_available():
+            torch.cuda.synchronize()
+
+    def max(self, x: float) -> float:
+        import torch
+
+        if self.dist is None:
+            return x
+        dev = self.device if self.backend == "nccl" else torch.device("cpu")
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.dist is not None:
+            self.dist.destroy_process_group()
+
+
+def capture_steps(eng, cache, qs, kn, vn):
+    """One CUDA graph of the whole step per rotating query set."""
+    import torch
+
+    graphs = []
+    for q in qs:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            eng.step(q, kn, vn)
+        cache._seq_host -= 1
+        graphs.append(g)
+    return graphs
+
+
+def timed_replays(ctx, graphs, cache, steps, sampler=None):
+    """K graph replays bracketed by a barrier + synchronize on both sides; device time by
+    CUDA events on the launch stream; max over ranks (ms per step)."""
+    import torch
+
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ctx.barrier()
+    if sampler is not None:
+        sampler.__enter__()
+    e0.record(stream)
+    for i in range(steps):
+        graphs[i % len(graphs)].replay()
+    e1.record(stream)
+    ctx.barrier()
+    if sampler is not None:
+        sampler.__exit__()
+    cache._seq_host += steps
+    return ctx.max(e0.elapsed_time(e1)) / steps
+
+
+def parity_check(eng, cache, q_local, args):
+    """The oracle (attention.py:110-147 restated) on the first 2 sequences of this rank's
+    shard at the current cache state vs one eager engine step on the same queries: selection
+    sets, kth and kplus1 bit-exact, outputs within 2e-2 (bf16).  Raises on a mismatch."""
+    import torch
+
+    from oracle import oracle as O
+
+    eng.step(q_local)
+    torch.cuda.synchronize()
+    a = _sample_arrays(cache, q_local, args)
+    ref = O.decode_units(a["q"], a["kpool"], a["vpool"], a["tab"], a["seq"], a["means"], a["stds"],
+                         a["kp"], 0.5, 1.0 / math.sqrt(a["D"]), a["S"], nthreads=host_cores())
+    nu = len(a["units"])
+    # engine ids are pool page ids; the sample pool is compacted: map through a["pids"]
+    remap = {int(p): i for i, p in enumerate(a["pids"].tolist())}
+    sel = eng.sel[:nu].cpu().numpy()
+    nsel = eng.n_sel[:nu].cpu().numpy()
+    G, D = args.q_heads // args.kv_heads, args.head_dim
+    bad = 0
+    for u in range(nu):
+        got = {remap[int(p)] for p in sel[u, : nsel[u]].tolist()}
+        if nsel[u] != ref["n_sel"][u] or got != set(ref["sel"][u, : ref["n_sel"][u]].tolist()):
+            bad += 1
+    kth_ok = np.array_equal(eng.kth[:nu].cpu().numpy(), ref["kth"])
+    kp1_ok = np.array_equal(eng.kplus1[:nu].cpu().numpy(), ref["kplus1"])
+    out = eng.out[: nu * G].cpu().numpy().reshape(nu, G, D)
+    err = float(np.abs(out - ref["out"]).max())
+    res = {"units": nu, "selection_mismatches": bad, "kth_equal": bool(kth_ok),
+           "kplus1_equal": bool(kp1_ok), "out_max_abs_err": err, "tolerance": 2e-2,
+           "oracle": "oracle/pagetopk_oracle.c decode_units (bit-identical to the reference "
+                     "backend), the cache's first 2 sequences"}
+    if bad or not kth_ok or not kp1_ok or err > 2e-2:
+        raise AssertionError(f"bench parity check failed: {res}")
+    return res, a
 
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "b200":
+        self_launch(args)
     import torch
 
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    dist = None
-    ndev = torch.cuda.device_count() if torch.cuda.is_available() else 1
-    # BENCH_DIST_BACKEND=gloo (+ more ranks than GPUs): a functional check of the multi-rank
-    # path on a single-GPU box; the driver's multi-GPU runs use NCCL, one rank per GPU
-    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
-    if world > 1:
-        import torch.distributed as dist
-
-        torch.cuda.set_device(local % ndev)
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            dist.init_process_group(backend)
-    device = torch.device("cuda", (local % ndev) if torch.cuda.is_available() else 0)
-    G = args.q_heads // args.kv_heads
     H, D, S = args.kv_heads, args.head_dim, args.page
+    G = args.q_heads // H
     kp = -(-args.budget // S)
     U = args.batch * H
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    n_gpus = max(world_env, args.gpus if args.impl == "reference" else world_env)
     config = {
-        "workload": "BASELINE configs[2]: Llama-3.1-8B attn shape, 32q/8kv d128, batch "
-                    f"{args.batch}/GPU, ctx {args.ctx}, page {S}, k={args.budget} tokens "
-                    f"({kp} pages), bf16 KV, {args.stats_dtype} page stats",
-        "global_batch": args.batch * world,
+        "workload": "BASELINE configs[2]: Llama-3.1-8B attn shape, 32q/8kv d128, global batch "
+                    f"{args.batch}, ctx {args.ctx}, page {S}, k={args.budget} tokens ({kp} pages), "
+                    f"bf16 KV, {args.stats_dtype} page stats"
+                    + ("" if args.no_mirror or args.stats_dtype != "f32" else
+                       " (+ bf16 mirror for bounded scoring)"),
+        "global_batch": args.batch,
         "seq_len": args.ctx,
-        "parallelism": f"units (batch x kv-head) sharded over {world} GPU(s), no data-path collective",
-        "l2": "inputs larger than L2 (~1.3 GB touched per step vs 126 MB L2); 4 rotating query sets",
+        "parallelism": f"{U} (sequence, kv-head) units split over {n_gpus} GPU(s) by sequence "
+                       "(strong scaling), no data-path collective",
+        "l2": "inputs larger than L2 (~0.8 GB touched per step vs 126 MB L2); 4 rotating query sets",
     }
 
     if args.impl == "reference":
-        if rank != 0:
+        if int(os.environ.get("RANK", "0")) != 0:
             return
-        from oracle import oracle as O
-
-        ncores = host_cores()
-        # the oracle sample needs the same cache contents: build a 2-sequence cache on the GPU
-        # when one is present, else generate on the host (identical distribution).
-        if torch.cuda.is_available():
-            a2 = argparse.Namespace(**vars(args))
-            a2.batch = 2
-            cache = build_cache(a2, device, seed=1234 + rank)
-            qg = torch.Generator(device=device)
-            qg.manual_seed(7)
-            q = torch.randn(cache.num_units * G, D, generator=qg, device=device).to(torch.bfloat16)
-            budget = args.cpu_seconds
-            vals = []
-            # the reference's own compiled kernels when oracle/_ref was built from the
-            # reference sources (kind "reference"), else the oracle port (kind "port")
-            r = ref_kernels_baseline(cache, q, a2, budget / 4, ncores)
-            if r is not None:
-                vals.append(r)
-                for _ in range(max(1, min(args.steps, 3)) - 1):
-                    vals.append(ref_kernels_baseline(cache, q, a2, budget / 4, ncores))
-            else:
-                for _ in range(args.warmup and 1):
-                    cpu_baseline(cache, q, a2, 0.5, ncores)
-                for _ in range(max(1, min(args.steps, 3))):
-                    vals.append(cpu_baseline(cache, q, a2, budget / 3, ncores))
-            v = statistics.median([x["value"] for x in vals])
-            cb = {k: vals[0][k] for k in ("unit", "cores", "kind", "sample")}
-            cb["value"] = v
-        else:
-            print(json.dumps({"impl": "reference", "unavailable": "no CUDA device to build the "
-                              "shared workload"}))
-            return
-        line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
-                "steps": len(vals), "warmup": 1, "ms_per_step": 1000.0 * 32 / v,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-                "data": "synthetic N(0,1) (reference workload distribution)", "config": config,
-                "cpu_baseline": cb,
-                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(line))
+        run_reference_arm(args, n_gpus, config)
         return
 
     import paper_2605_27740_b200 as pt
+    from paper_2605_27740_b200.shard import shard_units
 
-    cache = build_cache(args, device, seed=1234 + rank)
+    ctx = Ctx()
+    rank, world, device = ctx.rank, ctx.world, ctx.device
+    sh = shard_units(args.batch, H, G, world, rank)
+    Ul = sh.num_units
+    cache = build_cache(args, device, SEED, units=range(sh.u0, sh.u1))
     eng = pt.DecodeEngine(cache, G, kp)
-    qg = torch.Generator(device=device)
-    qg.manual_seed(7 + rank)
-    NQ = 4
-    qs = [torch.randn(U * G, D, generator=qg, device=device).to(torch.bfloat16) for _ in range(NQ)]
-    kn = torch.randn(U, D, generator=qg, device=device).to(torch.bfloat16)
-    vn = torch.randn(U, D, generator=qg, device=device).to(torch.bfloat16)
+    qs_g, kn_g, vn_g = step_inputs(args, device)
+    r0, r1 = sh.q_rows
+    qs = [q[r0:r1].contiguous() for q in qs_g]
+    kn = kn_g[sh.u0:sh.u1].contiguous()
+    vn = vn_g[sh.u0:sh.u1].contiguous()
     stream = torch.cuda.current_stream()
 
     if args.profile:
         for i in range(max(args.steps, 1)):
-            eng.step(qs[i % NQ], kn, vn)
+            eng.step(qs[i % len(qs)], kn, vn)
         torch.cuda.synchronize()
         if rank == 0:
             print(json.dumps({"profile": "done", "steps": args.steps}))
+        ctx.close()
         return
 
-    # warm-up (eager, configures kernel attributes), then capture NQ graphs
+    # warm-up (eager: kernel attributes, path decisions), then one graph per query set
     for i in range(max(args.warmup, 3)):
-        eng.step(qs[i % NQ], kn, vn)
+        eng.step(qs[i % len(qs)], kn, vn)
     torch.cuda.synchronize()
     cache.check_errors()
-    graphs = []
-    for i in range(NQ):
-        gph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(gph):
-            eng.step(qs[i], kn, vn)
-        cache._seq_host -= 1
-        graphs.append(gph)
+    graphs = capture_steps(eng, cache, qs, kn, vn)
     for i in range(args.warmup):
-        graphs[i % NQ].replay()
+        graphs[i % len(graphs)].replay()
         cache._seq_host += 1
     torch.cuda.synchronize()
 
-    def barrier():
-        if dist is not None:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    # ---- timed region: K graph replays -------------------------------------------
-    sampler = ClockSampler(local % ndev)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
-    with sampler:
-        e0.record(stream)
-        for i in range(args.steps):
-            graphs[i % NQ].replay()
-        e1.record(stream)
-        barrier()
-    cache._seq_host += args.steps
-    ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], device=device)
-    if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    ms_per_step = ms_max / args.steps
-    value = world * args.batch / (ms_per_step / 1000.0)
+    # ---- timed region: K graph replays ------------------------------------------------
+    sampler = ClockSampler(ctx.dev_index)
+    ms_per_step = timed_replays(ctx, graphs, cache, args.steps, sampler)
+    value = args.batch / (ms_per_step / 1000.0)
     cache.check_errors()
 
-    # ---- per-kernel breakdown (CUDA events on the launching stream) -----------------
+    # ---- per-kernel times (CUDA events on the launching stream, eager launches) -------
     reps = max(20, min(args.steps, 100))
     names = ["append", "lam_norms", "score", "select_attend"]
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(reps)]
     for r in range(reps):
-        q = qs[r % NQ]
+        q = qs[r % len(qs)]
         ev = evs[r]
         ev[0].record(stream)
         cache.append_batch(kn, vn)
@@ -447,154 +633,113 @@ def main():
         ev[4].record(stream)
     torch.cuda.synchronize()
     cache.check_errors()
+    bounded = bool(eng._step_bounded)
     brk = {n: statistics.median([evs[r][i].elapsed_time(evs[r][i + 1]) * 1000 for r in range(reps)])
            for i, n in enumerate(names)}
-    # the unfused K3 (pt_topk) over the same keys, for reference
-    ev2 = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(reps)]
-    eng.score_prenorm(qs[0])
-    for r in range(reps):
-        ev2[r][0].record(stream)
-        eng.select()
-        ev2[r][1].record(stream)
-    torch.cuda.synchronize()
-    brk["select_only"] = statistics.median([ev2[r][0].elapsed_time(ev2[r][1]) * 1000 for r in range(reps)])
-    # the unfused attention kernel over the same selection (pt_attend), for reference
-    ev3 = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(reps)]
-    for r in range(reps):
-        ev3[r][0].record(stream)
-        eng.attend(qs[r % NQ], nsplit=args.nsplit)
-        ev3[r][1].record(stream)
-    torch.cuda.synchronize()
-    brk["attend_only"] = statistics.median([ev3[r][0].elapsed_time(ev3[r][1]) * 1000 for r in range(reps)])
-    tune = None
-    if args.sweep:
-        tune = {}
-        def timeit(fn, reps=20):
-            for _ in range(3):
-                fn()
-            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a0.record(stream)
-            for r in range(reps):
-                fn()
-            a1.record(stream)
-            torch.cuda.synchronize()
-            return a0.elapsed_time(a1) * 1000 / reps
-        for nst in ("2", "3", "4", "6"):
-            for ctas in ("1", "2"):
-                os.environ["PT_ATTEND_NSTAGE"], os.environ["PT_ATTEND_CTAS"] = nst, ctas
-                try:
-                    tune[f"attend_stream_nst{nst}_ctas{ctas}"] = timeit(lambda: eng.attend(qs[0]))
-                except Exception as e:  # noqa: BLE001
-                    tune[f"attend_stream_nst{nst}_ctas{ctas}"] = str(e)[:60]
-        os.environ.pop("PT_ATTEND_NSTAGE"); os.environ.pop("PT_ATTEND_CTAS")
-        os.environ["PT_ATTEND_SPLIT"] = "1"
-        tune["attend_split_auto"] = timeit(lambda: eng.attend(qs[0]))
-        os.environ.pop("PT_ATTEND_SPLIT")
-        # streaming scorer: CTAs per SM (ring shape follows: 2 x 8 KB stages at <= 2 CTAs,
-        # 3 x 4 KB at 3) x tile order (contiguous per-warp ranges or grid-stride)
-        for ctas in ("1", "2", "3"):
-            for contig in ("0", "1"):
-                os.environ["PT_SS_CTAS"], os.environ["PT_SS_CONTIG"] = ctas, contig
-                tune[f"score_stream_ctas{ctas}_contig{contig}"] = timeit(lambda: eng.score(qs[0]))
-        os.environ.pop("PT_SS_CTAS"); os.environ.pop("PT_SS_CONTIG")
-        os.environ["PT_SCORE_CTA"] = "1"
-        tune["score_cta"] = timeit(lambda: eng.score(qs[0]))
-        os.environ.pop("PT_SCORE_CTA")
-        tune["select"] = timeit(lambda: eng.select())
-        for nt in ("256", "1024"):
-            os.environ["PT_TOPK_THREADS"] = nt
-            tune[f"select_nt{nt}"] = timeit(lambda: eng.select())
-        os.environ.pop("PT_TOPK_THREADS")
-        # same byte count, contiguous pages instead of the selected (scattered) ones
-        saved = eng.sel.clone()
-        eng.sel.copy_(cache.page_table[:, : eng.k])
-        tune["attend_contiguous_pages"] = timeit(lambda: eng.attend(qs[0]))
-        eng.sel.copy_(saved)
-        eng.fused_select = True
-        tune["score_select_fused_cta"] = timeit(lambda: eng.score_select(qs[0]))
-        eng.fused_select = False
-    nsplit_sweep = None
-    if args.sweep_nsplit:
-        nsplit_sweep = {}
-        for ns in (1, 2, 3, 4, 6, 8, 12, 16, 32):
-            for _ in range(3):
-                eng.attend(qs[0], nsplit=ns)
-            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a0.record(stream)
-            for r in range(20):
-                eng.attend(qs[r % NQ], nsplit=ns)
-            a1.record(stream)
-            torch.cuda.synchronize()
-            nsplit_sweep[ns] = a0.elapsed_time(a1) * 1000 / 20
 
-    # ---- dense denominator: same GPU, every page of every unit ------------------------
+    if args.dump_out:  # one eager step (no append) on every rank, gathered in unit order
+        eng.step(qs[0])
+        outs = eng.out.cpu()
+        if ctx.dist is not None:
+            src = eng.out if ctx.backend == "nccl" else outs
+            parts = [torch.empty_like(src) for _ in range(world)]
+            ctx.dist.all_gather(parts, src)
+            outs = torch.cat([x.cpu() for x in parts])
+        if rank == 0:
+            np.save(args.dump_out, outs.numpy())
+
+    # ---- in-bench parity: the oracle on a sample of this very workload ---------------
+    parity, sample = None, None
+    if rank == 0 and not args.no_parity:
+        parity, sample = parity_check(eng, cache, qs[0], args)
+
+    # ---- dense denominator: same GPU, every page of every local unit ------------------
     dense_us = None
     if not args.no_dense:
         for i in range(3):
-            eng.dense(qs[i % NQ])
+            eng.dense(qs[i % len(qs)])
         dreps = 20
         d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         d0.record(stream)
         for i in range(dreps):
-            eng.dense(qs[i % NQ])
+            eng.dense(qs[i % len(qs)])
         d1.record(stream)
         torch.cuda.synchronize()
-        dense_us = d0.elapsed_time(d1) * 1000 / dreps
+        dense_us = ctx.max(d0.elapsed_time(d1) * 1000 / dreps)
 
-    # ---- e2e: public API with pinned host buffers, H2D inputs + D2H result per step ----
-    # one step's inputs (q, k_new, v_new) live in one pinned host block and one device block
-    # (three views each), so a step's H2D is a single copy
-    nq, nk = qs[0].numel(), kn.numel()
-    host_in = [torch.empty(nq + 2 * nk, dtype=torch.bfloat16).pin_memory() for _ in range(NQ)]
-    for i in range(NQ):
-        host_in[i][:nq].copy_(qs[i].reshape(-1).cpu())
-        host_in[i][nq:nq + nk].copy_(kn.reshape(-1).cpu())
-        host_in[i][nq + nk:].copy_(vn.reshape(-1).cpu())
-    dev_in = host_in[0].to(device)
-    q_dev = dev_in[:nq].view(U * G, D)
-    kn_d = dev_in[nq:nq + nk].view(U, D)
-    vn_d = dev_in[nq + nk:].view(U, D)
-    out_h = torch.empty(U * G, D, dtype=torch.float32).pin_memory()
-    # the engine's public graph API: capture() one step over static input buffers, then per
-    # step H2D the inputs into them, replay(), D2H the output
-    eng.capture(q_dev, kn_d, vn_d)
-    e2e_steps = max(20, min(args.steps, 100))
-    for i in range(3 + e2e_steps):
-        if i == 3:
-            barrier()
-            t0 = time.perf_counter()
-        dev_in.copy_(host_in[i % NQ], non_blocking=True)
-        eng.replay()
-        out_h.copy_(eng.out, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-    e2e_s = (time.perf_counter() - t0) / e2e_steps
-    te = torch.tensor([e2e_s], device=device)
-    if dist is not None:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = world * args.batch / float(te.item())
-    cache.check_errors()
-    h2d = host_in[0].numel() * 2
-    d2h = out_h.numel() * 4
+    # ---- optional output all-gather (NCCL over NVLink) + the step with it -------------
+    allgather_us = step_with_gather_us = None
+    if ctx.dist is not None:
+        dist = ctx.dist
+        comm_dev = device if ctx.backend == "nccl" else torch.device("cpu")
+        full = torch.empty(args.batch * H * G, D, dtype=torch.float32, device=comm_dev)
 
-    # ---- optional output all-gather (NCCL over NVLink), reported beside the line ------
-    allgather_us = None
-    if dist is not None and backend == "nccl":
-        outs = [torch.empty_like(eng.out) for _ in range(world)]
+        def gather():
+            if ctx.backend == "nccl":
+                dist.all_gather_into_tensor(full, eng.out)
+            else:  # gloo: list all-gather of host copies (functional check only)
+                parts = [torch.empty_like(full[: Ul * G]) for _ in range(world)]
+                dist.all_gather(parts, eng.out.cpu())
+                full.copy_(torch.cat(parts))
+
         for _ in range(3):
-            dist.all_gather(outs, eng.out)
+            gather()
+        ctx.barrier()
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
         a0.record(stream)
         for _ in range(20):
-            dist.all_gather(outs, eng.out)
+            gather()
         a1.record(stream)
         torch.cuda.synchronize()
-        allgather_us = a0.elapsed_time(a1) * 1000 / 20
+        ag = a0.elapsed_time(a1) * 1000 / 20 if ctx.backend == "nccl" else (time.perf_counter() - t0) * 1e6 / 20
+        allgather_us = ctx.max(ag)
+        ctx.barrier()
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        b0.record(stream)
+        for i in range(20):
+            graphs[i % len(graphs)].replay()
+            gather()
+        b1.record(stream)
+        ctx.barrier()
+        cache._seq_host += 20
+        sg = b0.elapsed_time(b1) * 1000 / 20 if ctx.backend == "nccl" else (time.perf_counter() - t0) * 1e6 / 20
+        step_with_gather_us = ctx.max(sg)
+        # the gathered outputs are the unsharded result's rows (order = global unit order)
+        assert full.shape[0] == args.batch * H * G
 
-    # ---- roofline of the dominant kernel + whole step ----------------------------------
+    # ---- e2e: the serving API (PipelinedDecoder) with pinned host buffers --------------
+    dec = pt.PipelinedDecoder(cache, G, kp)
+    nq, nk = qs[0].numel(), kn.numel()
+    host_in = [torch.empty(nq + 2 * nk, dtype=torch.bfloat16).pin_memory() for _ in range(len(qs))]
+    for i, q in enumerate(qs):
+        host_in[i][:nq].copy_(q.reshape(-1).cpu())
+        host_in[i][nq:nq + nk].copy_(kn.reshape(-1).cpu())
+        host_in[i][nq + nk:].copy_(vn.reshape(-1).cpu())
+    host_out = [torch.empty(Ul * G, D, dtype=torch.float32).pin_memory() for _ in range(2)]
+    dec.capture(host_in[0].to(device))
+    e2e_steps = max(20, min(args.steps, 200))
+    for i in range(6):
+        dec.submit(host_in[i % len(host_in)], host_out[i % 2])
+    dec.synchronize()
+    ctx.barrier()
+    t0 = time.perf_counter()
+    for i in range(e2e_steps):
+        dec.submit(host_in[i % len(host_in)], host_out[i % 2])
+    dec.synchronize()
+    e2e_s = ctx.max(time.perf_counter() - t0) / e2e_steps
+    e2e_value = args.batch / e2e_s
+    cache.check_errors()
+    h2d = host_in[0].numel() * 2 * world
+    d2h = host_out[0].numel() * 4 * world
+
+    # ---- roofline of the dominant kernel + whole step (SURVEY 8(d) bytes) -------------
     peaks, peak_kind = measured_peaks()
-    e_st = 4 if args.stats_dtype == "f32" else 2
+    e_st = 2 if (bounded or args.stats_dtype == "bf16") else 4
     P = -(-args.ctx // S)
-    by = step_bytes(U, G, D, P, kp, S, 2, e_st, args.ctx)
+    by = step_bytes(Ul, G, D, P, kp, S, 2, e_st, args.ctx)
+    by_f32 = step_bytes(Ul, G, D, P, kp, S, 2, 4, args.ctx)
     kbytes = {"score": by["score"], "select_attend": by["topk"] + by["attend"]}
     dom = max(("score", "select_attend"), key=lambda n: brk[n])
     dom_bytes = kbytes[dom]
@@ -603,17 +748,39 @@ def main():
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):
         try:
-            traffic = json.load(open(tf)).get(dom)
+            t = json.load(open(tf))
+            key = ("score_bounded" if bounded else "score") if dom == "score" else dom
+            traffic = t.get(key)
+            if isinstance(traffic, dict):
+                traffic = traffic.get("bytes_per_launch")
         except Exception:
             traffic = None
     step_total = by["append"] + by["score"] + by["topk"] + by["attend"]
 
+    # ---- weak scaling (N > 1): 32 sequences per rank --------------------------------
+    weak = None
+    if world > 1 and not args.no_weak:
+        del dec, eng, graphs, cache
+        torch.cuda.empty_cache()
+        wargs = argparse.Namespace(**vars(args))
+        wcache = build_cache(wargs, device, SEED + 1 + rank)
+        weng = pt.DecodeEngine(wcache, G, kp)
+        wq = [q.contiguous() for q in qs_g]
+        for i in range(3):
+            weng.step(wq[i % len(wq)], kn_g, vn_g)
+        torch.cuda.synchronize()
+        wgraphs = capture_steps(weng, wcache, wq, kn_g, vn_g)
+        for i in range(max(args.warmup, 3)):
+            wgraphs[i % len(wgraphs)].replay()
+            wcache._seq_host += 1
+        wms = timed_replays(ctx, wgraphs, wcache, args.steps)
+        weak = {"value": world * args.batch / (wms / 1000.0), "unit": UNIT,
+                "batch_per_gpu": args.batch, "ms_per_step": wms, "scaling": "weak"}
+
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        from oracle import oracle as O
-
-        nth = host_cores()
-        r = cpu_baseline(cache, qs[0], args, args.cpu_seconds, nth)
+        a = sample if sample is not None else _sample_arrays(cache, qs[0], args)
+        r = cpu_baseline(a, args.cpu_seconds, host_cores())
         cb = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
 
     if rank == 0:
@@ -627,16 +794,18 @@ def main():
             "ms_per_step": ms_per_step,
             "us_per_step": ms_per_step * 1000,
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "strong",
             "vs_baseline": None,
             "dtype": "bf16",
-            "data": "synthetic N(0,1) K/V/q (reference workload distribution), generated on device",
-            "config": config,
-            "gpu_launches": 4 * args.steps,  # append | lam-norms (parallel branches), score, select+attend
-            "nsplit_sweep_us": nsplit_sweep,
-            "tune_us": tune,
+            "data": "synthetic N(0,1) K/V/q per unit from a global seed (reference workload "
+                    "distribution), generated on device",
+            "config": dict(config, batch_per_gpu=args.batch // world if args.batch % world == 0
+                           else round(args.batch / world, 3),
+                           units_per_gpu=Ul, scoring="bounded (bf16 mirror)" if bounded else "exact f32 means"),
+            "gpu_launches": 4 * args.steps,  # append, lam-norms, score, select+attend per step
             "breakdown_us": brk,
             "step_bytes": step_total,
+            "step_bytes_model": "SURVEY 8(d) (page means at the KV element size: e=2)",
             "step_hbm_gbs": step_total / (ms_per_step * 1e-3) / 1e9,
             "step_frac_of_hbm": step_total / (ms_per_step * 1e-3) / 1e9 / peaks["hbm_gbs"],
             "roofline": {
@@ -648,23 +817,30 @@ def main():
                 "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"],
                 "bytes_per_launch": dom_bytes,
+                "bytes_model": "SURVEY 8(d) algorithmic bytes (e=2 page means)",
                 "traffic": traffic,
+                "score_bytes_moved": bounded_score_moved(Ul, G, D, P) if bounded else by_f32["score"],
+                "score_frac_by_bytes_moved": ((bounded_score_moved(Ul, G, D, P) if bounded else by_f32["score"])
+                                              / (brk["score"] * 1e-6) / 1e9 / peaks["hbm_gbs"]),
             },
             "dense_us_per_step": dense_us,
-            "x_over_dense": (dense_us / (brk["score"] + brk["select_attend"])) if dense_us else None,
-            "x_over_dense_attn_only": (dense_us / brk["attend_only"]) if dense_us else None,
+            "x_over_dense": (dense_us / (ms_per_step * 1000)) if dense_us else None,
+            "x_over_dense_kernels": (dense_us / (brk["score"] + brk["select_attend"])) if dense_us else None,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1000,
-                    "path": "pinned host q/k/v (one block) -> one H2D -> DecodeEngine.replay() "
-                            "(captured step: append | norms, score, select+attend) -> D2H f32 "
-                            "out, sync per step"},
+                    "path": "PipelinedDecoder.submit() (native pt_pipe_submit): pinned host "
+                            "q|k|v block -> H2D (h2d stream) -> captured step graph (append, norms, "
+                            "score, select+attend) -> D2H f32 outputs (d2h stream), double-buffered, "
+                            "every step; wall clock over the steps, max over ranks"},
             "clocks": sampler.summary(),
             "allgather_us": allgather_us,
+            "us_per_step_with_allgather": step_with_gather_us,
+            "weak": weak,
+            "parity": parity,
             "cpu_baseline": cb,
         }
-        print(json.dumps(line))
-    if dist is not None:
-        dist.destroy_process_group()
+        print(json.dumps(line), flush=True)
+    ctx.close()
 
 
 if __name__ == "__main__":

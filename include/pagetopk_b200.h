@@ -264,6 +264,20 @@ PT_API int pt_gated_attend_bwd(const void *q, int q_dtype, const void *k_pool, c
 PT_API int pt_gate_bias(const double *gates, const int32_t *seq_len, int U, int S, int Pmax,
                         float *bias, int32_t *flag, void *stream);
 
+/* Serving loop (runtime.cu): a depth-slot pipeline of decode steps.  pt_pipe_submit queues
+ * one step on slot `slot`: H2D of in_bytes from pinned host_in into dev_in on the h2d
+ * stream, launch of the slot's captured step graph (cudaGraphExec_t) on the compute stream,
+ * D2H of out_bytes from dev_out into pinned host_out on the d2h stream -- with the event
+ * edges that overlap the copies of neighbouring steps with the kernels (a slot's next H2D
+ * waits for its graph, its next graph waits for its D2H).  pt_pipe_wait blocks until the
+ * slot's outputs are on the host. */
+PT_API int pt_pipe_create(void *compute_stream, void *h2d_stream, void *d2h_stream, int depth,
+                          void **pipe_out);
+PT_API int pt_pipe_submit(void *pipe, int slot, void *graph_exec, void *dev_in, const void *host_in,
+                          size_t in_bytes, void *host_out, const void *dev_out, size_t out_bytes);
+PT_API int pt_pipe_wait(void *pipe, int slot);
+PT_API int pt_pipe_destroy(void *pipe);
+
 /* Layout helper: row-major means f32 [U][P][D] -> tiled stats layout (stats_dtype). */
 PT_API int pt_tile_means(const float *means_rowmajor, int U, int P, int D, int Pmax, void *means_tiled,
                   int stats_dtype, void *stream);

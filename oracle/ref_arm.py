@@ -14,6 +14,11 @@ kernels exactly as the reference's ``decode_step`` does (``attention.py:110-147`
   (``kvcache.py:266-280``), then ``stream_attention`` with block = page size and a zero
   block bias (``attention.py:57-75,94-107``).
 
+With ``k_new`` / ``v_new`` a step first appends one K/V row per unit at position n (the
+same slot every step, so the state a step sees is constant: n + 1 tokens) and refreshes the
+tail page's stats with the reference's numpy ``compute_page_stats`` (``kvcache.py:59-71,
+185-208``) -- the decode step of a serving loop, as the B200 arm's step does.
+
 The compiled kernels hold the GIL (no ``nogil`` in the .pyx), so the units fan out over a
 fork-started process pool, one worker per host core (SURVEY §8(d) CPU baseline (ii)).
 Only ``bench.py --impl reference`` and tests use this module.
@@ -67,6 +72,41 @@ def _encode(bits: np.ndarray) -> np.ndarray:
     return np.where(neg, ~b, b | np.uint16(0x8000)).astype(np.uint16)
 
 
+def compute_page_stats(rows: np.ndarray):
+    """kvcache.py:59-71 (numpy, float64 accumulation, f32 results)."""
+    r = np.asarray(rows, dtype=np.float64)
+    mean = r.mean(axis=0)
+    var = np.mean((r - mean) ** 2, axis=0)
+    return mean.astype(np.float32), float(np.float32(np.sqrt(var.sum())))
+
+
+def append_unit(w, u: int) -> int:
+    """kvcache.py:185-208 for unit u: the step's row lands at position n (the tail page has
+    room: the workload keeps a spare page), the page's stats are recomputed; returns n + 1."""
+    S = w["S"]
+    n = int(w["seq"][u])
+    lp, row = n // S, n % S
+    pid = int(w["tab"][u, lp])
+    w["kpool"][pid, row] = w["kn"][u]
+    w["vpool"][pid, row] = w["vn"][u]
+    mean, std = compute_page_stats(w["kpool"][pid, : row + 1])
+    w["means"][u, lp] = mean
+    w["stds"][u, lp] = std
+    return n + 1
+
+
+def appended(w):
+    """(kpool, vpool, means, stds, seq) of the workload after one append per unit (for the
+    port / cross-checks; the workload dict itself is not modified)."""
+    v = dict(w)
+    U, D = w["q"].shape[0], w["q"].shape[2]
+    v["kpool"], v["vpool"] = w["kpool"].copy(), w["vpool"].copy()
+    v["means"] = w["means"].reshape(U, -1, D).copy()
+    v["stds"] = w["stds"].reshape(U, -1).copy()
+    seq = np.array([append_unit(v, u) for u in range(U)], dtype=np.int32)
+    return v["kpool"], v["vpool"], v["means"], v["stds"], seq
+
+
 def decode_unit(u: int):
     """decode_step for one unit on the reference kernels; returns (phys ids, out [G,D], lse [G])."""
     K = kernels()
@@ -74,7 +114,7 @@ def decode_unit(u: int):
     q = np.ascontiguousarray(w["q"][u], dtype=np.float32)
     G, D = q.shape
     S = w["S"]
-    n = int(w["seq"][u])
+    n = append_unit(w, u) if w.get("kn") is not None else int(w["seq"][u])
     P = -(-n // S)
     norms = np.sqrt(np.sum(q.astype(np.float64) ** 2, axis=1)).astype(np.float32)
     means = np.ascontiguousarray(w["means"][u, :P])
@@ -111,14 +151,14 @@ class RefArm:
     """Fork-started worker pool over units running the reference kernels."""
 
     def __init__(self, q, kpool, vpool, page_table, seq_len, means, stds, k, lam, page_size,
-                 nproc: int):
+                 nproc: int, k_new=None, v_new=None):
         global _W
         kernels()  # load (and fail loudly) before forking
         U, G, D = q.shape
         _W = dict(q=np.ascontiguousarray(q, dtype=np.float32), kpool=kpool, vpool=vpool,
                   tab=page_table, seq=seq_len, means=means.reshape(U, -1, D),
                   stds=stds.reshape(U, -1), k=int(k), lam=float(lam), S=int(page_size),
-                  scale=1.0 / math.sqrt(D))
+                  scale=1.0 / math.sqrt(D), kn=k_new, vn=v_new)
         self.U = U
         self.nproc = max(1, min(nproc, U))
         self.pool = mp.get_context("fork").Pool(self.nproc)

@@ -17,7 +17,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB_NAME = "libpagetopk_b200.so"
 LIB_PATH = os.path.join(HERE, LIB_NAME)
 SOURCES = ("stats.cu", "score.cu", "score_bounded.cu", "score_stream_q32.cu", "score_stream_q16.cu", "topk.cu", "attend.cu", "attend_mma.cu", "attend_fused.cu", "gated_bwd.cu", "attend_simt_f32.cu",
-           "attend_simt_bf16.cu", "capi.cu")
+           "attend_simt_bf16.cu", "capi.cu", "runtime.cu")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler",
               "-fvisibility=hidden", "--expt-relaxed-constexpr"]

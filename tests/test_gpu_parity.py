@@ -743,7 +743,10 @@ def test_bench_runs_end_to_end(cuda):
     line = json.loads(r.stdout.strip().splitlines()[-1])
     for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
                 "higher_is_better", "scaling", "dtype", "config", "roofline", "e2e", "clocks",
-                "gpu_launches", "cpu_baseline"):
+                "gpu_launches", "cpu_baseline", "parity"):
         assert key in line, key
     assert line["value"] > 0 and line["e2e"]["value"] > 0 and line["roofline"]["achieved"] > 0
     assert line["cpu_baseline"]["cores"] >= 1
+    # the in-bench oracle check ran on the sample and passed (bench.py raises otherwise)
+    assert line["parity"]["selection_mismatches"] == 0 and line["parity"]["units"] == 16
+    assert line["config"]["scoring"].startswith("bounded")

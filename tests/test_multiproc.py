@@ -1,8 +1,10 @@
-"""Multi-GPU sharding logic on CPU: world_size-2 gloo process group.
+"""Multi-GPU sharding logic on CPU: world_size-2 gloo process groups.
 
-Each rank runs the decode step for its own unit shard (here through the CPU oracle,
-the only compute available without a GPU) and the optional output all-gather
-reassembles the full [B*Hq, D] result, which must equal the unsharded step exactly.
+Each rank runs bench.py's multi-rank plumbing -- shard_units, the per-unit workload
+generators, Ctx (rank / gloo / max-over-ranks) -- and computes its shard's decode step
+(through the CPU oracle, the only compute available without a GPU); the optional output
+all-gather reassembles the full [B*Hq, D] result, which must equal the unsharded step
+exactly.  The same path on the GPU is tests/test_gpu_multirank.py.
 """
 
 from __future__ import annotations
@@ -41,58 +43,91 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def _problem(seed=5, B=3, H=2, G=4, D=32, S=8, N=200, k=6):
-    rng = np.random.default_rng(seed)
-    U = B * H
-    P = -(-N // S)
-    kpool = rng.standard_normal((U * P, S, D)).astype(np.float32)
-    vpool = rng.standard_normal((U * P, S, D)).astype(np.float32)
-    table = np.arange(U * P, dtype=np.int32).reshape(U, P)
-    seq = np.full(U, N, np.int32)
-    q = rng.standard_normal((U, G, D)).astype(np.float32)
-    return dict(B=B, H=H, G=G, D=D, S=S, k=k, kpool=kpool, vpool=vpool, table=table, seq=seq, q=q)
+def _args(batch=4):
+    import bench
+
+    return bench.parse(["--batch", str(batch), "--ctx", "200", "--q-heads", "8", "--kv-heads", "2",
+                        "--head-dim", "32", "--page", "8", "--budget", "48"])
 
 
-def _worker(rank, world, port, result_q):
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+def _units_step(args, units, q_rows):
+    """The decode step for global units ``units`` on the bench workload (bench.unit_rows /
+    bench.step_inputs on the CPU generator), computed by the oracle (no GPU here)."""
+    import bench
     from oracle import oracle as O
 
-    p = _problem()
-    sh = shard_units(p["B"], p["H"], p["G"], world, rank)
-    u = slice(sh.u0, sh.u1)
-    means, stds = O.build_stats(p["kpool"], p["table"][u], p["seq"][u], p["S"])
-    r = O.decode_units(p["q"][u], p["kpool"], p["vpool"], p["table"][u], p["seq"][u], means, stds,
-                       p["k"], 0.5, 1 / np.sqrt(p["D"]), p["S"])
-    local = torch.from_numpy(r["out"].reshape(-1, p["D"]))
-    full = gather_outputs(local, sh, p["B"] * p["H"])
-    # max-over-ranks timing reduction used by bench.py
-    t = torch.tensor([float(rank + 1)])
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    D, S = args.head_dim, args.page
+    G = args.q_heads // args.kv_heads
+    ks, vs = [], []
+    for kk, vv in bench.unit_rows(args, "cpu", bench.SEED, units, chunk=64):
+        ks.append(kk.float().numpy())
+        vs.append(vv.float().numpy())
+    K, V = np.concatenate(ks, axis=1), np.concatenate(vs, axis=1)
+    Ul, n = K.shape[0], K.shape[1]
+    P = -(-n // S)
+    kpool = np.zeros((Ul * P, S, D), np.float32)
+    vpool = np.zeros((Ul * P, S, D), np.float32)
+    for i in range(Ul):
+        kpool[i * P:(i + 1) * P].reshape(-1, D)[:n] = K[i]
+        vpool[i * P:(i + 1) * P].reshape(-1, D)[:n] = V[i]
+    table = (np.arange(Ul)[:, None] * P + np.arange(P)[None, :]).astype(np.int32)
+    seq = np.full(Ul, n, np.int32)
+    qs, _, _ = bench.step_inputs(args, "cpu", NQ=1)
+    q = qs[0][q_rows[0]:q_rows[1]].float().numpy().reshape(Ul, G, D)
+    means, stds = O.build_stats(kpool, table, seq, S)
+    k = -(-args.budget // S)
+    r = O.decode_units(q, kpool, vpool, table, seq, means, stds, k, 0.5, 1 / np.sqrt(D), S)
+    return r["out"].reshape(-1, D)
+
+
+def _worker(rank, world, port, batch, result_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank), BENCH_DIST_BACKEND="gloo")
+    import bench
+
+    ctx = bench.Ctx()  # the bench's rank / collective plumbing (gloo here)
+    args = _args(batch)
+    G = args.q_heads // args.kv_heads
+    sh = shard_units(args.batch, args.kv_heads, G, ctx.world, ctx.rank)
+    local = torch.from_numpy(_units_step(args, range(sh.u0, sh.u1), sh.q_rows))
+    full = gather_outputs(local, sh, args.batch * args.kv_heads)
+    tmax = ctx.max(float(rank + 1))  # max-over-ranks timing reduction of bench.py
     if rank == 0:
-        result_q.put((full.numpy(), float(t.item())))
-    dist.barrier()
-    dist.destroy_process_group()
+        result_q.put((full.numpy(), tmax))
+    ctx.barrier()
+    ctx.close()
 
 
-@pytest.mark.parametrize("world", [2])
-def test_sharded_step_gathers_to_the_unsharded_result(world):
-    from oracle import oracle as O
-
+@pytest.mark.parametrize("world,batch", [(2, 4), (2, 3)])
+def test_sharded_step_gathers_to_the_unsharded_result(world, batch):
+    """world ranks on gloo run bench.py's sharding (shard_units), workload generation
+    (unit_rows / step_inputs: per-unit generators) and collectives (Ctx, gather_outputs);
+    the gathered step equals the unsharded one bit for bit (batch 3 over 2 ranks splits a
+    sequence's kv-heads)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, batch, q)) for r in range(world)]
     for pr in procs:
         pr.start()
-    full, tmax = q.get(timeout=120)
+    full, tmax = q.get(timeout=180)
     for pr in procs:
-        pr.join(timeout=120)
+        pr.join(timeout=180)
         assert pr.exitcode == 0
-    p = _problem()
-    means, stds = O.build_stats(p["kpool"], p["table"], p["seq"], p["S"])
-    r = O.decode_units(p["q"], p["kpool"], p["vpool"], p["table"], p["seq"], means, stds, p["k"],
-                       0.5, 1 / np.sqrt(p["D"]), p["S"])
-    np.testing.assert_array_equal(full, r["out"].reshape(-1, p["D"]))
+    args = _args(batch)
+    G = args.q_heads // args.kv_heads
+    U = args.batch * args.kv_heads
+    ref = _units_step(args, range(U), (0, U * G))
+    np.testing.assert_array_equal(full, ref)
     assert tmax == float(world)
+
+
+def test_unit_rows_are_shard_stable():
+    """A shard's rows equal the corresponding rows of the unsharded workload."""
+    import bench
+
+    args = _args(4)
+    whole = [k.float() for k, _ in bench.unit_rows(args, "cpu", bench.SEED, range(8), chunk=64)]
+    part = [k.float() for k, _ in bench.unit_rows(args, "cpu", bench.SEED, range(3, 6), chunk=64)]
+    for a, b in zip(whole, part):
+        assert torch.equal(a[3:6], b)
