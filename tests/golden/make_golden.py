@@ -98,6 +98,20 @@ def main() -> None:
         out[f"decode{i}_kth"] = np.float64([x.kth_score for x in sels])
         out[f"decode{i}_kp1"] = np.float64([np.nan if x.kplus1_score is None else x.kplus1_score
                                             for x in sels])
+        # the reference's own cached page stats, and its UNQK snapshot of this cache
+        # (kvcache.py:289-320): PagedKvCache.load must rebuild the same stats from it
+        st = [wl.cache.stats_arrays(h) for h in range(hkv)]
+        out[f"decode{i}_means"] = np.stack([x[0] for x in st])
+        out[f"decode{i}_stds"] = np.stack([x[1] for x in st])
+        out[f"decode{i}_counts"] = np.stack([x[2] for x in st]).astype(np.int64)
+        snap = os.path.join(HERE, f"decode{i}.unqk")
+        wl.cache.save(snap)
+        # the reference's load -> save round trip is byte-identical
+        rt = snap + ".rt"
+        pt.PagedKvCache.load(snap).save(rt)
+        with open(snap, "rb") as a, open(rt, "rb") as b:
+            assert a.read() == b.read()
+        os.remove(rt)
 
     path = os.path.join(HERE, "golden.npz")
     np.savez_compressed(path, **out)

@@ -145,3 +145,38 @@ def test_public_names_cover_the_reference_hot_path():
     assert pt.backend.NAME == "b200"
     for fn in ("fused_scores", "radix_select_desc", "stream_attention"):
         assert callable(getattr(pt.backend, fn))
+
+
+def test_unqk_header_errors_raise_before_touching_a_device(tmp_path):
+    """PagedKvCache.load rejects a bad magic / version (kvcache.py:326-330) with the
+    reference's ValueError messages before any device allocation."""
+    import struct
+
+    import paper_2605_27740_b200 as pt
+
+    bad = tmp_path / "bad.unqk"
+    bad.write_bytes(b"XXXX" + struct.pack("<IIIII", 1, 1, 4, 2, 0))
+    with pytest.raises(ValueError, match="bad snapshot magic"):
+        pt.PagedKvCache.load(str(bad))
+    bad.write_bytes(b"UNQK" + struct.pack("<IIIII", 99, 1, 4, 2, 0))
+    with pytest.raises(ValueError, match="unsupported snapshot version"):
+        pt.PagedKvCache.load(str(bad))
+
+
+def test_reference_snapshot_fixture_header():
+    """The committed reference-written snapshots parse as the reference's format."""
+    import os
+    import struct
+
+    import numpy as np
+
+    gold = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    z = np.load(os.path.join(gold, "golden.npz"))
+    for i in (0, 1):
+        with open(os.path.join(gold, f"decode{i}.unqk"), "rb") as f:
+            assert f.read(4) == b"UNQK"
+            version, heads, dim, size, n = struct.unpack("<IIIII", f.read(20))
+            body = np.frombuffer(f.read(), dtype="<f4")
+        sn, sd, ss, shq, shkv, sk = z[f"decode{i}_shape"].tolist()
+        assert (version, heads, dim, size, n) == (1, shkv, sd, ss, sn)
+        np.testing.assert_array_equal(body.reshape(heads, 2, n, dim), z[f"decode{i}_kv"])
