@@ -82,16 +82,18 @@ __global__ void __launch_bounds__(kStatsWarps * 32)
 // ---------------------------------------------------------------------------
 // Decode append, one launch (kvcache.py:185-208 for every unit).
 //
-// CTA 0 snapshots every unit's length (global scratch) and publishes `flag_read`; if any
-// unit starts a new page it runs the deterministic unit-order allocation -- the batched
-// _alloc_page (kvcache.py:154-176): free list popped from its end (list.pop()), then the
-// bump pointer; exhaustion -> error flag, unit skipped -- and publishes `flag_alloc`.
-// Every warp owns one unit: units continuing their tail page (15 of 16 steps at S = 16)
-// never wait; a unit starting a page waits for the allocation.  The warp writes the new
-// K/V row and recomputes the tail page's stats from a shared-memory copy of its rows (one
-// load round), then -- once CTA 0's snapshot is taken (flag_read; normally long set) --
-// advances its own sequence length.  The last CTA to finish re-arms the flags.  CTA 0
-// never waits, so the scheme cannot deadlock while CTAs are dispatched in index order.
+// The FIRST CTA to arrive (an atomic ticket, not a fixed block index) snapshots every
+// unit's length (global scratch) and publishes `flag_read`; if any unit starts a new page it
+// runs the deterministic unit-order allocation -- the batched _alloc_page
+// (kvcache.py:154-176): free list popped from its end (list.pop()), then the bump pointer;
+// pool or page-table exhaustion -> error flag, unit skipped (no page consumed) -- and
+// publishes `flag_alloc`.  Every warp owns one unit: units continuing their tail page (15 of
+// 16 steps at S = 16) never wait; a unit starting a page waits for the allocation.  The warp
+// writes the new K/V row and recomputes the tail page's stats from a shared-memory copy of
+// its rows (one load round), then -- once the snapshot is taken (flag_read; normally long
+// set) -- advances its own sequence length.  The last CTA to finish re-arms the flags.
+// No deadlock for any dispatch order or grid size: waiting CTAs only ever wait for the
+// allocating CTA, which took the first ticket, i.e. is already resident and never waits.
 __host__ __device__ __forceinline__ size_t append_per_warp(int S, int D, int ES) {
     return (((size_t)S * D * ES + 15) & ~(size_t)15) + (size_t)D * 8;
 }
@@ -134,7 +136,13 @@ __device__ void alloc_scan(int32_t *__restrict__ page_table, const int *__restri
     for (int base = 0; base < U; base += blockDim.x) {
         const int u = base + tid;
         const int n = u < U ? sn[u] : 1;
-        const int need = (u < U && n % S == 0) ? 1 : 0;
+        const bool starts = u < U && n % S == 0;
+        // a unit whose page table is full takes no rank (no page is consumed for it)
+        const int need = (starts && n / S < Pmax) ? 1 : 0;
+        if (starts && !need) {
+            slot[u] = -1;
+            pool_state[3] = PT_ERR_CAPACITY;
+        }
         const unsigned m = __ballot_sync(0xffffffffu, need);
         const int wpre = __popc(m & ((1u << lane) - 1u));
         if (lane == 0) warp_tot[warp] = __popc(m);
@@ -148,7 +156,7 @@ __device__ void alloc_scan(int32_t *__restrict__ page_table, const int *__restri
         if (need) {
             const int pid = rank < free0 ? free_list[free0 - 1 - rank] : bump0 + (rank - free0);
             const int lp = n / S;
-            if (pid >= max_pages || lp >= Pmax) {
+            if (pid >= max_pages) {
                 slot[u] = -1;
                 pool_state[3] = PT_ERR_CAPACITY;
             } else {
@@ -194,7 +202,8 @@ __global__ void __launch_bounds__(256)
     __shared__ int carry;
     __shared__ int is_last;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpc = blockDim.x >> 5;
-    int *flag_alloc = slot + U, *done = slot + U + 1, *flag_read = slot + U + 2;
+    int *flag_alloc = slot + U, *done = slot + U + 1, *flag_read = slot + U + 2, *arrive = slot + U + 3;
+    __shared__ int first_cta;
     constexpr int ES = DT == PT_F32 ? 4 : 2;
     const size_t per_warp = append_per_warp(S, D, ES);
     const int64_t u = (int64_t)blockIdx.x * wpc + warp;
@@ -215,7 +224,9 @@ __global__ void __launch_bounds__(256)
             vb[j] = static_cast<const Bits *>(v_new)[u * D + d];
         }
     }
-    if (blockIdx.x == 0) {
+    if (threadIdx.x == 0) first_cta = atomicAdd(arrive, 1) == 0;
+    __syncthreads();
+    if (first_cta) {
         int *sn = slot + U + 4;  // global scratch: no per-CTA shared memory for U lengths
         int any = 0;
         for (int i = threadIdx.x; i < U; i += blockDim.x) {
@@ -242,7 +253,7 @@ __global__ void __launch_bounds__(256)
     app_stamp(pr, u, 2);
     if (u < U) {
         int pid;
-        if (n % S == 0) {  // starts a page: CTA 0's allocation
+        if (n % S == 0) {  // starts a page: the allocating CTA's result
             if (lane == 0) spin_flag(flag_alloc, true);
             __syncwarp();
             pid = __ldcg(&slot[u]);
@@ -304,7 +315,7 @@ __global__ void __launch_bounds__(256)
             if (lane == 0) {
                 stds[u * Pmax + n / S] = __double2float_rn(__dsqrt_rn(vsum));
                 app_stamp(pr, u, 5);
-                spin_flag(flag_read, false);  // CTA 0 has snapshotted every length (no data to acquire)
+                spin_flag(flag_read, false);  // every length is snapshotted (no data to acquire)
                 app_stamp(pr, u, 6);
                 seq_len[u] = n + 1;
             }
@@ -316,6 +327,7 @@ __global__ void __launch_bounds__(256)
         if (atomicAdd(done, 1) == (int)gridDim.x - 1) {  // re-arm for the next append
             atomicExch(flag_alloc, 0);
             atomicExch(flag_read, 0);
+            atomicExch(arrive, 0);
             atomicExch(done, 0);
         }
     }

@@ -306,6 +306,9 @@ class PagedKvCache:
             raise ValueError("keys/values must be matching (units, n, head_dim) arrays")
         n_max = keys.shape[1]
         nr = np.full(U, n_max, dtype=np.int64) if n_rows is None else np.asarray(n_rows, np.int64)
+        # device appends may have been refused (pool / page-table exhaustion, reported by
+        # check_errors): start from the lengths the device actually holds
+        self._seq_host = self.seq_lens.cpu().numpy().astype(np.int64)
         n0 = self._seq_host.copy()
         n1 = n0 + nr
         P0 = -(-n0 // S)

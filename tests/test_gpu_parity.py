@@ -750,3 +750,57 @@ def test_bench_runs_end_to_end(cuda):
     # the in-bench oracle check ran on the sample and passed (bench.py raises otherwise)
     assert line["parity"]["selection_mismatches"] == 0 and line["parity"]["units"] == 16
     assert line["config"]["scoring"].startswith("bounded")
+
+
+def test_append_grid_beyond_residency_and_unit_order_allocation(cuda, oracle):
+    """16384 units (2048 append CTAs, more than fit on the GPU at once), every unit starting
+    a new page: the allocation is taken by whichever CTA arrives first (no dependence on
+    dispatch order) and is the reference's unit-order _alloc_page (kvcache.py:154-176):
+    unit u gets bump + u.  Stats of the sampled touched pages are bit-exact."""
+    pt = _pt()
+    U, D, S = 16384, 64, 16
+    layout = pt.CacheLayout(num_kv_heads=1, head_dim=D, page_size=S, max_pages=U * 3)
+    cache = pt.PagedKvCache(layout, batch=U, dtype=torch.bfloat16, max_pages_per_head=32)
+    rng = np.random.default_rng(9)
+    K = torch.from_numpy(rng.standard_normal((U, S, D)).astype(np.float32))
+    cache.extend_units(K, K)  # one full page per unit: pids 0 .. U-1
+    bump0 = int(cache.pool_state[0].item())
+    kn = torch.from_numpy(rng.standard_normal((U, D)).astype(np.float32)).cuda().to(torch.bfloat16)
+    for _ in range(3):
+        cache.append_batch(kn, kn)
+    torch.cuda.synchronize()
+    cache.check_errors()
+    table = cache.page_table.cpu().numpy()
+    np.testing.assert_array_equal(table[:, 1], bump0 + np.arange(U))
+    assert int(cache.pool_state[0].item()) == bump0 + U
+    kpool, _, _, seq = readback(cache)
+    assert np.all(seq == S + 3)
+    gm, gs = gpu_stats(cache)
+    for u in rng.integers(0, U, 16).tolist():
+        rows = kpool[table[u, 1], :3]
+        mean, std = oracle.compute_page_stats(rows)
+        np.testing.assert_array_equal(gm[u, 1], mean)
+        assert gs[u, 1] == np.float32(std)
+
+
+def test_append_full_page_table_consumes_no_page(cuda):
+    """A unit whose page table is full cannot take a page: capacity error, and the pool's
+    bump pointer does not move (no leaked page)."""
+    pt = _pt()
+    D, S = 16, 8
+    layout = pt.CacheLayout(num_kv_heads=2, head_dim=D, page_size=S, max_pages=200)
+    cache = pt.PagedKvCache(layout, batch=1, max_pages_per_head=32)
+    x = np.zeros((32 * S, D), np.float32)
+    cache.extend(0, x, x)  # unit 0: page table full
+    cache.extend(1, x[:S], x[:S])
+    bump0 = int(cache.pool_state[0].item())
+    kn = torch.zeros(2, D, device="cuda")
+    cache.append_batch(kn, kn)  # unit 1 starts page 1: OK; unit 0 has no room
+    torch.cuda.synchronize()
+    with pytest.raises(pt.CapacityError):
+        cache.check_errors()
+    assert int(cache.pool_state[0].item()) == bump0 + 1
+    assert cache.seq_len(0) == 32 * S and cache.seq_len(1) == S + 1
+    # the host mirror follows the device: a later extend starts from the true lengths
+    cache.extend(1, x[:2], x[:2])
+    assert cache.seq_len(1) == S + 3
