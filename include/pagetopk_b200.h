@@ -278,6 +278,10 @@ PT_API int pt_pipe_submit(void *pipe, int slot, void *graph_exec, void *dev_in, 
 PT_API int pt_pipe_wait(void *pipe, int slot);
 PT_API int pt_pipe_destroy(void *pipe);
 
+/* dst[i] = max(dst[i], src[i]) over n ordered u16 keys: the group maximum of a GQA group of
+ * more than 8 query heads scored as sub-groups of <= 8 (the key of a max is the max of keys). */
+PT_API int pt_keys_max(uint16_t *dst, const uint16_t *src, int64_t n, void *stream);
+
 /* Layout helper: row-major means f32 [U][P][D] -> tiled stats layout (stats_dtype). */
 PT_API int pt_tile_means(const float *means_rowmajor, int U, int P, int D, int Pmax, void *means_tiled,
                   int stats_dtype, void *stream);

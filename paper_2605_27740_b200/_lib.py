@@ -69,6 +69,7 @@ _PROTOS = {
                                  _i, _f, _vp, _vp, _vp, _vp, _vp]),
     "pt_gate_bias": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp, _vp]),
     "pt_tile_means": (_i, [_vp, _i, _i, _i, _i, _vp, _i, _vp]),
+    "pt_keys_max": (_i, [_vp, _vp, _i64, _vp]),
     "pt_pipe_create": (_i, [_vp, _vp, _vp, _i, _vp]),
     "pt_pipe_submit": (_i, [_vp, _i, _vp, _vp, _vp, _sz, _vp, _vp, _sz]),
     "pt_pipe_wait": (_i, [_vp, _i]),

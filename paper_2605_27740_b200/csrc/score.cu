@@ -438,6 +438,24 @@ extern "C" int pt_score_select(const void *q, int q_dtype, const float *norms, c
     return dispatch_score(prm, q_dtype, stats_dtype, U, G, (cudaStream_t)stream);
 }
 
+// dst[i] = max(dst[i], src[i]) over ordered u16 keys: the group max of a GQA group wider
+// than the kernels' 8 heads, scored as sub-groups (key(max_g s_g) = max_g key(s_g): the
+// bf16 rounding and the ordered encoding are monotone)
+__global__ void k_keys_max(uint16_t *__restrict__ dst, const uint16_t *__restrict__ src, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = max(dst[i], src[i]);
+}
+
+extern "C" int pt_keys_max(uint16_t *dst, const uint16_t *src, int64_t n, void *stream) {
+    if (!dst || !src || n < 0) return PT_ERR_INVALID;
+    if (n == 0) return PT_OK;
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > (int64_t)pt_num_sms() * 8) blocks = (int64_t)pt_num_sms() * 8;
+    k_keys_max<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(dst, src, n);
+    PT_CUDA_TRY(cudaGetLastError());
+    return PT_OK;
+}
+
 extern "C" int pt_tile_means(const float *src, int U, int P, int D, int Pmax, void *dst,
                              int stats_dtype, void *stream) {
     if (!src || !dst || U < 0 || P < 0 || P > Pmax || Pmax % 32) return PT_ERR_INVALID;

@@ -90,6 +90,32 @@ class DecodeEngine:
         self._side = torch.cuda.Stream(device=d)
         # append -> norms -> score as one PDL chain (PT_NO_PDL=1: the fork/join instead)
         self.chain_norms = os.environ.get("PT_NO_PDL", "") != "1" and os.environ.get("PT_NORMS_FORK", "") != "1"
+        # GQA groups wider than the kernels' 8 heads (e.g. 128 q / 8 kv heads): sub-groups of
+        # <= 8 heads, scored separately (exact keys) and combined by a key max, one shared
+        # selection, attention per sub-group (see _step_wide)
+        self.subgroups: list[tuple[int, int]] = []
+        if self.G > 8:
+            self.bounded = False
+            nsub = -(-self.G // 8)
+            base, extra = divmod(self.G, nsub)
+            g0 = 0
+            for i in range(nsub):
+                g1 = g0 + base + (1 if i < extra else 0)
+                self.subgroups.append((g0, g1))
+                g0 = g1
+            self._wide = []
+            for (a, b) in self.subgroups:
+                Gs = b - a
+                self._wide.append(dict(
+                    G=Gs, q=None,
+                    lamnorm=torch.zeros(U * 8, dtype=torch.float32, device=d),
+                    keys=torch.zeros(U, Pmax, dtype=torch.int16, device=d),
+                    tile_max=torch.zeros(U, Pmax // 32, dtype=torch.int16, device=d),
+                    out=torch.zeros(U * Gs, D, dtype=torch.float32, device=d),
+                    lse=torch.zeros(U * Gs, dtype=torch.float32, device=d),
+                    ws=torch.zeros(_lib.load().pt_attend_workspace_bytes(U, Gs, D, self.k),
+                                   dtype=torch.uint8, device=d),
+                    tickets=torch.zeros(U, dtype=torch.int32, device=d)))
 
     # ------------------------------------------------------------------
     def _q(self, q: torch.Tensor) -> tuple[torch.Tensor, int]:
@@ -247,9 +273,65 @@ class DecodeEngine:
         self.select(stream=stream)
         self.attend(q, stream=stream)
 
+    def _step_wide(self, q: torch.Tensor, k_new, v_new, stream=None):
+        """The step for G > 8 query heads per unit: per sub-group of <= 8 heads (row gathers
+        of q, output scatters), lam*||q|| and exact scores; keys combined by max (the group
+        max of scoring.py:108-124 split over sub-groups); one selection (pt_topk); attention
+        per sub-group over the shared selection (attention.py:143-146)."""
+        q2, qc = self._q(q)
+        U, D, G = self.U, self.D, self.G
+        c = self.cache
+        sh = dev.stream_handle(stream)
+        if k_new is not None:
+            c.append_batch(k_new, v_new, stream=stream)
+        q3 = q2.view(U, G, D)
+        for i, ((a, b), w) in enumerate(zip(self.subgroups, self._wide)):
+            Gs = w["G"]
+            if w["q"] is None or w["q"].dtype != q2.dtype:
+                w["q"] = torch.empty(U * Gs, D, dtype=q2.dtype, device=q2.device)
+            w["q"].view(U, Gs, D).copy_(q3[:, a:b])
+            _lib.call("pt_lam_norms", w["q"].data_ptr(), qc, None, U, Gs, D, self.lam,
+                      w["lamnorm"].data_ptr(), None, sh)
+            keys = self.keys if i == 0 else w["keys"]
+            tmax = self.tile_max if i == 0 else w["tile_max"]
+            rc = _lib.load().pt_score_prenorm(
+                w["q"].data_ptr(), qc, w["lamnorm"].data_ptr(), c.means.data_ptr(), c.stats_code,
+                c.stds.data_ptr(), c.seq_lens.data_ptr(), U, Gs, D, c.layout.page_size, c.Pmax,
+                keys.data_ptr(), None, tmax.data_ptr(), sh)
+            if rc == _lib.PT_ERR_UNSUPPORTED:
+                _lib.call("pt_score", w["q"].data_ptr(), qc, None, c.means.data_ptr(), c.stats_code,
+                          c.stds.data_ptr(), c.seq_lens.data_ptr(), U, Gs, D, c.layout.page_size,
+                          c.Pmax, self.lam, keys.data_ptr(), None, w["lamnorm"].data_ptr(),
+                          tmax.data_ptr(), sh)
+            else:
+                _lib.check(rc, "pt_score_prenorm")
+            if i > 0:
+                _lib.call("pt_keys_max", self.keys.data_ptr(), keys.data_ptr(), self.keys.numel(), sh)
+                _lib.call("pt_keys_max", self.tile_max.data_ptr(), tmax.data_ptr(),
+                          self.tile_max.numel(), sh)
+        self._step_bounded = False
+        self.select(stream=stream)
+        o3, l2 = self.out.view(U, G, D), self.lse.view(U, G)
+        for (a, b), w in zip(self.subgroups, self._wide):
+            Gs = w["G"]
+            _lib.call("pt_attend", w["q"].data_ptr(), qc, c.k_pool.data_ptr(), c.v_pool.data_ptr(),
+                      c.kv_code, c.layout.max_pages, self.sel.data_ptr(), self.k,
+                      self.n_sel.data_ptr(), c.page_table.data_ptr(), c.seq_lens.data_ptr(), U, Gs,
+                      D, c.layout.page_size, c.Pmax, None, self.scale, w["out"].data_ptr(),
+                      w["lse"].data_ptr(), w["ws"].data_ptr(), w["ws"].numel(),
+                      w["tickets"].data_ptr(), 0, sh)
+            o3[:, a:b].copy_(w["out"].view(U, Gs, D))
+            l2[:, a:b].copy_(w["lse"].view(U, Gs))
+        return self.out, self.lse
+
     def step(self, q: torch.Tensor, k_new: torch.Tensor | None = None,
              v_new: torch.Tensor | None = None, stream=None):
         """One decode step: [append] -> score -> select+attend.  Returns (out, lse)."""
+        if self.subgroups:
+            if stream is not None:
+                with torch.cuda.stream(stream):
+                    return self._step_wide(q, k_new, v_new, stream)
+            return self._step_wide(q, k_new, v_new)
         if self.fused_select:
             if k_new is not None:
                 self.cache.append_batch(k_new, v_new, stream=stream)

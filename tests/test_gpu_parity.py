@@ -804,3 +804,26 @@ def test_append_full_page_table_consumes_no_page(cuda):
     # the host mirror follows the device: a later extend starts from the true lengths
     cache.extend(1, x[:2], x[:2])
     assert cache.seq_len(1) == S + 3
+
+
+@pytest.mark.parametrize("G,dtype,tol", [(16, "f32", 1e-5), (12, "bf16", 2e-2), (9, "f32", 1e-5)])
+def test_wide_gqa_group_vs_oracle(cuda, oracle, G, dtype, tol):
+    """More than 8 query heads per KV head (e.g. 128 q / 8 kv): sub-groups of <= 8 heads
+    scored separately and combined by a key max, one shared selection -- the reference's
+    decode_step for any group size (attention.py:128-146), bit-exact selections."""
+    pt = _pt()
+    rng = np.random.default_rng(G)
+    B, H, D, S, N, k = 1, 2, 128, 16, 3000, 24
+    cache = make_cache(rng, B, H, D, S, [N, N - 7], dtype=dtype)
+    q = torch.from_numpy(rng.standard_normal((B * H * G, D)).astype(np.float32)).cuda()
+    if dtype == "bf16":
+        q = q.to(torch.bfloat16)
+    outs, sels = pt.decode_step(cache, q.float().cpu().numpy() if dtype == "f32" else q, pt.DecodeConfig(k=k))
+    kpool, vpool, table, seq = readback(cache)
+    means, stds = oracle.build_stats(kpool, table, seq, S)
+    ref = oracle.decode_units(q.to(torch.float32).cpu().numpy().reshape(-1, G, D), kpool, vpool,
+                              table, seq, means, stds, k, 0.5, 1.0 / math.sqrt(D), S)
+    for u in range(B * H):
+        assert set(sels[u].physical_ids.tolist()) == set(ref["sel"][u, : ref["n_sel"][u]].tolist())
+    got = np.stack([o.out for o in outs]).reshape(-1, G, D)
+    np.testing.assert_allclose(got, ref["out"], rtol=tol, atol=tol)
