@@ -267,7 +267,9 @@ static int sb_env(const char *name, int dflt) {
 template <int G, int D>
 static int sb_nst(const BoundedScoreParams &sp, cudaStream_t st) {
     // ring depth x CTAs per SM (PT_SB_NST / PT_SB_CTAS: tuning)
-    const int nst = sb_env("PT_SB_NST", 2), ctas = sb_env("PT_SB_CTAS", 2);
+    // measured (tools/probe_score.py): D = 128: 2 stages x 2 CTAs (cfg3 82.5 us = 6.66 TB/s; deeper
+    // rings drop to one CTA per SM: 141-150 us); D = 64: 3 stages x 3 CTAs (cfg4 53.5 vs 69.7 us)
+    const int nst = sb_env("PT_SB_NST", D == 64 ? 3 : 2), ctas = sb_env("PT_SB_CTAS", D == 64 ? 3 : 2);
     switch (nst) {
         case 3: return sb_launch<G, D, 3>(sp, ctas, st);
         case 4: return sb_launch<G, D, 4>(sp, ctas, st);

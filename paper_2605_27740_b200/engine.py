@@ -76,7 +76,7 @@ class DecodeEngine:
         # bounded scoring (cache.mirror): upper keys of the score intervals and ||q|| bounds;
         # the selection resolves the straddling pages exactly
         self.bounded = (cache.mirror is not None and not keep_scores
-                        and os.environ.get("PT_NO_BOUNDED", "") != "1")
+                        and os.environ.get("PT_NO_BOUNDED", "") != "1" and self._bounded_pays(cache))
         self.keys_hi = torch.zeros(U, Pmax, dtype=torch.int16, device=d) if self.bounded else None
         self.qnorm = torch.zeros(U * 8, dtype=torch.float32, device=d) if self.bounded else None
         self._step_bounded = False  # the keys of the last scoring are intervals
@@ -116,6 +116,20 @@ class DecodeEngine:
                     ws=torch.zeros(_lib.load().pt_attend_workspace_bytes(U, Gs, D, self.k),
                                    dtype=torch.uint8, device=d),
                     tickets=torch.zeros(U, dtype=torch.int32, device=d)))
+
+    def _bounded_pays(self, cache: PagedKvCache) -> bool:
+        """Bounded scoring halves the scorer's bytes but adds the resolve step to every
+        selecting CTA and needs the CTA-per-unit selection: worth it when the f32-means bytes
+        it saves (at ~6.5 TB/s) clearly exceed that (>= 25 us: cfg3 saves ~80 us; cfg2 (one
+        sequence) < 1 us) and the warp-per-unit path (thousands of short units, small k) is not
+        the faster selection.  PT_BOUNDED=1 forces it (tests, tuning)."""
+        if os.environ.get("PT_BOUNDED", "") == "1":
+            return True
+        U, P, D = cache.num_units, cache.Pmax, cache.layout.head_dim
+        sms = torch.cuda.get_device_properties(cache.device).multi_processor_count
+        warp_path = U >= 4 * sms and self.k <= 64 and P <= 2048
+        saved_us = U * P * D * 2 / 6.5e6
+        return not warp_path and saved_us >= 25.0
 
     # ------------------------------------------------------------------
     def _q(self, q: torch.Tensor) -> tuple[torch.Tensor, int]:

@@ -23,6 +23,12 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True)
+def _force_bounded(monkeypatch):
+    """These shapes are small: the engine would pick exact scoring by its cost model."""
+    monkeypatch.setenv("PT_BOUNDED", "1")
+
+
 def _pt():
     import paper_2605_27740_b200 as pt
 

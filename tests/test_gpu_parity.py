@@ -736,9 +736,12 @@ def test_bench_runs_end_to_end(cuda):
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    # PT_BOUNDED=1: the bounded scorer even at this small shape (the engine's cost model would
+    # pick exact scoring), so the in-bench parity check covers the bench's default path
     r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--batch", "2", "--ctx", "8192",
                         "--steps", "5", "--warmup", "3", "--no-dense", "--cpu-seconds", "0.5"],
-                       capture_output=True, text=True, timeout=600, cwd=root)
+                       capture_output=True, text=True, timeout=600, cwd=root,
+                       env=dict(os.environ, PT_BOUNDED="1"))
     assert r.returncode == 0, r.stderr[-2000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
     for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",

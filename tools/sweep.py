@@ -49,6 +49,7 @@ def main():
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--only", default="")
+    ap.add_argument("--no-mirror", action="store_true", help="exact f32-means scoring")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     stream = torch.cuda.current_stream()
@@ -67,7 +68,7 @@ def main():
         P_cap = -(-(ctx + spare) // S)
         layout = pt.CacheLayout(num_kv_heads=Hkv, head_dim=D, page_size=S, max_pages=U * P_cap)
         cache = pt.PagedKvCache(layout, batch=B, dtype=torch.bfloat16, stats_dtype=torch.float32,
-                                max_pages_per_head=P_cap, device=dev)
+                                max_pages_per_head=P_cap, device=dev, mirror=not a.no_mirror)
         g = torch.Generator(device=dev)
         g.manual_seed(1234)
         chunk = max(1, min(ctx, (1 << 27) // (U * D)))  # <= 256 MB of staging per tensor
@@ -109,7 +110,7 @@ def main():
         brk = {}
         for nm, fn in (("append", lambda: cache.append_batch(kn, vn)),
                        ("lam_norms", lambda: eng.lam_norms(q)),
-                       ("score", lambda: eng.score_prenorm(q) or eng.score(q)),
+                       ("score", lambda: eng.score_step(q)),
                        ("select_attend", lambda: eng.select_attend(q))):
             fn()
             torch.cuda.synchronize()
@@ -127,6 +128,7 @@ def main():
             del gs
         cache._seq_host = cache.seq_lens.cpu().numpy().astype("int64")
         fused = eng.fused_attend
+        bounded = bool(eng._step_bounded)
         for _ in range(2):
             eng.dense(q)
         d0, d1 = ev(), ev()
@@ -137,7 +139,7 @@ def main():
         torch.cuda.synchronize()
         dense_us = d0.elapsed_time(d1) * 1000 / 5
         N = int(cache.seq_lens.max().item())
-        by = bench.step_bytes(U, G, D, -(-N // S), kp, S, 2, 4, N)
+        by = bench.step_bytes(U, G, D, -(-N // S), kp, S, 2, 2, N)  # e = 2
         step_total = by["append"] + by["score"] + by["topk"] + by["attend"]
         sparse_us = brk["score"] + brk["select_attend"]
         print(json.dumps({
@@ -145,7 +147,7 @@ def main():
             "ctx": ctx, "k_pages": kp, "units": U,
             "us_per_step": us, "tokens_per_s": B / (us * 1e-6),
             "step_bytes": step_total, "step_frac_of_hbm": step_total / (us * 1e-6) / 1e9 / peak,
-            "breakdown_us": brk, "fused_select_attend": fused,
+            "breakdown_us": brk, "fused_select_attend": fused, "scoring": "bounded" if bounded else "exact",
             "score_frac_of_hbm": by["score"] / (brk["score"] * 1e-6) / 1e9 / peak,
             "dense_us": dense_us, "x_over_dense": dense_us / sparse_us,
             "prefill_ms": pre_ms, "prefill_GBs": pre_bytes / (pre_ms * 1e-3) / 1e9,
