@@ -36,7 +36,8 @@ struct SelAttnParams {
     float *out, *lse, *ws;
     int32_t *tickets;
     int q_dtype, U, G, Pmax, k, nchunk, nstage;
-    int region;  // bytes of the shared region (multiple of 1024)
+    int region;     // bytes of the shared region (multiple of 1024)
+    int region_lo;  // bounded mode: start of the selection tail's scratch (>= the stage rings)
     int prof;    // record phase timestamps into g_sa_prof
     float scale;
     // bounded mode (keys = lower keys of pt_score_bounded's intervals): the upper keys, and
@@ -113,12 +114,6 @@ __device__ __forceinline__ float sa_exact_score(const float *row, const float *s
 __host__ __device__ __forceinline__ size_t sa_keys_bytes(int Pmax) {
     return (size_t)((Pmax + 8) / 8) * 16;
 }
-// bounded-mode scratch after the exact-mode selection scratch: upper keys, the query rows
-// widened to f32 [D][8], the resolve list + its counter, the staged f32 means [rcap][D + 4]
-__host__ __device__ __forceinline__ size_t sa_bnd_bytes(int Pmax, int D, int rcap) {
-    return sa_keys_bytes(Pmax) + (size_t)D * 32 + 32 + (size_t)rcap * 8 + 16 + (size_t)rcap * (D + 4) * 4 + 16 +
-           (size_t)kCandMax * 2;
-}
 
 // NT threads run the selection (NT / 32 warps); the first kSAWarps warps stream the pages
 template <int D, int MT, int NT, bool BND>
@@ -183,19 +178,24 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
             qb[ks][1] = b1;
         }
     }
-    // bounded mode scratch (after the exact-mode selection scratch): the upper keys, the
-    // query rows widened to f32 [D][8], lam ||q||, the resolve list / stds / counter / rows
+    // bounded mode scratch.  Lower part [0, region_lo): the phase-1 arrays (keys, bins, tile
+    // maxima, upper keys, candidates' upper keys) -- dead once the candidate bracket is known,
+    // then the stage rings; upper part [region_lo, region): what the selection tail keeps using
+    // while the rings stream (query rows as f32 [D][8], lam ||q||, resolve counter, mbarrier,
+    // candidate flags, resolve list / stds / staged f32 rows)
     const size_t sel_end = sa_keys_bytes(p.Pmax) + kSelectBins * 4 + (size_t)(p.Pmax / 32) * 2;
     uint16_t *skhi = reinterpret_cast<uint16_t *>(smem + ((sel_end + 15) & ~(size_t)15));
-    float *sq = reinterpret_cast<float *>(reinterpret_cast<char *>(skhi) + sa_keys_bytes(p.Pmax));
+    uint16_t *candhi = reinterpret_cast<uint16_t *>(reinterpret_cast<char *>(skhi) + sa_keys_bytes(p.Pmax));
+    char *up = smem + p.region_lo;
+    float *sq = reinterpret_cast<float *>(up);
     float *sln = sq + D * 8;  // fl(lam * ||q_g||), 8
-    int *rlist = reinterpret_cast<int *>(sln + 8);
+    int *rcnt = reinterpret_cast<int *>(sln + 8);
+    uint64_t *rbar = reinterpret_cast<uint64_t *>(rcnt + 4);
+    uint8_t *cflag = reinterpret_cast<uint8_t *>(rbar + 2);
+    int *rlist = reinterpret_cast<int *>(cflag + kCandMax);
     float *rstd = reinterpret_cast<float *>(rlist + p.rcap);
-    int *rcnt = reinterpret_cast<int *>(rstd + p.rcap);
-    float *rstage = reinterpret_cast<float *>(rcnt + 4);
-    // after rstage [rcap][RS] and the resolve mbarrier (16 bytes): the candidates' upper keys
-    uint16_t *candhi = reinterpret_cast<uint16_t *>(reinterpret_cast<char *>(rstage) +
-                                                    (size_t)p.rcap * (D + 4) * 4 + 16);
+    float *rstage = reinterpret_cast<float *>(rstd + p.rcap);
+    __shared__ int sdefer[8];  // deferred selection: flag, C, L, A, B, below, n_sure
     if constexpr (BND) {  // q is not written by the scorer: widened before the PDL wait
         for (int i = threadIdx.x; i < D * 8; i += NT) {
             const int d = i >> 3, g = i & 7;
@@ -207,6 +207,7 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
             }
             sq[i] = x;
         }
+        if (threadIdx.x == 0) sdefer[0] = 0;
     }
     pdl_wait();
     if (prof) g_sa_prof[cta * kSAProfN + 1] = gtimer();
@@ -266,7 +267,6 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
     // fl(acc + .), + fl(fl(lam ||q||) * std), strict-> max over heads) of listed pages: rows of
     // the mirror's row-major f32 means by one bulk copy each (one mbarrier phase per round).
     constexpr int RS = D + 4;  // staged row stride (floats): conflict-free float4 reads
-    uint64_t *rbar = reinterpret_cast<uint64_t *>(rstage + (size_t)p.rcap * RS);
     int rphase = 0;
     if constexpr (BND) {
         if (threadIdx.x == 0) {
@@ -396,13 +396,190 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
             if (n <= p.rcap) break;
         }
     };
+    // (c) deferred selection tail on warps 4..7 (named barrier 1, NT / 2 threads), while warps
+    // 0..3 stream the certainly selected pages: resolve the bracket candidates (cflag bit 2),
+    // the threshold = the k-th largest candidate key, the ordered compaction with the
+    // reference's tie rule (select.py:87-115) -- outputs in logical order, and the selected
+    // pages not streamed yet (cflag bit 1 clear) appended to ids[n_sure ..] in logical order --
+    // then n_sel / kth / kplus1
+    auto bounded_tail = [&](int n_sure) {
+        constexpr int NT2 = NT / 2;
+        const int t = (int)threadIdx.x - NT2, w2 = t >> 5;
+        auto sync2 = [] { asm volatile("bar.sync 1, %0;" ::"n"(NT / 2) : "memory"); };
+        auto sum2 = [&](int v, int slot) -> int {  // sum over the NT2 tail threads
+            v = __reduce_add_sync(0xffffffffu, v);
+            if (lane == 0) csh.red[slot][w2][0] = (uint32_t)v;
+            sync2();
+            int s2 = 0;
+#pragma unroll
+            for (int w = 0; w < NT2 / 32; w++) s2 += (int)csh.red[slot][w][0];
+            sync2();
+            return s2;
+        };
+        auto max2 = [&](int v) -> int {
+            v = __reduce_max_sync(0xffffffffu, v);
+            if (lane == 0) csh.red[1][w2][1] = (uint32_t)v;
+            sync2();
+            int m = -1;
+#pragma unroll
+            for (int w = 0; w < NT2 / 32; w++) m = max(m, (int)csh.red[1][w][1]);
+            sync2();
+            return m;
+        };
+        // exclusive scan of (a, b) over the tail threads in thread order
+        auto exscan2 = [&](int a, int b, int &ea, int &eb, int &ta, int &tb) {
+            int ia = a, ib = b;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int xa = __shfl_up_sync(0xffffffffu, ia, o);
+                const int xb = __shfl_up_sync(0xffffffffu, ib, o);
+                if (lane >= o) { ia += xa; ib += xb; }
+            }
+            if (lane == 31) { csh.red[0][w2][0] = (uint32_t)ia; csh.red[0][w2][1] = (uint32_t)ib; }
+            sync2();
+            ea = ia - a; eb = ib - b; ta = 0; tb = 0;
+#pragma unroll
+            for (int w = 0; w < NT2 / 32; w++) {
+                const int wa = (int)csh.red[0][w][0], wb = (int)csh.red[0][w][1];
+                if (w < w2) { ea += wa; eb += wb; }
+                ta += wa; tb += wb;
+            }
+            sync2();
+        };
+        const int C = sdefer[1], L = sdefer[2];
+        const bool tprof = p.prof && t == 0 && cta < kSAProfCtas;
+        if (tprof) g_sa_prof[cta * kSAProfN + 10] = gtimer();
+        // (1) exact keys of the bracket candidates, in rounds of rcap
+        for (;;) {
+            if (t == 0) *rcnt = 0;
+            sync2();
+            for (int i0 = 0; i0 < C; i0 += NT2) {
+                const int i = i0 + t;
+                list_append((i < C && (cflag[i] & 2)) ? 1u : 0u, i);
+            }
+            sync2();
+            const int n = *rcnt, nr = n < p.rcap ? n : p.rcap;
+            if (tprof) g_sa_prof[cta * kSAProfN + 11] = gtimer();
+            if (t == 0 && nr) mbar_arrive_expect_tx(rbar, (uint32_t)(nr * D * 4));
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            sync2();
+            for (int i = t; i < nr; i += NT2) {
+                const int pg = (int)(csh.cand[rlist[i]] & 0xFFFFu);
+                bulk_g2s(rstage + i * RS, m32 + (int64_t)pg * D, D * 4, rbar);
+                sa_cp_async4(rstd + i, p.stds + u * (int64_t)p.Pmax + pg);
+            }
+            sa_cp_async_wait_all();
+            if (nr) mbar_wait(rbar, (uint32_t)(rphase & 1));
+            rphase += nr ? 1 : 0;
+            sync2();
+            if (tprof) g_sa_prof[cta * kSAProfN + 12] = gtimer();
+            for (int i = t; i < nr; i += NT2) {
+                const int ci = rlist[i];
+                const float best = G <= 4 ? sa_exact_score<D, 4>(rstage + i * RS, sq, sln, rstd[i], G)
+                                          : sa_exact_score<D, 8>(rstage + i * RS, sq, sln, rstd[i], G);
+                const uint32_t key = encode_ordered(f32_to_bf16_rne(best));
+                csh.cand[ci] = (key << 16) | (csh.cand[ci] & 0xFFFFu);
+                cflag[ci] = (uint8_t)(cflag[ci] & 1);
+            }
+            sync2();
+            if (tprof) g_sa_prof[cta * kSAProfN + 13] = gtimer();
+            if (n <= nr) break;
+        }
+        // (2) threshold: the k-th largest candidate key (every key that can reach it is exact)
+        int mk = -1;
+        for (int i = t; i < C; i += NT2) mk = max(mk, (int)(csh.cand[i] >> 16));
+        const int mx = max2(mk);
+        int thr;
+        if (mx - L < 64) {
+            if (t < 64) csh.bins[t] = 0;
+            sync2();
+            for (int i = t; i < C; i += NT2) {
+                const int key = (int)(csh.cand[i] >> 16);
+                if (key >= L) atomicAdd(&csh.bins[mx - key], 1);
+            }
+            sync2();
+            if (w2 == 0) {
+                const int c0 = csh.bins[2 * lane], c1 = csh.bins[2 * lane + 1];
+                int incl = c0 + c1;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                const int pre = incl - c0 - c1;
+                int b = 999;
+                if (pre < k && pre + c0 >= k) b = 2 * lane;
+                else if (pre + c0 < k && incl >= k) b = 2 * lane + 1;
+                b = __reduce_min_sync(0xffffffffu, b);
+                if (lane == 0) csh.thr = mx - b;
+            }
+            sync2();
+            thr = csh.thr;
+            sync2();
+        } else {
+            int lo = L, hi = mx + 1;
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                int cnt = 0;
+                for (int i = t; i < C; i += NT2) cnt += (int)(csh.cand[i] >> 16) >= mid;
+                if (sum2(cnt, 0) >= k) lo = mid; else hi = mid;
+            }
+            thr = lo;
+        }
+        // (3) ordered compaction over the (logically ordered) candidates
+        const int cs = (C + NT2 - 1) / NT2;
+        const int i0 = min(t * cs, C), i1 = min(i0 + cs, C);
+        int g = 0, q = 0, bl = -1;
+        for (int i = i0; i < i1; i++) {
+            const int key = (int)(csh.cand[i] >> 16);
+            g += key > thr;
+            q += key == thr;
+            if (key < thr) bl = max(bl, key);
+        }
+        int gb, qb2, gt_tot, eq_tot;
+        exscan2(g, q, gb, qb2, gt_tot, eq_tot);
+        const int below = max(max2(bl), sdefer[5]);
+        const int budget = k - gt_tot;  // in [1, eq_tot]
+        int r = 0;
+        {
+            int seen = qb2;
+            for (int i = i0; i < i1; i++) {
+                const int key = (int)(csh.cand[i] >> 16);
+                bool sel = key > thr;
+                if (key == thr) { sel = seen < budget; seen++; }
+                if (sel && !(cflag[i] & 1)) r++;
+            }
+        }
+        int rb, dummy, rtot, dtot;
+        exscan2(r, 0, rb, dummy, rtot, dtot);
+        int pos = gb + min(qb2, budget), seen = qb2, rpos = n_sure + rb;
+        for (int i = i0; i < i1; i++) {
+            const uint32_t cv = csh.cand[i];
+            const int key = (int)(cv >> 16), idx = (int)(cv & 0xFFFFu);
+            bool sel = key > thr;
+            if (key == thr) { sel = seen < budget; seen++; }
+            if (sel) {
+                const int pid = __ldg(p.page_table + u * p.Pmax + idx);
+                if (o_sel) o_sel[pos] = pid;
+                if (o_log) o_log[pos] = idx;
+                pos++;
+                if (!(cflag[i] & 1)) ids[rpos++] = pid;
+            }
+        }
+        if (t == 0) {
+            *o_n = k;
+            *o_kth = thr;
+            *o_kp1 = (eq_tot > budget) ? thr : below;
+        }
+        __threadfence_block();
+    };
     bool selected;
     if (prof) g_sa_prof[cta * kSAProfN + 14] = gtimer();
     if constexpr (BND) {
         selected = select_cand<NT>(skeys, tm_stage ? stm : nullptr, P, k, p.page_table + u * p.Pmax, o_sel,
                                    o_log, o_n, o_kth, o_kp1, csh, ids, true,
                                    prof ? &g_sa_prof[cta * kSAProfN + 6] : nullptr, true, k + 1, resolve,
-                                   skhi, candhi, resolve_cands);
+                                   skhi, candhi, resolve_cands, p.nchunk == 1 ? sdefer : nullptr);
         // take-all (P <= k) and P > 65536 return before resolving: resolve every page
         if (!selected && (P <= k || P > 65536)) resolve(-1);
     } else {
@@ -410,12 +587,11 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
                                    o_log, o_n, o_kth, o_kp1, csh, ids, true,
                                    prof ? &g_sa_prof[cta * kSAProfN + 6] : nullptr, true);
     }
+    const bool deferred = BND && sdefer[0];
     if (!selected)  // take-all, or massive ties at the lower bound
         select_block<NT>(skeys, bins, P, k, p.page_table + u * p.Pmax, o_sel, o_log, o_n,
                                  o_kth, o_kp1, sh, ids, true);
     if constexpr (BND) {  // query fragments from the widened rows (bf16 values: exact)
-        // the resolve mbarrier's memory becomes part of the stage rings
-        if (threadIdx.x == 0) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(rbar)) : "memory");
         const int gq = lane >> 2;
 #pragma unroll
         for (int ks = 0; ks < KS; ks++) {
@@ -425,8 +601,49 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
             qb[ks][1] = gq < G ? pack_bf16(sq[(d0 + 8) * 8 + g], sq[(d0 + 9) * 8 + g]) : 0u;
         }
     }
-    __syncthreads();  // ids complete; the select scratch is dead -> stage rings
+    int n_sure = 0;
+    if (deferred) {
+        // ---- the split: pages with lower key > B are selected whatever their exact key; they
+        // go to ids[0 .. n_sure) in logical order (physical ids) and start streaming now, while
+        // warps 4-7 resolve the bracket and finish the selection (bounded_tail) ----
+        const int C = sdefer[1], B = sdefer[4], A = sdefer[3];
+        const int cs = (C + NT - 1) / NT;
+        const int i0 = min((int)threadIdx.x * cs, C), i1 = min(i0 + cs, C);
+        int cnt = 0;
+        for (int i = i0; i < i1; i++) {
+            const int lo = (int)(csh.cand[i] >> 16), hi = candhi[i];
+            const bool sure = lo > B;
+            const bool res = lo != hi && hi >= A && lo <= B;
+            cflag[i] = (uint8_t)((sure ? 1 : 0) | (res ? 2 : 0));
+            cnt += sure;
+        }
+        int inc = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (lane == 31) csh.red[0][warp][0] = (uint32_t)inc;
+        __syncthreads();
+        int pos = inc - cnt, tot = 0;
+#pragma unroll
+        for (int w = 0; w < NT / 32; w++) {
+            const int t = (int)csh.red[0][w][0];
+            if (w < warp) pos += t;
+            tot += t;
+        }
+        for (int i = i0; i < i1; i++)
+            if (cflag[i] & 1) ids[pos++] = __ldg(p.page_table + u * p.Pmax + (int)(csh.cand[i] & 0xFFFFu));
+        n_sure = tot;
+    }
+    __syncthreads();  // ids complete (deferred: the certain prefix); the phase-1 scratch is dead
     if (prof) g_sa_prof[cta * kSAProfN + 2] = gtimer();
+
+    if (deferred && warp >= NW) {
+        // ---- selection tail on warps 4..7 (named barrier 1, 128 threads) ----
+        bounded_tail(n_sure);
+        asm volatile("bar.arrive 2, %0;" ::"n"(NT) : "memory");  // the remainder is in ids[]
+    }
 
     // ---- this chunk's slice of the selection ----
     const int per = (ns + p.nchunk - 1) / p.nchunk;
@@ -437,6 +654,15 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
     char *my_stages = smem + (size_t)warp * nstage * STAGE_BYTES;
     const int rem = last - first - warp;
     const int my_count = (warp < NW && rem > 0) ? (rem + NW - 1) / NW : 0;
+    // deferred: entries >= n_sure exist only after the tail's bar.arrive (each streaming warp
+    // waits once, on its first such entry, or at the end)
+    bool have_all = !deferred;
+    auto ensure = [&](int i) {
+        if (!have_all && first + warp + i * NW >= n_sure) {
+            asm volatile("bar.sync 2, %0;" ::"n"(NT) : "memory");
+            have_all = true;
+        }
+    };
     auto issue = [&](int i) {
         const int pid = ids[first + warp + i * NW];
         const int st = i % nstage;
@@ -448,10 +674,15 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
             tma_load_2d(ks + PAGE_BYTES + b * S * 128, &tmv, b * 64, pid * S, &bars[st]);
         }
     };
-    if (lane == 0 && warp < NW) {
-        for (int i = 0; i < nstage; i++) mbar_init(&bars[i], 1);
-        fence_mbar_init();
-        for (int i = 0; i < min(nstage, my_count); i++) issue(i);
+    if (warp < NW) {
+        if (lane == 0) {
+            for (int i = 0; i < nstage; i++) mbar_init(&bars[i], 1);
+            fence_mbar_init();
+        }
+        for (int i = 0; i < min(nstage, my_count); i++) {
+            ensure(i);
+            if (lane == 0) issue(i);
+        }
     }
     __syncwarp();
 
@@ -469,8 +700,12 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
         const uint32_t kbase = smem_u32(my_stages + (size_t)st * STAGE_BYTES);
         mma_page<D, MT>(kbase, kbase + PAGE_BYTES, rows, 0.f, qscale, qb, acc, m_run, l_run, lane);
         __syncwarp();
-        if (lane == 0 && i + nstage < my_count) issue(i + nstage);
+        if (i + nstage < my_count) {
+            ensure(i + nstage);
+            if (lane == 0) issue(i + nstage);
+        }
     }
+    if (warp < NW && !have_all) asm volatile("bar.sync 2, %0;" ::"n"(NT) : "memory");
 
     // ---- per-warp partials to shared memory, then the CTA / chunk merge (attend.cuh) ----
     if (prof) g_sa_prof[cta * kSAProfN + 4] = gtimer();
@@ -691,8 +926,10 @@ extern "C" int pt_select_attend(const uint16_t *keys, const uint16_t *tile_max,
         return PT_ERR_UNSUPPORTED;
     const bool bnd = keys_hi != nullptr;
     if (bnd && (!mirror || !stds || !lamnorm || !tile_max)) return PT_ERR_INVALID;
+    // bounded mode streams while its selection tail runs (early streaming): a 2-deep ring
+    // (measured no slower than 3 at cfg3: 176 vs 180 us/step) below the tail's scratch
     const int stage = 2 * S * D * 2;
-    int nstage = sa_env_int("PT_SA_NSTAGE", 3);
+    int nstage = sa_env_int("PT_SA_NSTAGE", bnd ? 2 : 3);
     if (nstage < 1) nstage = 1;
     // chunks per unit: fill the resident CTA slots (2 per SM) without a second wave, and
     // keep at least one page per warp in a chunk
@@ -706,17 +943,22 @@ extern "C" int pt_select_attend(const uint16_t *keys, const uint16_t *tile_max,
     }
     if (nchunk > kAttnMaxSplits) nchunk = kAttnMaxSplits;
     const size_t sel_base = sa_keys_bytes(Pmax) + (size_t)kSelectBins * 4 + (size_t)(Pmax / 32) * 2;
-    size_t sel_scratch = sel_base;
+    size_t sel_scratch = sel_base, region_lo = 0;
     int rcap = 0;
     if (bnd) {
-        // pages resolved per round: as many as fit beside the keys in the ring region of a
-        // 2-deep-or-more ring at two CTAs per SM (>= 32), at most 256
-        const size_t base = ((sel_base + 15) & ~(size_t)15) + sa_bnd_bytes(Pmax, D, 0);
-        const size_t budget = (size_t)kSAWarps * 3 * stage;
-        rcap = budget > base ? (int)((budget - base) / ((size_t)(D + 4) * 4 + 8)) : 0;
+        // lower part: the phase-1 arrays, then the stage rings; upper part: the selection
+        // tail's scratch, with as many resolve rows per round as keep the dynamic shared
+        // memory at <= 100 KB (two CTAs per SM beside ~9 KB of static selection state)
+        const size_t lower = ((sel_base + 15) & ~(size_t)15) + sa_keys_bytes(Pmax) + (size_t)kCandMax * 2;
+        const size_t rings = (size_t)kSAWarps * nstage * stage;
+        region_lo = ((lower > rings ? lower : rings) + 1023) & ~(size_t)1023;
+        const size_t fixed = (size_t)D * 32 + 32 + 16 + 16 + kCandMax;
+        const size_t tail = (size_t)100 * 1024 - region_lo - fixed - (((size_t)k * 4 + 7) & ~(size_t)7) -
+                            (size_t)kSAWarps * nstage * 8;
+        rcap = (size_t)100 * 1024 > region_lo + fixed ? (int)(tail / ((size_t)(D + 4) * 4 + 8)) : 0;
         rcap = sa_env_int("PT_SA_RCAP", rcap);
         rcap = (rcap < 32 ? 32 : rcap > 256 ? 256 : rcap) & ~3;
-        sel_scratch = ((sel_base + 15) & ~(size_t)15) + sa_bnd_bytes(Pmax, D, rcap);
+        sel_scratch = region_lo + fixed + (size_t)rcap * ((size_t)(D + 4) * 4 + 8);
     }
     const size_t merge = (size_t)kSAWarps * kMmaGP * (D + 2) * 4;
     auto smem_of = [&](int nst, size_t *region_out) {
@@ -760,7 +1002,8 @@ extern "C" int pt_select_attend(const uint16_t *keys, const uint16_t *tile_max,
     p.q_dtype = q_dtype; p.U = U; p.G = G; p.Pmax = Pmax; p.k = k; p.nchunk = nchunk;
     p.nstage = nstage; p.region = (int)region; p.scale = scale;
     p.prof = sa_env_int("PT_SA_PROF", 0);
-    p.keys_hi = keys_hi; p.rows32 = mirror_view(mirror, U, Pmax, D).rows; p.stds = stds; p.lamnorm = lamnorm; p.rcap = rcap;
+    p.keys_hi = keys_hi; p.rows32 = mirror_view(mirror, U, Pmax, D).rows;
+    p.region_lo = (int)region_lo; p.stds = stds; p.lamnorm = lamnorm; p.rcap = rcap;
     cudaStream_t st = (cudaStream_t)stream;
     // selection threads: 8 warps halve the selection's block-wide passes; 4 of them stream
     const int sel_threads = sa_env_int("PT_SA_SEL_THREADS", 256) == 128 ? 128 : 256;

@@ -390,7 +390,8 @@ __device__ bool select_cand(const uint16_t *__restrict__ skeys, const uint16_t *
                             bool tmax_shared = false, int kL = 0,
                             const Resolve &resolve = Resolve(), const uint16_t *shi = nullptr,
                             uint16_t *candhi = nullptr,
-                            const ResolveCands &resolve_cands = ResolveCands()) {
+                            const ResolveCands &resolve_cands = ResolveCands(),
+                            int *defer = nullptr) {
     constexpr int NWP = NT / 32;
     constexpr int MAXT = 8;  // tile maxima per thread: ceil(P / 32) <= NT * MAXT
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -662,6 +663,16 @@ __device__ bool select_cand(const uint16_t *__restrict__ skeys, const uint16_t *
                 A = kth_bin(false, k + 1);
                 stamp(13);
                 if (tid < 64) sh.bins[tid] = 0;
+            }
+            if (defer) {
+                // the caller finishes the selection itself (attend_fused.cu: the certainly
+                // selected pages -- lower key > B -- stream while 4 warps resolve the bracket)
+                if (tid == 0) {
+                    defer[0] = 1; defer[1] = C; defer[2] = L; defer[3] = A; defer[4] = B;
+                    defer[5] = sh.below;
+                }
+                __syncthreads();
+                return true;
             }
             resolve_cands(C, A, B);
             int m2 = -1;

@@ -6,9 +6,9 @@ interval [klo, khi] of ordered keys that must contain the reference's exact key
 exact key of every page whose interval is not a single key and reaches the cut.  These tests
 check (1) the mirror and its error bound, (2) the intervals contain the exact keys -- on the
 reference workload and on adversarial value ranges, every G and D of the envelope -- and
-(3) the engine's selections, kth / kplus1 and outputs are bit-identical to the exact-key
-path and to the CPU oracle, including take-all, no-tile-maxima, massive ties and
-multi-round resolution.
+(3) the engine's selections, kth / kplus1 are bit-identical to the exact-key path and to the
+CPU oracle (outputs equal up to the f32 merge order), including take-all, no-tile-maxima,
+massive ties, multi-round resolution and the early-streaming split.
 """
 
 from __future__ import annotations
@@ -158,7 +158,13 @@ def _same_step(a, b, q, nsel_check=True):
     ob = (b.out, b.lse, b.sel, b.sel_logical, b.n_sel, b.kth, b.kplus1)
     names = ("out", "lse", "sel", "sel_logical", "n_sel", "kth", "kplus1")
     for name, x, y in zip(names, oa, ob):
-        assert torch.equal(x, y), f"bounded vs exact: {name} differs"
+        if name in ("out", "lse"):
+            # same pages; the bounded kernel streams the certainly selected pages first, so the
+            # online-softmax page order differs -- and with it the running maximum the bf16
+            # probabilities of the PV tensor-core product are rounded against (~2^-9 relative)
+            torch.testing.assert_close(x, y, rtol=2e-3, atol=2e-3)
+        else:
+            assert torch.equal(x, y), f"bounded vs exact: {name} differs"
 
 
 @pytest.mark.parametrize("n,k,G", [
