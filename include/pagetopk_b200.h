@@ -237,6 +237,10 @@ PT_API int pt_select_attend(const uint16_t *keys, const uint16_t *tile_max,
  * PT_SA_PROF=1 in the environment.  n <= 10 * 4096. */
 PT_API int pt_debug_sa_prof(unsigned long long *host, int n);
 
+/* Tuning aid: per-CTA timestamps (entry, after the PDL wait, exit) of the last
+ * pt_score_bounded launch made with PT_SB_PROF=1.  n <= 4 * 2048. */
+PT_API int pt_debug_sb_prof(unsigned long long *host, int n);
+
 /* Tuning aid: per-unit phase timestamps of the last pt_append launch made with PT_APP_PROF=1
  * (8 per unit: entry, after the PDL wait, row loaded, tail page id known, page staged, stats
  * stored, length snapshot seen, exit).  n <= 8 * 8192. */

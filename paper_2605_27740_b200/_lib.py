@@ -65,6 +65,7 @@ _PROTOS = {
                               _vp, _i, _i, _i, _i, _f, _vp, _vp, _vp, _sz, _vp, _vp]),
     "pt_debug_sa_prof": (_i, [_vp, _i]),
     "pt_debug_append_prof": (_i, [_vp, _i]),
+    "pt_debug_sb_prof": (_i, [_vp, _i]),
     "pt_gated_attend_bwd": (_i, [_vp, _i, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i,
                                  _i, _f, _vp, _vp, _vp, _vp, _vp]),
     "pt_gate_bias": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp, _vp]),

@@ -38,7 +38,16 @@ struct BoundedScoreParams {
     uint16_t *keys_lo, *keys_hi;  // [U][Pmax]
     uint16_t *tile_max;           // [U][Pmax/32]: max klo of each tile
     int U, S, Pmax;
+    int prof;  // PT_SB_PROF=1: per-CTA %globaltimer stamps (entry, after the PDL wait, exit)
 };
+
+constexpr int kSBProfCtas = 2048;
+__device__ unsigned long long g_sb_prof[kSBProfCtas * 4];
+__device__ __forceinline__ unsigned long long sb_gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 constexpr int kSBWarps = 4;
 constexpr int kSBMaxUnits = 2048;  // tile prefix over units in shared memory
@@ -74,12 +83,15 @@ __global__ void __launch_bounds__(kSBWarps * 32) k_score_bounded(const BoundedSc
     char *ring = smem + sb_hdr_bytes(U) + (size_t)warp * C::PER_WARP;
     char *uhdrs = ring + NST * C::TILE;
     char *thdrs = uhdrs + C::NHU * C::UHDR;
+    const bool prof = prm.prof && threadIdx.x == 0 && blockIdx.x < kSBProfCtas;
+    if (prof) g_sb_prof[blockIdx.x * 4 + 0] = sb_gtimer();
     if (lane == 0) {
         for (int i = 0; i < NST; i++) mbar_init(&bars[i], 1);
         fence_mbar_init();
     }
     pdl_wait();
     pdl_trigger();
+    if (prof) g_sb_prof[blockIdx.x * 4 + 1] = sb_gtimer();
     {  // tile prefix over units (block scan)
         __shared__ int wsum[kSBWarps];
         int carry = 0;
@@ -240,6 +252,10 @@ __global__ void __launch_bounds__(kSBWarps * 32) k_score_bounded(const BoundedSc
         if (lane == 0) prm.tile_max[(int64_t)cc.u * TPU + cc.t] = (uint16_t)m;
         advance(cc);
     }
+    if (prof) {
+        __syncwarp();
+        g_sb_prof[blockIdx.x * 4 + 2] = sb_gtimer();  // warp 0's last tile done
+    }
 }
 
 template <int G, int D, int NST>
@@ -296,6 +312,13 @@ static int sb_g(const BoundedScoreParams &sp, int G, cudaStream_t st) {
 
 using namespace pt;
 
+// tuning aid: copy the stamps of the last PT_SB_PROF=1 launch (n <= 4 * 2048)
+extern "C" int pt_debug_sb_prof(unsigned long long *host, int n) {
+    if (!host || n < 0 || n > kSBProfCtas * 4) return PT_ERR_INVALID;
+    PT_CUDA_TRY(cudaMemcpyFromSymbol(host, g_sb_prof, (size_t)n * 8));
+    return PT_OK;
+}
+
 extern "C" int pt_score_bounded(const void *q, int q_dtype, const float *lamnorm, const float *qnorm,
                                 const void *mirror, const float *stds, const int32_t *seq_len, int U,
                                 int G, int D, int S, int Pmax, uint16_t *keys_lo, uint16_t *keys_hi,
@@ -309,7 +332,7 @@ extern "C" int pt_score_bounded(const void *q, int q_dtype, const float *lamnorm
     if (U == 0) return PT_OK;
     const MirrorView mv = mirror_view(mirror, U, Pmax, D);
     BoundedScoreParams sp{static_cast<const uint16_t *>(q), lamnorm, qnorm, mv.tiles, stds, mv.err,
-                          seq_len, keys_lo, keys_hi, tile_max, U, S, Pmax};
+                          seq_len, keys_lo, keys_hi, tile_max, U, S, Pmax, sb_env("PT_SB_PROF", 0)};
     cudaStream_t st = (cudaStream_t)stream;
     return D == 128 ? sb_g<128>(sp, G, st) : sb_g<64>(sp, G, st);
 }

@@ -11,12 +11,14 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def eng_nchunk(U):
-    """chunks per unit of the fused kernel's grid (attend_fused.cu: 2 CTAs per SM)"""
+def eng_nchunk(U, k):
+    """chunks per unit of the fused kernel's grid (attend_fused.cu: 2 CTAs per SM, at least
+    4 pages per streaming warp per chunk)"""
     import torch
 
     sms = torch.cuda.get_device_properties(0).multi_processor_count
-    return max(1, (sms * 2) // U)
+    n = max(1, (sms * 2) // U)
+    return min(n, (k + 15) // 16)
 
 
 def main():
@@ -80,7 +82,7 @@ def main():
     eng.select_attend(q)
     torch.cuda.synchronize()
     os.environ.pop("PT_SA_PROF")
-    nch = int(eng_nchunk(U))
+    nch = int(eng_nchunk(U, a.budget // S))
     n = U * nch * 20
     buf = np.zeros(n, dtype=np.uint64)
     _lib.check(_lib.load().pt_debug_sa_prof(buf.ctypes.data, n))
