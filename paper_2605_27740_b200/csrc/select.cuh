@@ -365,6 +365,7 @@ struct SelectCandShared {
     uint32_t red[2][NT / 32][2];
     int bins[64];
     int below, thr, gt, eq;
+    int hist[256];  // radix rounds (no tile-maximum bound)
     uint32_t cand[kCandMax];
 };
 
@@ -744,8 +745,56 @@ __device__ bool select_cand(const uint16_t *__restrict__ skeys, const uint16_t *
             __syncthreads();
         }
     } else {
-        // ---- bisection over all keys: thr = max t with #(keys >= t) >= k ----
+        // ---- thr = max t with #(keys >= t) >= k ----
         int lo = L >= 0 ? L : mn, hi = mx + 1;
+        if (L < 0 && hi - lo > 64) {
+            // the full key range: two 8-bit radix rounds (select.py:87-115's scheme) instead of
+            // ~16 bisection passes -- the high byte's bucket holding the k-th largest key, then
+            // the low byte within it (shared-memory histograms, one warp scans 256 bins)
+            auto radix_round = [&](int shift, int hi_byte, int rank) -> int {
+                for (int i = tid; i < 256; i += NT) sh.hist[i] = 0;
+                __syncthreads();
+                for (int v = tid; v < nvec; v += NT) {
+                    uint32_t w[4];
+                    words(s4[v], w);
+#pragma unroll
+                    for (int e = 0; e < 8; e++) {
+                        const int key = (e & 1) ? (int)(w[e >> 1] >> 16) : (int)(w[e >> 1] & 0xFFFFu);
+                        if (v * 8 + e < P && (shift == 8 || (key >> 8) == hi_byte))
+                            atomicAdd(&sh.hist[(key >> shift) & 0xFF], 1);
+                    }
+                }
+                __syncthreads();
+                if (warp == 0) {  // lane l: bins 255 - 8 l .. 248 - 8 l (descending key order)
+                    int c8[8], sum = 0;
+#pragma unroll
+                    for (int j = 0; j < 8; j++) { c8[j] = sh.hist[255 - 8 * lane - j]; sum += c8[j]; }
+                    int incl = sum;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += y;
+                    }
+                    int cum = incl - sum, b = -1, before = 0;
+#pragma unroll
+                    for (int j = 0; j < 8; j++) {
+                        if (b < 0 && cum + c8[j] >= rank) { b = 255 - 8 * lane - j; before = cum; }
+                        cum += c8[j];
+                    }
+                    const unsigned hit = __ballot_sync(0xffffffffu, b >= 0);
+                    const int src = __ffs(hit) - 1;
+                    if (lane == src) { sh.thr = b; sh.gt = before; }
+                }
+                __syncthreads();
+                return sh.thr;
+            };
+            const int hb = radix_round(8, 0, k);
+            const int above = sh.gt;  // keys in higher buckets
+            __syncthreads();
+            const int lb = radix_round(0, hb, k - above);
+            lo = (hb << 8) | lb;
+            hi = lo + 1;
+        }
         while (hi - lo > 1) {
             const int mid = (lo + hi) >> 1;
             const uint32_t m16 = (uint32_t)mid * 0x10001u;
