@@ -457,7 +457,7 @@ __device__ bool select_cand(const uint16_t *__restrict__ skeys, const uint16_t *
         tm[i] = (use_tiles && t < ntiles) ? (int)(tmax_shared ? tmax_g[t] : __ldcg(tmax_g + t)) : -1;
     }
     if (tid < 64) sh.bins[tid] = 0;
-    if (tid == 0) sh.below = -1;
+    if (tid == 0) { sh.below = -1; sh.eq = -1; }
     int mx, mn = 0, L = -1;
     if (use_tiles) {
         int m = -1;
@@ -537,7 +537,7 @@ __device__ bool select_cand(const uint16_t *__restrict__ skeys, const uint16_t *
         // key vectors (so thread order is logical order) and one block scan ranks them ----
         constexpr int VPT = 4;
         const uint32_t L16 = (uint32_t)L * 0x10001u;
-        int run = 0, below = -1, par = 0;
+        int run = 0, below = -1, par = 0, mhi = -1;
         for (int v0 = 0; v0 < nvec; v0 += NT * VPT, par ^= 1) {
             const int vt = v0 + tid * VPT;
             uint4 x[VPT], y[VPT];
@@ -605,13 +605,15 @@ __device__ bool select_cand(const uint16_t *__restrict__ skeys, const uint16_t *
                                 if (candhi) candhi[pos] = (uint16_t)kh;
                             }
                             pos++;
+                            mhi = max(mhi, kh);
                         }
                     }
                 }
             }
         }
         below = __reduce_max_sync(0xffffffffu, below);
-        if (lane == 0) atomicMax(&sh.below, below);
+        mhi = __reduce_max_sync(0xffffffffu, mhi);
+        if (lane == 0) { atomicMax(&sh.below, below); atomicMax(&sh.eq, mhi); }  // eq: max upper key
         __syncthreads();
         if (run <= kCandMax) C = run;  // else: too many keys tie at L -- bisection below
     }
@@ -624,45 +626,43 @@ __device__ bool select_cand(const uint16_t *__restrict__ skeys, const uint16_t *
             // key: the others are certainly above the threshold (lower key > B) or certainly
             // below the (k+1)-th key (upper key < A), so their counts, ties and kplus1 are
             // decided either way.
-            int mh = -1;
-            for (int i = tid; i < C; i += NT) mh = max(mh, (int)candhi[i]);
-            const int mxh = block_max(mh);
+            const int mxh = sh.eq;  // the largest candidate upper key (candidate pass)
             stamp(11);
             int A = L, B = mxh;
             if (mxh - L < 64) {
-                auto kth_bin = [&](bool hi, int rank) -> int {
-                    if (tid < 64) sh.bins[tid] = 0;
-                    __syncthreads();
-                    for (int i = tid; i < C; i += NT) {
-                        const int key = hi ? (int)candhi[i] : (int)(sh.cand[i] >> 16);
-                        if (key >= L) atomicAdd(&sh.bins[mxh - key], 1);
-                    }
-                    __syncthreads();
-                    int b = 63;
-                    if (warp == 0) {
-                        const int c0 = sh.bins[2 * lane], c1 = sh.bins[2 * lane + 1];
-                        int incl = c0 + c1;
+                // both ranks from one pass: upper keys -> bins (B = k-th largest), lower keys
+                // reaching L -> hist (A = (k+1)-th largest); warps 0 and 1 scan in parallel
+                if (tid < 64) { sh.bins[tid] = 0; sh.hist[tid] = 0; }
+                __syncthreads();
+                for (int i = tid; i < C; i += NT) {
+                    atomicAdd(&sh.bins[mxh - (int)candhi[i]], 1);
+                    const int lo = (int)(sh.cand[i] >> 16);
+                    if (lo >= L) atomicAdd(&sh.hist[mxh - lo], 1);
+                }
+                __syncthreads();
+                if (warp < 2) {
+                    const int *hb = warp == 0 ? sh.bins : sh.hist;
+                    const int rank = warp == 0 ? k : k + 1;
+                    const int c0 = hb[2 * lane], c1 = hb[2 * lane + 1];
+                    int incl = c0 + c1;
 #pragma unroll
-                        for (int o = 1; o < 32; o <<= 1) {
-                            const int y2 = __shfl_up_sync(0xffffffffu, incl, o);
-                            if (lane >= o) incl += y2;
-                        }
-                        const int pre = incl - c0 - c1;
-                        int bb = 999;
-                        if (pre < rank && pre + c0 >= rank) bb = 2 * lane;
-                        else if (pre + c0 < rank && incl >= rank) bb = 2 * lane + 1;
-                        bb = __reduce_min_sync(0xffffffffu, bb);
-                        if (lane == 0) sh.thr = bb < 999 ? bb : 63;
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int y2 = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += y2;
                     }
-                    __syncthreads();
-                    b = sh.thr;
-                    __syncthreads();
-                    return mxh - b;
-                };
-                B = kth_bin(true, k);
+                    const int pre = incl - c0 - c1;
+                    int bb = 999;
+                    if (pre < rank && pre + c0 >= rank) bb = 2 * lane;
+                    else if (pre + c0 < rank && incl >= rank) bb = 2 * lane + 1;
+                    bb = __reduce_min_sync(0xffffffffu, bb);
+                    if (lane == 0) sh.red[1][warp][0] = (uint32_t)(bb < 999 ? bb : 63);
+                }
+                __syncthreads();
+                B = mxh - (int)sh.red[1][0][0];
+                A = mxh - (int)sh.red[1][1][0];
                 stamp(12);
-                A = kth_bin(false, k + 1);
                 stamp(13);
+                __syncthreads();
                 if (tid < 64) sh.bins[tid] = 0;
             }
             if (defer) {
