@@ -10,6 +10,8 @@ timeout 900 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1; echo
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke exit $?" >> $OUT/smoke.log
 timeout 600 python bench.py ${BENCH_ARGS:-} > $OUT/bench.json 2> $OUT/bench.err
 timeout 900 python bench.py --impl reference > $OUT/bench_ref.json 2> $OUT/bench_ref.err
+timeout 600 python tools/probe_step.py > $OUT/step_timeline.json 2>&1
+[ -z "${SKIP_SWEEP:-}" ] && timeout 1200 python tools/sweep.py --quick > $OUT/sweep.jsonl 2> $OUT/sweep.err
 if [ -z "${SKIP_NCU:-}" ]; then
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:^k_ -c 400 --csv \
     --log-file $OUT/launches.csv python bench.py --profile --steps 20 --warmup 3 > $OUT/launches.log 2>&1
