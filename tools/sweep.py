@@ -23,6 +23,8 @@ sys.path.insert(0, ROOT)
 def configs(quick: bool):
     out = [
         # name, batch, q_heads, kv_heads, head_dim, page, ctx, budget tokens
+        ("cfg1 f32 8q/8kv b1 4K k32pages", 1, 8, 8, 128, 16, 4096, 512),
+        ("cfg1 f32 8q/1kv b1 4K k32pages", 1, 8, 1, 128, 16, 4096, 512),
         ("cfg2 llama-8b b1 32K k2048", 1, 32, 8, 128, 16, 32768, 2048),
         ("cfg3 llama-8b b32 128K k2048", 32, 32, 8, 128, 16, 131072, 2048),
         ("cfg4 speech b64 60K d64 p32 k512", 64, 16, 16, 64, 32, 60000, 512),
@@ -67,16 +69,18 @@ def main():
         spare = 64 * 4 + 64
         P_cap = -(-(ctx + spare) // S)
         layout = pt.CacheLayout(num_kv_heads=Hkv, head_dim=D, page_size=S, max_pages=U * P_cap)
-        cache = pt.PagedKvCache(layout, batch=B, dtype=torch.bfloat16, stats_dtype=torch.float32,
-                                max_pages_per_head=P_cap, device=dev, mirror=not a.no_mirror)
+        kvdt = torch.float32 if name.startswith("cfg1") else torch.bfloat16  # cfg1: the f32 path
+        cache = pt.PagedKvCache(layout, batch=B, dtype=kvdt, stats_dtype=torch.float32,
+                                max_pages_per_head=P_cap, device=dev,
+                                mirror=(not a.no_mirror) and kvdt == torch.bfloat16)
         g = torch.Generator(device=dev)
         g.manual_seed(1234)
         chunk = max(1, min(ctx, (1 << 27) // (U * D)))  # <= 256 MB of staging per tensor
         done, pre_ms = 0, 0.0
         while done < ctx:
             n = min(chunk, ctx - done)
-            kk = torch.randn(U, n, D, generator=g, device=dev).to(torch.bfloat16)
-            vv = torch.randn(U, n, D, generator=g, device=dev).to(torch.bfloat16)
+            kk = torch.randn(U, n, D, generator=g, device=dev).to(kvdt)
+            vv = torch.randn(U, n, D, generator=g, device=dev).to(kvdt)
             e0, e1 = ev(), ev()
             e0.record(stream)
             cache.extend_units(kk, vv)
@@ -89,9 +93,9 @@ def main():
         # prefill bytes: staging K,V read + pool K,V written + stats written
         pre_bytes = U * (4 * ctx * D * 2 + P * (D * 4 + 4))
         eng = pt.DecodeEngine(cache, G, kp)
-        q = torch.randn(U * G, D, generator=g, device=dev).to(torch.bfloat16)
-        kn = torch.randn(U, D, generator=g, device=dev).to(torch.bfloat16)
-        vn = torch.randn(U, D, generator=g, device=dev).to(torch.bfloat16)
+        q = torch.randn(U * G, D, generator=g, device=dev).to(kvdt)
+        kn = torch.randn(U, D, generator=g, device=dev).to(kvdt)
+        vn = torch.randn(U, D, generator=g, device=dev).to(kvdt)
         for _ in range(3):
             eng.step(q, kn, vn)
         torch.cuda.synchronize()
@@ -139,7 +143,8 @@ def main():
         torch.cuda.synchronize()
         dense_us = d0.elapsed_time(d1) * 1000 / 5
         N = int(cache.seq_lens.max().item())
-        by = bench.step_bytes(U, G, D, -(-N // S), kp, S, 2, 2, N)  # e = 2
+        e = 4 if kvdt == torch.float32 else 2
+        by = bench.step_bytes(U, G, D, -(-N // S), kp, S, e, e, N)  # e = KV element
         step_total = by["append"] + by["score"] + by["topk"] + by["attend"]
         sparse_us = brk["score"] + brk["select_attend"]
         print(json.dumps({
