@@ -111,6 +111,42 @@ __device__ __forceinline__ float sa_exact_score(const float *row, const float *s
     return best;
 }
 
+// the same exact score for the warp-per-unit variant: the page's f32 row and the query rows
+// read straight from global memory (one lane per page; a handful of pages per unit)
+template <int D, int GG>
+__device__ __noinline__ float sa_exact_score_global(const float *row, const void *q, int q_dtype,
+                                                    int64_t qrow0, const float *lnp, float sd, int G) {
+    float acc[GG];
+#pragma unroll
+    for (int g = 0; g < GG; g++) acc[g] = 0.f;
+    for (int c = 0; c < D / 4; c++) {
+        const float4 m4 = __ldg(reinterpret_cast<const float4 *>(row) + c);
+        const float mv[4] = {m4.x, m4.y, m4.z, m4.w};
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+#pragma unroll
+            for (int g = 0; g < GG; g++) {
+                if (g < G) {
+                    const int64_t qi = (qrow0 + g) * D + 4 * c + e;
+                    const float qv = q_dtype == PT_BF16
+                                         ? bf16_bits_to_f32(__ldg(static_cast<const uint16_t *>(q) + qi))
+                                         : __ldg(static_cast<const float *>(q) + qi);
+                    acc[g] = __fadd_rn(acc[g], __fmul_rn(qv, mv[e]));
+                }
+            }
+        }
+    }
+    float best = -INFINITY;
+#pragma unroll
+    for (int g = 0; g < GG; g++) {
+        if (g < G) {
+            const float a = __fadd_rn(acc[g], __fmul_rn(__ldg(lnp + g), sd));
+            if (a > best) best = a;
+        }
+    }
+    return best;
+}
+
 __host__ __device__ __forceinline__ size_t sa_keys_bytes(int Pmax) {
     return (size_t)((Pmax + 8) / 8) * 16;
 }
@@ -678,6 +714,8 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
         if (lane == 0) {
             for (int i = 0; i < nstage; i++) mbar_init(&bars[i], 1);
             fence_mbar_init();
+            // the rings reuse the selection scratch written through the generic proxy
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
         for (int i = 0; i < min(nstage, my_count); i++) {
             ensure(i);
@@ -748,8 +786,8 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
 // ---------------------------------------------------------------------------
 constexpr int kSWMaxV = 8;  // keys per warp in registers: P <= 32 * 8 * 8 = 2048
 
-template <int D, int MT>
-__global__ void __launch_bounds__(128) k_select_attend_warp(const __grid_constant__ CUtensorMap tmk,
+template <int D, int MT, bool BND>
+__global__ void __launch_bounds__(128, 1) k_select_attend_warp(const __grid_constant__ CUtensorMap tmk,
                                                             const __grid_constant__ CUtensorMap tmv,
                                                             const SelAttnParams p) {
     constexpr int S = 16 * MT;
@@ -800,9 +838,25 @@ __global__ void __launch_bounds__(128) k_select_attend_warp(const __grid_constan
             qb[ks][1] = b1;
         }
     }
-    select_warp<kSWMaxV>(p.keys + u * (int64_t)p.Pmax, P, k, p.page_table + u * p.Pmax,
-                         p.sel + u * (int64_t)k, p.sel_logical ? p.sel_logical + u * (int64_t)k : nullptr,
-                         p.n_sel + u, p.kth + u, p.kplus1 + u, ids);
+    if constexpr (BND) {
+        // bounded keys: the exact key of a bracket page, one lane per page
+        auto exact = [&](int pg) -> int {
+            const float *row = p.rows32 + ((int64_t)u * p.Pmax + pg) * D;
+            const float sd = __ldg(p.stds + u * (int64_t)p.Pmax + pg);
+            const float best = p.G <= 4
+                ? sa_exact_score_global<D, 4>(row, p.q, p.q_dtype, u * p.G, p.lamnorm + u * 8, sd, p.G)
+                : sa_exact_score_global<D, 8>(row, p.q, p.q_dtype, u * p.G, p.lamnorm + u * 8, sd, p.G);
+            return (int)encode_ordered(f32_to_bf16_rne(best));
+        };
+        select_warp<kSWMaxV>(p.keys + u * (int64_t)p.Pmax, P, k, p.page_table + u * p.Pmax,
+                             p.sel + u * (int64_t)k, p.sel_logical ? p.sel_logical + u * (int64_t)k : nullptr,
+                             p.n_sel + u, p.kth + u, p.kplus1 + u, ids, p.keys_hi + u * (int64_t)p.Pmax,
+                             exact, reinterpret_cast<int *>(ring), (int)(nstage * STAGE_BYTES / 4));
+    } else {
+        select_warp<kSWMaxV>(p.keys + u * (int64_t)p.Pmax, P, k, p.page_table + u * p.Pmax,
+                             p.sel + u * (int64_t)k, p.sel_logical ? p.sel_logical + u * (int64_t)k : nullptr,
+                             p.n_sel + u, p.kth + u, p.kplus1 + u, ids);
+    }
     const int ns = P < k ? P : k;
     auto issue = [&](int i) {
         const int pid = ids[i];
@@ -818,6 +872,8 @@ __global__ void __launch_bounds__(128) k_select_attend_warp(const __grid_constan
     if (lane == 0) {
         for (int i = 0; i < nstage; i++) mbar_init(&bars[i], 1);
         fence_mbar_init();
+        // the ring held the bounded selection's generic-proxy scratch: order it before the TMA
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         for (int i = 0; i < min(nstage, ns); i++) issue(i);
     }
     __syncwarp();
@@ -856,17 +912,17 @@ __global__ void __launch_bounds__(128) k_select_attend_warp(const __grid_constan
     }
 }
 
-template <int D, int MT>
+template <int D, int MT, bool BND>
 static int launch_saw(const CUtensorMap &tk, const CUtensorMap &tv, const SelAttnParams &p, int nw,
                       size_t smem, cudaStream_t st) {
     static size_t configured = 0;
     if (smem > configured) {
-        PT_CUDA_TRY(cudaFuncSetAttribute(k_select_attend_warp<D, MT>,
+        PT_CUDA_TRY(cudaFuncSetAttribute(k_select_attend_warp<D, MT, BND>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured = smem;
     }
     dim3 grid((p.U + nw - 1) / nw);
-    PT_CUDA_TRY(pt_launch(k_select_attend_warp<D, MT>, grid, dim3(nw * 32), smem, st, tk, tv, p));
+    PT_CUDA_TRY(pt_launch(k_select_attend_warp<D, MT, BND>, grid, dim3(nw * 32), smem, st, tk, tv, p));
     return PT_OK;
 }
 
@@ -1007,12 +1063,14 @@ extern "C" int pt_select_attend(const uint16_t *keys, const uint16_t *tile_max,
     cudaStream_t st = (cudaStream_t)stream;
     // selection threads: 8 warps halve the selection's block-wide passes; 4 of them stream
     const int sel_threads = sa_env_int("PT_SA_SEL_THREADS", 256) == 128 ? 128 : 256;
-    if (w_per && !bnd) {
+    if (w_per) {
         SelAttnParams pw = p;
         pw.nstage = w_nst;
         pw.region = (int)w_per;
 #define PT_SAW(D_, MT_) \
-        if (D == D_ && S == 16 * MT_) return launch_saw<D_, MT_>(tk, tv, pw, w_nw, w_per * w_nw, st);
+        if (D == D_ && S == 16 * MT_)                                                                 \
+            return bnd ? launch_saw<D_, MT_, true>(tk, tv, pw, w_nw, w_per * w_nw, st)                  \
+                       : launch_saw<D_, MT_, false>(tk, tv, pw, w_nw, w_per * w_nw, st);
         PT_SAW(64, 1) PT_SAW(64, 2) PT_SAW(64, 4)
         PT_SAW(128, 1) PT_SAW(128, 2) PT_SAW(128, 4)
         PT_SAW(256, 1) PT_SAW(256, 2) PT_SAW(256, 4)

@@ -964,11 +964,24 @@ __device__ bool select_cand(const uint16_t *__restrict__ skeys, const uint16_t *
 // reference's rule; logical ids land in `ids` (warp-private shared memory) and are translated
 // to physical ids in one parallel round.  Same outputs as select_block.
 // ---------------------------------------------------------------------------
-template <int MAXV>
+// Bounded mode (pt_score_bounded's key intervals; keys_g = lower keys): hi_g = the upper keys
+// and exact(p) = the exact key of logical page p.  Before selecting, the warp computes the
+// bracket A = the (k+1)-th largest lower key, B = the k-th largest upper key and replaces the
+// lower key of every page whose interval is not one key and meets [A, B] (every uncertain page
+// when P <= k) by its exact key -- the same argument as select_cand's bounded mode: pages
+// above B are selected and pages below A are below the (k+1)-th key whatever their exact keys.
+struct NoExactKey {
+    __device__ int operator()(int) const { return 0; }
+};
+
+template <int MAXV, class ExactKey = NoExactKey>
 __device__ void select_warp(const uint16_t *__restrict__ keys_g, int P, int k,
                             const int32_t *__restrict__ map, int32_t *__restrict__ out,
                             int32_t *__restrict__ out_l, int32_t *__restrict__ n_sel,
-                            int32_t *__restrict__ kth, int32_t *__restrict__ kplus1, int *ids) {
+                            int32_t *__restrict__ kth, int32_t *__restrict__ kplus1, int *ids,
+                            const uint16_t *__restrict__ hi_g = nullptr,
+                            const ExactKey &exact = ExactKey(), int *scratch = nullptr,
+                            int scratch_cap = 0) {
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
     const uint4 *k4 = reinterpret_cast<const uint4 *>(keys_g);
@@ -982,6 +995,107 @@ __device__ void select_warp(const uint16_t *__restrict__ keys_g, int P, int k,
         const uint32_t w = e < 2 ? x.x : e < 4 ? x.y : e < 6 ? x.z : x.w;
         return (e & 1) ? (int)(w >> 16) : (int)(w & 0xFFFFu);
     };
+    int bracket_lo = -1, bracket_hi = -1;  // bounded: the threshold lies in [A, B]
+    if (hi_g) {
+        const uint4 *h4 = reinterpret_cast<const uint4 *>(hi_g);
+        uint4 hv[MAXV];
+#pragma unroll
+        for (int j = 0; j < MAXV; j++) {
+            const int base = (lane + 32 * j) * 8;
+            hv[j] = base < P ? __ldcg(h4 + lane + 32 * j) : make_uint4(0u, 0u, 0u, 0u);
+        }
+        // A = the (k+1)-th largest lower key, B = the k-th largest upper key: one bisection
+        // pass per round counting both arrays against their own midpoints
+        int amn = 0xFFFF, amx = 0, bmn = 0xFFFF, bmx = 0;
+#pragma unroll
+        for (int j = 0; j < MAXV; j++) {
+            const int base = (lane + 32 * j) * 8;
+#pragma unroll
+            for (int e = 0; e < 8; e++)
+                if (base + e < P) {
+                    const int x = keyof(v[j], e), y = keyof(hv[j], e);
+                    amn = min(amn, x); amx = max(amx, x); bmn = min(bmn, y); bmx = max(bmx, y);
+                }
+        }
+        int alo = __reduce_min_sync(0xffffffffu, amn), ahi = __reduce_max_sync(0xffffffffu, amx) + 1;
+        int blo = __reduce_min_sync(0xffffffffu, bmn), bhi = __reduce_max_sync(0xffffffffu, bmx) + 1;
+        if (P > k) {
+            while (ahi - alo > 1 || bhi - blo > 1) {
+                const int am = (alo + ahi) >> 1, bm = (blo + bhi) >> 1;
+                int ca = 0, cb = 0;
+#pragma unroll
+                for (int j = 0; j < MAXV; j++) {
+                    const int base = (lane + 32 * j) * 8;
+#pragma unroll
+                    for (int e = 0; e < 8; e++) {
+                        const bool ok = base + e < P;
+                        ca += ok && keyof(v[j], e) >= am;
+                        cb += ok && keyof(hv[j], e) >= bm;
+                    }
+                }
+                ca = __reduce_add_sync(0xffffffffu, ca);
+                cb = __reduce_add_sync(0xffffffffu, cb);
+                if (ahi - alo > 1) { if (ca >= k + 1) alo = am; else ahi = am; }
+                if (bhi - blo > 1) { if (cb >= k) blo = bm; else bhi = bm; }
+            }
+        }
+        const int A = P > k ? alo : 0, B = P > k ? blo : 0xFFFF;
+        bracket_lo = A;
+        bracket_hi = B;
+        // the bracket pages, compacted (lane-major) into the warp's scratch list in rounds of
+        // scratch_cap, resolved one lane per page, written back into the lower keys
+        uint64_t fl = 0ull;  // bit 8 j + e: page (lane + 32 j) * 8 + e needs its exact key
+#pragma unroll
+        for (int j = 0; j < MAXV; j++) {
+            const int base = (lane + 32 * j) * 8;
+#pragma unroll
+            for (int e = 0; e < 8; e++) {
+                const int lo_k = keyof(v[j], e), hi_k = keyof(hv[j], e);
+                if (base + e < P && lo_k != hi_k && hi_k >= A && lo_k <= B) fl |= 1ull << (8 * j + e);
+            }
+        }
+        const int nf = __popcll(fl);
+        int incl = nf;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int first = incl - nf, total = __shfl_sync(0xffffffffu, incl, 31);
+        for (int r0 = 0; r0 < total; r0 += scratch_cap) {
+            int rk = first;
+            uint64_t f = fl;
+            while (f) {  // list this lane's bracket pages with ranks in [r0, r0 + cap)
+                const int b = __ffsll((long long)f) - 1;
+                f &= f - 1;
+                if (rk >= r0 && rk < r0 + scratch_cap) scratch[rk - r0] = (lane + 32 * (b >> 3)) * 8 + (b & 7);
+                rk++;
+            }
+            __syncwarp();
+            const int nr = min(scratch_cap, total - r0);
+            for (int i = lane; i < nr; i += 32) scratch[i] = exact(scratch[i]);
+            __syncwarp();
+            rk = first;
+            f = fl;
+            while (f) {
+                const int b = __ffsll((long long)f) - 1;
+                f &= f - 1;
+                if (rk >= r0 && rk < r0 + scratch_cap) {
+                    const uint32_t x = (uint32_t)scratch[rk - r0];
+                    const int j = b >> 3, e = b & 7;
+#pragma unroll
+                    for (int jj = 0; jj < MAXV; jj++) {
+                        if (jj != j) continue;
+                        uint32_t w[4] = {v[jj].x, v[jj].y, v[jj].z, v[jj].w};
+                        w[e >> 1] = (e & 1) ? ((w[e >> 1] & 0xFFFFu) | (x << 16)) : ((w[e >> 1] & 0xFFFF0000u) | x);
+                        v[jj] = make_uint4(w[0], w[1], w[2], w[3]);
+                    }
+                }
+                rk++;
+            }
+            __syncwarp();
+        }
+    }
     int mn = 0xFFFF, mx = 0;
 #pragma unroll
     for (int j = 0; j < MAXV; j++) {
@@ -1013,8 +1127,9 @@ __device__ void select_warp(const uint16_t *__restrict__ keys_g, int P, int k,
         }
         return __reduce_add_sync(0xffffffffu, c);
     };
-    // thr = max t with #(keys >= t) >= k
+    // thr = max t with #(keys >= t) >= k (bounded: within the bracket [A, B])
     int lo = mn, hi = mx + 1;
+    if (bracket_lo >= 0) { lo = max(lo, bracket_lo); hi = min(hi, bracket_hi + 1); }
     while (hi - lo > 1) {
         const int mid = (lo + hi) >> 1;
         if (count_ge(mid) >= k) lo = mid; else hi = mid;

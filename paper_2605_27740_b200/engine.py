@@ -121,9 +121,9 @@ class DecodeEngine:
         """Bounded scoring halves the scorer's bytes but adds the resolve step to every
         selecting CTA and needs the CTA-per-unit selection: worth it when the f32-means bytes
         it saves (at ~6.5 TB/s) clearly exceed that (>= 25 us: cfg3 saves ~80 us; cfg2 (one
-        sequence) < 1 us), the tile-maximum bound applies (k < pages / 32) and the
-        warp-per-unit path (thousands of short units, small k) is not the faster selection
-        (profiles/r02/sweep_r02b.jsonl).  PT_BOUNDED=1 forces it (tests, tuning)."""
+        sequence) < 1 us) and -- for the CTA-per-unit selection -- the tile-maximum bound
+        applies (k < pages / 32; profiles/r02/sweep_r02b.jsonl); the warp-per-unit selection
+        (thousands of short units, small k) brackets in registers.  PT_BOUNDED=1 forces it."""
         if os.environ.get("PT_BOUNDED", "") == "1":
             return True
         U, P, D = cache.num_units, cache.Pmax, cache.layout.head_dim
@@ -134,6 +134,9 @@ class DecodeEngine:
         # is resolved: k = ctx/8 at 32K-128K measured 1.4-1.8x slower than exact), and the
         # bounded selection's shared memory keeps two CTAs per SM up to 16384 pages
         tile_bound = P // 32 >= self.k + 1 and P <= 16384
+        # the warp-per-unit path has a bounded variant (bracket by bisection in registers) but
+        # it measured slower than exact scoring (cfg4: 134.2 vs 130.0 us/step; its selection is
+        # issue-bound at ~7 warps per SM): PT_BOUNDED=1 only
         return not warp_path and tile_bound and saved_us >= 25.0
 
     # ------------------------------------------------------------------

@@ -250,3 +250,32 @@ def test_bounded_eager_steps_with_appends_vs_oracle(cuda, oracle):
         np.testing.assert_array_equal(kth, ref["kth"])
         np.testing.assert_array_equal(kp1, ref["kplus1"])
         np.testing.assert_allclose(out.reshape(-1, G, D), ref["out"], rtol=2e-2, atol=2e-2)
+
+
+def test_bounded_warp_per_unit_selection_equals_exact(cuda, oracle):
+    """The warp-per-unit select+attend (>= 4 x SMs units, k <= 64, P <= 2048: the cfg4 shape)
+    in bounded mode: bracket by bisection in registers, bracket pages resolved one lane each --
+    selections bit-identical to the exact path and to the oracle."""
+    pt = _pt()
+    rng = np.random.default_rng(4)
+    U, D, S, n, G, k = 600, 64, 32, 32 * 100 + 7, 1, 16
+    K = rng.standard_normal((U, n, D)).astype(np.float32)
+    V = rng.standard_normal((U, n, D)).astype(np.float32)
+    Pcap = -(-n // S) + 4
+    layout = pt.CacheLayout(num_kv_heads=1, head_dim=D, page_size=S, max_pages=U * Pcap)
+    cache = pt.PagedKvCache(layout, batch=U, dtype=torch.bfloat16, max_pages_per_head=Pcap)
+    cache.extend_units(torch.from_numpy(K), torch.from_numpy(V))
+    del K, V
+    a, b = _engines(cache, G, k)
+    for _ in range(2):
+        q = torch.from_numpy(rng.standard_normal((U * G, D)).astype(np.float32)).cuda().to(torch.bfloat16)
+        _same_step(a, b, q)
+    kpool, vpool, table, seq = readback(cache)
+    means, stds = oracle.build_stats(kpool, table, seq, S)
+    ref = oracle.decode_units(q.to(torch.float32).cpu().numpy().reshape(-1, G, D), kpool, vpool,
+                              table, seq, means, stds, k, 0.5, 1.0 / math.sqrt(D), S)
+    sel, nsel = a.sel.cpu().numpy(), a.n_sel.cpu().numpy()
+    for u in range(U):
+        assert set(sel[u, : nsel[u]].tolist()) == set(ref["sel"][u, : ref["n_sel"][u]].tolist())
+    np.testing.assert_array_equal(a.kth.cpu().numpy(), ref["kth"])
+    np.testing.assert_array_equal(a.kplus1.cpu().numpy(), ref["kplus1"])
