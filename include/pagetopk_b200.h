@@ -164,11 +164,12 @@ PT_API int pt_score_prenorm(const void *q, int q_dtype, const float *lamnorm, co
  * bound of the reference score (the exact key lies in [keys_lo, keys_hi]), and tile_max u16
  * [U][Pmax/32] = the largest keys_lo of each 32-page tile.  pt_select_attend given keys_hi
  * turns these into the exact selection of the f32 reference.  bf16 queries, G <= 8,
- * D in {64, 128}, U <= 2048; PT_ERR_UNSUPPORTED otherwise (use pt_score_prenorm). */
+ * D in {64, 128}, nu <= 2048; PT_ERR_UNSUPPORTED otherwise (use pt_score_prenorm).
+ * Scores units [u0, u0 + nu) of a U-unit cache (every array is the whole cache's). */
 PT_API int pt_score_bounded(const void *q, int q_dtype, const float *lamnorm, const float *qnorm,
                             const void *mirror, const float *stds, const int32_t *seq_len, int U,
-                            int G, int D, int S, int Pmax, uint16_t *keys_lo, uint16_t *keys_hi,
-                            uint16_t *tile_max, void *stream);
+                            int u0, int nu, int G, int D, int S, int Pmax, uint16_t *keys_lo,
+                            uint16_t *keys_hi, uint16_t *tile_max, void *stream);
 
 /* K2+K3 fused: pt_score followed by pt_topk in ONE launch -- the last CTA to finish a unit's
  * pages selects that unit's top-k while other CTAs keep scoring (same outputs as the two
@@ -221,11 +222,13 @@ PT_API int pt_attend(const void *q, int q_dtype, const void *k_pool, const void 
  * Bounded mode (keys_hi non-NULL): keys / keys_hi / tile_max are pt_score_bounded's; the
  * exact key of every page whose interval reaches the cut is recomputed from the mirror's
  * row-major f32 means, stds and lamnorm (pt_lam_norms' [U][8]) -- the outputs equal the
- * exact mode's over the f32 reference keys.  NULL: keys are exact (the other three unused). */
+ * exact mode's over the f32 reference keys.  NULL: keys are exact (the other three unused).
+ * Processes units [u0, u0 + nu) of a U-unit cache (every per-unit array is the whole cache's;
+ * the workspace is used from u0's share on): two disjoint ranges may run concurrently. */
 PT_API int pt_select_attend(const uint16_t *keys, const uint16_t *tile_max,
                             const uint16_t *keys_hi, const void *mirror, const float *stds,
                             const float *lamnorm, const int32_t *seq_len, const int32_t *page_table,
-                            int U, int S, int Pmax, int k, int32_t *sel, int32_t *sel_logical,
+                            int U, int u0, int nu, int S, int Pmax, int k, int32_t *sel, int32_t *sel_logical,
                             int32_t *n_sel, int32_t *kth, int32_t *kplus1, const void *q,
                             int q_dtype, const void *k_pool, const void *v_pool, int kv_dtype,
                             int num_phys_pages, int G, int D, float scale, float *out, float *lse,

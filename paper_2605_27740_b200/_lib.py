@@ -50,8 +50,8 @@ _PROTOS = {
                       _vp]),
     "pt_lam_norms": (_i, [_vp, _i, _vp, _i, _i, _i, _f, _vp, _vp, _vp]),
     "pt_lam_norms_chained": (_i, [_vp, _i, _vp, _i, _i, _i, _f, _vp, _vp, _vp]),
-    "pt_score_bounded": (_i, [_vp, _i, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _vp, _vp, _vp,
-                              _vp]),
+    "pt_score_bounded": (_i, [_vp, _i, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _vp, _vp,
+                              _vp, _vp]),
     "pt_score_prenorm": (_i, [_vp, _i, _vp, _vp, _i, _vp, _vp, _i, _i, _i, _i, _i, _vp, _vp, _vp,
                               _vp]),
     "pt_topk": (_i, [_vp, _vp, _vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp]),
@@ -60,7 +60,7 @@ _PROTOS = {
     "pt_attend_workspace_bytes": (_sz, [_i, _i, _i, _i]),
     "pt_attend": (_i, [_vp, _i, _vp, _vp, _i, _i, _vp, _i, _vp, _vp, _vp, _i, _i, _i, _i, _i, _vp,
                        _f, _vp, _vp, _vp, _sz, _vp, _i, _vp]),
-    "pt_select_attend": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp,
+    "pt_select_attend": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp,
                               _vp, _vp, _i, _vp,
                               _vp, _i, _i, _i, _i, _f, _vp, _vp, _vp, _sz, _vp, _vp]),
     "pt_debug_sa_prof": (_i, [_vp, _i]),

@@ -965,17 +965,39 @@ static int sa_env_int(const char *name, int dflt) {
 extern "C" int pt_select_attend(const uint16_t *keys, const uint16_t *tile_max,
                                 const uint16_t *keys_hi, const void *mirror, const float *stds,
                                 const float *lamnorm, const int32_t *seq_len,
-                                const int32_t *page_table, int U, int S, int Pmax, int k,
-                                int32_t *sel, int32_t *sel_logical, int32_t *n_sel, int32_t *kth,
+                                const int32_t *page_table, int U_all, int u0, int nu, int S, int Pmax,
+                                int k, int32_t *sel, int32_t *sel_logical, int32_t *n_sel, int32_t *kth,
                                 int32_t *kplus1, const void *q, int q_dtype, const void *k_pool,
                                 const void *v_pool, int kv_dtype, int num_phys_pages, int G, int D,
                                 float scale, float *out, float *lse, void *workspace,
                                 size_t workspace_bytes, int32_t *tickets, void *stream) {
     if (!keys || !seq_len || !page_table || !sel || !n_sel || !kth || !kplus1 || !q || !k_pool ||
-        !v_pool || !out || !lse || U < 0 || S < 1 || Pmax % 32 || G < 1)
+        !v_pool || !out || !lse || U_all < 0 || u0 < 0 || nu < 0 || u0 + nu > U_all || S < 1 ||
+        Pmax % 32 || G < 1)
         return PT_ERR_INVALID;
     if (k < 1) return PT_ERR_K;
-    if (U == 0) return PT_OK;
+    if (nu == 0) return PT_OK;
+    // units [u0, u0 + nu) of a U_all-unit cache: every per-unit array from u0 on (the
+    // workspace by its per-unit share), so two disjoint ranges can run concurrently
+    const float *rows_all = mirror ? mirror_view(mirror, U_all, Pmax, D).rows : nullptr;
+    {
+        const int64_t o = u0;
+        keys += o * Pmax; seq_len += o; page_table += o * Pmax;
+        sel += o * k; n_sel += o; kth += o; kplus1 += o; tickets += o;
+        if (tile_max) tile_max += o * (Pmax / 32);
+        if (keys_hi) keys_hi += o * Pmax;
+        if (stds) stds += o * Pmax;
+        if (lamnorm) lamnorm += o * 8;
+        if (sel_logical) sel_logical += o * k;
+        if (rows_all) rows_all += o * Pmax * D;
+        q = static_cast<const char *>(q) + o * G * D * (q_dtype == PT_F32 ? 4 : 2);
+        out += o * G * D; lse += o * G;
+        const size_t wsh = pt_attend_workspace_bytes((int)o, G, D, k);
+        if (workspace_bytes < wsh) return PT_ERR_UNSUPPORTED;
+        workspace = static_cast<char *>(workspace) + wsh;
+        workspace_bytes -= wsh;
+    }
+    const int U = nu;
     if (kv_dtype != PT_BF16 || G > 8 || !(D == 64 || D == 128 || D == 256) ||
         !(S == 16 || S == 32 || S == 64) || num_phys_pages <= 0 || !workspace || !tickets ||
         workspace_bytes < pt_attend_workspace_bytes(U, G, D, k) || sa_env_int("PT_NO_FUSED_SA", 0))
@@ -1058,7 +1080,7 @@ extern "C" int pt_select_attend(const uint16_t *keys, const uint16_t *tile_max,
     p.q_dtype = q_dtype; p.U = U; p.G = G; p.Pmax = Pmax; p.k = k; p.nchunk = nchunk;
     p.nstage = nstage; p.region = (int)region; p.scale = scale;
     p.prof = sa_env_int("PT_SA_PROF", 0);
-    p.keys_hi = keys_hi; p.rows32 = mirror_view(mirror, U, Pmax, D).rows;
+    p.keys_hi = keys_hi; p.rows32 = rows_all;
     p.region_lo = (int)region_lo; p.stds = stds; p.lamnorm = lamnorm; p.rcap = rcap;
     cudaStream_t st = (cudaStream_t)stream;
     // selection threads: 8 warps halve the selection's block-wide passes; 4 of them stream

@@ -90,6 +90,16 @@ class DecodeEngine:
         self._side = torch.cuda.Stream(device=d)
         # append -> norms -> score as one PDL chain (PT_NO_PDL=1: the fork/join instead)
         self.chain_norms = os.environ.get("PT_NO_PDL", "") != "1" and os.environ.get("PT_NORMS_FORK", "") != "1"
+        # half-batch pipelining of score -> select+attend (bounded mode, >= 128 units; split at
+        # a sequence boundary when possible): opt-in (PT_SPLIT=1) -- measured slower at cfg3
+        # (203 vs 168.5 us/step: the second half's select+attend runs alone at half occupancy,
+        # and the first half's CTAs delay the second scorer's static tile ranges)
+        h = U // 2
+        H = cache.layout.num_kv_heads
+        if U % H == 0 and (U // H) % 2 == 0:
+            h = (U // H // 2) * H
+        self.split_at = h
+        self.split = self.bounded and U >= 128 and os.environ.get("PT_SPLIT", "") == "1"
         # GQA groups wider than the kernels' 8 heads (e.g. 128 q / 8 kv heads): sub-groups of
         # <= 8 heads, scored separately (exact keys) and combined by a key max, one shared
         # selection, attention per sub-group (see _step_wide)
@@ -169,16 +179,17 @@ class DecodeEngine:
                   dev.ptr(norms), self.U, self.G, self.D, self.lam, self.lamnorm.data_ptr(),
                   dev.ptr(self.qnorm), dev.stream_handle(stream))
 
-    def score_bounded(self, q: torch.Tensor, stream=None) -> bool:
+    def score_bounded(self, q: torch.Tensor, stream=None, u0: int = 0, nu: int | None = None) -> bool:
         """K2b over the bf16 mirror (reads the norms of :meth:`lam_norms`): key intervals into
-        keys / keys_hi; False when the shape needs the exact scorer."""
+        keys / keys_hi for units [u0, u0 + nu); False when the shape needs the exact scorer."""
         if not self.bounded:
             return False
         q2, qc = self._q(q)
         c = self.cache
+        nu = self.U - u0 if nu is None else nu
         rc = _lib.load().pt_score_bounded(
             q2.data_ptr(), qc, self.lamnorm.data_ptr(), self.qnorm.data_ptr(), c.mirror.data_ptr(),
-            c.stds.data_ptr(), c.seq_lens.data_ptr(), self.U, self.G,
+            c.stds.data_ptr(), c.seq_lens.data_ptr(), self.U, u0, nu, self.G,
             self.D, c.layout.page_size, c.Pmax, self.keys.data_ptr(), self.keys_hi.data_ptr(),
             self.tile_max.data_ptr(), dev.stream_handle(stream))
         if rc == _lib.PT_ERR_UNSUPPORTED:
@@ -262,11 +273,31 @@ class DecodeEngine:
         self.score(q, norms, stream=stream)
         self.select(stream=stream)
 
-    def select_attend(self, q: torch.Tensor, stream=None) -> None:
+    def select_attend(self, q: torch.Tensor, stream=None, u0: int = 0, nu: int | None = None) -> bool:
         """K3 + K4 in one launch (pt_select_attend): per unit, select the top-k pages from the
         keys of :meth:`score`, then attend over them -- identical outputs to :meth:`select`
-        followed by :meth:`attend`, which run instead outside the fused kernel's envelope."""
+        followed by :meth:`attend`, which run instead outside the fused kernel's envelope.
+        A unit range [u0, u0 + nu) runs only on the fused kernel (False when unsupported)."""
         bnd = self._step_bounded
+        nu_ = self.U - u0 if nu is None else nu
+        if u0 != 0 or nu_ != self.U:
+            q2, qc = self._q(q)
+            c = self.cache
+            rc = _lib.load().pt_select_attend(
+                self.keys.data_ptr(), self.tile_max.data_ptr(),
+                self.keys_hi.data_ptr() if bnd else None, c.mirror.data_ptr() if bnd else None,
+                c.stds.data_ptr() if bnd else None, self.lamnorm.data_ptr() if bnd else None,
+                c.seq_lens.data_ptr(), c.page_table.data_ptr(), self.U, u0, nu_,
+                c.layout.page_size, c.Pmax, self.k, self.sel.data_ptr(),
+                dev.ptr(self.sel_logical), self.n_sel.data_ptr(), self.kth.data_ptr(),
+                self.kplus1.data_ptr(), q2.data_ptr(), qc, c.k_pool.data_ptr(),
+                c.v_pool.data_ptr(), c.kv_code, c.layout.max_pages, self.G, self.D, self.scale,
+                self.out.data_ptr(), self.lse.data_ptr(), self.ws.data_ptr(), self.ws.numel(),
+                self.tickets.data_ptr(), dev.stream_handle(stream))
+            if rc == _lib.PT_ERR_UNSUPPORTED:
+                return False
+            _lib.check(rc, "pt_select_attend")
+            return True
         if self.fused_attend or bnd:
             q2, qc = self._q(q)
             c = self.cache
@@ -274,7 +305,7 @@ class DecodeEngine:
                 self.keys.data_ptr(), self.tile_max.data_ptr(),
                 self.keys_hi.data_ptr() if bnd else None, c.mirror.data_ptr() if bnd else None,
                 c.stds.data_ptr() if bnd else None, self.lamnorm.data_ptr() if bnd else None,
-                c.seq_lens.data_ptr(), c.page_table.data_ptr(), self.U,
+                c.seq_lens.data_ptr(), c.page_table.data_ptr(), self.U, 0, self.U,
                 c.layout.page_size, c.Pmax, self.k, self.sel.data_ptr(),
                 dev.ptr(self.sel_logical), self.n_sel.data_ptr(), self.kth.data_ptr(),
                 self.kplus1.data_ptr(), q2.data_ptr(), qc, c.k_pool.data_ptr(),
@@ -282,7 +313,7 @@ class DecodeEngine:
                 self.out.data_ptr(), self.lse.data_ptr(), self.ws.data_ptr(), self.ws.numel(),
                 self.tickets.data_ptr(), dev.stream_handle(stream))
             if rc == _lib.PT_OK:
-                return
+                return True
             if rc != _lib.PT_ERR_UNSUPPORTED:
                 _lib.check(rc, "pt_select_attend")
             if bnd:
@@ -294,6 +325,7 @@ class DecodeEngine:
             self.fused_attend = False
         self.select(stream=stream)
         self.attend(q, stream=stream)
+        return True
 
     def _step_wide(self, q: torch.Tensor, k_new, v_new, stream=None):
         """The step for G > 8 query heads per unit: per sub-group of <= 8 heads (row gathers
@@ -374,6 +406,23 @@ class DecodeEngine:
             if k_new is not None:
                 self.cache.append_batch(k_new, v_new, stream=main)
             main.wait_stream(self._side)
+        if self.split and self.bounded:
+            # two half-batches: the first half's select+attend (side stream) runs beside the
+            # second half's scorer -- its selection prologue no longer leaves HBM idle
+            # (tools/probe_overlap.py: 143.5 vs 153 us for score + select+attend at cfg3)
+            h = self.split_at
+            self._step_bounded = False
+            if self.score_bounded(q, stream=main, u0=0, nu=h):
+                ev = torch.cuda.Event()
+                ev.record(main)
+                self._side.wait_event(ev)
+                ok = self.select_attend(q, stream=self._side, u0=0, nu=h)
+                ok = ok and self.score_bounded(q, stream=main, u0=h, nu=self.U - h)
+                ok = ok and self.select_attend(q, stream=main, u0=h, nu=self.U - h)
+                main.wait_stream(self._side)
+                if ok:
+                    return self.out, self.lse
+                self.split = False  # outside the fused kernel's envelope: the one-range step
         self.score_step(q, stream=main)
         self.select_attend(q, stream=main)
         return self.out, self.lse

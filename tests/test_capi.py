@@ -70,10 +70,10 @@ def test_invalid_arguments_rejected_without_touching_a_device():
         _lib.PT_ERR_INVALID
     assert L.pt_score(None, 0, None, None, 0, None, None, 1, 4, 128, 16, 32, 0.5, None, None,
                       None, None, None) == _lib.PT_ERR_INVALID
-    assert L.pt_select_attend(None, None, None, None, None, None, None, None, 1, 16, 32, 4, None,
+    assert L.pt_select_attend(None, None, None, None, None, None, None, None, 1, 0, 1, 16, 32, 4, None,
                               None, None, None, None, None, 1, None, None, 1, 8, 4, 128, 0.1, None,
                               None, None, 0, None, None) == _lib.PT_ERR_INVALID
-    assert L.pt_score_bounded(None, 1, None, None, None, None, None, 1, 4, 128, 16, 32, None,
+    assert L.pt_score_bounded(None, 1, None, None, None, None, None, 1, 0, 1, 4, 128, 16, 32, None,
                               None, None, None) == _lib.PT_ERR_INVALID
     assert L.pt_mirror_bytes(2, 64, 128) == 2 * 64 * 128 * 6 + 2 * 64 * 4
     assert L.pt_radix_select_desc_host(None, 10, 2, None, None, None) == _lib.PT_ERR_INVALID

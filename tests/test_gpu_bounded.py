@@ -279,3 +279,58 @@ def test_bounded_warp_per_unit_selection_equals_exact(cuda, oracle):
         assert set(sel[u, : nsel[u]].tolist()) == set(ref["sel"][u, : ref["n_sel"][u]].tolist())
     np.testing.assert_array_equal(a.kth.cpu().numpy(), ref["kth"])
     np.testing.assert_array_equal(a.kplus1.cpu().numpy(), ref["kplus1"])
+
+
+def test_half_batch_split_step_equals_one_range(cuda, oracle, monkeypatch):
+    """The two-stream half-batch step (score A -> [select+attend A on a side stream] beside
+    score B -> select+attend B, pt_score_bounded / pt_select_attend over unit ranges) gives
+    bit-identical outputs to the one-range bounded step, eagerly and from a captured graph
+    with appends, and the selections of the exact path and of the oracle."""
+    pt = _pt()
+    monkeypatch.setenv("PT_SPLIT", "1")
+    rng = np.random.default_rng(99)
+    U, H, D, S, G, k = 128, 8, 128, 16, 4, 64
+    n = 16 * 400 + 5
+    K = rng.standard_normal((U, n, D)).astype(np.float32)
+    V = rng.standard_normal((U, n, D)).astype(np.float32)
+    cache = _cache(K, V, H, S, spare=8)
+    del K, V
+    a = pt.DecodeEngine(cache, G, k, keep_logical=True)
+    c = pt.DecodeEngine(cache, G, k, keep_logical=True)
+    c.split = False
+    assert a.split and a.bounded and a.split_at == 64
+    _, b = _engines(cache, G, k)
+
+    def outs(e):
+        return [x.clone() for x in (e.out, e.lse, e.sel, e.sel_logical, e.n_sel, e.kth, e.kplus1)]
+
+    for _ in range(2):
+        q = torch.from_numpy(rng.standard_normal((U * G, D)).astype(np.float32)).cuda().to(torch.bfloat16)
+        a.step(q)
+        c.step(q)
+        torch.cuda.synchronize()
+        for x, y in zip(outs(a), outs(c)):
+            assert torch.equal(x, y)
+        _same_step(a, b, q)
+    # captured with appends: the replay's outputs equal an eager one-range step afterwards
+    qs = torch.empty((U * G, D), dtype=torch.bfloat16, device="cuda")
+    kn = torch.empty((U, D), dtype=torch.bfloat16, device="cuda")
+    a.capture(qs, kn, kn)
+    for _ in range(3):
+        qs.copy_(torch.from_numpy(rng.standard_normal((U * G, D)).astype(np.float32)))
+        kn.copy_(torch.from_numpy(rng.standard_normal((U, D)).astype(np.float32)))
+        a.replay()
+        c.step(qs)
+        torch.cuda.synchronize()
+        for x, y in zip(outs(a), outs(c)):
+            assert torch.equal(x, y)
+    cache.check_errors()
+    kpool, vpool, table, seq = readback(cache)
+    means, stds = oracle.build_stats(kpool, table, seq, S)
+    ref = oracle.decode_units(qs.to(torch.float32).cpu().numpy().reshape(-1, G, D), kpool, vpool,
+                              table, seq, means, stds, k, 0.5, 1.0 / math.sqrt(D), S)
+    sel, nsel = a.sel.cpu().numpy(), a.n_sel.cpu().numpy()
+    for u in range(U):
+        assert set(sel[u, : nsel[u]].tolist()) == set(ref["sel"][u, : ref["n_sel"][u]].tolist())
+    np.testing.assert_array_equal(a.kth.cpu().numpy(), ref["kth"])
+    np.testing.assert_array_equal(a.kplus1.cpu().numpy(), ref["kplus1"])
