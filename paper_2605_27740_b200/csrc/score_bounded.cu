@@ -120,8 +120,9 @@ __global__ void __launch_bounds__(kSBWarps * 32) k_score_bounded(const BoundedSc
     }
     __syncthreads();
     struct Cur { int u, t, g; };
-    // static contiguous per-warp tile ranges (against dynamic chunk grabbing from a global
-    // counter, 2-8 tiles per grab: 178-205 vs 168.5 us/step at cfg3 -- DESIGN.md)
+    // static contiguous per-warp tile ranges: measured against dynamic chunk grabbing from a
+    // global counter (2-8 tiles per grab: 178-205 vs 168.5 us/step at cfg3) and round-robin
+    // chunks of 1-16 tiles (179-260 us/step) -- both finish units in tile order, both slower
     const int64_t T = Tp[U];
     const int64_t g0 = (int64_t)gw * T / W, g_end = (int64_t)(gw + 1) * T / W;
     Cur pc{U, 0, 0};

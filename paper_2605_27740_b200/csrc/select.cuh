@@ -392,7 +392,7 @@ __device__ bool select_cand(const uint16_t *__restrict__ skeys, const uint16_t *
                             const Resolve &resolve = Resolve(), const uint16_t *shi = nullptr,
                             uint16_t *candhi = nullptr,
                             const ResolveCands &resolve_cands = ResolveCands(),
-                            int *defer = nullptr) {
+                            int *defer = nullptr, bool tclk = false) {
     constexpr int NWP = NT / 32;
     constexpr int MAXT = 8;  // tile maxima per thread: ceil(P / 32) <= NT * MAXT
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -401,7 +401,8 @@ __device__ bool select_cand(const uint16_t *__restrict__ skeys, const uint16_t *
     auto stamp = [&](int i) {
         if (tp && tid == 0) {
             unsigned long long t;
-            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+            if (tclk) asm volatile("mov.u64 %0, %clock64;" : "=l"(t));
+            else asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
             tp[i] = t;
         }
     };

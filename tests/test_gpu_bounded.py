@@ -284,8 +284,9 @@ def test_bounded_warp_per_unit_selection_equals_exact(cuda, oracle):
 def test_half_batch_split_step_equals_one_range(cuda, oracle, monkeypatch):
     """The two-stream half-batch step (score A -> [select+attend A on a side stream] beside
     score B -> select+attend B, pt_score_bounded / pt_select_attend over unit ranges) gives
-    bit-identical outputs to the one-range bounded step, eagerly and from a captured graph
-    with appends, and the selections of the exact path and of the oracle."""
+    the selections of the one-range bounded step bit for bit (outputs up to the chunk-merge
+    order: a 64-unit range splits each unit over more CTAs), eagerly and from a captured
+    graph with appends, and those of the exact path and of the oracle."""
     pt = _pt()
     monkeypatch.setenv("PT_SPLIT", "1")
     rng = np.random.default_rng(99)
@@ -304,13 +305,20 @@ def test_half_batch_split_step_equals_one_range(cuda, oracle, monkeypatch):
     def outs(e):
         return [x.clone() for x in (e.out, e.lse, e.sel, e.sel_logical, e.n_sel, e.kth, e.kplus1)]
 
+    def _same_outs(x, y):
+        torch.testing.assert_close(x[0], y[0], rtol=1e-4, atol=1e-5)
+        torch.testing.assert_close(x[1], y[1], rtol=1e-5, atol=1e-5)
+        for i in (3, 4, 5, 6):
+            assert torch.equal(x[i], y[i])
+        # sel lists the same pages per unit (order: the streaming order of each variant)
+        assert torch.equal(torch.sort(x[2], dim=1).values, torch.sort(y[2], dim=1).values)
+
     for _ in range(2):
         q = torch.from_numpy(rng.standard_normal((U * G, D)).astype(np.float32)).cuda().to(torch.bfloat16)
         a.step(q)
         c.step(q)
         torch.cuda.synchronize()
-        for x, y in zip(outs(a), outs(c)):
-            assert torch.equal(x, y)
+        _same_outs(outs(a), outs(c))
         _same_step(a, b, q)
     # captured with appends: the replay's outputs equal an eager one-range step afterwards
     qs = torch.empty((U * G, D), dtype=torch.bfloat16, device="cuda")
@@ -322,8 +330,7 @@ def test_half_batch_split_step_equals_one_range(cuda, oracle, monkeypatch):
         a.replay()
         c.step(qs)
         torch.cuda.synchronize()
-        for x, y in zip(outs(a), outs(c)):
-            assert torch.equal(x, y)
+        _same_outs(outs(a), outs(c))
     cache.check_errors()
     kpool, vpool, table, seq = readback(cache)
     means, stds = oracle.build_stats(kpool, table, seq, S)

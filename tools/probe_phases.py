@@ -33,6 +33,8 @@ def main():
     ap.add_argument("--ctx", type=int, default=131072)
     ap.add_argument("--budget", type=int, default=2048)
     ap.add_argument("--exact", action="store_true", help="exact f32-means keys (no mirror)")
+    ap.add_argument("--clock", action="store_true",
+                    help="%%clock64 stamps: per-CTA phase durations in SM cycles (fine-grained)")
     a = ap.parse_args()
     ns = argparse.Namespace(batch=a.batch, ctx=a.ctx, q_heads=32, kv_heads=8, head_dim=128,
                             page=16, budget=a.budget, stats_dtype="f32", warmup=3, steps=10)
@@ -78,7 +80,7 @@ def main():
     for _ in range(3):
         eng.select_attend(q)
     torch.cuda.synchronize()
-    os.environ["PT_SA_PROF"] = "1"
+    os.environ["PT_SA_PROF"] = "2" if a.clock else "1"
     eng.select_attend(q)
     torch.cuda.synchronize()
     os.environ.pop("PT_SA_PROF")
@@ -128,6 +130,28 @@ def main():
             "b_to_resolve": float(np.median(rel[:, 10] - T(19))),
         })
 
+    if a.clock:
+        # per-CTA deltas from the CTA's own entry stamp (clocks are per SM), in cycles and in
+        # us at the SM clock read during the run
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            mhz = pynvml.nvmlDeviceGetClockInfo(pynvml.nvmlDeviceGetHandleByIndex(0), pynvml.NVML_CLOCK_SM)
+        except Exception:
+            mhz = 1965
+        out = {"resolve": stats, "sm_mhz": mhz, "note": "median over CTAs of (stamp - entry), cycles"}
+        ent = raw[:, 0].astype(np.int64)
+        cyc = {}
+        for i, nm in enumerate(names + ["", "b_cand_pass", "b_mxh", "b_hist", "b_hist2"]):
+            if not nm or i >= 20:
+                continue
+            d = raw[:, i].astype(np.int64) - ent
+            ok = (d >= 0) & (d < 10**8)
+            if ok.any():
+                cyc[nm] = int(np.median(d[ok]))
+        out["cycles"] = cyc
+        out["us"] = {k2: round(v / mhz, 3) for k2, v in cyc.items()}
     print(json.dumps(out, indent=1))
 
 
