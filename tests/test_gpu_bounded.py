@@ -306,8 +306,10 @@ def test_half_batch_split_step_equals_one_range(cuda, oracle, monkeypatch):
         return [x.clone() for x in (e.out, e.lse, e.sel, e.sel_logical, e.n_sel, e.kth, e.kplus1)]
 
     def _same_outs(x, y):
-        torch.testing.assert_close(x[0], y[0], rtol=1e-4, atol=1e-5)
-        torch.testing.assert_close(x[1], y[1], rtol=1e-5, atol=1e-5)
+        # same pages, another streaming order (chunking, sure-first) -- the bf16 probabilities
+        # of the PV product are rounded against another running maximum (see _same_step)
+        torch.testing.assert_close(x[0], y[0], rtol=2e-3, atol=2e-3)
+        torch.testing.assert_close(x[1], y[1], rtol=2e-3, atol=2e-3)
         for i in (3, 4, 5, 6):
             assert torch.equal(x[i], y[i])
         # sel lists the same pages per unit (order: the streaming order of each variant)
