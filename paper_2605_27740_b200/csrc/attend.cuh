@@ -404,6 +404,17 @@ __device__ __forceinline__ void tma_load_2d(void *smem_dst, const CUtensorMap *t
         : "memory");
 }
 
+// the same with an L2 cache policy (evict-first for pages read once per step: the stream
+// then does not push the step's small re-read state -- keys, tables, kernel code -- out of L2)
+__device__ __forceinline__ void tma_load_2d_hint(void *smem_dst, const CUtensorMap *tm, int c0, int c1,
+                                                 uint64_t *bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, "
+        "{%2, %3}], [%4], %5;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
 // byte offset of element (t, d) inside a staged page: 64-column boxes of S rows x 128 B,
 // 16-byte chunk index XOR (row & 7) (CU_TENSOR_MAP_SWIZZLE_128B)
 __device__ __forceinline__ uint32_t swz(int t, int chunk16, int S) {

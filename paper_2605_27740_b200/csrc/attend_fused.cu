@@ -45,6 +45,7 @@ struct SelAttnParams {
     const uint16_t *keys_hi;
     const float *rows32, *stds, *lamnorm;  // rows32: the mirror's row-major f32 means
     int rcap;  // pages resolved per round (their f32 means staged in shared memory)
+    int kv_evict_first;  // L2 policy of the page stream (PT_SA_KV_EVICT=normal: 0)
 };
 
 constexpr int kSAWarps = 4;
@@ -55,9 +56,12 @@ constexpr int kSAWarps = 4;
 constexpr int kSAProfCtas = 4096;
 constexpr int kSAProfN = 20;
 __device__ unsigned long long g_sa_prof[kSAProfCtas * kSAProfN];
-__device__ __forceinline__ unsigned long long gtimer() {
+// PT_SA_PROF=1: %globaltimer (ns, comparable across SMs, ~1 us update granularity);
+// PT_SA_PROF=2: %clock64 (SM cycles: phase durations within a CTA only)
+__device__ __forceinline__ unsigned long long gtimer(bool clk) {
     unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    if (clk) asm volatile("mov.u64 %0, %clock64;" : "=l"(t));
+    else asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
 
@@ -116,22 +120,32 @@ __device__ __forceinline__ float sa_exact_score(const float *row, const float *s
 template <int D, int GG>
 __device__ __noinline__ float sa_exact_score_global(const float *row, const void *q, int q_dtype,
                                                     int64_t qrow0, const float *lnp, float sd, int G) {
+    // the row in chunks of 8 float4 (32 dims) whose loads are all in flight together -- a
+    // load per step of the sequential sum would pay one memory latency per 4 dims
+    constexpr int CH = 8;
+    static_assert((D / 4) % CH == 0, "row chunks");
     float acc[GG];
 #pragma unroll
     for (int g = 0; g < GG; g++) acc[g] = 0.f;
-    for (int c = 0; c < D / 4; c++) {
-        const float4 m4 = __ldg(reinterpret_cast<const float4 *>(row) + c);
-        const float mv[4] = {m4.x, m4.y, m4.z, m4.w};
+    const float4 *row4 = reinterpret_cast<const float4 *>(row);
+    for (int c0 = 0; c0 < D / 4; c0 += CH) {
+        float4 m4[CH];
 #pragma unroll
-        for (int e = 0; e < 4; e++) {
+        for (int i = 0; i < CH; i++) m4[i] = __ldg(row4 + c0 + i);
 #pragma unroll
-            for (int g = 0; g < GG; g++) {
-                if (g < G) {
-                    const int64_t qi = (qrow0 + g) * D + 4 * c + e;
-                    const float qv = q_dtype == PT_BF16
-                                         ? bf16_bits_to_f32(__ldg(static_cast<const uint16_t *>(q) + qi))
-                                         : __ldg(static_cast<const float *>(q) + qi);
-                    acc[g] = __fadd_rn(acc[g], __fmul_rn(qv, mv[e]));
+        for (int i = 0; i < CH; i++) {
+            const float mv[4] = {m4[i].x, m4[i].y, m4[i].z, m4[i].w};
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+#pragma unroll
+                for (int g = 0; g < GG; g++) {
+                    if (g < G) {
+                        const int64_t qi = (qrow0 + g) * D + 4 * (c0 + i) + e;
+                        const float qv = q_dtype == PT_BF16
+                                             ? bf16_bits_to_f32(__ldg(static_cast<const uint16_t *>(q) + qi))
+                                             : __ldg(static_cast<const float *>(q) + qi);
+                        acc[g] = __fadd_rn(acc[g], __fmul_rn(qv, mv[e]));
+                    }
                 }
             }
         }
@@ -181,7 +195,7 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
     const bool lead = (c == 0);
     const int cta = blockIdx.y * gridDim.x + blockIdx.x;
     const bool prof = p.prof && threadIdx.x == 0 && cta < kSAProfCtas;
-    if (prof) g_sa_prof[cta * kSAProfN + 0] = gtimer();
+    if (prof) g_sa_prof[cta * kSAProfN + 0] = gtimer(p.prof == 2);
     if (P == 0) {
         if (lead && threadIdx.x == 0) { p.n_sel[u] = 0; p.kth[u] = 0; p.kplus1[u] = -1; }
         return;
@@ -246,7 +260,7 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
         if (threadIdx.x == 0) sdefer[0] = 0;
     }
     pdl_wait();
-    if (prof) g_sa_prof[cta * kSAProfN + 1] = gtimer();
+    if (prof) g_sa_prof[cta * kSAProfN + 1] = gtimer(p.prof == 2);
 
     // ---- selection (select.py:87-115): physical ids land in `ids` in emission order ----
     // candidate selection (select_cand: tile-maximum lower bound or bisection, then the
@@ -327,7 +341,7 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
         if (nr) mbar_wait(rbar, (uint32_t)(rphase & 1));
         rphase += nr ? 1 : 0;
         __syncthreads();
-        if (prof) g_sa_prof[cta * kSAProfN + 12] = gtimer();
+        if (prof) g_sa_prof[cta * kSAProfN + 12] = gtimer(p.prof == 2);
         for (int i = threadIdx.x; i < nr; i += NT) {
             const float best = G <= 4 ? sa_exact_score<D, 4>(rstage + i * RS, sq, sln, rstd[i], G)
                                       : sa_exact_score<D, 8>(rstage + i * RS, sq, sln, rstd[i], G);
@@ -336,7 +350,7 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
             mxr = max(mxr, (int)key);
         }
         __syncthreads();
-        if (prof) g_sa_prof[cta * kSAProfN + 13] = gtimer();
+        if (prof) g_sa_prof[cta * kSAProfN + 13] = gtimer(p.prof == 2);
         return mxr;
     };
     // warp-aggregated append of the flagged entries (bit e of f: entry base_e + e) to rlist
@@ -376,7 +390,7 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
         int mxr = -1;
         const int nvec = (P + 7) >> 3;
         const uint32_t Lc = (uint32_t)(L < 0 ? 0 : L);
-        if (prof) g_sa_prof[cta * kSAProfN + 10] = gtimer();
+        if (prof) g_sa_prof[cta * kSAProfN + 10] = gtimer(p.prof == 2);
         for (;;) {
             if (threadIdx.x == 0) *rcnt = 0;
             __syncthreads();
@@ -397,7 +411,7 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
                 list_append(f, v * 8);
             }
             __syncthreads();
-            if (prof) g_sa_prof[cta * kSAProfN + 11] = gtimer();
+            if (prof) g_sa_prof[cta * kSAProfN + 11] = gtimer(p.prof == 2);
             const int n = *rcnt;
             mxr = max(mxr, resolve_batch(n < p.rcap ? n : p.rcap, [](int e) { return e; },
                                          [&](int e, uint16_t key) { skeys[e] = key; skhi[e] = key; }));
@@ -408,7 +422,7 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
     // (b) the candidate list of select_cand: candidates with an uncertain key whose interval
     // meets the threshold bracket [A, B]; exact keys go into the list entries
     auto resolve_cands = [&](int C, int A, int B) {
-        if (prof) g_sa_prof[cta * kSAProfN + 10] = gtimer();
+        if (prof) g_sa_prof[cta * kSAProfN + 10] = gtimer(p.prof == 2);
         for (;;) {
             if (threadIdx.x == 0) *rcnt = 0;
             __syncthreads();
@@ -422,7 +436,7 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
                 list_append(f, i);
             }
             __syncthreads();
-            if (prof) g_sa_prof[cta * kSAProfN + 11] = gtimer();
+            if (prof) g_sa_prof[cta * kSAProfN + 11] = gtimer(p.prof == 2);
             const int n = *rcnt;
             resolve_batch(n < p.rcap ? n : p.rcap, [&](int i) { return (int)(csh.cand[i] & 0xFFFFu); },
                           [&](int i, uint16_t key) {
@@ -484,7 +498,7 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
         };
         const int C = sdefer[1], L = sdefer[2];
         const bool tprof = p.prof && t == 0 && cta < kSAProfCtas;
-        if (tprof) g_sa_prof[cta * kSAProfN + 10] = gtimer();
+        if (tprof) g_sa_prof[cta * kSAProfN + 10] = gtimer(p.prof == 2);
         // (1) exact keys of the bracket candidates, in rounds of rcap
         for (;;) {
             if (t == 0) *rcnt = 0;
@@ -495,7 +509,7 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
             }
             sync2();
             const int n = *rcnt, nr = n < p.rcap ? n : p.rcap;
-            if (tprof) g_sa_prof[cta * kSAProfN + 11] = gtimer();
+            if (tprof) g_sa_prof[cta * kSAProfN + 11] = gtimer(p.prof == 2);
             if (t == 0 && nr) mbar_arrive_expect_tx(rbar, (uint32_t)(nr * D * 4));
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             sync2();
@@ -508,7 +522,7 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
             if (nr) mbar_wait(rbar, (uint32_t)(rphase & 1));
             rphase += nr ? 1 : 0;
             sync2();
-            if (tprof) g_sa_prof[cta * kSAProfN + 12] = gtimer();
+            if (tprof) g_sa_prof[cta * kSAProfN + 12] = gtimer(p.prof == 2);
             for (int i = t; i < nr; i += NT2) {
                 const int ci = rlist[i];
                 const float best = G <= 4 ? sa_exact_score<D, 4>(rstage + i * RS, sq, sln, rstd[i], G)
@@ -518,7 +532,7 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
                 cflag[ci] = (uint8_t)(cflag[ci] & 1);
             }
             sync2();
-            if (tprof) g_sa_prof[cta * kSAProfN + 13] = gtimer();
+            if (tprof) g_sa_prof[cta * kSAProfN + 13] = gtimer(p.prof == 2);
             if (n <= nr) break;
         }
         // (2) threshold: the k-th largest candidate key (every key that can reach it is exact)
@@ -610,12 +624,13 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
         __threadfence_block();
     };
     bool selected;
-    if (prof) g_sa_prof[cta * kSAProfN + 14] = gtimer();
+    if (prof) g_sa_prof[cta * kSAProfN + 14] = gtimer(p.prof == 2);
     if constexpr (BND) {
         selected = select_cand<NT>(skeys, tm_stage ? stm : nullptr, P, k, p.page_table + u * p.Pmax, o_sel,
                                    o_log, o_n, o_kth, o_kp1, csh, ids, true,
                                    prof ? &g_sa_prof[cta * kSAProfN + 6] : nullptr, true, k + 1, resolve,
-                                   skhi, candhi, resolve_cands, p.nchunk == 1 ? sdefer : nullptr);
+                                   skhi, candhi, resolve_cands, p.nchunk == 1 ? sdefer : nullptr,
+                                   p.prof == 2);
         // take-all (P <= k) and P > 65536 return before resolving: resolve every page
         if (!selected && (P <= k || P > 65536)) resolve(-1);
     } else {
@@ -673,7 +688,7 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
         n_sure = tot;
     }
     __syncthreads();  // ids complete (deferred: the certain prefix); the phase-1 scratch is dead
-    if (prof) g_sa_prof[cta * kSAProfN + 2] = gtimer();
+    if (prof) g_sa_prof[cta * kSAProfN + 2] = gtimer(p.prof == 2);
 
     if (deferred && warp >= NW) {
         // ---- selection tail on warps 4..7 (named barrier 1, 128 threads) ----
@@ -699,6 +714,7 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
             have_all = true;
         }
     };
+    const uint64_t kv_pol = p.kv_evict_first ? l2_evict_first_policy() : l2_evict_normal_policy();
     auto issue = [&](int i) {
         const int pid = ids[first + warp + i * NW];
         const int st = i % nstage;
@@ -706,8 +722,8 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
         mbar_arrive_expect_tx(&bars[st], STAGE_BYTES);
 #pragma unroll
         for (int b = 0; b < D / 64; b++) {
-            tma_load_2d(ks + b * S * 128, &tmk, b * 64, pid * S, &bars[st]);
-            tma_load_2d(ks + PAGE_BYTES + b * S * 128, &tmv, b * 64, pid * S, &bars[st]);
+            tma_load_2d_hint(ks + b * S * 128, &tmk, b * 64, pid * S, &bars[st], kv_pol);
+            tma_load_2d_hint(ks + PAGE_BYTES + b * S * 128, &tmv, b * 64, pid * S, &bars[st], kv_pol);
         }
     };
     if (warp < NW) {
@@ -734,7 +750,7 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
         const int pid = ids[first + warp + i * NW];
         const int rows = (pid == tail_pid) ? tail_rows : S;
         mbar_wait(&bars[st], (uint32_t)((i / nstage) & 1));
-        if (prof && i == 0) g_sa_prof[cta * kSAProfN + 3] = gtimer();
+        if (prof && i == 0) g_sa_prof[cta * kSAProfN + 3] = gtimer(p.prof == 2);
         const uint32_t kbase = smem_u32(my_stages + (size_t)st * STAGE_BYTES);
         mma_page<D, MT>(kbase, kbase + PAGE_BYTES, rows, 0.f, qscale, qb, acc, m_run, l_run, lane);
         __syncwarp();
@@ -746,7 +762,7 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
     if (warp < NW && !have_all) asm volatile("bar.sync 2, %0;" ::"n"(NT) : "memory");
 
     // ---- per-warp partials to shared memory, then the CTA / chunk merge (attend.cuh) ----
-    if (prof) g_sa_prof[cta * kSAProfN + 4] = gtimer();
+    if (prof) g_sa_prof[cta * kSAProfN + 4] = gtimer(p.prof == 2);
     __syncthreads();
     float *macc = reinterpret_cast<float *>(smem);             // [NW][8][D]
     float *mml = macc + (size_t)NW * kMmaGP * D;                // [NW][8][2]
@@ -772,7 +788,7 @@ __global__ void __launch_bounds__(NT, 2) k_select_attend(const __grid_constant__
     ap.out = p.out; ap.lse = p.lse; ap.ws = p.ws; ap.tickets = p.tickets;
     ap.G = G; ap.D = D; ap.maxs = kAttnMaxSplits;
     cta_finish(ap, macc, mml, NW, kMmaGP, u, c, nchunk_u);
-    if (prof) g_sa_prof[cta * kSAProfN + 5] = gtimer();
+    if (prof) g_sa_prof[cta * kSAProfN + 5] = gtimer(p.prof == 2);
 }
 
 // ---------------------------------------------------------------------------
@@ -802,17 +818,18 @@ __global__ void __launch_bounds__(128, 1) k_select_attend_warp(const __grid_cons
     int *ids = reinterpret_cast<int *>(ring + (size_t)nstage * STAGE_BYTES);
     uint64_t *bars = reinterpret_cast<uint64_t *>(ids + ((k + 1) & ~1));
     pdl_trigger();
-    pdl_wait();
     const int64_t u = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
     if (u >= p.U) return;
+    const bool prof = p.prof && lane == 0 && u < kSAProfCtas;
+    const bool pclk = p.prof == 2;
+    if (prof) g_sa_prof[u * kSAProfN + 0] = gtimer(pclk);
+    // lengths, the tail page and the query fragments are not written by the scoring kernel
+    // (the append that wrote them completed before the scorer triggered this launch): read
+    // before the PDL wait, beside the scorer's drain, as the CTA-per-unit kernel does
     const int S_ = S;
     const int n = p.seq_len[u];
     const int P = (n + S_ - 1) / S_;
-    if (P == 0) {
-        if (lane == 0) { p.n_sel[u] = 0; p.kth[u] = 0; p.kplus1[u] = -1; }
-        return;
-    }
-    const int tail_pid = p.page_table[u * p.Pmax + P - 1];
+    const int tail_pid = P > 0 ? p.page_table[u * p.Pmax + P - 1] : -1;
     const int tail_rows = n - (P - 1) * S_;
     uint32_t qb[KS][2];
     {
@@ -838,6 +855,12 @@ __global__ void __launch_bounds__(128, 1) k_select_attend_warp(const __grid_cons
             qb[ks][1] = b1;
         }
     }
+    pdl_wait();
+    if (prof) g_sa_prof[u * kSAProfN + 1] = gtimer(pclk);
+    if (P == 0) {
+        if (lane == 0) { p.n_sel[u] = 0; p.kth[u] = 0; p.kplus1[u] = -1; }
+        return;
+    }
     if constexpr (BND) {
         // bounded keys: the exact key of a bracket page, one lane per page
         auto exact = [&](int pg) -> int {
@@ -851,13 +874,27 @@ __global__ void __launch_bounds__(128, 1) k_select_attend_warp(const __grid_cons
         select_warp<kSWMaxV>(p.keys + u * (int64_t)p.Pmax, P, k, p.page_table + u * p.Pmax,
                              p.sel + u * (int64_t)k, p.sel_logical ? p.sel_logical + u * (int64_t)k : nullptr,
                              p.n_sel + u, p.kth + u, p.kplus1 + u, ids, p.keys_hi + u * (int64_t)p.Pmax,
-                             exact, reinterpret_cast<int *>(ring), (int)(nstage * STAGE_BYTES / 4));
+                             exact, reinterpret_cast<int *>(ring), (int)(nstage * STAGE_BYTES / 4),
+                             p.tile_max ? p.tile_max + u * (int64_t)(p.Pmax >> 5) : nullptr,
+                             prof && pclk ? &g_sa_prof[u * kSAProfN] : nullptr,
+                             [&](int pg) {  // the page's f32 row and std into L1
+                                 const char *row = reinterpret_cast<const char *>(
+                                     p.rows32 + ((int64_t)u * p.Pmax + pg) * D);
+#pragma unroll
+                                 for (int l = 0; l < D * 4 / 128; l++)
+                                     asm volatile("prefetch.global.L1 [%0];" ::"l"(row + 128 * l));
+                                 asm volatile("prefetch.global.L1 [%0];" ::"l"(p.stds + u * (int64_t)p.Pmax + pg));
+                             });
     } else {
         select_warp<kSWMaxV>(p.keys + u * (int64_t)p.Pmax, P, k, p.page_table + u * p.Pmax,
                              p.sel + u * (int64_t)k, p.sel_logical ? p.sel_logical + u * (int64_t)k : nullptr,
-                             p.n_sel + u, p.kth + u, p.kplus1 + u, ids);
+                             p.n_sel + u, p.kth + u, p.kplus1 + u, ids, nullptr, NoExactKey(), nullptr, 0,
+                             p.tile_max ? p.tile_max + u * (int64_t)(p.Pmax >> 5) : nullptr,
+                             prof && pclk ? &g_sa_prof[u * kSAProfN] : nullptr);
     }
+    if (prof) g_sa_prof[u * kSAProfN + 2] = gtimer(pclk);
     const int ns = P < k ? P : k;
+    const uint64_t kv_pol = p.kv_evict_first ? l2_evict_first_policy() : l2_evict_normal_policy();
     auto issue = [&](int i) {
         const int pid = ids[i];
         const int st = i % nstage;
@@ -865,8 +902,8 @@ __global__ void __launch_bounds__(128, 1) k_select_attend_warp(const __grid_cons
         mbar_arrive_expect_tx(&bars[st], STAGE_BYTES);
 #pragma unroll
         for (int b = 0; b < D / 64; b++) {
-            tma_load_2d(ks + b * S * 128, &tmk, b * 64, pid * S, &bars[st]);
-            tma_load_2d(ks + PAGE_BYTES + b * S * 128, &tmv, b * 64, pid * S, &bars[st]);
+            tma_load_2d_hint(ks + b * S * 128, &tmk, b * 64, pid * S, &bars[st], kv_pol);
+            tma_load_2d_hint(ks + PAGE_BYTES + b * S * 128, &tmv, b * 64, pid * S, &bars[st], kv_pol);
         }
     };
     if (lane == 0) {
@@ -887,11 +924,13 @@ __global__ void __launch_bounds__(128, 1) k_select_attend_warp(const __grid_cons
         const int pid = ids[i];
         const int rows = (pid == tail_pid) ? tail_rows : S;
         mbar_wait(&bars[st], (uint32_t)((i / nstage) & 1));
+        if (prof && i == 0) g_sa_prof[u * kSAProfN + 3] = gtimer(pclk);
         const uint32_t kbase = smem_u32(ring + (size_t)st * STAGE_BYTES);
         mma_page<D, MT>(kbase, kbase + PAGE_BYTES, rows, 0.f, qscale, qb, acc, m_run, l_run, lane);
         __syncwarp();
         if (lane == 0 && i + nstage < ns) issue(i + nstage);
     }
+    if (prof) g_sa_prof[u * kSAProfN + 4] = gtimer(pclk);
     const int g0 = 2 * (lane & 3);
     const float inv0 = 1.f / l_run[0], inv1 = 1.f / l_run[1];
 #pragma unroll
@@ -910,6 +949,7 @@ __global__ void __launch_bounds__(128, 1) k_select_attend_warp(const __grid_cons
         if (g0 < p.G) p.lse[u * p.G + g0] = (m_run[0] + log2f(l_run[0])) * kLn2;
         if (g0 + 1 < p.G) p.lse[u * p.G + g0 + 1] = (m_run[1] + log2f(l_run[1])) * kLn2;
     }
+    if (prof) g_sa_prof[u * kSAProfN + 5] = gtimer(pclk);
 }
 
 template <int D, int MT, bool BND>
@@ -1080,6 +1120,7 @@ extern "C" int pt_select_attend(const uint16_t *keys, const uint16_t *tile_max,
     p.q_dtype = q_dtype; p.U = U; p.G = G; p.Pmax = Pmax; p.k = k; p.nchunk = nchunk;
     p.nstage = nstage; p.region = (int)region; p.scale = scale;
     p.prof = sa_env_int("PT_SA_PROF", 0);
+    p.kv_evict_first = sa_env_int("PT_SA_KV_EVICT_FIRST", 1);
     p.keys_hi = keys_hi; p.rows32 = rows_all;
     p.region_lo = (int)region_lo; p.stds = stds; p.lamnorm = lamnorm; p.rcap = rcap;
     cudaStream_t st = (cudaStream_t)stream;

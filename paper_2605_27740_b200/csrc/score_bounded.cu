@@ -153,8 +153,8 @@ __global__ void __launch_bounds__(kSBWarps * 32) k_score_bounded(const BoundedSc
                 mbar_arrive_expect_tx(&bars[slot], C::TILE + C::THDR + (new_run ? C::QB + 64 : 0));
                 bulk_g2s_hint(ring + slot * C::TILE, prm.mirror + pg * D, C::TILE, &bars[slot], evict_first);
                 char *th = thdrs + (issued % C::NHDR) * C::THDR;
-                bulk_g2s(th, prm.stds + pg, 128, &bars[slot]);
-                bulk_g2s(th + 128, prm.merr + pg, 128, &bars[slot]);
+                bulk_g2s_hint(th, prm.stds + pg, 128, &bars[slot], evict_first);
+                bulk_g2s_hint(th + 128, prm.merr + pg, 128, &bars[slot], evict_first);
                 if (new_run) {
                     char *h = uhdrs + (p_run % C::NHU) * C::UHDR;
                     bulk_g2s(h, prm.q + (int64_t)pc.u * G * D, C::QB, &bars[slot]);

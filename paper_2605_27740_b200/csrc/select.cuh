@@ -974,15 +974,28 @@ __device__ bool select_cand(const uint16_t *__restrict__ skeys, const uint16_t *
 struct NoExactKey {
     __device__ int operator()(int) const { return 0; }
 };
+struct NoPrefetch {
+    __device__ void operator()(int) const {}
+};
 
-template <int MAXV, class ExactKey = NoExactKey>
+template <int MAXV, class ExactKey = NoExactKey, class PrefetchRow = NoPrefetch>
 __device__ void select_warp(const uint16_t *__restrict__ keys_g, int P, int k,
                             const int32_t *__restrict__ map, int32_t *__restrict__ out,
                             int32_t *__restrict__ out_l, int32_t *__restrict__ n_sel,
                             int32_t *__restrict__ kth, int32_t *__restrict__ kplus1, int *ids,
                             const uint16_t *__restrict__ hi_g = nullptr,
                             const ExactKey &exact = ExactKey(), int *scratch = nullptr,
-                            int scratch_cap = 0) {
+                            int scratch_cap = 0, const uint16_t *__restrict__ tmax_g = nullptr,
+                            unsigned long long *tp = nullptr,
+                            const PrefetchRow &prefetch = PrefetchRow()) {
+    // tuning aid: %clock64 phase stamps tp[i] (lane 0)
+    auto sw_stamp = [&](int i) {
+        if (tp && (threadIdx.x & 31) == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %clock64;" : "=l"(t));
+            tp[i] = t;
+        }
+    };
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
     const uint4 *k4 = reinterpret_cast<const uint4 *>(keys_g);
@@ -992,10 +1005,64 @@ __device__ void select_warp(const uint16_t *__restrict__ keys_g, int P, int k,
         const int base = (lane + 32 * j) * 8;
         v[j] = base < P ? __ldcg(k4 + lane + 32 * j) : make_uint4(0u, 0u, 0u, 0u);
     }
+    // the scorer's per-32-page tile maxima (of the lower keys): Lt = the (k+1)-th largest is
+    // a lower bound of the threshold, of the (k+1)-th largest key and (bounded) of A and B --
+    // k + 1 distinct tiles each hold a page whose (lower) key reaches it -- so every bisection
+    // below starts from [Lt, max] instead of [min, max] (up to 64 tiles: P <= 2048)
+    const int ntl = (P + 31) >> 5;
+    const bool use_tm = tmax_g != nullptr && P > k && ntl >= k + 1 && ntl <= 64;
+    int tm0 = -1, tm1 = -1;
+    if (use_tm) {
+        if (lane < ntl) tm0 = (int)__ldcg(tmax_g + lane);
+        if (lane + 32 < ntl) tm1 = (int)__ldcg(tmax_g + lane + 32);
+    }
     auto keyof = [&](const uint4 &x, int e) -> int {
         const uint32_t w = e < 2 ? x.x : e < 4 ? x.y : e < 6 ? x.z : x.w;
         return (e & 1) ? (int)(w >> 16) : (int)(w & 0xFFFFu);
     };
+    // keys past P read as 0 (below every real key: the ordered encoding of a finite or
+    // infinite bf16 score is >= 0x7F), so the bisection counts below need no validity mask
+    auto zero_tail = [&](uint4 (&a)[MAXV]) {
+#pragma unroll
+        for (int j = 0; j < MAXV; j++) {
+            const int base = (lane + 32 * j) * 8;
+            if (base < P && base + 8 > P) {
+                const int nk = P - base;  // 1..7 valid keys
+                uint32_t w[4] = {a[j].x, a[j].y, a[j].z, a[j].w};
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    const uint32_t m = (2 * q < nk ? 0x0000FFFFu : 0u) | (2 * q + 1 < nk ? 0xFFFF0000u : 0u);
+                    w[q] &= m;
+                }
+                a[j] = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+        }
+    };
+    // #keys >= t in this lane's vectors (t >= 1), two u16 keys per SIMD compare
+    auto cnt_ge = [&](const uint4 (&a)[MAXV], int t) -> int {
+        const uint32_t t16 = (uint32_t)t * 0x10001u;
+        int c = 0;
+#pragma unroll
+        for (int j = 0; j < MAXV; j++) {
+            c += __popc(__vcmpgeu2(a[j].x, t16)) + __popc(__vcmpgeu2(a[j].y, t16)) +
+                 __popc(__vcmpgeu2(a[j].z, t16)) + __popc(__vcmpgeu2(a[j].w, t16));
+        }
+        return c >> 4;
+    };
+    zero_tail(v);
+    sw_stamp(6);
+    int Lt = -1;
+    if (use_tm) {
+        int lo2 = __reduce_min_sync(0xffffffffu, (unsigned)(tm0 < 0 ? 0xFFFF : min(tm0, tm1 < 0 ? 0xFFFF : tm1)));
+        int hi2 = __reduce_max_sync(0xffffffffu, (unsigned)max(max(tm0, tm1), 0)) + 1;
+        while (hi2 - lo2 > 1) {
+            const int mid = (lo2 + hi2) >> 1;
+            const int c = __reduce_add_sync(0xffffffffu, (unsigned)((tm0 >= mid) + (tm1 >= mid)));
+            if (c >= k + 1) lo2 = mid; else hi2 = mid;
+        }
+        Lt = lo2;
+    }
+    sw_stamp(7);
     int bracket_lo = -1, bracket_hi = -1;  // bounded: the threshold lies in [A, B]
     if (hi_g) {
         const uint4 *h4 = reinterpret_cast<const uint4 *>(hi_g);
@@ -1005,6 +1072,7 @@ __device__ void select_warp(const uint16_t *__restrict__ keys_g, int P, int k,
             const int base = (lane + 32 * j) * 8;
             hv[j] = base < P ? __ldcg(h4 + lane + 32 * j) : make_uint4(0u, 0u, 0u, 0u);
         }
+        zero_tail(hv);
         // A = the (k+1)-th largest lower key, B = the k-th largest upper key: one bisection
         // pass per round counting both arrays against their own midpoints
         int amn = 0xFFFF, amx = 0, bmn = 0xFFFF, bmx = 0;
@@ -1020,22 +1088,14 @@ __device__ void select_warp(const uint16_t *__restrict__ keys_g, int P, int k,
         }
         int alo = __reduce_min_sync(0xffffffffu, amn), ahi = __reduce_max_sync(0xffffffffu, amx) + 1;
         int blo = __reduce_min_sync(0xffffffffu, bmn), bhi = __reduce_max_sync(0xffffffffu, bmx) + 1;
+        alo = max(alo, Lt);  // Lt <= A <= B (Lt < 0 without tile maxima)
+        blo = max(blo, Lt);
         if (P > k) {
             while (ahi - alo > 1 || bhi - blo > 1) {
                 const int am = (alo + ahi) >> 1, bm = (blo + bhi) >> 1;
-                int ca = 0, cb = 0;
-#pragma unroll
-                for (int j = 0; j < MAXV; j++) {
-                    const int base = (lane + 32 * j) * 8;
-#pragma unroll
-                    for (int e = 0; e < 8; e++) {
-                        const bool ok = base + e < P;
-                        ca += ok && keyof(v[j], e) >= am;
-                        cb += ok && keyof(hv[j], e) >= bm;
-                    }
-                }
-                ca = __reduce_add_sync(0xffffffffu, ca);
-                cb = __reduce_add_sync(0xffffffffu, cb);
+                // am, bm >= 1: the zeroed keys past P are never counted
+                const int ca = __reduce_add_sync(0xffffffffu, (unsigned)cnt_ge(v, max(am, 1)));
+                const int cb = __reduce_add_sync(0xffffffffu, (unsigned)cnt_ge(hv, max(bm, 1)));
                 if (ahi - alo > 1) { if (ca >= k + 1) alo = am; else ahi = am; }
                 if (bhi - blo > 1) { if (cb >= k) blo = bm; else bhi = bm; }
             }
@@ -1043,6 +1103,7 @@ __device__ void select_warp(const uint16_t *__restrict__ keys_g, int P, int k,
         const int A = P > k ? alo : 0, B = P > k ? blo : 0xFFFF;
         bracket_lo = A;
         bracket_hi = B;
+    sw_stamp(8);
         // the bracket pages, compacted (lane-major) into the warp's scratch list in rounds of
         // scratch_cap, resolved one lane per page, written back into the lower keys
         uint64_t fl = 0ull;  // bit 8 j + e: page (lane + 32 j) * 8 + e needs its exact key
@@ -1074,6 +1135,8 @@ __device__ void select_warp(const uint16_t *__restrict__ keys_g, int P, int k,
             }
             __syncwarp();
             const int nr = min(scratch_cap, total - r0);
+            // every row of the round requested before the first (latency-bound) exact sum
+            for (int i = lane; i < nr; i += 32) prefetch(scratch[i]);
             for (int i = lane; i < nr; i += 32) scratch[i] = exact(scratch[i]);
             __syncwarp();
             rk = first;
@@ -1097,6 +1160,7 @@ __device__ void select_warp(const uint16_t *__restrict__ keys_g, int P, int k,
             __syncwarp();
         }
     }
+    sw_stamp(9);
     int mn = 0xFFFF, mx = 0;
 #pragma unroll
     for (int j = 0; j < MAXV; j++) {
@@ -1106,6 +1170,7 @@ __device__ void select_warp(const uint16_t *__restrict__ keys_g, int P, int k,
             if (base + e < P) { const int x = keyof(v[j], e); mn = min(mn, x); mx = max(mx, x); }
     }
     mn = __reduce_min_sync(0xffffffffu, mn);
+    sw_stamp(11);
     mx = __reduce_max_sync(0xffffffffu, mx);
     if (P <= k) {  // _take_all (select.py:75-84)
         for (int i = lane; i < P; i += 32) {
@@ -1119,79 +1184,90 @@ __device__ void select_warp(const uint16_t *__restrict__ keys_g, int P, int k,
         return;
     }
     auto count_ge = [&](int t) -> int {
-        int c = 0;
-#pragma unroll
-        for (int j = 0; j < MAXV; j++) {
-            const int base = (lane + 32 * j) * 8;
-#pragma unroll
-            for (int e = 0; e < 8; e++) c += (base + e < P) && keyof(v[j], e) >= t;
-        }
-        return __reduce_add_sync(0xffffffffu, c);
+        return __reduce_add_sync(0xffffffffu, (unsigned)cnt_ge(v, max(t, 1)));
     };
     // thr = max t with #(keys >= t) >= k (bounded: within the bracket [A, B])
-    int lo = mn, hi = mx + 1;
+    int lo = max(mn, Lt), hi = mx + 1;  // Lt <= thr
     if (bracket_lo >= 0) { lo = max(lo, bracket_lo); hi = min(hi, bracket_hi + 1); }
     while (hi - lo > 1) {
         const int mid = (lo + hi) >> 1;
         if (count_ge(mid) >= k) lo = mid; else hi = mid;
     }
     const int thr = lo;
+    sw_stamp(12);
+    // counts and the ordered compaction on u16x2 SIMD compares (the keys past P are 0: never
+    // > or == thr, and below 0 means no key below thr); short loops, not per-key unrolled code
+    // -- this runs once per warp, so its instruction footprint is its cost
+    const uint32_t t16 = (uint32_t)thr * 0x10001u;
+    auto pack2 = [](uint32_t m) -> uint32_t { return (m & 1u) | ((m >> 15) & 2u); };
     int gt = 0, eq = 0, below = -1;
+    {
+        uint32_t blw = 0u;
 #pragma unroll
-    for (int j = 0; j < MAXV; j++) {
-        const int base = (lane + 32 * j) * 8;
+        for (int j = 0; j < MAXV; j++) {
+            const uint32_t w[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
 #pragma unroll
-        for (int e = 0; e < 8; e++) {
-            if (base + e >= P) continue;
-            const int x = keyof(v[j], e);
-            gt += x > thr;
-            eq += x == thr;
-            if (x < thr) below = max(below, x);
+            for (int q = 0; q < 4; q++) {
+                gt += __popc(__vcmpgtu2(w[q], t16));
+                eq += __popc(__vcmpeq2(w[q], t16));
+                blw = __vmaxu2(blw, w[q] & ~__vcmpgeu2(w[q], t16));
+            }
         }
+        gt >>= 4;
+        eq >>= 4;
+        const int b = (int)max(blw & 0xFFFFu, blw >> 16);
+        below = b > 0 ? b : -1;
     }
     const int gt_tot = __reduce_add_sync(0xffffffffu, gt);
     const int eq_tot = __reduce_add_sync(0xffffffffu, eq);
-    below = __reduce_max_sync(0xffffffffu, below);
+    below = (int)__reduce_max_sync(0xffffffffu, (unsigned)(below + 1)) - 1;
     const int budget = k - gt_tot;
+    sw_stamp(13);
     int run_sel = 0, run_eq = 0;
-#pragma unroll
-    for (int j = 0; j < MAXV; j++) {
-        if (j * 256 >= P) break;
-        const int base = (lane + 32 * j) * 8;
-        int myeq = 0;
-#pragma unroll
-        for (int e = 0; e < 8; e++) myeq += (base + e < P) && keyof(v[j], e) == thr;
-        int inc = myeq;
+    auto scan_excl = [&](int x, int &tot) -> int {
+        int inc = x;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int y = __shfl_up_sync(0xffffffffu, inc, o);
             if (lane >= o) inc += y;
         }
-        int tie = run_eq + inc - myeq;  // ties before this lane's vector
-        uint32_t selmask = 0u;
+        tot = __shfl_sync(0xffffffffu, inc, 31);
+        return inc - x;
+    };
 #pragma unroll
-        for (int e = 0; e < 8; e++) {
-            if (base + e >= P) continue;
-            const int x = keyof(v[j], e);
-            bool sl = x > thr;
-            if (x == thr) { sl = tie < budget; tie++; }
-            if (sl) selmask |= 1u << e;
+    for (int j = 0; j < MAXV; j++) {
+        if (j * 256 >= P) break;
+        const int base = (lane + 32 * j) * 8;
+        const uint32_t w[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+        uint32_t gm = 0u, em = 0u;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            gm |= pack2(__vcmpgtu2(w[q], t16)) << (2 * q);
+            em |= pack2(__vcmpeq2(w[q], t16)) << (2 * q);
         }
-        const int mine = __popc(selmask);
-        int sinc = mine;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, sinc, o);
-            if (lane >= o) sinc += y;
+        uint32_t keep = 0u;  // the ties this lane's vector may take: the lowest `allow` of em
+        if (__any_sync(0xffffffffu, em != 0u)) {
+            const int myeq = __popc(em);
+            int tot;
+            const int before = run_eq + scan_excl(myeq, tot);
+            int allow = min(max(budget - before, 0), myeq);
+            uint32_t e2 = em;
+            for (; allow > 0; allow--) {
+                keep |= e2 & (0u - e2);
+                e2 &= e2 - 1u;
+            }
+            run_eq += tot;
         }
-        int pos = run_sel + sinc - mine;
-#pragma unroll
-        for (int e = 0; e < 8; e++)
-            if (selmask & (1u << e)) ids[pos++] = base + e;
-        run_eq += __shfl_sync(0xffffffffu, inc, 31);
-        run_sel += __shfl_sync(0xffffffffu, sinc, 31);
+        const uint32_t selmask = gm | keep;
+        if (__any_sync(0xffffffffu, selmask != 0u)) {
+            int tot;
+            int pos = run_sel + scan_excl(__popc(selmask), tot);
+            for (uint32_t m = selmask; m; m &= m - 1u) ids[pos++] = base + __ffs(m) - 1;
+            run_sel += tot;
+        }
     }
     (void)lt;
+    sw_stamp(14);
     __syncwarp();
     for (int t = lane; t < k; t += 32) {
         const int li = ids[t];
