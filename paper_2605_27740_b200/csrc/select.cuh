@@ -589,25 +589,35 @@ __device__ bool select_cand(const uint16_t *__restrict__ skeys, const uint16_t *
                 run += t;
             }
             if (c) {
+                // the vector's candidates as an 8-bit mask, appended by a loop over its set bits
+                // (a short loop, not 8 unrolled copies: this code runs once per CTA, so its
+                // instruction footprint is most of its cost)
 #pragma unroll
                 for (int j = 0; j < VPT; j++) {
                     if (!cv[j]) continue;
                     const int v = vt + j;
-                    uint32_t w[4], wh[4];
-                    words(x[j], w);
+                    uint32_t wh[4], mk[4];
                     words(y[j], wh);
+                    vmask(v, mk);
+                    uint32_t bits = 0u;
 #pragma unroll
-                    for (int e = 0; e < 8; e++) {
-                        const int key = (e & 1) ? (int)(w[e >> 1] >> 16) : (int)(w[e >> 1] & 0xFFFFu);
-                        const int kh = (e & 1) ? (int)(wh[e >> 1] >> 16) : (int)(wh[e >> 1] & 0xFFFFu);
-                        if (v * 8 + e < P && kh >= L) {
-                            if (pos < kCandMax) {
-                                sh.cand[pos] = ((uint32_t)key << 16) | (uint32_t)(v * 8 + e);
-                                if (candhi) candhi[pos] = (uint16_t)kh;
-                            }
-                            pos++;
-                            mhi = max(mhi, kh);
+                    for (int q = 0; q < 4; q++) {
+                        const uint32_t ge = __vcmpgeu2(wh[q], L16) & mk[q];
+                        bits |= ((ge & 1u) | ((ge >> 15) & 2u)) << (2 * q);
+                    }
+                    const uint64_t lo64 = ((uint64_t)x[j].y << 32) | x[j].x, lo64b = ((uint64_t)x[j].w << 32) | x[j].z;
+                    const uint64_t hi64 = ((uint64_t)y[j].y << 32) | y[j].x, hi64b = ((uint64_t)y[j].w << 32) | y[j].z;
+                    for (; bits; bits &= bits - 1u) {
+                        const int e = __ffs(bits) - 1;
+                        const int sft = 16 * (e & 3);
+                        const int key = (int)(((e < 4 ? lo64 : lo64b) >> sft) & 0xFFFFu);
+                        const int kh = (int)(((e < 4 ? hi64 : hi64b) >> sft) & 0xFFFFu);
+                        if (pos < kCandMax) {
+                            sh.cand[pos] = ((uint32_t)key << 16) | (uint32_t)(v * 8 + e);
+                            if (candhi) candhi[pos] = (uint16_t)kh;
                         }
+                        pos++;
+                        mhi = max(mhi, kh);
                     }
                 }
             }
