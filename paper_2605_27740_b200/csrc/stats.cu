@@ -181,10 +181,12 @@ __device__ void alloc_scan(int32_t *__restrict__ page_table, const int *__restri
 // read back with pt_debug_append_prof().  8 stamps per unit.
 constexpr int kAppProfUnits = 8192;
 __device__ unsigned long long g_app_prof[kAppProfUnits * 8];
-__device__ __forceinline__ void app_stamp(bool on, int64_t u, int i) {
+// PT_APP_PROF=1: %globaltimer; PT_APP_PROF=2: %clock64 (per-unit phase durations only)
+__device__ __forceinline__ void app_stamp(bool on, int64_t u, int i, bool clk = false) {
     if (on) {
         unsigned long long t;
-        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        if (clk) asm volatile("mov.u64 %0, %clock64;" : "=l"(t));
+        else asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
         g_app_prof[u * 8 + i] = t;
     }
 }
@@ -208,10 +210,10 @@ __global__ void __launch_bounds__(256)
     const size_t per_warp = append_per_warp(S, D, ES);
     const int64_t u = (int64_t)blockIdx.x * wpc + warp;
     const bool pr = prof && lane == 0 && u < U && u < kAppProfUnits;
-    app_stamp(pr, u, 0);
+    app_stamp(pr, u, 0, prof == 2);
     pdl_trigger();
     pdl_wait();
-    app_stamp(pr, u, 1);
+    app_stamp(pr, u, 1, prof == 2);
     using Bits = typename std::conditional<DT == PT_F32, uint32_t, uint16_t>::type;
     // this unit's length (read before anyone advances it) and the new K/V row
     const int n = u < U ? seq_len[u] : 0;
@@ -250,7 +252,7 @@ __global__ void __launch_bounds__(256)
         return DT == PT_F32 ? (double)__uint_as_float((uint32_t)rows_s[i])
                             : (double)bf16_bits_to_f32((uint32_t)rows_s[i]);
     };
-    app_stamp(pr, u, 2);
+    app_stamp(pr, u, 2, prof == 2);
     if (u < U) {
         int pid;
         if (n % S == 0) {  // starts a page: the allocating CTA's result
@@ -260,7 +262,7 @@ __global__ void __launch_bounds__(256)
         } else {
             pid = page_table[u * Pmax + n / S];
         }
-        app_stamp(pr, u, 3);
+        app_stamp(pr, u, 3, prof == 2);
         if (pid >= 0) {
             const int row = n % S;
             const int64_t base = (int64_t)pid * S * D;
@@ -277,7 +279,7 @@ __global__ void __launch_bounds__(256)
                 }
             }
             __syncwarp();
-            app_stamp(pr, u, 4);
+            app_stamp(pr, u, 4, prof == 2);
             const int cnt = row + 1;
             // rows outer, the lane's DJ columns inner: DJ independent f64 chains in flight (each
             // column still sums its rows in row order, as numpy's axis-0 reduction)
@@ -314,9 +316,9 @@ __global__ void __launch_bounds__(256)
             const double vsum = np_sum_warp(var_s, D, lane);
             if (lane == 0) {
                 stds[u * Pmax + n / S] = __double2float_rn(__dsqrt_rn(vsum));
-                app_stamp(pr, u, 5);
+                app_stamp(pr, u, 5, prof == 2);
                 spin_flag(flag_read, false);  // every length is snapshotted (no data to acquire)
-                app_stamp(pr, u, 6);
+                app_stamp(pr, u, 6, prof == 2);
                 seq_len[u] = n + 1;
             }
         }
@@ -331,7 +333,7 @@ __global__ void __launch_bounds__(256)
             atomicExch(done, 0);
         }
     }
-    if (prof && lane == 0 && u < U && u < kAppProfUnits) app_stamp(true, u, 7);
+    if (prof && lane == 0 && u < U && u < kAppProfUnits) app_stamp(true, u, 7, prof == 2);
 }
 
 // ---------------------------------------------------------------------------
@@ -548,7 +550,7 @@ static int launch_append(const void *kn, const void *vn, void *kp, void *vp, int
     const int grid = (U + wpc - 1) / wpc;
     const int dj = (D + 31) / 32;
     const char *pe = getenv("PT_APP_PROF");
-    const int app_prof = (pe && *pe == '1') ? 1 : 0;
+    const int app_prof = (pe && (*pe == '1' || *pe == '2')) ? *pe - '0' : 0;
 #define PT_APP_CASE(DJ_)                                                                      \
     case DJ_: {                                                                               \
         static size_t configured = 0;                                                         \

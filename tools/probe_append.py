@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--ctx", type=int, default=131072)
     ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--clock", action="store_true", help="%%clock64 stamps: per-unit durations (cycles)")
     a = ap.parse_args()
     ns = argparse.Namespace(batch=a.batch, ctx=a.ctx, q_heads=32, kv_heads=8, head_dim=128,
                             page=16, budget=2048, stats_dtype="f32", warmup=3, steps=10)
@@ -37,7 +38,7 @@ def main():
     for _ in range(3):
         cache.append_batch(kn, vn)
     torch.cuda.synchronize()
-    os.environ["PT_APP_PROF"] = "1"
+    os.environ["PT_APP_PROF"] = "2" if a.clock else "1"
     per = []
     for _ in range(a.steps):
         cache.append_batch(kn, vn)
@@ -45,7 +46,10 @@ def main():
         buf = np.zeros(U * 8, dtype=np.uint64)
         _lib.check(_lib.load().pt_debug_append_prof(buf.ctypes.data, U * 8))
         t = buf.reshape(U, 8).astype(np.float64)
-        per.append((t - t[:, 0].min()) / 1000.0)
+        if a.clock:  # per unit, relative to its own entry; cycles -> us at 1.965 GHz
+            per.append((t - t[:, :1]) / 1965.0)
+        else:
+            per.append((t - t[:, 0].min()) / 1000.0)
     os.environ.pop("PT_APP_PROF")
     rel = np.stack(per)  # [steps, U, 8]
     out = {nm: {"median": float(np.median(rel[:, :, i])), "max": float(np.median(rel[:, :, i].max(axis=1)))}
