@@ -115,13 +115,12 @@ __device__ __forceinline__ float sa_exact_score(const float *row, const float *s
     return best;
 }
 
-// the same exact score for the warp-per-unit variant: the page's f32 row and the query rows
-// read straight from global memory (one lane per page; a handful of pages per unit)
+// the same with the page's f32 row from global memory (chunks of 32 dims in flight together)
+// and the query rows from shared memory (f32 [D][8], as sa_exact_score): the warp-per-unit
+// variant's resolution, one lane per page
 template <int D, int GG>
-__device__ __noinline__ float sa_exact_score_global(const float *row, const void *q, int q_dtype,
-                                                    int64_t qrow0, const float *lnp, float sd, int G) {
-    // the row in chunks of 8 float4 (32 dims) whose loads are all in flight together -- a
-    // load per step of the sequential sum would pay one memory latency per 4 dims
+__device__ __noinline__ float sa_exact_score_rowg(const float *row, const float *sq, const float *lnp,
+                                                  float sd, int G) {
     constexpr int CH = 8;
     static_assert((D / 4) % CH == 0, "row chunks");
     float acc[GG];
@@ -137,16 +136,15 @@ __device__ __noinline__ float sa_exact_score_global(const float *row, const void
             const float mv[4] = {m4[i].x, m4[i].y, m4[i].z, m4[i].w};
 #pragma unroll
             for (int e = 0; e < 4; e++) {
-#pragma unroll
-                for (int g = 0; g < GG; g++) {
-                    if (g < G) {
-                        const int64_t qi = (qrow0 + g) * D + 4 * (c0 + i) + e;
-                        const float qv = q_dtype == PT_BF16
-                                             ? bf16_bits_to_f32(__ldg(static_cast<const uint16_t *>(q) + qi))
-                                             : __ldg(static_cast<const float *>(q) + qi);
-                        acc[g] = __fadd_rn(acc[g], __fmul_rn(qv, mv[e]));
-                    }
+                const float4 *q4 = reinterpret_cast<const float4 *>(sq + (4 * (c0 + i) + e) * 8);
+                const float4 qa = q4[0];
+                float qv[8] = {qa.x, qa.y, qa.z, qa.w, 0.f, 0.f, 0.f, 0.f};
+                if constexpr (GG > 4) {
+                    const float4 qc = q4[1];
+                    qv[4] = qc.x; qv[5] = qc.y; qv[6] = qc.z; qv[7] = qc.w;
                 }
+#pragma unroll
+                for (int g = 0; g < GG; g++) acc[g] = __fadd_rn(acc[g], __fmul_rn(qv[g], mv[e]));
             }
         }
     }
@@ -855,6 +853,22 @@ __global__ void __launch_bounds__(128, 1) k_select_attend_warp(const __grid_cons
             qb[ks][1] = b1;
         }
     }
+    // bounded: the query rows as f32 [D][8] at the end of the (still unused) ring, for the
+    // resolution's exact sums (not written by the scorer: before the PDL wait)
+    float *qsw = reinterpret_cast<float *>(ring + (size_t)nstage * STAGE_BYTES) - D * 8;
+    if constexpr (BND) {
+        for (int i = lane; i < D * 8; i += 32) {
+            const int d = i >> 3, g = i & 7;
+            float x = 0.f;
+            if (g < p.G) {
+                const int64_t e = (u * p.G + g) * (int64_t)D + d;
+                x = p.q_dtype == PT_BF16 ? bf16_bits_to_f32(static_cast<const uint16_t *>(p.q)[e])
+                                         : static_cast<const float *>(p.q)[e];
+            }
+            qsw[i] = x;
+        }
+        __syncwarp();
+    }
     pdl_wait();
     if (prof) g_sa_prof[u * kSAProfN + 1] = gtimer(pclk);
     if (P == 0) {
@@ -866,15 +880,14 @@ __global__ void __launch_bounds__(128, 1) k_select_attend_warp(const __grid_cons
         auto exact = [&](int pg) -> int {
             const float *row = p.rows32 + ((int64_t)u * p.Pmax + pg) * D;
             const float sd = __ldg(p.stds + u * (int64_t)p.Pmax + pg);
-            const float best = p.G <= 4
-                ? sa_exact_score_global<D, 4>(row, p.q, p.q_dtype, u * p.G, p.lamnorm + u * 8, sd, p.G)
-                : sa_exact_score_global<D, 8>(row, p.q, p.q_dtype, u * p.G, p.lamnorm + u * 8, sd, p.G);
+            const float best = p.G <= 4 ? sa_exact_score_rowg<D, 4>(row, qsw, p.lamnorm + u * 8, sd, p.G)
+                                        : sa_exact_score_rowg<D, 8>(row, qsw, p.lamnorm + u * 8, sd, p.G);
             return (int)encode_ordered(f32_to_bf16_rne(best));
         };
         select_warp<kSWMaxV>(p.keys + u * (int64_t)p.Pmax, P, k, p.page_table + u * p.Pmax,
                              p.sel + u * (int64_t)k, p.sel_logical ? p.sel_logical + u * (int64_t)k : nullptr,
                              p.n_sel + u, p.kth + u, p.kplus1 + u, ids, p.keys_hi + u * (int64_t)p.Pmax,
-                             exact, reinterpret_cast<int *>(ring), (int)(nstage * STAGE_BYTES / 4),
+                             exact, reinterpret_cast<int *>(ring), (int)(nstage * STAGE_BYTES / 4) - D * 8,
                              p.tile_max ? p.tile_max + u * (int64_t)(p.Pmax >> 5) : nullptr,
                              prof && pclk ? &g_sa_prof[u * kSAProfN] : nullptr,
                              [&](int pg) {  // the page's f32 row and std into L1

@@ -132,22 +132,18 @@ class DecodeEngine:
         selecting CTA and needs the CTA-per-unit selection: worth it when the f32-means bytes
         it saves (at ~6.5 TB/s) clearly exceed that (>= 25 us: cfg3 saves ~80 us; cfg2 (one
         sequence) < 1 us) and -- for the CTA-per-unit selection -- the tile-maximum bound
-        applies (k < pages / 32; profiles/r02/sweep_r02b.jsonl); the warp-per-unit selection
-        (thousands of short units, small k) brackets in registers.  PT_BOUNDED=1 forces it."""
+        applies (k < pages / 32; profiles/r02/sweep_r02b.jsonl) -- for the CTA-per-unit and
+        the warp-per-unit selection alike (cfg4: 107.3 vs 118.5 us/step, r02g).  PT_BOUNDED=1
+        forces it."""
         if os.environ.get("PT_BOUNDED", "") == "1":
             return True
         U, P, D = cache.num_units, cache.Pmax, cache.layout.head_dim
-        sms = torch.cuda.get_device_properties(cache.device).multi_processor_count
-        warp_path = U >= 4 * sms and self.k <= 64 and P <= 2048
         saved_us = U * P * D * 2 / 6.5e6
         # the selection's lower bound needs k + 1 tiles of 32 pages (else every uncertain page
         # is resolved: k = ctx/8 at 32K-128K measured 1.4-1.8x slower than exact), and the
         # bounded selection's shared memory keeps two CTAs per SM up to 16384 pages
         tile_bound = P // 32 >= self.k + 1 and P <= 16384
-        # the warp-per-unit path has a bounded variant (bracket by bisection in registers) but
-        # it measured slower than exact scoring (cfg4: 134.2 vs 130.0 us/step; its selection is
-        # issue-bound at ~7 warps per SM): PT_BOUNDED=1 only
-        return not warp_path and tile_bound and saved_us >= 25.0
+        return tile_bound and saved_us >= 25.0
 
     # ------------------------------------------------------------------
     def _q(self, q: torch.Tensor) -> tuple[torch.Tensor, int]:
