@@ -287,8 +287,9 @@ template <int G, int D>
 static int sb_nst(const BoundedScoreParams &sp, cudaStream_t st) {
     // ring depth x CTAs per SM (PT_SB_NST / PT_SB_CTAS: tuning)
     // measured (tools/probe_score.py): D = 128: 2 stages x 2 CTAs (cfg3 82.5 us = 6.66 TB/s; deeper
-    // rings drop to one CTA per SM: 141-150 us); D = 64: 3 stages x 3 CTAs (cfg4 53.5 vs 69.7 us)
-    const int nst = sb_env("PT_SB_NST", D == 64 ? 3 : 2), ctas = sb_env("PT_SB_CTAS", D == 64 ? 3 : 2);
+    // rings drop to one CTA per SM: 141-150 us); D = 64: 2 stages x 5 CTAs (the cfg4 step 101.4
+    // vs 107.5 us with 3 x 3, 103.2 with 2 x 4, 116.0 with 2 x 3: profiles/r02/score_d64_r02i.txt)
+    const int nst = sb_env("PT_SB_NST", 2), ctas = sb_env("PT_SB_CTAS", D == 64 ? 5 : 2);
     switch (nst) {
         case 3: return sb_launch<G, D, 3>(sp, ctas, st);
         case 4: return sb_launch<G, D, 4>(sp, ctas, st);
