@@ -1059,6 +1059,21 @@ __device__ void select_warp(const uint16_t *__restrict__ keys_g, int P, int k,
         }
         return c >> 4;
     };
+    // min (over the non-zero = real keys) and max of this lane's keys, two per SIMD op
+    auto minmax = [&](const uint4 (&a)[MAXV], int &mn_, int &mx_) {
+        uint32_t lo = 0xFFFFFFFFu, hi = 0u;
+#pragma unroll
+        for (int j = 0; j < MAXV; j++) {
+            const uint32_t w[4] = {a[j].x, a[j].y, a[j].z, a[j].w};
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                hi = __vmaxu2(hi, w[q]);
+                lo = __vminu2(lo, w[q] | __vcmpeq2(w[q], 0u));
+            }
+        }
+        mn_ = (int)min(lo & 0xFFFFu, lo >> 16);
+        mx_ = (int)max(hi & 0xFFFFu, hi >> 16);
+    };
     zero_tail(v);
     sw_stamp(6);
     int Lt = -1;
@@ -1085,17 +1100,9 @@ __device__ void select_warp(const uint16_t *__restrict__ keys_g, int P, int k,
         zero_tail(hv);
         // A = the (k+1)-th largest lower key, B = the k-th largest upper key: one bisection
         // pass per round counting both arrays against their own midpoints
-        int amn = 0xFFFF, amx = 0, bmn = 0xFFFF, bmx = 0;
-#pragma unroll
-        for (int j = 0; j < MAXV; j++) {
-            const int base = (lane + 32 * j) * 8;
-#pragma unroll
-            for (int e = 0; e < 8; e++)
-                if (base + e < P) {
-                    const int x = keyof(v[j], e), y = keyof(hv[j], e);
-                    amn = min(amn, x); amx = max(amx, x); bmn = min(bmn, y); bmx = max(bmx, y);
-                }
-        }
+        int amn, amx, bmn, bmx;
+        minmax(v, amn, amx);
+        minmax(hv, bmn, bmx);
         int alo = __reduce_min_sync(0xffffffffu, amn), ahi = __reduce_max_sync(0xffffffffu, amx) + 1;
         int blo = __reduce_min_sync(0xffffffffu, bmn), bhi = __reduce_max_sync(0xffffffffu, bmx) + 1;
         alo = max(alo, Lt);  // Lt <= A <= B (Lt < 0 without tile maxima)
@@ -1171,14 +1178,8 @@ __device__ void select_warp(const uint16_t *__restrict__ keys_g, int P, int k,
         }
     }
     sw_stamp(9);
-    int mn = 0xFFFF, mx = 0;
-#pragma unroll
-    for (int j = 0; j < MAXV; j++) {
-        const int base = (lane + 32 * j) * 8;
-#pragma unroll
-        for (int e = 0; e < 8; e++)
-            if (base + e < P) { const int x = keyof(v[j], e); mn = min(mn, x); mx = max(mx, x); }
-    }
+    int mn, mx;
+    minmax(v, mn, mx);
     mn = __reduce_min_sync(0xffffffffu, mn);
     sw_stamp(11);
     mx = __reduce_max_sync(0xffffffffu, mx);
@@ -1233,21 +1234,15 @@ __device__ void select_warp(const uint16_t *__restrict__ keys_g, int P, int k,
     below = (int)__reduce_max_sync(0xffffffffu, (unsigned)(below + 1)) - 1;
     const int budget = k - gt_tot;
     sw_stamp(13);
-    int run_sel = 0, run_eq = 0;
-    auto scan_excl = [&](int x, int &tot) -> int {
-        int inc = x;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += y;
-        }
-        tot = __shfl_sync(0xffffffffu, inc, 31);
-        return inc - x;
-    };
+    // ordered compaction in one sweep: per (lane, vector j) 8-bit masks of the keys > thr and
+    // == thr; the ties a vector may take and every vector's output offset come from warp scans
+    // of per-j counts packed in 16-bit fields (4 vectors per 64-bit word) -- a handful of
+    // shuffles for all j instead of two dependent scans per j
+    static_assert(MAXV <= 8, "packed per-vector counts");
+    uint64_t gmp = 0ull, emp = 0ull;   // byte j: the vector's > / == masks
+    uint64_t ec[2] = {0ull, 0ull};     // 16-bit field j: #(== thr) in vector j
 #pragma unroll
     for (int j = 0; j < MAXV; j++) {
-        if (j * 256 >= P) break;
-        const int base = (lane + 32 * j) * 8;
         const uint32_t w[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
         uint32_t gm = 0u, em = 0u;
 #pragma unroll
@@ -1255,25 +1250,54 @@ __device__ void select_warp(const uint16_t *__restrict__ keys_g, int P, int k,
             gm |= pack2(__vcmpgtu2(w[q], t16)) << (2 * q);
             em |= pack2(__vcmpeq2(w[q], t16)) << (2 * q);
         }
-        uint32_t keep = 0u;  // the ties this lane's vector may take: the lowest `allow` of em
-        if (__any_sync(0xffffffffu, em != 0u)) {
-            const int myeq = __popc(em);
-            int tot;
-            const int before = run_eq + scan_excl(myeq, tot);
-            int allow = min(max(budget - before, 0), myeq);
-            uint32_t e2 = em;
+        gmp |= (uint64_t)gm << (8 * j);
+        emp |= (uint64_t)em << (8 * j);
+        ec[j >> 2] |= (uint64_t)__popc(em) << (16 * (j & 3));
+    }
+    auto scan64 = [&](uint64_t x) -> uint64_t {  // inclusive, field-wise (no field overflows)
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        return x;
+    };
+    auto f16 = [](uint64_t x, int j) -> int { return (int)((x >> (16 * (j & 3))) & 0xFFFFull); };
+    uint64_t sc[2] = {0ull, 0ull};  // 16-bit field j: keys this vector selects
+    uint64_t keepp = 0ull;          // byte j: the ties vector j takes
+    {
+        const uint64_t ei0 = scan64(ec[0]), ei1 = scan64(ec[1]);
+        const uint64_t et0 = __shfl_sync(0xffffffffu, ei0, 31), et1 = __shfl_sync(0xffffffffu, ei1, 31);
+        int before_j = 0;  // ties in vectors j' < j over all lanes
+#pragma unroll
+        for (int j = 0; j < MAXV; j++) {
+            const uint64_t inc = j < 4 ? ei0 : ei1, tot = j < 4 ? et0 : et1, own = ec[j >> 2];
+            const int mine = f16(own, j);
+            const int before = before_j + f16(inc, j) - mine;
+            int allow = min(max(budget - before, 0), mine);
+            uint32_t e2 = (uint32_t)((emp >> (8 * j)) & 0xFFu), keep = 0u;
             for (; allow > 0; allow--) {
                 keep |= e2 & (0u - e2);
                 e2 &= e2 - 1u;
             }
-            run_eq += tot;
+            keepp |= (uint64_t)keep << (8 * j);
+            const int cnt = __popc((uint32_t)((gmp >> (8 * j)) & 0xFFu)) + __popc(keep);
+            sc[j >> 2] |= (uint64_t)cnt << (16 * (j & 3));
+            before_j += f16(tot, j);
         }
-        const uint32_t selmask = gm | keep;
-        if (__any_sync(0xffffffffu, selmask != 0u)) {
-            int tot;
-            int pos = run_sel + scan_excl(__popc(selmask), tot);
-            for (uint32_t m = selmask; m; m &= m - 1u) ids[pos++] = base + __ffs(m) - 1;
-            run_sel += tot;
+    }
+    {
+        const uint64_t si0 = scan64(sc[0]), si1 = scan64(sc[1]);
+        const uint64_t st0 = __shfl_sync(0xffffffffu, si0, 31), st1 = __shfl_sync(0xffffffffu, si1, 31);
+        int base_j = 0;  // selected keys in vectors j' < j over all lanes
+#pragma unroll
+        for (int j = 0; j < MAXV; j++) {
+            const uint64_t inc = j < 4 ? si0 : si1, tot = j < 4 ? st0 : st1, own = sc[j >> 2];
+            uint32_t m = (uint32_t)(((gmp | keepp) >> (8 * j)) & 0xFFu);
+            int pos = base_j + f16(inc, j) - f16(own, j);
+            const int base = (lane + 32 * j) * 8;
+            for (; m; m &= m - 1u) ids[pos++] = base + __ffs(m) - 1;
+            base_j += f16(tot, j);
         }
     }
     (void)lt;

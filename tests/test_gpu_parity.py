@@ -830,3 +830,43 @@ def test_wide_gqa_group_vs_oracle(cuda, oracle, G, dtype, tol):
         assert set(sels[u].physical_ids.tolist()) == set(ref["sel"][u, : ref["n_sel"][u]].tolist())
     got = np.stack([o.out for o in outs]).reshape(-1, G, D)
     np.testing.assert_allclose(got, ref["out"], rtol=tol, atol=tol)
+
+
+@pytest.mark.parametrize("bounded", [False, True])
+def test_warp_per_unit_selection_ties_equal_oracle(cuda, oracle, monkeypatch, bounded):
+    """The warp-per-unit selection under heavy ties (every page of a unit one score; a few
+    score levels; pages straddling the threshold with equal keys): ties go to the lowest
+    logical indices (select.py:87-115), kth / kplus1 as the reference's -- exact and bounded."""
+    pt = _pt()
+    monkeypatch.setenv("PT_SA_WARP", "1")
+    if bounded:
+        monkeypatch.setenv("PT_BOUNDED", "1")
+    rng = np.random.default_rng(31)
+    B, H, G, D, S, k = 4, 2, 4, 128, 16, 24
+    n = 16 * 700 + 5
+    U = B * H
+    row = rng.standard_normal(D).astype(np.float32)
+    K = np.broadcast_to(row, (U, n, D)).copy()
+    lev = rng.integers(-2, 3, (U, -(-n // S), 1, 1)).astype(np.float32) * 0.25
+    # odd units: five score levels by page (many pages tie at the threshold); even: all equal
+    K[1::2] += np.repeat(lev[1::2][:, :, 0, 0], S, axis=1)[:, :n, None]
+    V = rng.standard_normal((U, n, D)).astype(np.float32)
+    Pcap = -(-n // S) + 4
+    layout = pt.CacheLayout(num_kv_heads=H, head_dim=D, page_size=S, max_pages=U * Pcap)
+    cache = pt.PagedKvCache(layout, batch=B, dtype=torch.bfloat16, max_pages_per_head=Pcap)
+    cache.extend_units(torch.from_numpy(K), torch.from_numpy(V))
+    eng = pt.DecodeEngine(cache, G, k, keep_logical=True)
+    assert eng.bounded == bounded
+    q = torch.from_numpy(rng.standard_normal((U * G, D)).astype(np.float32)).cuda().to(torch.bfloat16)
+    eng.step(q)
+    torch.cuda.synchronize()
+    kpool, vpool, table, seq = readback(cache)
+    means, stds = oracle.build_stats(kpool, table, seq, S)
+    ref = oracle.decode_units(q.to(torch.float32).cpu().numpy().reshape(-1, G, D), kpool, vpool,
+                              table, seq, means, stds, k, 0.5, 1.0 / math.sqrt(D), S)
+    sel, nsel = eng.sel.cpu().numpy(), eng.n_sel.cpu().numpy()
+    for u in range(U):
+        assert nsel[u] == ref["n_sel"][u]
+        assert set(sel[u, : nsel[u]].tolist()) == set(ref["sel"][u, : nsel[u]].tolist())
+    np.testing.assert_array_equal(eng.kth.cpu().numpy(), ref["kth"])
+    np.testing.assert_array_equal(eng.kplus1.cpu().numpy(), ref["kplus1"])
