@@ -1123,15 +1123,21 @@ __device__ void select_warp(const uint16_t *__restrict__ keys_g, int P, int k,
     sw_stamp(8);
         // the bracket pages, compacted (lane-major) into the warp's scratch list in rounds of
         // scratch_cap, resolved one lane per page, written back into the lower keys
-        uint64_t fl = 0ull;  // bit 8 j + e: page (lane + 32 j) * 8 + e needs its exact key
+        // bit 8 j + e: page (lane + 32 j) * 8 + e needs its exact key -- interval not one key
+        // and meeting [A, B] (the zeroed keys past P have lo == hi); two keys per SIMD compare
+        uint64_t fl = 0ull;
+        const uint32_t A16 = (uint32_t)A * 0x10001u, B16 = (uint32_t)min(B, 0xFFFF) * 0x10001u;
 #pragma unroll
         for (int j = 0; j < MAXV; j++) {
-            const int base = (lane + 32 * j) * 8;
+            const uint32_t lw[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+            const uint32_t hw[4] = {hv[j].x, hv[j].y, hv[j].z, hv[j].w};
+            uint32_t m = 0u;
 #pragma unroll
-            for (int e = 0; e < 8; e++) {
-                const int lo_k = keyof(v[j], e), hi_k = keyof(hv[j], e);
-                if (base + e < P && lo_k != hi_k && hi_k >= A && lo_k <= B) fl |= 1ull << (8 * j + e);
+            for (int q = 0; q < 4; q++) {
+                const uint32_t f = ~__vcmpeq2(lw[q], hw[q]) & __vcmpgeu2(hw[q], A16) & __vcmpleu2(lw[q], B16);
+                m |= ((f & 1u) | ((f >> 15) & 2u)) << (2 * q);
             }
+            fl |= (uint64_t)m << (8 * j);
         }
         const int nf = __popcll(fl);
         int incl = nf;
