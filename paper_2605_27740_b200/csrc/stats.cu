@@ -544,7 +544,10 @@ static int launch_append(const void *kn, const void *vn, void *kp, void *vp, int
     int wpc = (int)((200 * 1024) / per_warp);
     // spread the latency-bound per-unit warps over more SMs; thousands of units: keep the
     // whole grid resident in one wave
-    const int wmax = U >= 2048 ? 8 : 4;
+    int wmax = U >= 2048 ? 8 : 4;
+    if (const char *we = getenv("PT_APP_WPC")) {  // tuning
+        if (atoi(we) >= 1) wmax = atoi(we);
+    }
     if (wpc > wmax) wpc = wmax;
     const size_t smem = per_warp * wpc;
     const int grid = (U + wpc - 1) / wpc;
