@@ -171,6 +171,26 @@ PT_API int pt_score_bounded(const void *q, int q_dtype, const float *lamnorm, co
                             int u0, int nu, int G, int D, int S, int Pmax, uint16_t *keys_lo,
                             uint16_t *keys_hi, uint16_t *tile_max, void *stream);
 
+/* The decode step's K1b + K2b with the scorer overlapping the append (no reference
+ * counterpart: an internal schedule of DecodeEngine.step).  pt_append_step = pt_append that
+ * also publishes, in step_sync (int32[4], zero-initialised once, one per step sequence),
+ * when every unit's length is snapshotted and when all its stores are visible;
+ * pt_score_bounded_step, launched right after it on the same stream with the same
+ * slot_scratch / step_sync (all U units), streams every 32-page tile except the units' tail
+ * tiles from the snapshot lengths + 1 while the append runs, then the tail tiles.  Same
+ * keys as pt_append + pt_score_bounded.  The two calls must be paired (PT_ERR_UNSUPPORTED
+ * from the scorer where pt_score_bounded is unsupported: check before appending). */
+PT_API int pt_append_step(const void *k_new, const void *v_new, void *k_pool, void *v_pool,
+                          int kv_dtype, int32_t *page_table, int32_t *seq_len, int U, int S, int D,
+                          int Pmax, void *means, int stats_dtype, float *stds, int32_t *pool_state,
+                          const int32_t *free_list, int32_t *slot_scratch, void *mirror,
+                          int32_t *step_sync, void *stream);
+PT_API int pt_score_bounded_step(const void *q, int q_dtype, const float *lamnorm,
+                                 const float *qnorm, const void *mirror, const float *stds,
+                                 const int32_t *seq_len, int U, int G, int D, int S, int Pmax,
+                                 uint16_t *keys_lo, uint16_t *keys_hi, uint16_t *tile_max,
+                                 const int32_t *slot_scratch, int32_t *step_sync, void *stream);
+
 /* K2+K3 fused: pt_score followed by pt_topk in ONE launch -- the last CTA to finish a unit's
  * pages selects that unit's top-k while other CTAs keep scoring (same outputs as the two
  * separate calls).  counters: int32 [U] zero-initialised once (self-resetting).  Returns

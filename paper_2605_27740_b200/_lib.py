@@ -52,6 +52,10 @@ _PROTOS = {
     "pt_lam_norms_chained": (_i, [_vp, _i, _vp, _i, _i, _i, _f, _vp, _vp, _vp]),
     "pt_score_bounded": (_i, [_vp, _i, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _vp, _vp,
                               _vp, _vp]),
+    "pt_score_bounded_step": (_i, [_vp, _i, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _vp, _vp,
+                                   _vp, _vp, _vp, _vp]),
+    "pt_append_step": (_i, [_vp, _vp, _vp, _vp, _i, _vp, _vp, _i, _i, _i, _i, _vp, _i, _vp, _vp,
+                            _vp, _vp, _vp, _vp, _vp]),
     "pt_score_prenorm": (_i, [_vp, _i, _vp, _vp, _i, _vp, _vp, _i, _i, _i, _i, _i, _vp, _vp, _vp,
                               _vp]),
     "pt_topk": (_i, [_vp, _vp, _vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp]),

@@ -39,7 +39,28 @@ struct BoundedScoreParams {
     uint16_t *tile_max;           // [U][Pmax/32]: max klo of each tile
     int U, S, Pmax;
     int prof;  // PT_SB_PROF=1: per-CTA %globaltimer stamps (entry, after the PDL wait, exit)
+    // early mode (pt_score_bounded_step): no PDL wait for the append -- the lengths come from
+    // the append's snapshot (+ the one row it appends), the tiles streamed before the append
+    // has finished are every tile but the units' tail tiles, which each warp defers to the end
+    // of its range; step_sync = {append: lengths snapshotted, append: stores visible, scorer
+    // steps completed, scorer CTA ticket} (see pt_append_step)
+    const int32_t *snap;
+    int32_t *sync;
 };
+
+__device__ __forceinline__ int sb_ld_acquire(const int32_t *p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ int sb_ld_relaxed(const int32_t *p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void sb_spin_until(const int32_t *p, int target) {
+    while (sb_ld_acquire(p) < target) __nanosleep(64);
+}
 
 constexpr int kSBProfCtas = 2048;
 __device__ unsigned long long g_sb_prof[kSBProfCtas * 4];
@@ -64,12 +85,12 @@ struct SBCfg {
 };
 
 __host__ __device__ __forceinline__ size_t sb_hdr_bytes(int U) {
-    const size_t ps = ((size_t)(U + 1) * 4 + 15) & ~(size_t)15;
+    const size_t ps = ((size_t)(2 * U + 1) * 4 + 15) & ~(size_t)15;  // tile prefix | pages
     return (ps + (size_t)kSBWarps * 8 * 8 + 127) & ~(size_t)127;
 }
 
 template <int G, int D, int NST>
-__global__ void __launch_bounds__(kSBWarps * 32) k_score_bounded(const BoundedScoreParams prm) {
+__global__ void __launch_bounds__(kSBWarps * 32, 1) k_score_bounded(const BoundedScoreParams prm) {
     using C = SBCfg<G, D, NST>;
     constexpr int KS = D / 16;
     extern __shared__ __align__(1024) char smem[];
@@ -79,7 +100,8 @@ __global__ void __launch_bounds__(kSBWarps * 32) k_score_bounded(const BoundedSc
     const int W = gridDim.x * kSBWarps;
     const int gw = blockIdx.x * kSBWarps + warp;
     int *Tp = reinterpret_cast<int *>(smem);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + (((size_t)(U + 1) * 4 + 15) & ~(size_t)15)) + warp * 8;
+    int *Pu = Tp + U + 1;  // pages per unit
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + (((size_t)(2 * U + 1) * 4 + 15) & ~(size_t)15)) + warp * 8;
     char *ring = smem + sb_hdr_bytes(U) + (size_t)warp * C::PER_WARP;
     char *uhdrs = ring + NST * C::TILE;
     char *thdrs = uhdrs + C::NHU * C::UHDR;
@@ -89,15 +111,38 @@ __global__ void __launch_bounds__(kSBWarps * 32) k_score_bounded(const BoundedSc
         for (int i = 0; i < NST; i++) mbar_init(&bars[i], 1);
         fence_mbar_init();
     }
-    pdl_wait();
-    pdl_trigger();
+    const bool early = prm.sync != nullptr;
+    __shared__ int s_my;
+    int my = 0;
+    if (!early) {
+        pdl_wait();
+        pdl_trigger();
+    } else {
+        // the append (the previous kernel) publishes the snapshot of the lengths right after
+        // its own PDL wait: the predecessor's readers of the keys / norms are done by then
+        if (threadIdx.x == 0) {
+            const int m = sb_ld_acquire(prm.sync + 2) + 1;
+            sb_spin_until(prm.sync, m);
+            s_my = m;
+        }
+        __syncthreads();
+        my = s_my;
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // bulk copies after the acquire
+    }
+    // unit length: early mode -- the append's snapshot + its row (the kernel reads nothing
+    // the running append writes before step_sync[1])
+    auto unit_len = [&](int uu) -> int {
+        return early ? __ldcg(prm.snap + uu) + 1 : __ldcg(prm.seq_len + uu);
+    };
     if (prof) g_sb_prof[blockIdx.x * 4 + 1] = sb_gtimer();
     {  // tile prefix over units (block scan)
         __shared__ int wsum[kSBWarps];
         int carry = 0;
         for (int b0 = 0; b0 < U; b0 += kSBWarps * 32) {
             const int uu = b0 + threadIdx.x;
-            const int nt = uu < U ? ((prm.seq_len[uu] + S - 1) / S + 31) >> 5 : 0;
+            const int np = uu < U ? (unit_len(uu) + S - 1) / S : 0;
+            if (uu < U) Pu[uu] = np;
+            const int nt = (np + 31) >> 5;
             int inc = nt;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -119,32 +164,70 @@ __global__ void __launch_bounds__(kSBWarps * 32) k_score_bounded(const BoundedSc
         if (threadIdx.x == 0) Tp[U] = carry;
     }
     __syncthreads();
-    struct Cur { int u, t, g; };
+    struct Cur { int u, t, g, pass; };
     // static contiguous per-warp tile ranges: measured against dynamic chunk grabbing from a
     // global counter (2-8 tiles per grab: 178-205 vs 168.5 us/step at cfg3) and round-robin
     // chunks of 1-16 tiles (179-260 us/step) -- both finish units in tile order, both slower
     const int64_t T = Tp[U];
     const int64_t g0 = (int64_t)gw * T / W, g_end = (int64_t)(gw + 1) * T / W;
-    Cur pc{U, 0, 0};
+    // early mode: pass 0 = the range's tiles but the units' tail tiles (the append may still
+    // be rewriting them), pass 1 = those tail tiles, after step_sync[1]
+    Cur pc{U, 0, 0, 0};
+    int u_first = U;
     if (g0 < g_end) {
         int lo = 0, hi = U;  // last unit with Tp[u] <= g0
         while (hi - lo > 1) {
             const int mid = (lo + hi) >> 1;
             if (Tp[mid] <= g0) lo = mid; else hi = mid;
         }
-        pc = Cur{lo, (int)(g0 - Tp[lo]), (int)g0};
+        pc = Cur{lo, (int)(g0 - Tp[lo]), (int)g0, 0};
+        u_first = lo;
     }
-    auto advance = [&](Cur &c) {
-        c.g++;
-        if (c.g >= g_end) { c.u = U; return; }
-        c.t++;
-        while (c.t >= Tp[c.u + 1] - Tp[c.u]) { c.u++; c.t = 0; }
+    auto nt_of = [&](int uu) { return Tp[uu + 1] - Tp[uu]; };
+    auto settle = [&](Cur &c) {  // forward to the next tile of this warp's visiting order
+        for (;;) {
+            if (c.u >= U) return;
+            if (c.pass == 0) {
+                if (c.g >= g_end) {
+                    if (!early) { c.u = U; return; }
+                    c.pass = 1;
+                    c.u = u_first;
+                    continue;
+                }
+                while (c.t >= nt_of(c.u)) { c.u++; c.t = 0; }
+                if (!early || c.t != nt_of(c.u) - 1) return;
+                c.g++;
+                c.t++;
+            } else {
+                while (c.u < U && nt_of(c.u) == 0) c.u++;
+                if (c.u >= U) return;
+                const int64_t gt = (int64_t)Tp[c.u + 1] - 1;
+                if (gt >= g_end) { c.u = U; return; }
+                if (gt < g0) { c.u++; continue; }
+                c.t = nt_of(c.u) - 1;
+                c.g = (int)gt;
+                return;
+            }
+        }
     };
+    auto advance = [&](Cur &c) {
+        if (c.pass == 0) { c.g++; c.t++; } else { c.u++; }
+        settle(c);
+    };
+    settle(pc);
     Cur cc = pc;
     int issued = 0, p_run = -1, p_unit = -1;
+    bool tails_ok = !early, triggered = !early;
     const uint64_t evict_first = l2_evict_first_policy();
     auto fill = [&](int consumed) {
         while (pc.u < U && issued < consumed + NST) {
+            if (pc.pass == 1 && !tails_ok) {  // the append's stores are visible from here on
+                if (lane == 0) sb_spin_until(prm.sync + 1, my);
+                __syncwarp();
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                tails_ok = true;
+                if (!triggered) { pdl_trigger(); triggered = true; }
+            }
             const int slot = issued % NST;
             const bool new_run = pc.u != p_unit;
             if (new_run) { p_run++; p_unit = pc.u; }
@@ -171,17 +254,25 @@ __global__ void __launch_bounds__(kSBWarps * 32) k_score_bounded(const BoundedSc
     const int gq = lane >> 2;
     uint32_t qb[KS][2];
     float ln0 = 0.f, ln1 = 0.f, qn0 = 0.f, qn1 = 0.f;
-    int consumed = 0, c_run = -1, c_unit = -1;
+    int consumed = 0, c_run = -1, c_unit = -1, c_pages = 0;
     // ldmatrix row address of this lane within a tile: matrix mi = lane / 8 holds pages
     // (mi & 1) * 8 + lane % 8 of the 16-page block, dims 8 * (2 ks + (mi >> 1)) ..
     const int lrow = ((lane >> 3) & 1) * 8 + (lane & 7);
     const int lchk = lane >> 4;
+    int pv = 0;  // early mode: step_sync[1] polled one tile ahead of its use (latency hidden)
     while (cc.u < U) {
         const int slot = consumed % NST;
+        if (!triggered) {
+            // the select+attend grid may launch (and read lengths / page table / pool rows
+            // before its own wait) only once the append is complete
+            if (pv >= my) { pdl_trigger(); triggered = true; }
+            else pv = sb_ld_relaxed(prm.sync + 1);
+        }
         mbar_wait(&bars[slot], (uint32_t)((consumed / NST) & 1));
         if (cc.u != c_unit) {  // a new run: the unit's query fragments and norms
             c_run++;
             c_unit = cc.u;
+            c_pages = Pu[cc.u];
             const char *uh = uhdrs + (c_run % C::NHU) * C::UHDR;
             const uint16_t *qh = reinterpret_cast<const uint16_t *>(uh);
 #pragma unroll
@@ -244,7 +335,7 @@ __global__ void __launch_bounds__(kSBWarps * 32) k_score_bounded(const BoundedSc
         const float l = j == 0 ? lo[0] : j == 1 ? lo[1] : j == 2 ? lo[2] : lo[3];
         const float h = j == 0 ? hi[0] : j == 1 ? hi[1] : j == 2 ? hi[2] : hi[3];
         const int p = cc.t * 32 + gq + 8 * j;
-        const int Pc = (__ldg(prm.seq_len + cc.u) + S - 1) / S;
+        const int Pc = c_pages;
         const uint32_t klo = encode_ordered(f32_to_bf16_rne(l));
         const uint32_t khi = encode_ordered(f32_to_bf16_rne(h));
         if (p < Pc) {
@@ -255,9 +346,23 @@ __global__ void __launch_bounds__(kSBWarps * 32) k_score_bounded(const BoundedSc
         if (lane == 0) prm.tile_max[(int64_t)cc.u * TPU + cc.t] = (uint16_t)m;
         advance(cc);
     }
-    if (prof) {
+    if (prm.prof) {
         __syncwarp();
-        g_sb_prof[blockIdx.x * 4 + 2] = sb_gtimer();  // warp 0's last tile done
+        if (prof) g_sb_prof[blockIdx.x * 4 + 2] = sb_gtimer();  // warp 0's last tile done
+    }
+    if (early) {
+        if (!triggered) {
+            if (lane == 0) sb_spin_until(prm.sync + 1, my);
+            __syncwarp();
+            pdl_trigger();
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && atomicAdd(prm.sync + 3, 1) == (int)gridDim.x - 1) {
+            // every CTA has read the step count: this scorer step is done
+            atomicExch(prm.sync + 3, 0);
+            __threadfence();
+            atomicAdd(prm.sync + 2, 1);
+        }
     }
 }
 
@@ -323,10 +428,11 @@ extern "C" int pt_debug_sb_prof(unsigned long long *host, int n) {
     return PT_OK;
 }
 
-extern "C" int pt_score_bounded(const void *q, int q_dtype, const float *lamnorm, const float *qnorm,
-                                const void *mirror, const float *stds, const int32_t *seq_len, int U_all,
-                                int u0, int nu, int G, int D, int S, int Pmax, uint16_t *keys_lo,
-                                uint16_t *keys_hi, uint16_t *tile_max, void *stream) {
+static int score_bounded_impl(const void *q, int q_dtype, const float *lamnorm, const float *qnorm,
+                              const void *mirror, const float *stds, const int32_t *seq_len, int U_all,
+                              int u0, int nu, int G, int D, int S, int Pmax, uint16_t *keys_lo,
+                              uint16_t *keys_hi, uint16_t *tile_max, void *stream,
+                              const int32_t *snap, int32_t *step_sync) {
     if (!q || !lamnorm || !qnorm || !mirror || !stds || !seq_len || !keys_lo || !keys_hi ||
         !tile_max || U_all < 0 || u0 < 0 || nu < 0 || u0 + nu > U_all || S < 1 || Pmax % 32 || G < 1)
         return PT_ERR_INVALID;
@@ -340,7 +446,30 @@ extern "C" int pt_score_bounded(const void *q, int q_dtype, const float *lamnorm
     BoundedScoreParams sp{static_cast<const uint16_t *>(q) + o * G * D, lamnorm + o * 8, qnorm + o * 8,
                           mv.tiles + o * Pmax * D, stds + o * Pmax, mv.err + o * Pmax, seq_len + o,
                           keys_lo + o * Pmax, keys_hi + o * Pmax, tile_max + o * (Pmax / 32), U, S, Pmax,
-                          sb_env("PT_SB_PROF", 0)};
+                          sb_env("PT_SB_PROF", 0), snap ? snap + o : nullptr, step_sync};
     cudaStream_t st = (cudaStream_t)stream;
     return D == 128 ? sb_g<128>(sp, G, st) : sb_g<64>(sp, G, st);
+}
+
+extern "C" int pt_score_bounded(const void *q, int q_dtype, const float *lamnorm, const float *qnorm,
+                                const void *mirror, const float *stds, const int32_t *seq_len, int U_all,
+                                int u0, int nu, int G, int D, int S, int Pmax, uint16_t *keys_lo,
+                                uint16_t *keys_hi, uint16_t *tile_max, void *stream) {
+    return score_bounded_impl(q, q_dtype, lamnorm, qnorm, mirror, stds, seq_len, U_all, u0, nu, G, D,
+                              S, Pmax, keys_lo, keys_hi, tile_max, stream, nullptr, nullptr);
+}
+
+// The decode step's scorer launched right after pt_append_step (same slot_scratch and
+// step_sync, every unit): it streams every tile but the units' tail tiles while the append
+// runs, then the tail tiles once the append's stores are visible.  PT_ERR_UNSUPPORTED exactly
+// where pt_score_bounded is unsupported (then the caller must not have launched the append
+// with step_sync).
+extern "C" int pt_score_bounded_step(const void *q, int q_dtype, const float *lamnorm,
+                                     const float *qnorm, const void *mirror, const float *stds,
+                                     const int32_t *seq_len, int U, int G, int D, int S, int Pmax,
+                                     uint16_t *keys_lo, uint16_t *keys_hi, uint16_t *tile_max,
+                                     const int32_t *slot_scratch, int32_t *step_sync, void *stream) {
+    if (!slot_scratch || !step_sync) return PT_ERR_INVALID;
+    return score_bounded_impl(q, q_dtype, lamnorm, qnorm, mirror, stds, seq_len, U, 0, U, G, D, S,
+                              Pmax, keys_lo, keys_hi, tile_max, stream, slot_scratch + U + 4, step_sync);
 }

@@ -198,7 +198,8 @@ __global__ void __launch_bounds__(256)
              int32_t *__restrict__ page_table, int32_t *__restrict__ seq_len, int U, int S, int D,
              int Pmax, void *__restrict__ means, float *__restrict__ stds,
              int32_t *__restrict__ pool_state, const int32_t *__restrict__ free_list,
-             int32_t *__restrict__ slot, int prof, const MirrorView mv) {
+             int32_t *__restrict__ slot, int prof, const MirrorView mv,
+             int32_t *__restrict__ step_sync) {
     extern __shared__ __align__(16) char asmem[];
     __shared__ int warp_tot[8];
     __shared__ int carry;
@@ -236,8 +237,11 @@ __global__ void __launch_bounds__(256)
             sn[i] = ni;
             any |= (ni % S == 0);
         }
+        if (step_sync) __threadfence();  // every thread's snapshot stores, before the epoch
         any = __syncthreads_or(any);
         if (threadIdx.x == 0) { __threadfence(); atomicExch(flag_read, 1); }
+        // decode step with an early scorer (pt_score_bounded_step): the lengths are snapshotted
+        if (step_sync && threadIdx.x == 0) atomicAdd(&step_sync[0], 1);
         if (any) alloc_scan(page_table, sn, U, S, Pmax, pool_state, free_list, slot, warp_tot, &carry);
         __threadfence();
         __syncthreads();
@@ -323,6 +327,7 @@ __global__ void __launch_bounds__(256)
             }
         }
     }
+    if (step_sync) __threadfence();  // this CTA's row / stats / length stores, before the epoch
     __syncthreads();
     if (threadIdx.x == 0) {
         // every flag use of this CTA precedes this atomic in program order: no fence needed
@@ -331,6 +336,8 @@ __global__ void __launch_bounds__(256)
             atomicExch(flag_read, 0);
             atomicExch(arrive, 0);
             atomicExch(done, 0);
+            // every CTA's stores are visible: the early scorer may read the tail tiles now
+            if (step_sync) { __threadfence(); atomicAdd(&step_sync[1], 1); }
         }
     }
     if (prof && lane == 0 && u < U && u < kAppProfUnits) app_stamp(true, u, 7, prof == 2);
@@ -538,7 +545,7 @@ template <int DT, int SDT>
 static int launch_append(const void *kn, const void *vn, void *kp, void *vp, int32_t *ptab,
                          int32_t *sl, int U, int S, int D, int Pmax, void *means, float *stds,
                          int32_t *pool_state, const int32_t *free_list, int32_t *slot,
-                         const MirrorView mv, cudaStream_t st) {
+                         const MirrorView mv, cudaStream_t st, int32_t *step_sync) {
     const size_t per_warp = append_per_warp(S, D, DT == PT_F32 ? 4 : 2);
     if (per_warp > 200 * 1024) return PT_ERR_UNSUPPORTED;
     int wpc = (int)((200 * 1024) / per_warp);
@@ -561,11 +568,14 @@ static int launch_append(const void *kn, const void *vn, void *kp, void *vp, int
             PT_CUDA_TRY(cudaFuncSetAttribute(k_append<DT, SDT, DJ_>,                          \
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,    \
                                              (int)smem));                                     \
+            PT_CUDA_TRY(cudaFuncSetAttribute(k_append<DT, SDT, DJ_>,                          \
+                                             cudaFuncAttributePreferredSharedMemoryCarveout, \
+                                             (int)cudaSharedmemCarveoutMaxShared));           \
             configured = smem;                                                                \
         }                                                                                     \
         PT_CUDA_TRY(pt_launch(k_append<DT, SDT, DJ_>, dim3(grid), dim3(wpc * 32), smem, st,   \
                               kn, vn, kp, vp, ptab, sl, U, S, D, Pmax, means, stds,           \
-                              pool_state, free_list, slot, app_prof, mv));                    \
+                              pool_state, free_list, slot, app_prof, mv, step_sync));         \
         break;                                                                                \
     }
     switch (dj) {
@@ -582,11 +592,11 @@ static int launch_append(const void *kn, const void *vn, void *kp, void *vp, int
     return PT_OK;
 }
 
-extern "C" int pt_append(const void *k_new, const void *v_new, void *k_pool, void *v_pool,
-                         int kv_dtype, int32_t *page_table, int32_t *seq_len, int U, int S, int D,
-                         int Pmax, void *means, int stats_dtype, float *stds,
-                         int32_t *pool_state, const int32_t *free_list, int32_t *slot_scratch,
-                         void *mirror, void *stream) {
+static int append_impl(const void *k_new, const void *v_new, void *k_pool, void *v_pool,
+                       int kv_dtype, int32_t *page_table, int32_t *seq_len, int U, int S, int D,
+                       int Pmax, void *means, int stats_dtype, float *stds,
+                       int32_t *pool_state, const int32_t *free_list, int32_t *slot_scratch,
+                       void *mirror, void *stream, int32_t *step_sync) {
     if (!k_new || !v_new || !k_pool || !v_pool || !page_table || !seq_len || !means || !stds ||
         !pool_state || !slot_scratch || U < 0 || S < 1 || Pmax % 32 ||
         (mirror && (stats_dtype != PT_F32 || D % 8)))
@@ -596,14 +606,39 @@ extern "C" int pt_append(const void *k_new, const void *v_new, void *k_pool, voi
     cudaStream_t st = (cudaStream_t)stream;
     int32_t *slot = slot_scratch;
     if (kv_dtype == PT_F32 && stats_dtype == PT_F32)
-        return launch_append<PT_F32, PT_F32>(k_new, v_new, k_pool, v_pool, page_table, seq_len, U, S, D, Pmax, means, stds, pool_state, free_list, slot, mirror_view(mirror, U, Pmax, D), st);
+        return launch_append<PT_F32, PT_F32>(k_new, v_new, k_pool, v_pool, page_table, seq_len, U, S, D, Pmax, means, stds, pool_state, free_list, slot, mirror_view(mirror, U, Pmax, D), st, step_sync);
     if (kv_dtype == PT_BF16 && stats_dtype == PT_F32)
-        return launch_append<PT_BF16, PT_F32>(k_new, v_new, k_pool, v_pool, page_table, seq_len, U, S, D, Pmax, means, stds, pool_state, free_list, slot, mirror_view(mirror, U, Pmax, D), st);
+        return launch_append<PT_BF16, PT_F32>(k_new, v_new, k_pool, v_pool, page_table, seq_len, U, S, D, Pmax, means, stds, pool_state, free_list, slot, mirror_view(mirror, U, Pmax, D), st, step_sync);
     if (kv_dtype == PT_BF16 && stats_dtype == PT_BF16)
-        return launch_append<PT_BF16, PT_BF16>(k_new, v_new, k_pool, v_pool, page_table, seq_len, U, S, D, Pmax, means, stds, pool_state, free_list, slot, mirror_view(mirror, U, Pmax, D), st);
+        return launch_append<PT_BF16, PT_BF16>(k_new, v_new, k_pool, v_pool, page_table, seq_len, U, S, D, Pmax, means, stds, pool_state, free_list, slot, mirror_view(mirror, U, Pmax, D), st, step_sync);
     if (kv_dtype == PT_F32 && stats_dtype == PT_BF16)
-        return launch_append<PT_F32, PT_BF16>(k_new, v_new, k_pool, v_pool, page_table, seq_len, U, S, D, Pmax, means, stds, pool_state, free_list, slot, mirror_view(mirror, U, Pmax, D), st);
+        return launch_append<PT_F32, PT_BF16>(k_new, v_new, k_pool, v_pool, page_table, seq_len, U, S, D, Pmax, means, stds, pool_state, free_list, slot, mirror_view(mirror, U, Pmax, D), st, step_sync);
     return PT_ERR_INVALID;
+}
+
+extern "C" int pt_append(const void *k_new, const void *v_new, void *k_pool, void *v_pool,
+                         int kv_dtype, int32_t *page_table, int32_t *seq_len, int U, int S, int D,
+                         int Pmax, void *means, int stats_dtype, float *stds,
+                         int32_t *pool_state, const int32_t *free_list, int32_t *slot_scratch,
+                         void *mirror, void *stream) {
+    return append_impl(k_new, v_new, k_pool, v_pool, kv_dtype, page_table, seq_len, U, S, D, Pmax,
+                       means, stats_dtype, stds, pool_state, free_list, slot_scratch, mirror, stream,
+                       nullptr);
+}
+
+// pt_append as the first link of a decode step whose scorer starts before the append has
+// finished (pt_score_bounded_step, same step_sync): the append publishes two epochs --
+// step_sync[0] once every unit's length is snapshotted (slot_scratch + U + 4), step_sync[1]
+// once all its stores are visible
+extern "C" int pt_append_step(const void *k_new, const void *v_new, void *k_pool, void *v_pool,
+                              int kv_dtype, int32_t *page_table, int32_t *seq_len, int U, int S,
+                              int D, int Pmax, void *means, int stats_dtype, float *stds,
+                              int32_t *pool_state, const int32_t *free_list, int32_t *slot_scratch,
+                              void *mirror, int32_t *step_sync, void *stream) {
+    if (!step_sync) return PT_ERR_INVALID;
+    return append_impl(k_new, v_new, k_pool, v_pool, kv_dtype, page_table, seq_len, U, S, D, Pmax,
+                       means, stats_dtype, stds, pool_state, free_list, slot_scratch, mirror, stream,
+                       step_sync);
 }
 
 // tuning aid: copy the phase timestamps of the last PT_APP_PROF=1 append (n <= 8 * 8192)

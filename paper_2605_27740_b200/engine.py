@@ -100,6 +100,12 @@ class DecodeEngine:
             h = (U // H // 2) * H
         self.split_at = h
         self.split = self.bounded and U >= 128 and os.environ.get("PT_SPLIT", "") == "1"
+        # decode steps with an append: norms -> append -> bounded scorer, the scorer streaming
+        # every tile but the units' tail tiles while the append runs (pt_append_step /
+        # pt_score_bounded_step; PT_EARLY=0: append -> norms -> scorer, one PDL chain)
+        self.early = (self.bounded and self.chain_norms and os.environ.get("PT_EARLY", "1") != "0"
+                      and self.G <= 8 and D in (64, 128) and U <= 2048)
+        self.step_sync = torch.zeros(4, dtype=torch.int32, device=d)
         # GQA groups wider than the kernels' 8 heads (e.g. 128 q / 8 kv heads): sub-groups of
         # <= 8 heads, scored separately (exact keys) and combined by a key max, one shared
         # selection, attention per sub-group (see _step_wide)
@@ -392,6 +398,23 @@ class DecodeEngine:
         # link of one chain (append -> norms -> score -> select+attend); without PDL, on a
         # side stream (a fork/join that CUDA-graph capture records as two parallel branches)
         main = stream if stream is not None else torch.cuda.current_stream()
+        if (self.early and not self.split and k_new is not None and self.bounded
+                and q.dtype == torch.bfloat16):
+            # the norms first (they store after the previous step's select+attend), then the
+            # append and the scorer that overlaps it -- a paired launch: nothing between them
+            # may fail (shape checks above mirror pt_score_bounded's envelope)
+            q2, qc = self._q(q)
+            c = self.cache
+            self.lam_norms(q, stream=main, chained=True)
+            self.cache.append_batch(k_new, v_new, stream=main, step_sync=self.step_sync)
+            _lib.call("pt_score_bounded_step", q2.data_ptr(), qc, self.lamnorm.data_ptr(),
+                      self.qnorm.data_ptr(), c.mirror.data_ptr(), c.stds.data_ptr(),
+                      c.seq_lens.data_ptr(), self.U, self.G, self.D, c.layout.page_size, c.Pmax,
+                      self.keys.data_ptr(), self.keys_hi.data_ptr(), self.tile_max.data_ptr(),
+                      c._slot.data_ptr(), self.step_sync.data_ptr(), dev.stream_handle(main))
+            self._step_bounded = True
+            self.select_attend(q, stream=main)
+            return self.out, self.lse
         if self.chain_norms:
             if k_new is not None:
                 self.cache.append_batch(k_new, v_new, stream=main)

@@ -381,11 +381,13 @@ class PagedKvCache:
         self.extend(head, k[None], v[None])
         return pos
 
-    def append_batch(self, keys: torch.Tensor, values: torch.Tensor, stream=None) -> None:
+    def append_batch(self, keys: torch.Tensor, values: torch.Tensor, stream=None,
+                     step_sync: torch.Tensor | None = None) -> None:
         """Decode-step append: one row per unit, on the device, no host sync (K1b).
 
         Allocation happens on the device; pool exhaustion sets an error flag that
-        :meth:`check_errors` turns into ``CapacityError``.
+        :meth:`check_errors` turns into ``CapacityError``.  ``step_sync`` (int32[4]): the
+        append of a :class:`DecodeEngine` step whose scorer overlaps it (pt_append_step).
         """
         U, D = self.num_units, self.layout.head_dim
         if tuple(keys.shape) != (U, D) or tuple(values.shape) != (U, D):
@@ -393,12 +395,16 @@ class PagedKvCache:
         if keys.dtype != self.dtype or values.dtype != self.dtype or not keys.is_cuda:
             raise ValueError("keys/values must be device tensors of the cache dtype")
         keys, values = keys.contiguous(), values.contiguous()
-        _lib.call("pt_append", keys.data_ptr(), values.data_ptr(), self.k_pool.data_ptr(),
-                  self.v_pool.data_ptr(), self.kv_code, self.page_table.data_ptr(),
-                  self.seq_lens.data_ptr(), U, self.layout.page_size, D, self.Pmax,
-                  self.means.data_ptr(), self.stats_code, self.stds.data_ptr(),
-                  self.pool_state.data_ptr(), self.free_list_dev.data_ptr(),
-                  self._slot.data_ptr(), *self._mirror_args(), dev.stream_handle(stream))
+        args = (keys.data_ptr(), values.data_ptr(), self.k_pool.data_ptr(),
+                self.v_pool.data_ptr(), self.kv_code, self.page_table.data_ptr(),
+                self.seq_lens.data_ptr(), U, self.layout.page_size, D, self.Pmax,
+                self.means.data_ptr(), self.stats_code, self.stds.data_ptr(),
+                self.pool_state.data_ptr(), self.free_list_dev.data_ptr(),
+                self._slot.data_ptr(), *self._mirror_args())
+        if step_sync is None:
+            _lib.call("pt_append", *args, dev.stream_handle(stream))
+        else:
+            _lib.call("pt_append_step", *args, step_sync.data_ptr(), dev.stream_handle(stream))
         self._seq_host += 1
 
     def check_errors(self) -> None:

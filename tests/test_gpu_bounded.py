@@ -343,3 +343,71 @@ def test_half_batch_split_step_equals_one_range(cuda, oracle, monkeypatch):
         assert set(sel[u, : nsel[u]].tolist()) == set(ref["sel"][u, : ref["n_sel"][u]].tolist())
     np.testing.assert_array_equal(a.kth.cpu().numpy(), ref["kth"])
     np.testing.assert_array_equal(a.kplus1.cpu().numpy(), ref["kplus1"])
+
+
+@pytest.mark.parametrize("U,H,n0,ragged", [
+    (16, 8, 16 * 4096 - 3, True),    # ~2K tiles over ~1.2K scorer warps: ranges cross units
+    (6, 2, 16 * 64 * 3 - 2, False),  # tail page / tail tile boundaries crossed within the run
+    (256, 8, 16 * 40 + 5, True),     # many short units: several tail tiles per warp range
+])
+def test_early_scorer_step_equals_chained_step(cuda, monkeypatch, U, H, n0, ragged):
+    """DecodeEngine.step with the scorer overlapping the append (pt_append_step +
+    pt_score_bounded_step: non-tail tiles streamed from the snapshot lengths, tail tiles
+    deferred until the append's stores are visible) == the append -> norms -> scorer chain
+    (PT_EARLY=0): key intervals, tile maxima, selections, kth / kplus1 and outputs bit for bit,
+    over eager steps (new pages, new 32-page tiles) and CUDA-graph replays."""
+    pt = _pt()
+    D, S, G, k = 128, 16, 4, 8
+    rng = np.random.default_rng(U + n0)
+    nr = (n0 - rng.integers(0, 40, U)) if ragged else np.full(U, n0)
+    dev = torch.device("cuda")
+    K = torch.randn(U, n0, D, device=dev).to(torch.bfloat16)
+    V = torch.randn(U, n0, D, device=dev).to(torch.bfloat16)
+    steps = 12
+    engines, caches = [], []
+    for early in ("1", "0"):
+        monkeypatch.setenv("PT_EARLY", early)
+        Pcap = -(-(n0 + steps + 8) // S) + 2
+        layout = pt.CacheLayout(num_kv_heads=H, head_dim=D, page_size=S, max_pages=U * Pcap)
+        cache = pt.PagedKvCache(layout, batch=U // H, dtype=torch.bfloat16, max_pages_per_head=Pcap,
+                                mirror=True)
+        cache.extend_units(K, V, n_rows=nr)
+        eng = pt.DecodeEngine(cache, G, k)
+        assert eng.early == (early == "1") and eng.bounded
+        engines.append(eng)
+        caches.append(cache)
+    qs = [torch.randn(U * G, D, device=dev).to(torch.bfloat16) for _ in range(steps)]
+    kn = [torch.randn(U, D, device=dev).to(torch.bfloat16) for _ in range(steps)]
+
+    def compare():
+        a, b = engines
+        seq = caches[0].seq_lens
+        assert torch.equal(seq, caches[1].seq_lens)
+        P = (-(-seq // S)).cpu().numpy()
+        ka, kb = a.keys.cpu().numpy(), b.keys.cpu().numpy()
+        ha, hb = a.keys_hi.cpu().numpy(), b.keys_hi.cpu().numpy()
+        ta, tb = a.tile_max.cpu().numpy(), b.tile_max.cpu().numpy()
+        for u in range(U):
+            np.testing.assert_array_equal(ka[u, : P[u]], kb[u, : P[u]])
+            np.testing.assert_array_equal(ha[u, : P[u]], hb[u, : P[u]])
+            np.testing.assert_array_equal(ta[u, : -(-P[u] // 32)], tb[u, : -(-P[u] // 32)])
+        assert torch.equal(a.sel.sort(dim=1).values, b.sel.sort(dim=1).values)
+        for x, y in ((a.n_sel, b.n_sel), (a.kth, b.kth), (a.kplus1, b.kplus1), (a.out, b.out),
+                     (a.lse, b.lse)):
+            assert torch.equal(x, y)
+
+    for t in range(steps // 2):  # eager, back to back (no sync in between), then compared
+        for eng in engines:
+            eng.step(qs[t], kn[t], kn[t])
+        torch.cuda.synchronize()
+        compare()
+    assert int(engines[0].step_sync[0]) == int(engines[0].step_sync[2]) == steps // 2
+    for eng in engines:  # graph replays of the same step
+        eng.capture(qs[0], kn[0], kn[0])
+    for t in range(steps // 2):
+        for eng in engines:
+            eng.replay()
+        torch.cuda.synchronize()
+        compare()
+    for c in caches:
+        c.check_errors()
