@@ -829,8 +829,8 @@ def main():
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1000,
                     "path": "PipelinedDecoder.submit() (native pt_pipe_submit): pinned host "
-                            "q|k|v block -> H2D (h2d stream) -> captured step graph (append, norms, "
-                            "score, select+attend) -> D2H f32 outputs (d2h stream), double-buffered, "
+                            "q|k|v block -> H2D (h2d stream) -> captured step graph (norms, append, "
+                            "scorer overlapping the append, select+attend) -> D2H f32 outputs (d2h stream), double-buffered, "
                             "every step; wall clock over the steps, max over ranks"},
             "clocks": sampler.summary(),
             "allgather_us": allgather_us,
